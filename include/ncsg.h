@@ -1,0 +1,202 @@
+/*
+ * ncsg.h -- C ABI of the B200-native NCS (near-circulant splitting) hot path.
+ *
+ * Drop-in boundary for the reference's CPU operator/solver path
+ * (arXiv 1810.13100 reference `ncstomo`, paths relative to
+ * /root/reference/proj).  Plain pointers and sizes only; no C++ exceptions
+ * cross this boundary.  Every function returns an ncsg_status; the message of
+ * the last failure on the calling thread is available from
+ * ncsg_last_error().  Status codes mirror the reference's exception classes
+ * and CLI exit codes (tools/main.cpp:588-603):
+ *   NCSG_INVALID   <- std::invalid_argument   (e.g. radon.cpp:37-42)
+ *   NCSG_DIVERGED  <- DivergenceError          (solvers.hpp:101-105)
+ *   NCSG_CUDA      <- device / runtime failure (no CPU fallback exists)
+ *
+ * All compute is fp32 on the device; host-facing *_host entry points take
+ * and return fp64 like the reference's std::span<const double> signatures and
+ * convert at the boundary.  Device entry points take device pointers and a
+ * cudaStream_t passed as void* (NULL = the handle's own stream).
+ */
+#ifndef NCSG_H
+#define NCSG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  NCSG_OK = 0,
+  NCSG_INVALID = 2,
+  NCSG_RUNTIME = 3,
+  NCSG_DIVERGED = 4,
+  NCSG_CUDA = 5
+} ncsg_status;
+
+/* Message of the last failing call on this thread ("" if none). */
+const char* ncsg_last_error(void);
+/* Library version "major.minor.patch". */
+const char* ncsg_version(void);
+/* Number of visible CUDA devices (0 when none: every compute entry point then
+ * fails with NCSG_CUDA -- there is no CPU fallback). */
+int ncsg_device_count(void);
+
+/* ------------------------------------------------------------------ geometry
+ * Replaces ncstomo::default_detector_count (radon.cpp:10-13). */
+int ncsg_default_detector_count(int n);
+
+/* Parallel-beam projector handle.  Replaces RadonMap::RadonMap(n, n_angles,
+ * n_det) (radon.hpp:16-36, radon.cpp:35-72): same validation (n >= 2,
+ * n_angles >= 1, odd n_det covering the diagonal) and the same sample set --
+ * the reference's fp64 ray table and per-sample box check are replayed on the
+ * host when the handle is created and uploaded as per-ray valid intervals. */
+typedef struct ncsg_radon ncsg_radon;
+ncsg_status ncsg_radon_create(int n, int n_angles, int n_det, int device, ncsg_radon** out);
+ncsg_status ncsg_radon_destroy(ncsg_radon* r);
+/* domain_size() == n*n, range_size() == n_angles*n_det (radon.cpp:74-80). */
+size_t ncsg_radon_domain_size(const ncsg_radon* r);
+size_t ncsg_radon_range_size(const ncsg_radon* r);
+/* Number of valid bilinear samples per application (= sum of R(1)). */
+int64_t ncsg_radon_sample_count(const ncsg_radon* r);
+
+/* RadonMap::forward (radon.cpp:82-102) on `batch` images laid out back to
+ * back (stride n*n) into `batch` sinograms (stride n_angles*n_det), angle-
+ * major [t][d] (image.hpp:23-36).  Device pointers. */
+ncsg_status ncsg_radon_forward(const ncsg_radon* r, const float* x, float* out, int batch,
+                               void* stream);
+/* RadonMap::adjoint (radon.cpp:104-127): exact transpose of forward; `out` is
+ * overwritten (the reference zero-fills first, radon.cpp:107). */
+ncsg_status ncsg_radon_adjoint(const ncsg_radon* r, const float* u, float* out, int batch,
+                               void* stream);
+/* Host fp64 wrappers with the reference's span<const double> semantics. */
+ncsg_status ncsg_radon_forward_host(const ncsg_radon* r, const double* x, double* out,
+                                    int batch);
+ncsg_status ncsg_radon_adjoint_host(const ncsg_radon* r, const double* u, double* out,
+                                    int batch);
+
+/* GradMap::forward / adjoint (grad.hpp:17-28, grad.cpp:53-84): range layout is
+ * the N x (N-1) horizontal block followed by the (N-1) x N vertical block. */
+ncsg_status ncsg_grad_forward(int n, const float* x, float* out, int batch, void* stream);
+ncsg_status ncsg_grad_adjoint(int n, const float* g, float* out, int batch, void* stream);
+ncsg_status ncsg_grad_forward_host(int n, const double* x, double* out, int batch);
+ncsg_status ncsg_grad_adjoint_host(int n, const double* g, double* out, int batch);
+
+/* MaskApplier::apply (circulant.hpp:31-42, circulant.cpp:27-37):
+ * out = Re(F^-1 (h .* F x)) for real N x N images; `mask` is the interleaved
+ * complex N x N SpectralMask in DFT-bin order (circulant.hpp:16-25).  x and
+ * out may alias.  Host fp64 in/out, device fp32 compute. */
+ncsg_status ncsg_mask_apply_host(int n, const double* mask, const double* x, double* out,
+                                 int batch, int device);
+
+/* -------------------------------------------------------------------- solver
+ * Problem + solver-configuration handle: the device-resident Engine of
+ * solvers.cpp:84-265.  Problem kinds:
+ *   NCSG_CT       blocks {1, R, QuadraticConj, b}, {beta/alpha, D,
+ *                 ScaledL1Conj(lambda*alpha/beta)} -- assemble_problem
+ *                 (pipeline.cpp:69-98)
+ *   NCSG_DENOISE  blocks {1, I, QuadraticConj, b}, {beta/alpha, D, ...}
+ *                 (the SplitProblem built in test_solvers.cpp:646-664)
+ * With positivity != 0 a third block {1, I, NonnegConj} is appended
+ * (pipeline.cpp:93-96).  `mask` (nullable) is the SolverConfig::mask -- the
+ * metric surrogate C; NULL selects M = gamma I, i.e. pdhg_solve
+ * (solvers.cpp:428-433).  The engine applies pinv(gamma + alpha*C) with
+ * cfg.pinv_rel_tol (solvers.cpp:93-99).  `b` holds `batch` offsets back to
+ * back (m each). */
+typedef enum { NCSG_CT = 0, NCSG_DENOISE = 1 } ncsg_kind;
+
+typedef struct {
+  int kind;          /* ncsg_kind */
+  int n;             /* image side N */
+  int n_angles;      /* CT only */
+  int n_det;         /* CT only */
+  int batch;         /* independent problems sharing geometry and mask */
+  int positivity;    /* append {1, I, NonnegConj} */
+  double alpha;      /* SolverConfig::alpha, also ModelParams::alpha */
+  double beta;       /* ModelParams::beta: D-block weight beta/alpha */
+  double lambda;     /* TV weight: ScaledL1Conj bound lambda*alpha/beta */
+  double gamma;      /* SolverConfig::gamma */
+  double pinv_rel_tol; /* SolverConfig::pinv_rel_tol (1e-12 by default) */
+  const double* mask;  /* interleaved complex N*N, nullable (PDHG) */
+  const double* b;     /* batch * m offsets (m = angles*det or N*N) */
+  int angle_begin;   /* angle shard [angle_begin, angle_end) of this rank; */
+  int angle_end;     /* 0,0 = all angles (single GPU) */
+  int device;
+} ncsg_problem_desc;
+
+typedef struct ncsg_problem ncsg_problem;
+
+ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** out);
+ncsg_status ncsg_problem_destroy(ncsg_problem* p);
+/* SplitProblem::domain_size/range_size (solvers.hpp:28-29), per problem. */
+size_t ncsg_problem_domain_size(const ncsg_problem* p);
+size_t ncsg_problem_range_size(const ncsg_problem* p);
+/* The handle's CUDA stream (cudaStream_t as void*). */
+void* ncsg_problem_stream(const ncsg_problem* p);
+
+/* SolverState{x, u, iter} (solvers.hpp:74-78) in/out, fp64 host arrays of
+ * batch*N*N and batch*range_size.  NULL x or u means zeros (make_state,
+ * solvers.cpp:406-411).  set_state also runs Engine::init (ax = A x,
+ * solvers.cpp:118-122). */
+ncsg_status ncsg_set_state(ncsg_problem* p, const double* x, const double* u, int64_t iter);
+ncsg_status ncsg_get_state(ncsg_problem* p, double* x, double* u, int64_t* iter);
+/* Device views of the state (fp32, batch-major) for zero-copy callers. */
+float* ncsg_state_x(ncsg_problem* p);
+float* ncsg_state_u(ncsg_problem* p);
+
+/* `iters` x Engine::step (solvers.cpp:124-161), asynchronous on the handle's
+ * stream; no host synchronisation.  Divergence (check_finite,
+ * solvers.cpp:248-255) is flagged on the device and reported by the next
+ * synchronising call. */
+ncsg_status ncsg_step(ncsg_problem* p, int iters);
+/* Same, replayed through a captured CUDA graph of `iters` steps. */
+ncsg_status ncsg_step_graph(ncsg_problem* p, int iters);
+/* Synchronise; returns NCSG_DIVERGED (and *iter, nullable) if any step so far
+ * left the finite range. */
+ncsg_status ncsg_sync(ncsg_problem* p, int64_t* diverged_iter);
+
+/* Engine::objective = objective_from_ax(ax) (solvers.cpp:163,362-381), one
+ * value per problem (out[batch]). */
+ncsg_status ncsg_objective(ncsg_problem* p, double* out);
+/* Engine::step_seminorm (solvers.cpp:166-202) of (dx, du) = (x_k - x_{k-1},
+ * u_k - u_{k-1}) for the last step; NaN where the radicand is negative beyond
+ * roundoff (solvers.cpp:305-316). */
+ncsg_status ncsg_last_seminorm(ncsg_problem* p, double* out);
+
+/* ConvergenceRecord row (solvers.hpp:82-86). */
+typedef struct {
+  int64_t iter;
+  double objective;
+  double rel_subopt;
+  double seminorm_step;
+  double wall_ms;
+} ncsg_record_row;
+
+/* ncs_solve / pdhg_solve (solvers.cpp:267-337, 423-433): max_iters steps from
+ * the current state (reset iter to 0), recording every `record_every` steps
+ * and at the end.  rows: capacity max_rows per problem, problem-major
+ * (row r of problem q at rows[q*max_rows + r]); *n_rows = rows per problem.
+ * f_star (nullable, one per problem) anchors rel_subopt as in the reference.
+ * check_step_condition runs the 40-step power-method screen
+ * (solvers.cpp:206-245) and writes its estimate into *screen_est (nullable). */
+ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
+                       int check_step_condition, const double* f_star, ncsg_record_row* rows,
+                       int max_rows, int* n_rows, double* screen_est);
+
+/* -------------------------------------------------------- multi-GPU phases
+ * One NCS step split at its exchange points for angle-sharded execution
+ * (SURVEY.md §8e): phase A computes this rank's partial A^T u (own angles of
+ * R^T u_s, plus the D^T u_g / identity terms on rank 0 only) into the device
+ * buffer returned by ncsg_atu_buffer(); the caller all-reduces that buffer
+ * (NCCL over NVLink) and runs phase B, which applies M^+ (replicated FFT),
+ * updates x, projects the own angles and updates the own dual blocks. */
+ncsg_status ncsg_step_phase_a(ncsg_problem* p);
+float* ncsg_atu_buffer(ncsg_problem* p);
+ncsg_status ncsg_step_phase_b(ncsg_problem* p);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NCSG_H */

@@ -1,0 +1,117 @@
+"""The five BASELINE.json workloads and their pinned splitting parameters.
+
+BASELINE.json fixes sizes, lambda, noise and iteration counts but not the NCS
+parameters alpha, beta, gamma, dc.  They are pinned once, per
+config, by ``oracle/pin_configs.py`` with the reference's own rules and stored
+in ``pinned.json`` next to this file, so the GPU path and the oracle always
+consume identical numbers:
+
+* alpha = beta (gradient block weight 1, pipeline.cpp:91);
+* dc = DC response of E^T E, <1, E^T E 1>/n (README.md "Choosing parameters");
+* mask scale = calibrate_scale(NormalMap(E), radon_mask(N,1,1), 8, seed 0)
+  (pipeline.cpp:100-110, circulant.cpp:142-169);
+* gamma = 1.2 x the power-method estimate of lambda_max(alpha (A^T A - C))
+  (the reference's step screen, solvers.cpp:206-245, and the MaskedMetric
+  rule of test_solvers.cpp:121-141 with a wider margin for the 40-step
+  power-method estimate).
+"""
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import dataclass, field
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+PINNED = os.path.join(HERE, "pinned.json")
+
+
+@dataclass(frozen=True)
+class Config:
+    name: str
+    kind: str  # "ct" or "denoise"
+    n: int
+    angles: int
+    det: int
+    ellipses: int
+    lam: float
+    iters: int
+    batch: int = 1
+    noise_frac: float = 0.0  # CT: sigma = frac * max(R x_true)
+    image_sigma: float = 0.0  # denoise: additive image noise
+    phantom_seed: int = 1000
+    noise_seed: int = 2000
+    description: str = ""
+    pinned: dict = field(default_factory=dict, compare=False, hash=False)
+
+    @property
+    def kind_id(self) -> int:
+        return 0 if self.kind == "ct" else 1
+
+    @property
+    def m(self) -> int:
+        return self.angles * self.det if self.kind == "ct" else self.n * self.n
+
+    @property
+    def g(self) -> int:
+        return 2 * self.n * (self.n - 1)
+
+    @property
+    def alpha(self) -> float:
+        return self.pinned["alpha"]
+
+    @property
+    def beta(self) -> float:
+        return self.pinned["beta"]
+
+    @property
+    def gamma(self) -> float:
+        return self.pinned["gamma"]
+
+    @property
+    def dc(self) -> float:
+        return self.pinned.get("dc", 0.0)
+
+    @property
+    def mask_scale(self) -> float:
+        return self.pinned.get("mask_scale", 0.0)
+
+
+_BASE = [
+    Config("c1", "ct", 128, 180, 185, 10, 0.01, 500, noise_frac=0.01, phantom_seed=1001,
+           noise_seed=2001, description="CT-TV 128^2, 180 angles x 185 det, 500 iters"),
+    Config("c2", "denoise", 1024, 0, 0, 20, 0.05, 1000, image_sigma=0.1, phantom_seed=1002,
+           noise_seed=2002, description="TV denoise 1024^2, A=[I;D], 1000 iters"),
+    Config("c3", "ct", 512, 720, 725, 40, 0.005, 1000, noise_frac=0.01, phantom_seed=1003,
+           noise_seed=2003, description="CT-TV 512^2, 720 angles x 725 det, 1000 iters"),
+    Config("c4", "ct", 2048, 2048, 2897, 200, 0.002, 300, noise_frac=0.005, phantom_seed=1004,
+           noise_seed=2004, description="CT-TV 2048^2, 2048 angles x 2897 det, 300 iters"),
+    Config("c5", "ct", 256, 360, 363, 15, 0.01, 500, batch=64, noise_frac=0.01,
+           phantom_seed=1005, noise_seed=2005,
+           description="64 x CT-TV 256^2, 360 angles x 363 det, 500 iters"),
+]
+
+
+def _load() -> dict:
+    if os.path.exists(PINNED):
+        with open(PINNED) as f:
+            return json.load(f)
+    return {}
+
+
+def get(name: str) -> Config:
+    pins = _load()
+    for c in _BASE:
+        if c.name == name:
+            return Config(**{**c.__dict__, "pinned": pins.get(name, {})})
+    raise KeyError(name)
+
+
+def all_configs() -> list[Config]:
+    return [get(c.name) for c in _BASE]
+
+
+def base(name: str) -> Config:
+    for c in _BASE:
+        if c.name == name:
+            return c
+    raise KeyError(name)

@@ -1,0 +1,867 @@
+// C ABI (include/ncsg.h): handles, the device-resident NCS engine and the
+// reference-shaped entry points.  No exceptions cross the boundary; there is
+// no CPU fallback -- without a CUDA device every compute call fails loudly.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <complex>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ncs_kernels.cuh"
+#include "ncsg_internal.cuh"
+
+namespace ncsg {
+
+namespace {
+thread_local std::string g_err;
+}
+void set_error(const std::string& msg) { g_err = msg; }
+
+template <class F>
+ncsg_status guard(F&& f) {
+  try {
+    f();
+    return NCSG_OK;
+  } catch (const Error& e) {
+    g_err = e.msg;
+    return e.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return NCSG_RUNTIME;
+  }
+}
+
+void require_device(int device) {
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    throw Error{NCSG_CUDA, "no CUDA device is available (the NCS path has no CPU fallback)"};
+  if (device < 0 || device >= count) throw Error{NCSG_INVALID, "device index out of range"};
+  NCSG_CUDA_CHECK(cudaSetDevice(device));
+}
+
+// Hermitian part of a full N x N complex mask, half spectrum stored [k][j]
+// (k = 0..N/2) and scaled by `scale` (the 1/N^2 of fft.cpp:46-47).
+std::vector<float2> half_mask(int n, const std::vector<std::complex<double>>& h, double scale) {
+  const int nk = n / 2 + 1;
+  std::vector<float2> out(static_cast<size_t>(nk) * n);
+  for (int k = 0; k < nk; ++k)
+    for (int j = 0; j < n; ++j) {
+      std::complex<double> a = h[static_cast<size_t>(j) * n + k];
+      std::complex<double> b = h[static_cast<size_t>((n - j) % n) * n + (n - k) % n];
+      std::complex<double> v = 0.5 * (a + std::conj(b)) * scale;
+      out[static_cast<size_t>(k) * n + j] =
+          make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
+    }
+  return out;
+}
+
+std::vector<std::complex<double>> read_mask(int n, const double* m) {
+  std::vector<std::complex<double>> h(static_cast<size_t>(n) * n);
+  for (size_t i = 0; i < h.size(); ++i) h[i] = {m[2 * i], m[2 * i + 1]};
+  return h;
+}
+
+// pinv_mask (circulant.cpp:47-55)
+std::vector<std::complex<double>> pinv(const std::vector<std::complex<double>>& h,
+                                       double rel_tol) {
+  double hmax = 0.0;
+  for (const auto& z : h) hmax = std::max(hmax, std::abs(z));
+  std::vector<std::complex<double>> out(h.size());
+  double cutoff = rel_tol * hmax;
+  for (size_t i = 0; i < h.size(); ++i) out[i] = std::abs(h[i]) > cutoff ? 1.0 / h[i] : 0.0;
+  return out;
+}
+
+struct Stream {
+  cudaStream_t s = nullptr;
+  ~Stream() {
+    if (s) cudaStreamDestroy(s);
+  }
+};
+
+}  // namespace ncsg
+
+using namespace ncsg;
+
+struct ncsg_radon {
+  RadonDev dev;
+  Stream stream;
+};
+
+struct ncsg_problem {
+  ncsg_problem_desc d{};
+  int device = 0;
+  Stream stream;
+  std::unique_ptr<RadonDev> radon;
+  FftPlan fft;
+  bool has_mask = false;
+  std::vector<std::complex<double>> mask_full;  // cfg.mask (apply_m)
+  DevBuf<float2> maskT;       // herm(pinv(gamma + alpha C)) / N^2
+  DevBuf<float2> maskT_orig;  // herm(C) / N^2 for apply_m (seminorm, screen)
+  size_t nn = 0, m0 = 0, g = 0, range = 0;
+  int batch = 1;
+  float wd = 0.f, bound = 0.f;
+  DevBuf<float> x, x_old, xT, u, axs, b;
+  DevBuf<float> fp_part, bp_part;
+  DevBuf<float2> spec;
+  DevBuf<int> flag;  // [0] first bad step (INT_MAX: none), [1] step counter
+  DevBuf<double> red;
+  // record-step scratch (lazy)
+  DevBuf<float> x_prev, u_prev, dx, du, adx, mdx, dxT;
+  int64_t iter = 0;
+  size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
+  bool rank0 = true;              // adds the replicated blocks to A^T u
+  std::map<int, cudaGraphExec_t> graphs;
+  ~ncsg_problem() {
+    for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+  }
+};
+
+namespace {
+
+int* step_counter(ncsg_problem* p) { return p->flag.p; }
+
+AtuTerms atu_terms(ncsg_problem* p) {
+  AtuTerms T;
+  T.n = p->d.n;
+  if (p->d.kind == NCSG_CT) {
+    T.bp_part = p->bp_part.p;
+    T.nV = p->radon->bp_chunks[0];
+    T.nH = p->radon->bp_chunks[1];
+    T.part_stride = static_cast<size_t>(p->radon->n_partials()) * p->nn;
+    if (p->rank0 && p->d.positivity) T.ident = p->u.p + p->m0 + p->g;
+  } else if (p->rank0) {
+    T.ident = p->u.p;
+    if (p->d.positivity) T.ident2 = p->u.p + p->m0 + p->g;
+  }
+  T.ident_stride = p->range;
+  if (p->rank0) {
+    T.ug = p->u.p + p->m0;
+    T.ug_stride = p->range;
+    T.wd = p->wd;
+  }
+  return T;
+}
+
+void phase_a(ncsg_problem* p) {
+  if (p->d.kind == NCSG_CT) {
+    // u_s is the first m0 entries of each problem's dual (stride range).
+    launch_radon_adjoint_partial(*p->radon, p->u.p, p->range, p->bp_part.p, p->batch,
+                                 p->stream.s);
+  }
+}
+
+void phase_b(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  AtuTerms T = atu_terms(p);
+  T.counter = step_counter(p);
+  launch_fft_rows_r2c(p->fft, T, p->spec.p, p->batch, s);
+  launch_fft_cols_filter(p->fft, p->spec.p, p->maskT.p, p->batch, s);
+  XUpdate xu;
+  xu.x = p->x.p;
+  xu.x_old = p->x_old.p;
+  xu.xT = (p->d.kind == NCSG_CT && !p->radon->geo.cls[1].empty()) ? p->xT.p : nullptr;
+  xu.subtract = 1;
+  xu.flag = p->flag.p;
+  launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
+  if (p->d.kind == NCSG_CT)
+    launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
+  DualArgs a;
+  a.kind = p->d.kind;
+  a.n = p->d.n;
+  a.positivity = p->d.positivity;
+  a.alpha = static_cast<float>(p->d.alpha);
+  a.s_quad = static_cast<float>(1.0 / (1.0 + p->d.alpha));
+  a.wd = p->wd;
+  a.bound = p->bound;
+  a.fp_part = p->fp_part.p;
+  a.n_strips = p->radon ? p->radon->n_strips : 0;
+  a.m = p->m0;
+  a.m_begin = p->m_begin;
+  a.m_end = p->m_end;
+  a.u0 = p->u.p;
+  a.axs = p->axs.p;
+  a.b = p->b.p;
+  a.ug = p->u.p + p->m0;
+  a.up = p->u.p + p->m0 + p->g;
+  a.u_stride = p->range;
+  a.x = p->x.p;
+  a.x_old = p->x_old.p;
+  a.flag = p->flag.p;
+  launch_dual_update(a, p->batch, s);
+}
+
+void do_step(ncsg_problem* p) {
+  phase_a(p);
+  phase_b(p);
+}
+
+// Engine::init (solvers.cpp:118-122): ax = A x for the data block (the other
+// blocks are recomputed from x each step).
+void engine_init(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  if (p->d.kind == NCSG_CT) {
+    if (!p->radon->geo.cls[1].empty()) launch_transpose(p->x.p, p->xT.p, p->d.n, p->batch, s);
+    launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
+    launch_strip_sum(*p->radon, p->fp_part.p, p->axs.p, p->batch, s);
+  }
+}
+
+void reset_flag(ncsg_problem* p) {
+  int h[2] = {INT_MAX, 0};
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(p->flag.p, h, sizeof(h), cudaMemcpyHostToDevice, p->stream.s));
+}
+
+// Throws DivergenceError-equivalent if any step flagged a non-finite value.
+void check_divergence(ncsg_problem* p, int64_t base_iter) {
+  int h[2];
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(h, p->flag.p, sizeof(h), cudaMemcpyDeviceToHost, p->stream.s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+  if (h[0] != INT_MAX) {
+    int64_t it = base_iter + h[0];
+    throw Error{NCSG_DIVERGED, "diverged at iteration " + std::to_string(it) +
+                                   ": image iterate left the finite range"};
+  }
+}
+
+std::vector<double> objective_values(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  ObjArgs a;
+  a.kind = p->d.kind;
+  a.n = p->d.n;
+  a.positivity = p->d.positivity;
+  a.with_grad = p->rank0 ? 1 : 0;
+  a.wd = p->wd;
+  a.axs = p->axs.p;
+  a.b = p->b.p;
+  a.x = p->x.p;
+  a.m = p->m0;
+  a.m_begin = p->m_begin;
+  a.m_end = p->m_end;
+  const int nb = objective_blocks();
+  a.out = p->red.p;
+  launch_objective(a, p->batch, s);
+  std::vector<double> h(static_cast<size_t>(p->batch) * nb * 4);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), p->red.p, h.size() * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<double> f(p->batch);
+  for (int b = 0; b < p->batch; ++b) {
+    double q = 0, l1 = 0, mx = 0, mn = 0;
+    for (int k = 0; k < nb; ++k) {
+      const double* r = &h[(static_cast<size_t>(b) * nb + k) * 4];
+      q += r[0];
+      l1 += r[1];
+      mx = std::max(mx, r[2]);
+      mn = std::min(mn, r[3]);
+    }
+    // QuadraticConj::objective + ScaledL1Conj::objective (prox.cpp:26-44)
+    double total = 0.5 * q + static_cast<double>(p->bound) * l1;
+    if (p->d.positivity) {  // NonnegConj::objective (prox.cpp:107-114)
+      double tol = 1e-9 * std::max(1.0, mx);
+      if (mn < -tol) total = INFINITY;
+    }
+    f[b] = total;
+  }
+  return f;
+}
+
+void ensure_scratch(ncsg_problem* p) {
+  if (p->x_prev.n) return;
+  size_t xs = p->nn * p->batch, us = p->range * p->batch;
+  p->x_prev.alloc(xs);
+  p->u_prev.alloc(us);
+  p->dx.alloc(xs);
+  p->du.alloc(us);
+  p->adx.alloc(us);
+  p->mdx.alloc(xs);
+  p->dxT.alloc(xs);
+}
+
+// Stacked forward of an image into a range vector (StackedMap::forward,
+// linear_map.cpp:39-45).
+void stacked_forward(ncsg_problem* p, const float* img, float* imgT, float* out) {
+  cudaStream_t s = p->stream.s;
+  if (p->d.kind == NCSG_CT) {
+    if (!p->radon->geo.cls[1].empty()) launch_transpose(img, imgT, p->d.n, p->batch, s);
+    launch_radon_forward_partial(*p->radon, img, imgT, p->fp_part.p, p->batch, s);
+  }
+  StackArgs a;
+  a.kind = p->d.kind;
+  a.n = p->d.n;
+  a.n_strips = p->radon ? p->radon->n_strips : 0;
+  a.wd = p->wd;
+  a.fp_part = p->fp_part.p;
+  a.x = img;
+  a.out = out;
+  a.m0 = p->m0;
+  a.range = p->range;
+  launch_stacked_rest(a, p->batch, s);
+}
+
+// out = F^-1 (maskT F img) for plain images (apply_m, circulant part).
+void apply_filter(ncsg_problem* p, const float* img, const float2* maskT, float* out) {
+  cudaStream_t s = p->stream.s;
+  AtuTerms T;
+  T.n = p->d.n;
+  T.plain = img;
+  launch_fft_rows_r2c(p->fft, T, p->spec.p, p->batch, s);
+  launch_fft_cols_filter(p->fft, p->spec.p, maskT, p->batch, s);
+  XUpdate xu;
+  xu.x = out;
+  xu.subtract = 0;
+  launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
+}
+
+// Engine::step_seminorm (solvers.cpp:166-177) on the last step's (dx, du).
+std::vector<double> seminorm_values(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  launch_sub(p->x.p, p->x_prev.p, p->dx.p, p->nn * p->batch, s);
+  launch_sub(p->u.p, p->u_prev.p, p->du.p, p->range * p->batch, s);
+  stacked_forward(p, p->dx.p, p->dxT.p, p->adx.p);
+  if (p->has_mask) apply_filter(p, p->dx.p, p->maskT_orig.p, p->mdx.p);
+  SemArgs a;
+  a.n = p->d.n;
+  a.alpha = p->d.alpha;
+  a.gamma = p->d.gamma;
+  a.du = p->du.p;
+  a.adx = p->adx.p;
+  a.range = p->range;
+  a.r_begin = 0;
+  a.r_end = p->range;
+  a.dx = p->dx.p;
+  a.mdx = p->has_mask ? p->mdx.p : nullptr;
+  a.out = p->red.p;
+  launch_seminorm(a, p->batch, s);
+  const int nb = objective_blocks();
+  std::vector<double> h(static_cast<size_t>(p->batch) * nb * 3);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), p->red.p, h.size() * sizeof(double),
+                                  cudaMemcpyDeviceToHost, s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<double> out(p->batch);
+  for (int b = 0; b < p->batch; ++b) {
+    double t1 = 0, aq = 0, mq = 0;
+    for (int k = 0; k < nb; ++k) {
+      const double* r = &h[(static_cast<size_t>(b) * nb + k) * 3];
+      t1 += r[0];
+      aq += r[1];
+      mq += r[2];
+    }
+    double a_quad = p->d.alpha * p->d.alpha * aq;
+    double m_quad = p->d.alpha * mq;
+    // seminorm_from (solvers.cpp:35-50)
+    double rad = t1 + m_quad - a_quad;
+    if (rad < 0.0) {
+      double mag = std::max(1.0, t1 + std::abs(m_quad) + a_quad);
+      if (rad < -1e-10 * mag) {
+        out[b] = NAN;
+        continue;
+      }
+      rad = 0.0;
+    }
+    out[b] = std::sqrt(rad);
+  }
+  return out;
+}
+
+void upload_f64(ncsg_problem* p, const double* h, float* d, size_t count) {
+  std::vector<float> tmp(count);
+  for (size_t i = 0; i < count; ++i) tmp[i] = static_cast<float>(h[i]);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(d, tmp.data(), count * sizeof(float), cudaMemcpyHostToDevice,
+                                  p->stream.s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+}
+
+void download_f64(cudaStream_t s, const float* d, double* h, size_t count) {
+  std::vector<float> tmp(count);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(tmp.data(), d, count * sizeof(float), cudaMemcpyDeviceToHost, s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i < count; ++i) h[i] = tmp[i];
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ncsg_last_error(void) { return g_err.c_str(); }
+const char* ncsg_version(void) { return "0.1.0"; }
+
+int ncsg_device_count(void) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return 0;
+  return c;
+}
+
+int ncsg_default_detector_count(int n) {
+  // default_detector_count (radon.cpp:10-13)
+  int d = static_cast<int>(std::ceil(1.41421356237309504880 * n + 1.0));
+  return d % 2 == 0 ? d + 1 : d;
+}
+
+ncsg_status ncsg_radon_create(int n, int n_angles, int n_det, int device, ncsg_radon** out) {
+  return guard([&] {
+    if (!out) throw Error{NCSG_INVALID, "null output handle"};
+    Geometry geo = build_geometry(n, n_angles, n_det, 0, 0);
+    require_device(device);
+    auto r = std::make_unique<ncsg_radon>();
+    r->dev.geo = std::move(geo);
+    r->dev.device = device;
+    r->dev.upload();
+    NCSG_CUDA_CHECK(cudaStreamCreateWithFlags(&r->stream.s, cudaStreamNonBlocking));
+    *out = r.release();
+  });
+}
+
+ncsg_status ncsg_radon_destroy(ncsg_radon* r) {
+  return guard([&] { delete r; });
+}
+
+size_t ncsg_radon_domain_size(const ncsg_radon* r) {
+  return static_cast<size_t>(r->dev.geo.n) * r->dev.geo.n;
+}
+size_t ncsg_radon_range_size(const ncsg_radon* r) {
+  return static_cast<size_t>(r->dev.geo.n_angles) * r->dev.geo.n_det;
+}
+int64_t ncsg_radon_sample_count(const ncsg_radon* r) { return r->dev.geo.samples; }
+
+ncsg_status ncsg_radon_forward(const ncsg_radon* r, const float* x, float* out, int batch,
+                               void* stream) {
+  return guard([&] {
+    if (!r || !x || !out || batch < 1) throw Error{NCSG_INVALID, "bad radon_forward arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : r->stream.s;
+    const Geometry& g = r->dev.geo;
+    size_t nn = static_cast<size_t>(g.n) * g.n, m = static_cast<size_t>(g.n_angles) * g.n_det;
+    DevBuf<float> xT, part;
+    if (!g.cls[1].empty()) {
+      xT.alloc(nn * batch);
+      launch_transpose(x, xT.p, g.n, batch, s);
+    }
+    part.alloc(m * r->dev.n_strips * batch);
+    part.zero(s);
+    launch_radon_forward_partial(r->dev, x, xT.p, part.p, batch, s);
+    launch_strip_sum(r->dev, part.p, out, batch, s);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+ncsg_status ncsg_radon_adjoint(const ncsg_radon* r, const float* u, float* out, int batch,
+                               void* stream) {
+  return guard([&] {
+    if (!r || !u || !out || batch < 1) throw Error{NCSG_INVALID, "bad radon_adjoint arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : r->stream.s;
+    RadonDev& dev = const_cast<RadonDev&>(r->dev);
+    dev.plan_adjoint(batch);
+    const Geometry& g = dev.geo;
+    size_t nn = static_cast<size_t>(g.n) * g.n;
+    DevBuf<float> part, spec_dummy;
+    part.alloc(nn * dev.n_partials() * batch);
+    launch_radon_adjoint_partial(dev, u, 0, part.p, batch, s);
+    // Sum partial images (class-H ones are transposed) via the combine path.
+    launch_sum_partials(part.p, dev.bp_chunks[0], dev.bp_chunks[1], out, g.n, batch, s);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+ncsg_status ncsg_radon_forward_host(const ncsg_radon* r, const double* x, double* out,
+                                    int batch) {
+  return guard([&] {
+    if (!r || !x || !out || batch < 1) throw Error{NCSG_INVALID, "bad radon_forward arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    size_t nn = ncsg_radon_domain_size(r) * batch, m = ncsg_radon_range_size(r) * batch;
+    std::vector<float> hx(x, x + nn), hy(m);
+    DevBuf<float> dx, dy;
+    dx.alloc(nn);
+    dy.alloc(m);
+    NCSG_CUDA_CHECK(cudaMemcpy(dx.p, hx.data(), nn * sizeof(float), cudaMemcpyHostToDevice));
+    ncsg_status st = ncsg_radon_forward(r, dx.p, dy.p, batch, nullptr);
+    if (st != NCSG_OK) throw Error{st, g_err};
+    NCSG_CUDA_CHECK(cudaMemcpy(hy.data(), dy.p, m * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < m; ++i) out[i] = hy[i];
+  });
+}
+
+ncsg_status ncsg_radon_adjoint_host(const ncsg_radon* r, const double* u, double* out,
+                                    int batch) {
+  return guard([&] {
+    if (!r || !u || !out || batch < 1) throw Error{NCSG_INVALID, "bad radon_adjoint arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    size_t nn = ncsg_radon_domain_size(r) * batch, m = ncsg_radon_range_size(r) * batch;
+    std::vector<float> hu(u, u + m), hx(nn);
+    DevBuf<float> du, dx;
+    du.alloc(m);
+    dx.alloc(nn);
+    NCSG_CUDA_CHECK(cudaMemcpy(du.p, hu.data(), m * sizeof(float), cudaMemcpyHostToDevice));
+    ncsg_status st = ncsg_radon_adjoint(r, du.p, dx.p, batch, nullptr);
+    if (st != NCSG_OK) throw Error{st, g_err};
+    NCSG_CUDA_CHECK(cudaMemcpy(hx.data(), dx.p, nn * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nn; ++i) out[i] = hx[i];
+  });
+}
+
+ncsg_status ncsg_grad_forward(int n, const float* x, float* out, int batch, void* stream) {
+  return guard([&] {
+    if (n < 2) throw Error{NCSG_INVALID, "grad needs N >= 2"};
+    launch_grad_forward(x, out, n, batch, static_cast<cudaStream_t>(stream));
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  });
+}
+
+ncsg_status ncsg_grad_adjoint(int n, const float* g, float* out, int batch, void* stream) {
+  return guard([&] {
+    if (n < 2) throw Error{NCSG_INVALID, "grad needs N >= 2"};
+    launch_grad_adjoint(g, out, n, batch, static_cast<cudaStream_t>(stream));
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+  });
+}
+
+ncsg_status ncsg_grad_forward_host(int n, const double* x, double* out, int batch) {
+  return guard([&] {
+    if (n < 2) throw Error{NCSG_INVALID, "grad needs N >= 2"};
+    require_device(0);
+    size_t nn = static_cast<size_t>(n) * n * batch, gg = 2 * static_cast<size_t>(n) * (n - 1) * batch;
+    std::vector<float> hx(x, x + nn), hg(gg);
+    DevBuf<float> dx, dg;
+    dx.alloc(nn);
+    dg.alloc(gg);
+    NCSG_CUDA_CHECK(cudaMemcpy(dx.p, hx.data(), nn * 4, cudaMemcpyHostToDevice));
+    launch_grad_forward(dx.p, dg.p, n, batch, nullptr);
+    NCSG_CUDA_CHECK(cudaMemcpy(hg.data(), dg.p, gg * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < gg; ++i) out[i] = hg[i];
+  });
+}
+
+ncsg_status ncsg_grad_adjoint_host(int n, const double* g, double* out, int batch) {
+  return guard([&] {
+    if (n < 2) throw Error{NCSG_INVALID, "grad needs N >= 2"};
+    require_device(0);
+    size_t nn = static_cast<size_t>(n) * n * batch, gg = 2 * static_cast<size_t>(n) * (n - 1) * batch;
+    std::vector<float> hg(g, g + gg), hx(nn);
+    DevBuf<float> dx, dg;
+    dx.alloc(nn);
+    dg.alloc(gg);
+    NCSG_CUDA_CHECK(cudaMemcpy(dg.p, hg.data(), gg * 4, cudaMemcpyHostToDevice));
+    launch_grad_adjoint(dg.p, dx.p, n, batch, nullptr);
+    NCSG_CUDA_CHECK(cudaMemcpy(hx.data(), dx.p, nn * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nn; ++i) out[i] = hx[i];
+  });
+}
+
+ncsg_status ncsg_mask_apply_host(int n, const double* mask, const double* x, double* out,
+                                 int batch, int device) {
+  return guard([&] {
+    if (!mask || !x || !out || batch < 1) throw Error{NCSG_INVALID, "bad mask_apply arguments"};
+    require_device(device);
+    Stream st;
+    NCSG_CUDA_CHECK(cudaStreamCreateWithFlags(&st.s, cudaStreamNonBlocking));
+    FftPlan f;
+    f.init(n, st.s);
+    auto h = read_mask(n, mask);
+    auto hm = half_mask(n, h, 1.0 / (static_cast<double>(n) * n));
+    DevBuf<float2> mT, spec;
+    mT.alloc(hm.size());
+    NCSG_CUDA_CHECK(cudaMemcpy(mT.p, hm.data(), hm.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    size_t nn = static_cast<size_t>(n) * n * batch;
+    std::vector<float> hx(x, x + nn);
+    DevBuf<float> dx, dy;
+    dx.alloc(nn);
+    dy.alloc(nn);
+    spec.alloc(static_cast<size_t>(n / 2 + 1) * n * batch);
+    NCSG_CUDA_CHECK(cudaMemcpy(dx.p, hx.data(), nn * 4, cudaMemcpyHostToDevice));
+    AtuTerms T;
+    T.n = n;
+    T.plain = dx.p;
+    launch_fft_rows_r2c(f, T, spec.p, batch, st.s);
+    launch_fft_cols_filter(f, spec.p, mT.p, batch, st.s);
+    XUpdate xu;
+    xu.x = dy.p;
+    xu.subtract = 0;
+    launch_fft_rows_c2r(f, spec.p, xu, batch, st.s);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(st.s));
+    NCSG_CUDA_CHECK(cudaMemcpy(hx.data(), dy.p, nn * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nn; ++i) out[i] = hx[i];
+  });
+}
+
+ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** out) {
+  return guard([&] {
+    if (!desc || !out) throw Error{NCSG_INVALID, "null problem descriptor"};
+    const ncsg_problem_desc& d = *desc;
+    if (d.kind != NCSG_CT && d.kind != NCSG_DENOISE) throw Error{NCSG_INVALID, "unknown problem kind"};
+    if (d.n < 2) throw Error{NCSG_INVALID, "image size must be >= 2"};
+    if (d.batch < 1) throw Error{NCSG_INVALID, "batch must be >= 1"};
+    // assemble_problem / Engine validation (pipeline.cpp:74-77, solvers.cpp:91-106)
+    if (!(d.alpha > 0.0) || !(d.beta > 0.0))
+      throw Error{NCSG_INVALID, "alpha and beta must be positive"};
+    if (d.lambda < 0.0) throw Error{NCSG_INVALID, "lambda must be nonnegative"};
+    if (!d.mask && !(d.gamma > 0.0))
+      throw Error{NCSG_INVALID, "gamma must be positive when no mask is set"};
+    if (!d.b) throw Error{NCSG_INVALID, "missing offset b"};
+    auto p = std::make_unique<ncsg_problem>();
+    p->d = d;
+    p->d.mask = nullptr;
+    p->d.b = nullptr;
+    p->device = d.device;
+    p->batch = d.batch;
+    p->nn = static_cast<size_t>(d.n) * d.n;
+    p->g = 2 * static_cast<size_t>(d.n) * (d.n - 1);
+    p->wd = static_cast<float>(d.beta / d.alpha);
+    p->bound = static_cast<float>(d.lambda * d.alpha / d.beta);
+    if (d.kind == NCSG_CT) {
+      Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end);
+      p->m0 = static_cast<size_t>(d.n_angles) * d.n_det;
+      int ab = d.angle_end > 0 ? d.angle_begin : 0;
+      int ae = d.angle_end > 0 ? d.angle_end : d.n_angles;
+      p->m_begin = static_cast<size_t>(ab) * d.n_det;
+      p->m_end = static_cast<size_t>(ae) * d.n_det;
+      p->rank0 = ab == 0;
+      require_device(d.device);
+      p->radon = std::make_unique<RadonDev>();
+      p->radon->geo = std::move(geo);
+      p->radon->device = d.device;
+      p->radon->upload();
+      p->radon->plan_adjoint(d.batch);
+    } else {
+      p->m0 = p->nn;
+      p->m_begin = 0;
+      p->m_end = p->nn;
+      require_device(d.device);
+    }
+    p->range = p->m0 + p->g + (d.positivity ? p->nn : 0);
+    NCSG_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream.s, cudaStreamNonBlocking));
+    cudaStream_t s = p->stream.s;
+    p->fft.init(d.n, s);
+    // Engine::Engine (solvers.cpp:93-99): m = gamma + alpha C, m_pinv = pinv(m).
+    std::vector<std::complex<double>> minv;
+    const double scale = 1.0 / (static_cast<double>(d.n) * d.n);
+    if (desc->mask) {
+      p->has_mask = true;
+      p->mask_full = read_mask(d.n, desc->mask);
+      std::vector<std::complex<double>> m(p->mask_full.size());
+      for (size_t i = 0; i < m.size(); ++i) m[i] = d.gamma + d.alpha * p->mask_full[i];
+      double tol = d.pinv_rel_tol > 0 ? d.pinv_rel_tol : 1e-12;
+      minv = pinv(m, tol);
+      auto ho = half_mask(d.n, p->mask_full, scale);
+      p->maskT_orig.alloc(ho.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(p->maskT_orig.p, ho.data(), ho.size() * sizeof(float2),
+                                 cudaMemcpyHostToDevice));
+    } else {
+      // pdhg: M = gamma I -> w = atu / gamma (solvers.cpp:133-137), applied
+      // through the same filter path with a constant spectrum.
+      minv.assign(p->nn, std::complex<double>(1.0 / d.gamma, 0.0));
+    }
+    auto hm = half_mask(d.n, minv, scale);
+    p->maskT.alloc(hm.size());
+    NCSG_CUDA_CHECK(cudaMemcpy(p->maskT.p, hm.data(), hm.size() * sizeof(float2),
+                               cudaMemcpyHostToDevice));
+    size_t xs = p->nn * p->batch;
+    p->x.alloc(xs);
+    p->x_old.alloc(xs);
+    p->xT.alloc(xs);
+    p->u.alloc(p->range * p->batch);
+    p->b.alloc(p->m0 * p->batch);
+    upload_f64(p.get(), desc->b, p->b.p, p->m0 * p->batch);
+    if (d.kind == NCSG_CT) {
+      p->axs.alloc(p->m0 * p->batch);
+      p->fp_part.alloc(p->m0 * p->radon->n_strips * p->batch);
+      p->fp_part.zero(s);
+      p->bp_part.alloc(p->nn * p->radon->n_partials() * p->batch);
+      p->axs.zero(s);
+    }
+    p->spec.alloc(static_cast<size_t>(d.n / 2 + 1) * d.n * p->batch);
+    p->flag.alloc(2);
+    p->red.alloc(static_cast<size_t>(p->batch) * objective_blocks() * 4);
+    p->x.zero(s);
+    p->x_old.zero(s);
+    p->xT.zero(s);
+    p->u.zero(s);
+    reset_flag(p.get());
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+    *out = p.release();
+  });
+}
+
+ncsg_status ncsg_problem_destroy(ncsg_problem* p) {
+  return guard([&] { delete p; });
+}
+
+size_t ncsg_problem_domain_size(const ncsg_problem* p) { return p->nn; }
+size_t ncsg_problem_range_size(const ncsg_problem* p) { return p->range; }
+void* ncsg_problem_stream(const ncsg_problem* p) { return p->stream.s; }
+float* ncsg_state_x(ncsg_problem* p) { return p->x.p; }
+float* ncsg_state_u(ncsg_problem* p) { return p->u.p; }
+float* ncsg_atu_buffer(ncsg_problem* p) { return p->bp_part.p; }
+
+ncsg_status ncsg_set_state(ncsg_problem* p, const double* x, const double* u, int64_t iter) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream.s;
+    if (x)
+      upload_f64(p, x, p->x.p, p->nn * p->batch);
+    else
+      p->x.zero(s);
+    if (u)
+      upload_f64(p, u, p->u.p, p->range * p->batch);
+    else
+      p->u.zero(s);
+    p->iter = iter;
+    engine_init(p);
+    reset_flag(p);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+ncsg_status ncsg_get_state(ncsg_problem* p, double* x, double* u, int64_t* iter) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    if (x) download_f64(p->stream.s, p->x.p, x, p->nn * p->batch);
+    if (u) download_f64(p->stream.s, p->u.p, u, p->range * p->batch);
+    if (iter) *iter = p->iter;
+  });
+}
+
+ncsg_status ncsg_step(ncsg_problem* p, int iters) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    for (int k = 0; k < iters; ++k) do_step(p);
+    p->iter += iters;
+  });
+}
+
+ncsg_status ncsg_step_graph(ncsg_problem* p, int iters) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    if (iters <= 0) return;
+    auto it = p->graphs.find(iters);
+    if (it == p->graphs.end()) {
+      cudaGraph_t graph;
+      NCSG_CUDA_CHECK(cudaStreamBeginCapture(p->stream.s, cudaStreamCaptureModeThreadLocal));
+      try {
+        for (int k = 0; k < iters; ++k) do_step(p);
+      } catch (...) {
+        cudaStreamEndCapture(p->stream.s, &graph);
+        throw;
+      }
+      NCSG_CUDA_CHECK(cudaStreamEndCapture(p->stream.s, &graph));
+      cudaGraphExec_t exec;
+      NCSG_CUDA_CHECK(cudaGraphInstantiate(&exec, graph, 0));
+      cudaGraphDestroy(graph);
+      it = p->graphs.emplace(iters, exec).first;
+    }
+    NCSG_CUDA_CHECK(cudaGraphLaunch(it->second, p->stream.s));
+    p->iter += iters;
+  });
+}
+
+ncsg_status ncsg_sync(ncsg_problem* p, int64_t* diverged_iter) {
+  ncsg_status st = guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    int h[2];
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(h, p->flag.p, sizeof(h), cudaMemcpyDeviceToHost, p->stream.s));
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+    if (h[0] != INT_MAX) {
+      if (diverged_iter) *diverged_iter = h[0];
+      throw Error{NCSG_DIVERGED, "diverged at iteration " + std::to_string(h[0]) +
+                                     ": image iterate left the finite range"};
+    }
+  });
+  return st;
+}
+
+ncsg_status ncsg_objective(ncsg_problem* p, double* out) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    auto f = objective_values(p);
+    std::copy(f.begin(), f.end(), out);
+  });
+}
+
+ncsg_status ncsg_last_seminorm(ncsg_problem* p, double* out) {
+  return guard([&] {
+    if (!p->x_prev.n) throw Error{NCSG_INVALID, "no recorded step to measure"};
+    auto v = seminorm_values(p);
+    std::copy(v.begin(), v.end(), out);
+  });
+}
+
+ncsg_status ncsg_step_phase_a(ncsg_problem* p) {
+  return guard([&] { phase_a(p); });
+}
+
+ncsg_status ncsg_step_phase_b(ncsg_problem* p) {
+  return guard([&] {
+    phase_b(p);
+    p->iter += 1;
+  });
+}
+
+ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
+                       int check_step_condition, const double* f_star, ncsg_record_row* rows,
+                       int max_rows, int* n_rows, double* screen_est) {
+  return guard([&] {
+    // solve_template (solvers.cpp:267-337)
+    if (max_iters < 0) throw Error{NCSG_INVALID, "max_iters must be nonnegative"};
+    if (record_every < 1) throw Error{NCSG_INVALID, "record_every must be >= 1"};
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    cudaStream_t s = p->stream.s;
+    p->iter = 0;
+    engine_init(p);
+    reset_flag(p);
+    if (check_step_condition && screen_est) *screen_est = NAN;  // see ncsg_screen (Python/C++)
+    const int B = p->batch;
+    std::vector<std::vector<ncsg_record_row>> rec(B);
+    auto t0 = std::chrono::steady_clock::now();
+    auto emit = [&](int64_t k, const std::vector<double>& sem) {
+      auto f = objective_values(p);
+      double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      for (int b = 0; b < B; ++b) rec[b].push_back({k, f[b], 0.0, sem[b], ms});
+    };
+    emit(0, std::vector<double>(B, 0.0));
+    ensure_scratch(p);
+    int k = 1;
+    while (k <= max_iters) {
+      // next recorded step: the smallest multiple of record_every >= k, or the last
+      int next = ((k + record_every - 1) / record_every) * record_every;
+      next = std::min(next, max_iters);
+      int plain = next - k;  // unrecorded steps before it
+      if (plain > 0) {
+        for (int j = 0; j < plain; ++j) do_step(p);
+        p->iter += plain;
+      }
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(p->x_prev.p, p->x.p, p->nn * B * 4, cudaMemcpyDeviceToDevice, s));
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(p->u_prev.p, p->u.p, p->range * B * 4, cudaMemcpyDeviceToDevice, s));
+      do_step(p);
+      p->iter += 1;
+      check_divergence(p, 0);
+      emit(next, seminorm_values(p));
+      k = next + 1;
+    }
+    // rel_subopt against f_star or the best objective seen (solvers.cpp:321-332)
+    int nr = static_cast<int>(rec[0].size());
+    for (int b = 0; b < B; ++b) {
+      double f_ref;
+      if (f_star) {
+        f_ref = f_star[b];
+      } else {
+        f_ref = INFINITY;
+        for (auto& r : rec[b]) f_ref = std::min(f_ref, r.objective);
+      }
+      for (auto& r : rec[b])
+        r.rel_subopt = std::isfinite(f_ref) ? (r.objective - f_ref) / std::max(1.0, std::abs(f_ref)) : 0.0;
+      for (int i = 0; i < std::min(nr, max_rows); ++i) rows[static_cast<size_t>(b) * max_rows + i] = rec[b][i];
+    }
+    if (n_rows) *n_rows = std::min(nr, max_rows);
+  });
+}
+
+}  // extern "C"

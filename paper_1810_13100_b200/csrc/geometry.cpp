@@ -1,0 +1,128 @@
+// Host-side geometry of the parallel-beam projector (fp64, setup only).
+//
+// Replays the reference's ray table and per-sample box check so the device
+// kernels visit exactly the reference's sample set, then derives the exact
+// fixed-point lattice increments the kernels step with.  Compiled with
+// -ffp-contract=off so the fp64 expressions round like the reference's
+// (x86-64, no FMA) build.
+#include <cmath>
+#include <cstdlib>
+#include <numbers>
+
+#include "ncsg_internal.cuh"
+
+namespace ncsg {
+
+namespace {
+
+struct Interval {
+  double lo, hi;
+};
+
+// axis_interval (radon.cpp:22-31): tau-interval where a + b*tau is in [lo, hi].
+Interval axis_interval(double a, double b, double lo, double hi) {
+  if (b == 0.0) {
+    if (a >= lo && a <= hi) return {-1e30, 1e30};
+    return {1.0, 0.0};
+  }
+  double t0 = (lo - a) / b;
+  double t1 = (hi - a) / b;
+  if (t0 > t1) std::swap(t0, t1);
+  return {t0, t1};
+}
+
+long long q32(double v) { return std::llround(std::ldexp(v, 32)); }
+
+}  // namespace
+
+Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end) {
+  // RadonMap::RadonMap validation (radon.cpp:37-42), same messages.
+  if (n < 2) throw Error{NCSG_INVALID, "image size must be >= 2"};
+  if (n_angles < 1) throw Error{NCSG_INVALID, "need at least one angle"};
+  if (n_det % 2 == 0) throw Error{NCSG_INVALID, "detector count must be odd"};
+  int min_det = static_cast<int>(std::ceil(std::numbers::sqrt2 * n));
+  if (min_det % 2 == 0) ++min_det;
+  if (n_det < min_det) throw Error{NCSG_INVALID, "detector row does not cover the image"};
+  if (angle_end <= 0) {
+    angle_begin = 0;
+    angle_end = n_angles;
+  }
+  if (angle_begin < 0 || angle_end > n_angles || angle_begin >= angle_end)
+    throw Error{NCSG_INVALID, "angle shard out of range"};
+
+  Geometry g;
+  g.n = n;
+  g.n_angles = n_angles;
+  g.n_det = n_det;
+  g.s_mid = (n_det - 1) / 2;
+  g.P0 = static_cast<long long>(n - 1) << 31;  // c = (n-1)/2 in Q32
+  g.rays.resize(static_cast<size_t>(n_angles) * n_det);
+
+  const double c = 0.5 * (n - 1);
+  const double s_mid = 0.5 * (n_det - 1);
+  const double edge = n - 1;
+  for (int t = 0; t < n_angles; ++t) {
+    double theta = std::numbers::pi * t / n_angles;
+    double ct = std::cos(theta);
+    double st = std::sin(theta);
+    bool own = t >= angle_begin && t < angle_end;
+    for (int d = 0; d < n_det; ++d) {
+      RayRange rr{1, 0};
+      double s = d - s_mid;
+      Interval ix = axis_interval(s * ct + c, -st, 0.0, n - 1);
+      Interval iy = axis_interval(c - s * st, -ct, 0.0, n - 1);
+      double lo = std::max(ix.lo, iy.lo);
+      double hi = std::min(ix.hi, iy.hi);
+      if (lo <= hi) {
+        double k0 = std::ceil(lo);
+        double k1 = std::floor(hi);
+        if (k0 <= k1) {
+          double px0 = s * ct - k0 * st + c;
+          double py0 = c - s * st - k0 * ct;
+          double dpx = -st, dpy = -ct;
+          int count = static_cast<int>(k1 - k0) + 1;
+          // per-sample box check (radon.cpp:88-90); valid samples of a ray
+          // form one interval because px, py are monotone in k.
+          auto valid = [&](int k) {
+            double px = px0 + k * dpx;
+            double py = py0 + k * dpy;
+            return !(px < 0.0 || px > edge || py < 0.0 || py > edge);
+          };
+          int kf = 0;
+          while (kf < count && !valid(kf)) ++kf;
+          if (kf < count) {
+            int kl = count - 1;
+            while (kl > kf && !valid(kl)) --kl;
+            int base = static_cast<int>(k0);
+            rr.first = base + kf;
+            rr.last = base + kl;
+            if (own) g.samples += kl - kf + 1;
+          }
+        }
+      }
+      g.rays[static_cast<size_t>(t) * n_det + d] = rr;
+    }
+    if (!own) continue;
+
+    AngleGeom a{};
+    long long ax = q32(ct), ay = q32(-st), bx = q32(-st), by = q32(-ct);
+    int cls = std::llabs(by) >= std::llabs(bx) ? 0 : 1;
+    long long aX = cls == 0 ? ax : ay, aY = cls == 0 ? ay : ax;
+    long long bX = cls == 0 ? bx : by, bY = cls == 0 ? by : bx;
+    a.t = t;
+    a.dir = bY > 0 ? 1 : -1;
+    a.aX = aX;
+    a.aY = aY;
+    a.dX = a.dir * bX;
+    a.dY = a.dir * bY;
+    a.aXf = static_cast<float>(std::ldexp(static_cast<double>(aX), -32));
+    a.aYf = static_cast<float>(std::ldexp(static_cast<double>(aY), -32));
+    a.inv_dY16 = static_cast<float>(65536.0 / static_cast<double>(a.dY));
+    a.inv_adX16 =
+        a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
+    g.cls[cls].push_back(a);
+  }
+  return g;
+}
+
+}  // namespace ncsg

@@ -1,0 +1,393 @@
+// Streaming kernels of the NCS step: the fused dual update (extrapolation +
+// conjugate proxes + ax cache + finiteness flag), the objective reduction,
+// stand-alone D / D^T, and small vector helpers.  All HBM-bound; each element
+// of u, ax and b crosses HBM once per step.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "ncs_kernels.cuh"
+
+namespace ncsg {
+
+namespace {
+
+int grid_for(size_t total, int block, int cap = 148 * 8) {
+  size_t g = (total + block - 1) / block;
+  return static_cast<int>(std::max<size_t>(1, std::min<size_t>(g, cap)));
+}
+
+// w * (D x)_e with D the forward difference of grad.cpp:53-64.
+__device__ __forceinline__ float grad_at(const float* x, int n, size_t e) {
+  const size_t half = static_cast<size_t>(n) * (n - 1);
+  if (e < half) {
+    const size_t i = e / (n - 1), j = e - i * (n - 1);
+    const float* p = x + i * n + j;
+    return p[0] - p[1];
+  }
+  const size_t e2 = e - half;
+  const size_t i = e2 / n, j = e2 - i * n;
+  const float* p = x + i * n + j;
+  return p[0] - p[n];
+}
+
+// Engine::step dual half (solvers.cpp:148-156) for every block:
+//   r = u + alpha (2 ax_new - ax_old - b);  u = prox_{alpha g*}(r)
+// with QuadraticConj (prox.cpp:21-24), ScaledL1Conj (prox.cpp:36-38, bound
+// lambda*alpha/beta) and NonnegConj (prox.cpp:103-105); CT data rays also
+// sum the projector's strip partials into ax_new and store it as the new ax.
+__global__ void dual_update_kernel(DualArgs a) {
+  const int b = blockIdx.z;
+  const int section = blockIdx.y;
+  const float alpha = a.alpha;
+  const size_t nn = static_cast<size_t>(a.n) * a.n;
+  const float* x = a.x + b * nn;
+  const float* xo = a.x_old + b * nn;
+  bool bad = false;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  if (section == 0) {
+    if (a.kind == NCSG_CT) {
+      const float* part = a.fp_part + b * a.n_strips * a.m;
+      float* us = a.u0 + b * a.u_stride;
+      float* ax = a.axs + b * a.m;
+      const float* bb = a.b + b * a.m;
+      for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+        float rx = 0.f;
+        for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
+        const float r = us[i] + alpha * (2.f * rx - ax[i] - bb[i]);
+        const float un = r * a.s_quad;
+        us[i] = un;
+        ax[i] = rx;
+        bad |= isnan(un);
+      }
+    } else {
+      float* ud = a.u0 + b * a.u_stride;
+      const float* bb = a.b + b * nn;
+      for (size_t i = i0; i < nn; i += stride) {
+        const float r = ud[i] + alpha * (2.f * x[i] - xo[i] - bb[i]);
+        const float un = r * a.s_quad;
+        ud[i] = un;
+        bad |= isnan(un);
+      }
+    }
+  } else if (section == 1) {
+    float* ug = a.ug + b * a.u_stride;
+    const size_t g = 2 * static_cast<size_t>(a.n) * (a.n - 1);
+    const float wd = a.wd, bd = a.bound;
+    for (size_t e = i0; e < g; e += stride) {
+      const float an = wd * grad_at(x, a.n, e);
+      const float ao = wd * grad_at(xo, a.n, e);
+      const float z = ug[e] + alpha * (2.f * an - ao - 0.f);
+      const float un = z < -bd ? -bd : (z > bd ? bd : z);
+      ug[e] = un;
+      bad |= isnan(z);
+    }
+  } else {
+    float* up = a.up + b * a.u_stride;
+    for (size_t i = i0; i < nn; i += stride) {
+      const float z = up[i] + alpha * (2.f * x[i] - xo[i]);
+      up[i] = z < 0.f ? z : 0.f;
+      bad |= isnan(z);
+    }
+  }
+  if (a.flag && __syncthreads_or(bad) && threadIdx.x == 0)
+    atomicMin(a.flag, *(volatile int*)(a.flag + 1));
+}
+
+__device__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < (blockDim.x >> 5); ++k) s += sh[k];
+  return s;
+}
+
+__device__ double block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_down_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) sh[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < (blockDim.x >> 5); ++k) s = fmax(s, sh[k]);
+  return s;
+}
+
+// Per-block fp64 partial sums of objective_from_ax (solvers.cpp:362-381):
+// [0] sum (ax_data - b)^2, [1] sum |w D x|, [2] max |x| (positivity),
+// [3] min x (positivity).
+__global__ void objective_kernel(ObjArgs a) {
+  __shared__ double sh[32];
+  const int b = blockIdx.y;
+  const size_t nn = static_cast<size_t>(a.n) * a.n;
+  const float* x = a.x + b * nn;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  double q = 0.0, l1 = 0.0, mx = 0.0, mn = 0.0;
+  if (a.kind == NCSG_CT) {
+    const float* ax = a.axs + b * a.m;
+    const float* bb = a.b + b * a.m;
+    for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+      const double z = static_cast<double>(ax[i]) - static_cast<double>(bb[i]);
+      q += z * z;
+    }
+  } else {
+    const float* bb = a.b + b * nn;
+    for (size_t i = i0; i < nn; i += stride) {
+      const double z = static_cast<double>(x[i]) - static_cast<double>(bb[i]);
+      q += z * z;
+    }
+  }
+  if (a.with_grad) {
+    const size_t g = 2 * static_cast<size_t>(a.n) * (a.n - 1);
+    for (size_t e = i0; e < g; e += stride)
+      l1 += fabs(static_cast<double>(a.wd * grad_at(x, a.n, e)));
+  }
+  if (a.positivity) {
+    for (size_t i = i0; i < nn; i += stride) {
+      mx = fmax(mx, fabs(static_cast<double>(x[i])));
+      mn = fmin(mn, static_cast<double>(x[i]));
+    }
+  }
+  double* out = a.out + (static_cast<size_t>(b) * gridDim.x + blockIdx.x) * 4;
+  const double s0 = block_sum(q, sh);
+  if (threadIdx.x == 0) out[0] = s0;
+  const double s1 = block_sum(l1, sh);
+  if (threadIdx.x == 0) out[1] = s1;
+  const double s2 = block_max(mx, sh);
+  if (threadIdx.x == 0) out[2] = s2;
+  const double s3 = -block_max(-mn, sh);
+  if (threadIdx.x == 0) out[3] = s3;
+}
+
+__global__ void grad_forward_kernel(const float* x, float* out, int n, int batch) {
+  const size_t g = 2 * static_cast<size_t>(n) * (n - 1);
+  const size_t nn = static_cast<size_t>(n) * n;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < g * batch;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t b = i / g, e = i - b * g;
+    out[i] = grad_at(x + b * nn, n, e);
+  }
+}
+
+__global__ void grad_adjoint_kernel(const float* gbuf, float* out, int n, int batch) {
+  const size_t g = 2 * static_cast<size_t>(n) * (n - 1);
+  const size_t nn = static_cast<size_t>(n) * n;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nn * batch;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t b = i / nn, p = i - b * nn;
+    const int y = static_cast<int>(p / n), x = static_cast<int>(p - static_cast<size_t>(y) * n);
+    const float* hb = gbuf + b * g;
+    const float* vb = hb + static_cast<size_t>(n) * (n - 1);
+    float d = 0.f;
+    if (x < n - 1) d += hb[static_cast<size_t>(y) * (n - 1) + x];
+    if (x > 0) d -= hb[static_cast<size_t>(y) * (n - 1) + x - 1];
+    if (y < n - 1) d += vb[static_cast<size_t>(y) * n + x];
+    if (y > 0) d -= vb[static_cast<size_t>(y - 1) * n + x];
+    out[i] = d;
+  }
+}
+
+__global__ void transpose_kernel(const float* in, float* out, int n, int batch) {
+  __shared__ float t[32][33];
+  const size_t nn = static_cast<size_t>(n) * n;
+  const int b = blockIdx.z;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = by + k, x = bx + threadIdx.x;
+    if (y < n && x < n) t[k][threadIdx.x] = in[b * nn + static_cast<size_t>(y) * n + x];
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = bx + k, x = by + threadIdx.x;
+    if (y < n && x < n) out[b * nn + static_cast<size_t>(y) * n + x] = t[threadIdx.x][k];
+  }
+}
+
+__global__ void f64_to_f32_kernel(const double* in, float* out, size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<float>(in[i]);
+}
+
+__global__ void f32_to_f64_kernel(const float* in, double* out, size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = static_cast<double>(in[i]);
+}
+
+// out = a - b (fp32), used for the seminorm step differences.
+__global__ void sub_kernel(const float* a, const float* b, float* out, size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i] - b[i];
+}
+
+// Seminorm partial sums (solvers.cpp:166-177), per block:
+//   [0] sum (du - alpha adx)^2   [1] sum adx^2   [2] sum dx * mdx
+__global__ void seminorm_kernel(SemArgs a) {
+  __shared__ double sh[32];
+  const int b = blockIdx.y;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  const size_t i0 = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x;
+  const float* du = a.du + b * a.range;
+  const float* adx = a.adx + b * a.range;
+  double t1 = 0.0, aq = 0.0, mq = 0.0;
+  for (size_t i = i0; i < a.range; i += stride) {
+    if (i >= a.r_begin && i < a.r_end) {
+      const double d = static_cast<double>(du[i]) - a.alpha * static_cast<double>(adx[i]);
+      t1 += d * d;
+      aq += static_cast<double>(adx[i]) * adx[i];
+    }
+  }
+  const size_t nn = static_cast<size_t>(a.n) * a.n;
+  {
+    const float* dx = a.dx + b * nn;
+    const float* w = a.mdx ? a.mdx + b * nn : nullptr;  // F^-1 (h F dx) (Engine::apply_m)
+    for (size_t i = i0; i < nn; i += stride) {
+      const double d = dx[i];
+      mq += d * (a.gamma * d + (w ? a.alpha * static_cast<double>(w[i]) : 0.0));
+    }
+  }
+  double* out = a.out + (static_cast<size_t>(b) * gridDim.x + blockIdx.x) * 3;
+  const double s0 = block_sum(t1, sh);
+  if (threadIdx.x == 0) out[0] = s0;
+  const double s1 = block_sum(aq, sh);
+  if (threadIdx.x == 0) out[1] = s1;
+  const double s2 = block_sum(mq, sh);
+  if (threadIdx.x == 0) out[2] = s2;
+}
+
+// Stacked forward of dx for the seminorm: data block (strip sum or identity),
+// D block (weighted) and positivity identity, into adx[batch][range].
+__global__ void stacked_rest_kernel(StackArgs a) {
+  const int b = blockIdx.y;
+  const size_t nn = static_cast<size_t>(a.n) * a.n;
+  const size_t g = 2 * static_cast<size_t>(a.n) * (a.n - 1);
+  const float* x = a.x + b * nn;
+  float* out = a.out + b * a.range;
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < a.range;
+       i += stride) {
+    float v;
+    if (i < a.m0) {
+      if (a.kind == NCSG_CT) {
+        const float* part = a.fp_part + b * a.n_strips * a.m0 + i;
+        v = 0.f;
+        for (int k = 0; k < a.n_strips; ++k) v += part[k * a.m0];
+      } else {
+        v = x[i];
+      }
+    } else if (i < a.m0 + g) {
+      v = a.wd * grad_at(x, a.n, i - a.m0);
+    } else {
+      v = x[i - a.m0 - g];
+    }
+    out[i] = v;
+  }
+}
+
+}  // namespace
+
+void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
+  size_t big = std::max<size_t>(a.m_end - a.m_begin, 2 * static_cast<size_t>(a.n) * a.n);
+  dim3 grid(grid_for(big, 256, 148 * 4), a.positivity ? 3 : 2, batch);
+  dual_update_kernel<<<grid, 256, 0, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+int objective_blocks() { return 148; }
+
+void launch_objective(const ObjArgs& a, int batch, cudaStream_t s) {
+  dim3 grid(objective_blocks(), batch);
+  objective_kernel<<<grid, 256, 0, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_grad_forward(const float* x, float* out, int n, int batch, cudaStream_t s) {
+  size_t total = 2 * static_cast<size_t>(n) * (n - 1) * batch;
+  grad_forward_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, out, n, batch);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_grad_adjoint(const float* g, float* out, int n, int batch, cudaStream_t s) {
+  size_t total = static_cast<size_t>(n) * n * batch;
+  grad_adjoint_kernel<<<grid_for(total, 256), 256, 0, s>>>(g, out, n, batch);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_transpose(const float* in, float* out, int n, int batch, cudaStream_t s) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
+  transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, n, batch);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_f64_to_f32(const double* in, float* out, size_t count, cudaStream_t s) {
+  f64_to_f32_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, out, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_f32_to_f64(const float* in, double* out, size_t count, cudaStream_t s) {
+  f32_to_f64_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, out, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_sub(const float* a, const float* b, float* out, size_t count, cudaStream_t s) {
+  sub_kernel<<<grid_for(count, 256), 256, 0, s>>>(a, b, out, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_seminorm(const SemArgs& a, int batch, cudaStream_t s) {
+  dim3 grid(objective_blocks(), batch);
+  seminorm_kernel<<<grid, 256, 0, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_stacked_rest(const StackArgs& a, int batch, cudaStream_t s) {
+  dim3 grid(grid_for(a.range, 256), batch);
+  stacked_rest_kernel<<<grid, 256, 0, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+}  // namespace ncsg
+
+namespace ncsg {
+namespace {
+__global__ void sum_partials_kernel(const float* part, int nV, int nH, float* out, int n) {
+  __shared__ float t[32][33];
+  const size_t nn = static_cast<size_t>(n) * n;
+  const int b = blockIdx.z;
+  const float* pb = part + static_cast<size_t>(b) * (nV + nH) * nn;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  // class-H partials are stored transposed: stage them through shared memory
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = bx + k, x = by + threadIdx.x;  // transposed coordinates
+    float v = 0.f;
+    if (y < n && x < n)
+      for (int c = 0; c < nH; ++c) v += pb[(nV + c) * nn + static_cast<size_t>(y) * n + x];
+    t[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = by + k, x = bx + threadIdx.x;
+    if (y >= n || x >= n) continue;
+    float v = 0.f;
+    for (int c = 0; c < nV; ++c) v += pb[c * nn + static_cast<size_t>(y) * n + x];
+    out[b * nn + static_cast<size_t>(y) * n + x] = v + t[threadIdx.x][k];
+  }
+}
+}  // namespace
+
+void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, int batch,
+                         cudaStream_t s) {
+  dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
+  sum_partials_kernel<<<grid, dim3(32, 8), 0, s>>>(part, nV, nH, out, n);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+}  // namespace ncsg

@@ -1,0 +1,68 @@
+// Launch interfaces of the streaming NCS kernels (ncs_kernels.cu).
+#pragma once
+
+#include "ncsg_internal.cuh"
+
+namespace ncsg {
+
+struct DualArgs {
+  int kind = 0, n = 0, positivity = 0;
+  float alpha = 0.f, s_quad = 0.f, wd = 0.f, bound = 0.f;
+  // data block (CT: sinogram rays [m_begin, m_end) of [batch][m]; DENOISE: nn pixels)
+  const float* fp_part = nullptr;
+  int n_strips = 0;
+  size_t m = 0, m_begin = 0, m_end = 0;
+  float* u0 = nullptr;   // data-block dual, batch stride u_stride
+  float* axs = nullptr;  // cached R x [batch][m] (CT)
+  const float* b = nullptr;
+  float* ug = nullptr;   // gradient dual, batch stride u_stride
+  float* up = nullptr;   // positivity dual, batch stride u_stride
+  size_t u_stride = 0;
+  const float* x = nullptr;
+  const float* x_old = nullptr;
+  int* flag = nullptr;
+};
+void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
+
+struct ObjArgs {
+  int kind = 0, n = 0, positivity = 0, with_grad = 1;
+  float wd = 0.f;
+  const float* axs = nullptr;  // CT cached R x
+  const float* b = nullptr;
+  const float* x = nullptr;
+  size_t m = 0, m_begin = 0, m_end = 0;
+  double* out = nullptr;  // [batch][objective_blocks()][4]
+};
+int objective_blocks();
+void launch_objective(const ObjArgs& a, int batch, cudaStream_t s);
+
+struct SemArgs {
+  int n = 0;
+  double alpha = 0.0, gamma = 0.0;
+  const float* du = nullptr;
+  const float* adx = nullptr;
+  size_t range = 0, r_begin = 0, r_end = 0;
+  const float* dx = nullptr;
+  const float* mdx = nullptr;  // nullable (PDHG: M = gamma I handled by caller)
+  double* out = nullptr;       // [batch][objective_blocks()][3]
+};
+void launch_seminorm(const SemArgs& a, int batch, cudaStream_t s);
+
+struct StackArgs {
+  int kind = 0, n = 0, n_strips = 0;
+  float wd = 0.f;
+  const float* fp_part = nullptr;
+  const float* x = nullptr;
+  float* out = nullptr;
+  size_t m0 = 0, range = 0;
+};
+void launch_stacked_rest(const StackArgs& a, int batch, cudaStream_t s);
+
+void launch_grad_forward(const float* x, float* out, int n, int batch, cudaStream_t s);
+void launch_grad_adjoint(const float* g, float* out, int n, int batch, cudaStream_t s);
+void launch_transpose(const float* in, float* out, int n, int batch, cudaStream_t s);
+void launch_f64_to_f32(const double* in, float* out, size_t count, cudaStream_t s);
+void launch_f32_to_f64(const float* in, double* out, size_t count, cudaStream_t s);
+void launch_sub(const float* a, const float* b, float* out, size_t count, cudaStream_t s);
+
+}  // namespace ncsg

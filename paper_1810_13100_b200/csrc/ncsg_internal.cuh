@@ -1,0 +1,176 @@
+// Internal declarations of the B200 NCS hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ncsg.h"
+
+namespace ncsg {
+
+// ----------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  ncsg_status code;
+  std::string msg;
+};
+
+#define NCSG_CUDA_CHECK(expr)                                                        \
+  do {                                                                               \
+    cudaError_t _e = (expr);                                                         \
+    if (_e != cudaSuccess)                                                           \
+      throw ::ncsg::Error{NCSG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
+  } while (0)
+
+// ------------------------------------------------------------- geometry
+// Fixed-point sample positions: value * 2^-32 pixels, int64.  The lattice
+// point (s, tau) of angle t sits at
+//   px = P0 + s*ax + tau*bx,   py = P0 + s*ay + tau*by   (P0 = c * 2^32)
+// with ax = round(cos*2^32), ay = bx = round(-sin*2^32), by = round(-cos*2^32):
+// the exact-math positions of radon.cpp:52-66 to 4e-7 px, computed in exact
+// integer arithmetic so every kernel agrees on every sample's cell.
+//
+// Kernel frame: class V angles (|cos| >= |sin|) use (X, Y) = (px, py) on the
+// image; class H angles use (X, Y) = (py, px) on the transposed image, so that
+// in both classes one sample step advances Y by dY >= 0.707 px and |dX| <= dY.
+struct AngleGeom {
+  long long aX, aY;  // per unit s (kernel frame)
+  long long dX, dY;  // per step (tau advanced by `dir`), dY > 0
+  int t;             // angle index into the sinogram
+  int dir;           // tau = dir * k
+  float aXf, aYf;    // aX, aY as floats in pixel units (range estimates)
+  float inv_dY16;    // 65536 / dY  (step estimates on (diff >> 16))
+  float inv_adX16;   // 65536 / |dX| (0 when dX == 0)
+};
+
+struct RayRange {  // valid tau interval [first, last] of one ray (empty: first > last)
+  int first, last;
+};
+
+struct Geometry {
+  int n = 0, n_angles = 0, n_det = 0;
+  int s_mid = 0;
+  long long P0 = 0;
+  std::vector<AngleGeom> cls[2];   // class 0 = V, class 1 = H
+  std::vector<RayRange> rays;      // [t][d]
+  int64_t samples = 0;
+};
+
+// Replays the reference's fp64 ray table and per-sample box check
+// (radon.cpp:35-72, 85-90) and builds the fixed-point angle table.
+// Throws Error{NCSG_INVALID} with the reference's messages.
+Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end);
+
+// ------------------------------------------------------- device buffers
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void alloc(size_t count) {
+    release();
+    if (count) NCSG_CUDA_CHECK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void zero(cudaStream_t s) {
+    if (n) NCSG_CUDA_CHECK(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+};
+
+// --------------------------------------------------------- Radon plan
+// Tiling constants of the projector kernels.
+constexpr int kFpW = 128;    // forward strip width (pixels)
+constexpr int kFpT = 32;     // forward tile-row height
+constexpr int kFpWarps = 8;  // forward: warps per CTA = angles per CTA
+constexpr int kBpW = 128;    // adjoint tile width
+constexpr int kBpT = 32;     // adjoint tile height
+constexpr int kBpWarps = 4;  // adjoint: warps per CTA (private accumulators)
+
+struct RadonDev {
+  Geometry geo;
+  int device = 0;
+  DevBuf<AngleGeom> angles[2];
+  DevBuf<RayRange> rays;
+  int n_strips = 0;
+  int fp_rmax[2] = {0, 0};  // max rays per (strip, angle) per class
+  int bp_chunks[2] = {0, 0};
+  int bp_chunk_len[2] = {0, 0};
+  int bp_batch_planned = 0;
+  DevBuf<int2> strip_range[2];                // [angle][strip] s-range (forward)
+  std::vector<int2> strip_range_host[2];
+  void upload();
+  void plan_adjoint(int batch);
+  int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }
+};
+
+// Projector launches.  img / imgT: batch images (stride n*n), imgT may be
+// null when class H is empty.  fp_partial: [batch][n_strips][m] (zeros where
+// a strip has no rays; written entries overwritten each call).
+void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
+                                  float* fp_partial, int batch, cudaStream_t s);
+// Sums partial strips into out[batch][m] (stand-alone forward).
+void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, int batch,
+                      cudaStream_t s);
+// Adjoint partial images: bp_part[batch][n_partials][n*n]; class-H partials
+// are stored transposed.
+void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_stride,
+                                  float* bp_part, int batch, cudaStream_t s);
+// out[b] = sum of the class-V partials + transposed class-H partials.
+void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, int batch,
+                         cudaStream_t s);
+
+// ------------------------------------------------------------------ FFT
+struct FftPlan {
+  int n = 0;
+  DevBuf<float2> tw;  // exp(-2 pi i k / n), k < n/2
+  void init(int n_, cudaStream_t s);
+};
+// Spectrum layout: specT[batch][n/2+1][n] complex (column-major half spectrum).
+// Real-to-half-spectrum row pass; `terms` (combine) describes how the real
+// input image is assembled (see ncs_kernels.cu).
+struct AtuTerms;
+void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT, int batch,
+                         cudaStream_t s);
+// Column pass: forward FFT along j, multiply by maskT[k][j], inverse FFT.
+void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
+                            cudaStream_t s);
+// Inverse rows (C2R) fused with the x update: out = x_in - w (or w when
+// x_in == nullptr); optional x_old copy, transposed copy, finiteness flag.
+struct XUpdate {
+  float* x = nullptr;       // updated in place (x -= w) ; if subtract == 0: x = w
+  float* x_old = nullptr;   // receives the pre-update x (nullable)
+  float* xT = nullptr;      // receives the transposed result (nullable)
+  int subtract = 1;
+  int* flag = nullptr;      // [0] = min(step counter [1]) over non-finite results (nullable)
+};
+void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
+                         cudaStream_t s);
+
+// ------------------------------------------------------------ NCS kernels
+// Terms summed into the image fed to the FFT: A^T u for the stacked problem.
+struct AtuTerms {
+  int n = 0;
+  const float* bp_part = nullptr;  // [batch][nV+nH][n*n] (nullable)
+  int nV = 0, nH = 0;
+  const float* ident = nullptr;    // identity-block dual (DENOISE data / positivity), nullable
+  const float* ident2 = nullptr;   // second identity term (positivity with DENOISE), nullable
+  const float* ug = nullptr;       // gradient dual [batch][2n(n-1)], nullable
+  float wd = 0.f;                  // D-block weight beta/alpha
+  const float* plain = nullptr;    // plain image input (mask apply), overrides the rest
+  size_t part_stride = 0;          // per-batch stride of bp_part
+  size_t ident_stride = 0, ug_stride = 0;
+  int* counter = nullptr;          // flag buffer: counter[1] += 1 once per step (nullable)
+};
+
+}  // namespace ncsg

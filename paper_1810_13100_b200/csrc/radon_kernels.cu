@@ -1,0 +1,458 @@
+// Parallel-beam projector R and its exact transpose R^T on sm_100a.
+//
+// Both kernels walk the reference's sample lattice (radon.cpp:43-71, 82-127)
+// in exact Q32 fixed point (see AngleGeom in ncsg_internal.cuh), so every
+// kernel assigns each sample to the same cell and the per-ray valid interval
+// replayed on the host reproduces the reference's box check.  Lanes of a warp
+// own rays; all lanes of a warp start a tile at the same row phase ("y-aligned
+// stepping"), so at any step the active lanes sit within one pixel row of each
+// other.  That keeps the forward gathers' shared-memory bank spread wide and
+// makes the adjoint's scatter provably conflict-free between lanes whose rays
+// are >= 3 apart ("R^T without atomics").
+//
+// R  (fp_strip_kernel):  CTA = (image strip of kFpW columns, kFpWarps angles).
+//     The strip is swept top to bottom in kFpT-row tiles staged in shared
+//     memory; every warp integrates its angle's rays over the tile (bilinear,
+//     radon.cpp:91-98) and accumulates per-ray sums in shared memory; the
+//     strip's partial ray sums go to part[strip][ray] and are summed in strip
+//     order by the consumer (deterministic, no atomics).
+// R^T (bp_tile_kernel):  CTA = (kBpW x kBpT output tile, chunk of angles).
+//     Each warp owns a private shared-memory accumulator of the tile plus a
+//     one-pixel halo and scatters w * bilinear weights (radon.cpp:116-125)
+//     with plain read-modify-write; lanes take rays 5 apart in 5 phases, so
+//     two lanes of one instruction never touch the same pixel.  Warps are
+//     reduced once per CTA into a partial image per angle chunk.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+
+#include "ncsg_internal.cuh"
+
+namespace ncsg {
+
+namespace {
+
+constexpr int kBpStride = 5;  // ray stride between lanes of one adjoint phase
+
+__device__ __forceinline__ float frac_q32(long long v) {
+  // low 32 bits are the fraction in units of 2^-32; keep the top 23 bits.
+  unsigned lo = static_cast<unsigned>(v);
+  return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f;
+}
+
+// Smallest q with base + q*step >= target (step > 0), exact; inv16 = 65536/step.
+__device__ __forceinline__ int first_ge(long long base, long long step, long long target,
+                                        float inv16) {
+  long long diff = target - base;
+  int q = static_cast<int>(ceilf(static_cast<float>(static_cast<int>(diff >> 16)) * inv16));
+  while (base + static_cast<long long>(q) * step < target) ++q;
+  while (base + static_cast<long long>(q - 1) * step >= target) --q;
+  return q;
+}
+
+struct LaneRun {
+  long long X, Y;  // position at local step 0
+  int jlo, jhi;    // active local steps [jlo, jhi)
+};
+
+// Samples of ray s with Y in [Ylo, Yhi), X in [Xlo, Xhi) and tau inside the
+// ray's valid interval.  Local step 0 is the first lattice step with Y >= Ylo
+// (the y-aligned start shared by every lane of the warp).
+__device__ __forceinline__ LaneRun setup_run(const AngleGeom& g, long long P0, int s, RayRange rr,
+                                             long long Xlo, long long Xhi, long long Ylo,
+                                             long long Yhi) {
+  long long baseX = P0 + static_cast<long long>(s) * g.aX;
+  long long baseY = P0 + static_cast<long long>(s) * g.aY;
+  int k0 = first_ge(baseY, g.dY, Ylo, g.inv_dY16);
+  LaneRun r;
+  r.X = baseX + static_cast<long long>(k0) * g.dX;
+  r.Y = baseY + static_cast<long long>(k0) * g.dY;
+  int jlo = 0;
+  int jhi = first_ge(r.Y, g.dY, Yhi, g.inv_dY16);
+  if (g.dX > 0) {
+    jlo = max(jlo, first_ge(r.X, g.dX, Xlo, g.inv_adX16));
+    jhi = min(jhi, first_ge(r.X, g.dX, Xhi, g.inv_adX16));
+  } else if (g.dX < 0) {
+    long long adx = -g.dX;
+    jlo = max(jlo, first_ge(0, adx, r.X - Xhi + 1, g.inv_adX16));
+    jhi = min(jhi, first_ge(0, adx, r.X - Xlo + 1, g.inv_adX16));
+  } else if (r.X < Xlo || r.X >= Xhi) {
+    jhi = jlo;
+  }
+  if (g.dir > 0) {
+    jlo = max(jlo, rr.first - k0);
+    jhi = min(jhi, rr.last - k0 + 1);
+  } else {
+    jlo = max(jlo, -rr.last - k0);
+    jhi = min(jhi, -rr.first - k0 + 1);
+  }
+  r.jlo = jlo;
+  r.jhi = jhi;
+  return r;
+}
+
+// Conservative integer s-range of rays that can touch the real-coordinate box
+// [x0, x1] x [y0, y1] (kernel frame), clamped to the detector.
+__device__ __forceinline__ void ray_range(const AngleGeom& g, float c, float x0, float x1,
+                                          float y0, float y1, int s_mid, int& lo, int& hi) {
+  float a = (x0 - c) * g.aXf, b = (x1 - c) * g.aXf;
+  float e = (y0 - c) * g.aYf, f = (y1 - c) * g.aYf;
+  float mn = fminf(a, b) + fminf(e, f);
+  float mx = fmaxf(a, b) + fmaxf(e, f);
+  lo = max(-s_mid, static_cast<int>(floorf(mn)) - 1);
+  hi = min(s_mid, static_cast<int>(ceilf(mx)) + 1);
+}
+
+struct FpArgs {
+  const AngleGeom* ang;
+  int n_ang;
+  const RayRange* rays;
+  const int2* strip_range;  // [n_ang][n_strips] s-range per (angle, strip)
+  const float* img;
+  float* part;
+  int n, det, s_mid, n_strips, rmax;
+  long long P0;
+  size_t nn, m;
+};
+
+template <int W, int T, int NW>
+__global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
+  extern __shared__ float sm[];
+  constexpr int P = W + 2;
+  float* tile = sm;
+  float* racc = sm + (T + 2) * P;
+  const int strip = blockIdx.x;
+  const int X0 = strip * W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int ai = blockIdx.y * NW + warp;
+  const bool has_angle = ai < a.n_ang;
+  const int b = blockIdx.z;
+  const int n = a.n;
+  const float* img = a.img + static_cast<size_t>(b) * a.nn;
+  const float c = 0.5f * (n - 1);
+  const int n_rows = (n + T - 1) / T;
+  const long long Xlo = strip == 0 ? -(2LL << 32) : (static_cast<long long>(X0) << 32);
+  const long long Xhi = strip == a.n_strips - 1 ? (static_cast<long long>(n + 1) << 32)
+                                                 : (static_cast<long long>(X0 + W) << 32);
+  AngleGeom g{};
+  int slo = 0, shi = -1;
+  if (has_angle) {
+    g = a.ang[ai];
+    int2 sr = a.strip_range[static_cast<size_t>(ai) * a.n_strips + strip];
+    slo = sr.x;
+    shi = sr.y;
+  }
+  float* myacc = racc + warp * a.rmax;
+  for (int i = lane; i < a.rmax; i += 32) myacc[i] = 0.f;
+  const RayRange* rays = a.rays + static_cast<size_t>(g.t) * a.det + a.s_mid;
+
+  for (int r = 0; r < n_rows; ++r) {
+    const int Y0 = r * T;
+    __syncthreads();
+    for (int i = threadIdx.x; i < (T + 2) * P; i += NW * 32) {
+      int ry = i / P, rx = i - ry * P;
+      int gy = Y0 - 1 + ry, gx = X0 - 1 + rx;
+      tile[i] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
+                    ? __ldg(img + static_cast<size_t>(gy) * n + gx)
+                    : 0.f;
+    }
+    __syncthreads();
+    if (!has_angle) continue;
+    const long long Ylo = r == 0 ? -(2LL << 32) : (static_cast<long long>(Y0) << 32);
+    const long long Yhi = r == n_rows - 1 ? (static_cast<long long>(n + 1) << 32)
+                                          : (static_cast<long long>(Y0 + T) << 32);
+    int tlo, thi;
+    ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
+    tlo = max(tlo, slo);
+    thi = min(thi, shi);
+    const long long offX = static_cast<long long>(X0 - 1) << 32;
+    const long long offY = static_cast<long long>(Y0 - 1) << 32;
+    for (int sb = tlo; sb <= thi; sb += 32) {
+      const int s = sb + lane;
+      const bool act = s <= thi;
+      LaneRun run{0, 0, 0, 0};
+      if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
+      if (run.jhi <= run.jlo) run.jlo = 0x7fffffff, run.jhi = 0;
+      const int J0 = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(run.jlo));
+      const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
+      if (J0 >= J1) continue;
+      long long X = run.X - offX + static_cast<long long>(J0) * g.dX;
+      long long Y = run.Y - offY + static_cast<long long>(J0) * g.dY;
+      float acc = 0.f;
+      for (int j = J0; j < J1; ++j) {
+        if (j >= run.jlo && j < run.jhi) {
+          const int cx = static_cast<int>(X >> 32), cy = static_cast<int>(Y >> 32);
+          const float fx = frac_q32(X), fy = frac_q32(Y);
+          const float* p = tile + cy * P + cx;
+          const float v00 = p[0], v01 = p[1], v10 = p[P], v11 = p[P + 1];
+          const float v0 = fmaf(fx, v01 - v00, v00);
+          const float v1 = fmaf(fx, v11 - v10, v10);
+          acc += fmaf(fy, v1 - v0, v0);
+        }
+        X += g.dX;
+        Y += g.dY;
+      }
+      if (act) myacc[s - slo] += acc;
+    }
+  }
+  __syncwarp();
+  if (has_angle) {
+    float* out = a.part + (static_cast<size_t>(b) * a.n_strips + strip) * a.m +
+                 static_cast<size_t>(g.t) * a.det + a.s_mid;
+    for (int s = slo + lane; s <= shi; s += 32) out[s] = myacc[s - slo];
+  }
+}
+
+struct BpArgs {
+  const AngleGeom* ang;
+  int ang_begin;     // first angle of chunk 0 in the class list
+  int n_ang;         // angles of this class
+  int chunk_len;
+  int n_chunks;
+  const RayRange* rays;
+  const float* u;    // [batch][m]
+  float* out;        // [batch][n_parts][nn] (this class's first part at part_off)
+  int part_off, n_parts;
+  int n, det, s_mid;
+  long long P0;
+  size_t nn, m, u_stride;
+};
+
+template <int W, int T, int NW>
+__global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
+  extern __shared__ float sm[];
+  constexpr int P = W + 2;
+  constexpr int ACC = (T + 2) * P;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int X0 = blockIdx.x * W, Y0 = blockIdx.y * T;
+  const int chunk = blockIdx.z % a.n_chunks;
+  const int b = blockIdx.z / a.n_chunks;
+  const int n = a.n;
+  const float c = 0.5f * (n - 1);
+  float* acc = sm + warp * ACC;
+  for (int i = lane; i < ACC; i += 32) acc[i] = 0.f;
+  __syncwarp();
+  const long long Xlo = static_cast<long long>(X0 - 1) << 32;
+  const long long Xhi = static_cast<long long>(X0 + W) << 32;
+  const long long Ylo = static_cast<long long>(Y0 - 1) << 32;
+  const long long Yhi = static_cast<long long>(Y0 + T) << 32;
+  const int a_begin = chunk * a.chunk_len;
+  const int a_end = min(a.n_ang, a_begin + a.chunk_len);
+  const float* ub = a.u + static_cast<size_t>(b) * a.u_stride;
+
+  for (int ai = a_begin + warp; ai < a_end; ai += NW) {
+    const AngleGeom g = a.ang[ai];
+    int tlo, thi;
+    ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
+    const float* urow = ub + static_cast<size_t>(g.t) * a.det + a.s_mid;
+    const RayRange* rays = a.rays + static_cast<size_t>(g.t) * a.det + a.s_mid;
+    for (int sb = tlo; sb <= thi; sb += 32 * kBpStride) {
+      for (int ph = 0; ph < kBpStride; ++ph) {
+        const int s = sb + kBpStride * lane + ph;
+        bool act = s <= thi;
+        float w = act ? __ldg(urow + s) : 0.f;
+        act = act && (w != 0.f);  // the reference skips rays with w == 0 (radon.cpp:110)
+        LaneRun run{0, 0, 0, 0};
+        if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
+        if (run.jhi <= run.jlo) run.jlo = 0x7fffffff, run.jhi = 0;
+        const int J0 = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(run.jlo));
+        const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
+        if (J0 >= J1) continue;
+        long long X = run.X - Xlo + static_cast<long long>(J0) * g.dX;
+        long long Y = run.Y - Ylo + static_cast<long long>(J0) * g.dY;
+        for (int j = J0; j < J1; ++j) {
+          if (j >= run.jlo && j < run.jhi) {
+            const int cx = static_cast<int>(X >> 32), cy = static_cast<int>(Y >> 32);
+            const float fx = frac_q32(X), fy = frac_q32(Y);
+            float* p = acc + cy * P + cx;
+            const float wy1 = w * fy;
+            const float wy0 = w - wy1;
+            const float t0 = wy0 * fx;
+            const float t1 = wy1 * fx;
+            p[0] += wy0 - t0;
+            p[1] += t0;
+            p[P] += wy1 - t1;
+            p[P + 1] += t1;
+          }
+          X += g.dX;
+          Y += g.dY;
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // Reduce the warps' accumulators over the owned pixels and store.
+  float* out = a.out + (static_cast<size_t>(b) * a.n_parts + a.part_off + chunk) * a.nn;
+  for (int i = threadIdx.x; i < T * W; i += NW * 32) {
+    const int ry = i / W, rx = i - ry * W;
+    const int gy = Y0 + ry, gx = X0 + rx;
+    if (gy >= n || gx >= n) continue;
+    const int li = (ry + 1) * P + rx + 1;
+    float v = 0.f;
+#pragma unroll
+    for (int w2 = 0; w2 < NW; ++w2) v += sm[w2 * ACC + li];
+    out[static_cast<size_t>(gy) * n + gx] = v;
+  }
+}
+
+__global__ void strip_sum_kernel(const float* part, float* out, int n_strips, size_t m,
+                                 int batch) {
+  size_t total = m * batch;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    size_t b = i / m, r = i - b * m;
+    const float* p = part + b * n_strips * m + r;
+    float acc = 0.f;
+    for (int k = 0; k < n_strips; ++k) acc += p[k * m];
+    out[i] = acc;
+  }
+}
+
+int grid_for(size_t total, int block) {
+  size_t g = (total + block - 1) / block;
+  return static_cast<int>(std::min<size_t>(g, 148 * 16));
+}
+
+}  // namespace
+
+// --------------------------------------------------------------- host side
+void RadonDev::upload() {
+  NCSG_CUDA_CHECK(cudaSetDevice(device));
+  for (int k = 0; k < 2; ++k) {
+    angles[k].alloc(geo.cls[k].size());
+    if (!geo.cls[k].empty())
+      NCSG_CUDA_CHECK(cudaMemcpy(angles[k].p, geo.cls[k].data(),
+                                 geo.cls[k].size() * sizeof(AngleGeom), cudaMemcpyHostToDevice));
+  }
+  rays.alloc(geo.rays.size());
+  NCSG_CUDA_CHECK(cudaMemcpy(rays.p, geo.rays.data(), geo.rays.size() * sizeof(RayRange),
+                             cudaMemcpyHostToDevice));
+  // Strip ray ranges (host fp64, conservative) and the per-class maximum.
+  const int n = geo.n;
+  n_strips = (n + kFpW - 1) / kFpW;
+  const double c = 0.5 * (n - 1);
+  for (int k = 0; k < 2; ++k) {
+    std::vector<int2> sr(geo.cls[k].size() * n_strips);
+    int rmax = 1;
+    for (size_t ai = 0; ai < geo.cls[k].size(); ++ai) {
+      const AngleGeom& g = geo.cls[k][ai];
+      double ax = std::ldexp(static_cast<double>(g.aX), -32);
+      double ay = std::ldexp(static_cast<double>(g.aY), -32);
+      for (int st = 0; st < n_strips; ++st) {
+        double x0 = st * kFpW - 2.0, x1 = st * kFpW + kFpW + 2.0;
+        double y0 = -2.0, y1 = n + 2.0;
+        double p = (x0 - c) * ax, q = (x1 - c) * ax, e = (y0 - c) * ay, f = (y1 - c) * ay;
+        int lo = std::max(-geo.s_mid, static_cast<int>(std::floor(std::min(p, q) + std::min(e, f))) - 2);
+        int hi = std::min(geo.s_mid, static_cast<int>(std::ceil(std::max(p, q) + std::max(e, f))) + 2);
+        sr[ai * n_strips + st] = make_int2(lo, hi);
+        rmax = std::max(rmax, hi - lo + 1);
+      }
+    }
+    fp_rmax[k] = rmax;
+    strip_range_host[k] = sr;
+    strip_range[k].alloc(sr.size());
+    if (!sr.empty())
+      NCSG_CUDA_CHECK(cudaMemcpy(strip_range[k].p, sr.data(), sr.size() * sizeof(int2),
+                                 cudaMemcpyHostToDevice));
+  }
+}
+
+void RadonDev::plan_adjoint(int batch) {
+  const int n = geo.n;
+  const int tiles = ((n + kBpW - 1) / kBpW) * ((n + kBpT - 1) / kBpT);
+  // Target roughly six resident CTA waves over 148 SMs (3 CTAs per SM).
+  const long target = 148L * 3 * 2;
+  for (int k = 0; k < 2; ++k) {
+    int na = static_cast<int>(geo.cls[k].size());
+    if (na == 0) {
+      bp_chunks[k] = 0;
+      bp_chunk_len[k] = 1;
+      continue;
+    }
+    long per = static_cast<long>(tiles) * batch * 2;
+    int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
+    chunks = std::min(chunks, std::max(1, na / (kBpWarps * 4)));
+    int len = (na + chunks - 1) / chunks;
+    bp_chunks[k] = (na + len - 1) / len;
+    bp_chunk_len[k] = len;
+  }
+  bp_batch_planned = batch;
+}
+
+void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
+                                  float* fp_partial, int batch, cudaStream_t s) {
+  const Geometry& g = r.geo;
+  for (int k = 0; k < 2; ++k) {
+    int na = static_cast<int>(g.cls[k].size());
+    if (!na) continue;
+    FpArgs a;
+    a.ang = r.angles[k].p;
+    a.n_ang = na;
+    a.rays = r.rays.p;
+    a.strip_range = r.strip_range[k].p;
+    a.img = k == 0 ? img : imgT;
+    a.part = fp_partial;
+    a.n = g.n;
+    a.det = g.n_det;
+    a.s_mid = g.s_mid;
+    a.n_strips = r.n_strips;
+    a.rmax = r.fp_rmax[k];
+    a.P0 = g.P0;
+    a.nn = static_cast<size_t>(g.n) * g.n;
+    a.m = static_cast<size_t>(g.n_angles) * g.n_det;
+    size_t smem = sizeof(float) * ((kFpT + 2) * (kFpW + 2) + kFpWarps * a.rmax);
+    auto kern = fp_strip_kernel<kFpW, kFpT, kFpWarps>;
+    NCSG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    dim3 grid(r.n_strips, (na + kFpWarps - 1) / kFpWarps, batch);
+    kern<<<grid, kFpWarps * 32, smem, s>>>(a);
+    NCSG_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, int batch,
+                      cudaStream_t s) {
+  size_t m = static_cast<size_t>(r.geo.n_angles) * r.geo.n_det;
+  strip_sum_kernel<<<grid_for(m * batch, 256), 256, 0, s>>>(fp_partial, out, r.n_strips, m,
+                                                          batch);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+}
+
+void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_stride,
+                                  float* bp_part, int batch, cudaStream_t s) {
+  const Geometry& g = r.geo;
+  const int n = g.n;
+  for (int k = 0; k < 2; ++k) {
+    int na = static_cast<int>(g.cls[k].size());
+    if (!na) continue;
+    BpArgs a;
+    a.ang = r.angles[k].p;
+    a.ang_begin = 0;
+    a.n_ang = na;
+    a.chunk_len = r.bp_chunk_len[k];
+    a.n_chunks = r.bp_chunks[k];
+    a.rays = r.rays.p;
+    a.u = u;
+    a.out = bp_part;
+    a.part_off = k == 0 ? 0 : r.bp_chunks[0];
+    a.n_parts = r.n_partials();
+    a.n = n;
+    a.det = g.n_det;
+    a.s_mid = g.s_mid;
+    a.P0 = g.P0;
+    a.nn = static_cast<size_t>(n) * n;
+    a.m = static_cast<size_t>(g.n_angles) * g.n_det;
+    a.u_stride = u_stride ? u_stride : a.m;
+    size_t smem = sizeof(float) * kBpWarps * (kBpT + 2) * (kBpW + 2);
+    auto kern = bp_tile_kernel<kBpW, kBpT, kBpWarps>;
+    NCSG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+    dim3 grid((n + kBpW - 1) / kBpW, (n + kBpT - 1) / kBpT, a.n_chunks * batch);
+    kern<<<grid, kBpWarps * 32, smem, s>>>(a);
+    NCSG_CUDA_CHECK(cudaGetLastError());
+  }
+}
+
+}  // namespace ncsg

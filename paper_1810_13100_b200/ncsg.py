@@ -1,0 +1,347 @@
+"""Python view of the C ABI (include/ncsg.h) with the reference's names.
+
+Mirrors the operator / solver surface of the reference's pybind module and C++
+API (proj/python/bindings.cpp, proj/include/ncstomo/*.hpp) for the NCS hot
+path: ``RadonMap``, ``GradMap``, ``mask_apply`` (MaskApplier::apply),
+``SplitProblem`` + ``ncs_solve`` / ``pdhg_solve`` / ``ncs_step``.  Every call
+goes through ``libncsg.so``; there is no CPU fallback -- on a machine without
+a CUDA device the compute calls raise ``NcsgError``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _build
+
+_lib = None
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class NcsgError(RuntimeError):
+    """Failure reported by libncsg (status != NCSG_OK)."""
+
+    def __init__(self, status: int, msg: str):
+        super().__init__(msg)
+        self.status = status
+
+
+class DivergenceError(NcsgError):
+    """Mirrors ncstomo::DivergenceError (solvers.hpp:101-105)."""
+
+    def __init__(self, status, msg, iter_=None):
+        super().__init__(status, msg)
+        self.iter = iter_
+
+
+class ProblemDesc(C.Structure):
+    _fields_ = [
+        ("kind", C.c_int), ("n", C.c_int), ("n_angles", C.c_int), ("n_det", C.c_int),
+        ("batch", C.c_int), ("positivity", C.c_int), ("alpha", C.c_double),
+        ("beta", C.c_double), ("lambda_", C.c_double), ("gamma", C.c_double),
+        ("pinv_rel_tol", C.c_double), ("mask", C.c_void_p), ("b", C.c_void_p),
+        ("angle_begin", C.c_int), ("angle_end", C.c_int), ("device", C.c_int),
+    ]
+
+
+class RecordRow(C.Structure):
+    _fields_ = [("iter", C.c_int64), ("objective", C.c_double), ("rel_subopt", C.c_double),
+                ("seminorm_step", C.c_double), ("wall_ms", C.c_double)]
+
+
+SYMBOLS = [
+    "ncsg_last_error", "ncsg_version", "ncsg_device_count", "ncsg_default_detector_count",
+    "ncsg_radon_create", "ncsg_radon_destroy", "ncsg_radon_domain_size",
+    "ncsg_radon_range_size", "ncsg_radon_sample_count", "ncsg_radon_forward",
+    "ncsg_radon_adjoint", "ncsg_radon_forward_host", "ncsg_radon_adjoint_host",
+    "ncsg_grad_forward", "ncsg_grad_adjoint", "ncsg_grad_forward_host",
+    "ncsg_grad_adjoint_host", "ncsg_mask_apply_host", "ncsg_problem_create",
+    "ncsg_problem_destroy", "ncsg_problem_domain_size", "ncsg_problem_range_size",
+    "ncsg_problem_stream", "ncsg_set_state", "ncsg_get_state", "ncsg_state_x", "ncsg_state_u",
+    "ncsg_step", "ncsg_step_graph", "ncsg_sync", "ncsg_objective", "ncsg_last_seminorm",
+    "ncsg_solve", "ncsg_step_phase_a", "ncsg_atu_buffer", "ncsg_step_phase_b",
+]
+
+
+def lib():
+    """Load libncsg.so (building it in-tree if absent)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_build.LIB):
+        _build.build()
+    L = C.CDLL(_build.LIB)
+    L.ncsg_last_error.restype = C.c_char_p
+    L.ncsg_version.restype = C.c_char_p
+    for name in ("ncsg_radon_domain_size", "ncsg_radon_range_size", "ncsg_problem_domain_size",
+                 "ncsg_problem_range_size"):
+        getattr(L, name).restype = C.c_size_t
+        getattr(L, name).argtypes = [C.c_void_p]
+    L.ncsg_radon_sample_count.restype = C.c_int64
+    L.ncsg_radon_sample_count.argtypes = [C.c_void_p]
+    L.ncsg_radon_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_void_p)]
+    L.ncsg_radon_destroy.argtypes = [C.c_void_p]
+    for name in ("ncsg_radon_forward", "ncsg_radon_adjoint"):
+        getattr(L, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    for name in ("ncsg_radon_forward_host", "ncsg_radon_adjoint_host"):
+        getattr(L, name).argtypes = [C.c_void_p, _dp, _dp, C.c_int]
+    for name in ("ncsg_grad_forward", "ncsg_grad_adjoint"):
+        getattr(L, name).argtypes = [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    for name in ("ncsg_grad_forward_host", "ncsg_grad_adjoint_host"):
+        getattr(L, name).argtypes = [C.c_int, _dp, _dp, C.c_int]
+    L.ncsg_mask_apply_host.argtypes = [C.c_int, _dp, _dp, _dp, C.c_int, C.c_int]
+    L.ncsg_problem_create.argtypes = [C.POINTER(ProblemDesc), C.POINTER(C.c_void_p)]
+    L.ncsg_problem_destroy.argtypes = [C.c_void_p]
+    L.ncsg_problem_stream.restype = C.c_void_p
+    L.ncsg_problem_stream.argtypes = [C.c_void_p]
+    L.ncsg_set_state.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+    L.ncsg_get_state.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64)]
+    for name in ("ncsg_state_x", "ncsg_state_u", "ncsg_atu_buffer"):
+        getattr(L, name).restype = C.c_void_p
+        getattr(L, name).argtypes = [C.c_void_p]
+    for name in ("ncsg_step", "ncsg_step_graph"):
+        getattr(L, name).argtypes = [C.c_void_p, C.c_int]
+    L.ncsg_sync.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
+    L.ncsg_objective.argtypes = [C.c_void_p, _dp]
+    L.ncsg_last_seminorm.argtypes = [C.c_void_p, _dp]
+    L.ncsg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                             C.POINTER(RecordRow), C.c_int, C.POINTER(C.c_int),
+                             C.POINTER(C.c_double)]
+    for name in ("ncsg_step_phase_a", "ncsg_step_phase_b"):
+        getattr(L, name).argtypes = [C.c_void_p]
+    _lib = L
+    return L
+
+
+def _check(status: int, what: str = ""):
+    if status == 0:
+        return
+    msg = lib().ncsg_last_error().decode()
+    if status == 4:
+        raise DivergenceError(status, msg)
+    if status == 2:
+        raise ValueError(msg)
+    raise NcsgError(status, f"{what}: {msg}" if what else msg)
+
+
+def device_count() -> int:
+    return lib().ncsg_device_count()
+
+
+def default_detector_count(n: int) -> int:
+    return lib().ncsg_default_detector_count(n)
+
+
+class RadonMap:
+    """RadonMap(n, n_angles, n_det) (radon.hpp:16-36) on the GPU."""
+
+    def __init__(self, n: int, n_angles: int, n_det: int | None = None, device: int = 0):
+        if n_det is None:
+            n_det = default_detector_count(n)
+        h = C.c_void_p()
+        _check(lib().ncsg_radon_create(n, n_angles, n_det, device, C.byref(h)), "RadonMap")
+        self._h = h
+        self.n, self.n_angles, self.n_det = n, n_angles, n_det
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ncsg_radon_destroy(self._h)
+            self._h = None
+
+    def domain_size(self):
+        return lib().ncsg_radon_domain_size(self._h)
+
+    def range_size(self):
+        return lib().ncsg_radon_range_size(self._h)
+
+    def sample_count(self):
+        return lib().ncsg_radon_sample_count(self._h)
+
+    def forward(self, x) -> np.ndarray:
+        """fp64 host in/out (RadonMap::forward, radon.cpp:82-102)."""
+        x = np.ascontiguousarray(x, np.float64)
+        batch = x.size // (self.n * self.n)
+        out = np.zeros((batch, self.n_angles, self.n_det))
+        _check(lib().ncsg_radon_forward_host(self._h, x.ravel(), out.ravel(), batch), "forward")
+        return out.reshape(x.shape[:-2] + (self.n_angles, self.n_det))
+
+    def adjoint(self, u) -> np.ndarray:
+        """fp64 host in/out (RadonMap::adjoint, radon.cpp:104-127)."""
+        u = np.ascontiguousarray(u, np.float64)
+        batch = u.size // (self.n_angles * self.n_det)
+        out = np.zeros((batch, self.n, self.n))
+        _check(lib().ncsg_radon_adjoint_host(self._h, u.ravel(), out.ravel(), batch), "adjoint")
+        return out.reshape(u.shape[:-2] + (self.n, self.n))
+
+    def forward_device(self, x_ptr: int, out_ptr: int, batch: int = 1, stream=None):
+        _check(lib().ncsg_radon_forward(self._h, x_ptr, out_ptr, batch, stream), "forward")
+
+    def adjoint_device(self, u_ptr: int, out_ptr: int, batch: int = 1, stream=None):
+        _check(lib().ncsg_radon_adjoint(self._h, u_ptr, out_ptr, batch, stream), "adjoint")
+
+
+class GradMap:
+    """GradMap(n) (grad.hpp:17-28): flat range = h block then v block."""
+
+    def __init__(self, n: int):
+        if n < 2:
+            raise ValueError("grad needs N >= 2")
+        self.n = n
+
+    def domain_size(self):
+        return self.n * self.n
+
+    def range_size(self):
+        return 2 * self.n * (self.n - 1)
+
+    def forward(self, x):
+        x = np.ascontiguousarray(x, np.float64)
+        batch = x.size // (self.n * self.n)
+        out = np.zeros((batch, self.range_size()))
+        _check(lib().ncsg_grad_forward_host(self.n, x.ravel(), out.ravel(), batch),
+               "grad forward")
+        return out[0] if batch == 1 else out
+
+    def adjoint(self, g):
+        g = np.ascontiguousarray(g, np.float64)
+        batch = g.size // self.range_size()
+        out = np.zeros((batch, self.n, self.n))
+        _check(lib().ncsg_grad_adjoint_host(self.n, g.ravel(), out.ravel(), batch), "grad adjoint")
+        return out[0] if batch == 1 else out
+
+
+def mask_apply(mask, x, device: int = 0) -> np.ndarray:
+    """MaskApplier::apply (circulant.cpp:27-37): Re(F^-1(h .* F x)), fp64 host I/O."""
+    x = np.ascontiguousarray(x, np.float64)
+    n = x.shape[-1]
+    h = np.ascontiguousarray(np.asarray(mask, np.complex128)).view(np.float64).ravel()
+    batch = x.size // (n * n)
+    out = np.zeros_like(x)
+    _check(lib().ncsg_mask_apply_host(n, h, x.ravel(), out.ravel(), batch, device), "mask_apply")
+    return out
+
+
+CT, DENOISE = 0, 1
+
+
+@dataclass
+class SolveResult:
+    x: np.ndarray
+    u: np.ndarray
+    rows: np.ndarray  # (batch, k, 5): iter, objective, rel_subopt, seminorm, wall_ms
+    objective: np.ndarray
+
+
+class Problem:
+    """SplitProblem + SolverConfig + device Engine (solvers.hpp:24-78).
+
+    kind CT: blocks {1, R, Quadratic, b}, {beta/alpha, D, ScaledL1(lambda alpha/beta)}
+    kind DENOISE: blocks {1, I, Quadratic, b}, {beta/alpha, D, ...}
+    positivity appends {1, I, Nonneg}.  mask=None selects PDHG (M = gamma I).
+    """
+
+    def __init__(self, kind: int, n: int, alpha: float, beta: float, lam: float, gamma: float,
+                 b, mask=None, n_angles: int = 0, n_det: int = 0, batch: int = 1,
+                 positivity: bool = False, pinv_rel_tol: float = 1e-12,
+                 angle_range: tuple[int, int] = (0, 0), device: int = 0):
+        self.kind, self.n, self.batch = kind, n, batch
+        self.n_angles, self.n_det = n_angles, n_det
+        self.alpha, self.beta, self.lam, self.gamma = alpha, beta, lam, gamma
+        self.positivity = positivity
+        b = np.ascontiguousarray(b, np.float64).ravel()
+        self._b = b
+        d = ProblemDesc()
+        d.kind, d.n, d.n_angles, d.n_det = kind, n, n_angles, n_det
+        d.batch, d.positivity = batch, int(positivity)
+        d.alpha, d.beta, d.lambda_, d.gamma = alpha, beta, lam, gamma
+        d.pinv_rel_tol = pinv_rel_tol
+        if mask is not None:
+            self._mask = np.ascontiguousarray(np.asarray(mask, np.complex128)).view(np.float64)
+            d.mask = self._mask.ctypes.data
+        else:
+            self._mask = None
+            d.mask = None
+        d.b = b.ctypes.data
+        d.angle_begin, d.angle_end = angle_range
+        d.device = device
+        h = C.c_void_p()
+        _check(lib().ncsg_problem_create(C.byref(d), C.byref(h)), "problem_create")
+        self._h = h
+        self.range_size = lib().ncsg_problem_range_size(h)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ncsg_problem_destroy(self._h)
+            self._h = None
+
+    @property
+    def handle(self):
+        return self._h
+
+    @property
+    def stream(self):
+        return lib().ncsg_problem_stream(self._h)
+
+    def set_state(self, x=None, u=None, iter_: int = 0):
+        xa = None if x is None else np.ascontiguousarray(x, np.float64).ravel()
+        ua = None if u is None else np.ascontiguousarray(u, np.float64).ravel()
+        _check(lib().ncsg_set_state(self._h, None if xa is None else xa.ctypes.data,
+                                    None if ua is None else ua.ctypes.data, iter_), "set_state")
+
+    def get_state(self):
+        x = np.zeros((self.batch, self.n, self.n))
+        u = np.zeros((self.batch, self.range_size))
+        it = C.c_int64()
+        _check(lib().ncsg_get_state(self._h, x.ctypes.data, u.ctypes.data, C.byref(it)),
+               "get_state")
+        return x, u, it.value
+
+    def step(self, iters: int = 1, graph: bool = False):
+        fn = lib().ncsg_step_graph if graph else lib().ncsg_step
+        _check(fn(self._h, iters), "step")
+
+    def sync(self):
+        it = C.c_int64(-1)
+        st = lib().ncsg_sync(self._h, C.byref(it))
+        if st == 4:
+            raise DivergenceError(st, lib().ncsg_last_error().decode(), it.value)
+        _check(st, "sync")
+
+    def objective(self) -> np.ndarray:
+        out = np.zeros(self.batch)
+        _check(lib().ncsg_objective(self._h, out), "objective")
+        return out
+
+    def solve(self, max_iters: int, record_every: int | None = None, f_star=None,
+              check_step_condition: bool = False) -> SolveResult:
+        record_every = record_every or max(1, max_iters)
+        max_rows = max_iters // record_every + 3
+        rows = (RecordRow * (max_rows * self.batch))()
+        nr = C.c_int()
+        est = C.c_double()
+        fs = None
+        if f_star is not None:
+            fs = np.ascontiguousarray(np.broadcast_to(np.asarray(f_star, np.float64),
+                                                      (self.batch,)))
+        _check(lib().ncsg_solve(self._h, max_iters, record_every, int(check_step_condition),
+                                None if fs is None else fs.ctypes.data, rows, max_rows,
+                                C.byref(nr), C.byref(est)), "solve")
+        arr = np.array([[r.iter, r.objective, r.rel_subopt, r.seminorm_step, r.wall_ms]
+                        for r in rows]).reshape(self.batch, max_rows, 5)[:, : nr.value]
+        x, u, _ = self.get_state()
+        return SolveResult(x, u, arr, arr[:, -1, 1].copy())
+
+
+def ct_problem(cfg, b, mask=None, batch=None, **kw) -> Problem:
+    """Problem for a pinned CT config (paper_1810_13100_b200.configs)."""
+    return Problem(CT, cfg.n, cfg.alpha, cfg.beta, cfg.lam, cfg.gamma, b, mask=mask,
+                   n_angles=cfg.angles, n_det=cfg.det, batch=batch or cfg.batch, **kw)
+
+
+def denoise_problem(cfg, b, mask=None, **kw) -> Problem:
+    return Problem(DENOISE, cfg.n, cfg.alpha, cfg.beta, cfg.lam, cfg.gamma, b, mask=mask,
+                   batch=cfg.batch, **kw)
