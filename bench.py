@@ -1,0 +1,305 @@
+#!/usr/bin/env python
+"""NCS iterations/s on the BASELINE.json metric config (C3: 512^2 CT-TV, 720
+angles x 725 detectors), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c3]
+    python bench.py --impl reference ...     # the reference's own CPU NCS
+
+A "step" is one NCS iteration (Engine::step, solvers.cpp:124-161) of the
+config's problem with its state resident in HBM.  Each timed step is
+bracketed by CUDA events on the solver's stream; L2 is flushed (a 256 MiB
+write) between timed steps, outside the events.  `value` = K / sum(step
+times).  `e2e` times the public API end to end (problem upload from host
+memory, K steps, objective + state download).  Multi-GPU (torchrun): the
+problem is sharded by projection angle; one NCCL all-reduce of the partial
+A^T u per step, replicated circulant solve,
+device time = max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "NCS iters/s on 512² CT-TV (720 angles), 1/2/4/8 B200; % of HBM roofline"
+PEAKS = os.path.join(ROOT, "MEASURED_PEAKS.json")
+THROTTLE_BITS = {
+    0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+    0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+    0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting",
+}
+
+
+def peaks():
+    if os.path.exists(PEAKS):
+        with open(PEAKS) as f:
+            p = json.load(f)
+        return p, "measured"
+    return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index=0):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}",
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 3:
+                try:
+                    self.rows.append((float(parts[0]), float(parts[1]), int(parts[2], 16)))
+                except ValueError:
+                    pass
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [r[0] for r in self.rows]
+        mask = 0
+        for r in self.rows:
+            mask |= r[2]
+        reasons = [name for bit, name in THROTTLE_BITS.items() if mask & bit and bit != 0x1]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(sm)}
+
+
+def algorithmic_bytes(cfg, n_strips, n_parts):
+    """Per-step HBM bytes of the minimal fused design and of
+    each phase as implemented (fp32)."""
+    n, m, g = cfg.n * cfg.n, cfg.m, cfg.g
+    f = 4
+    return {
+        "adjoint": f * (m + n_parts * n),                 # read u_s, write partial images
+        "fft_rows_r2c": f * (n_parts * n + g + (n + 2 * n)),  # partials + u_g in, half spectrum out
+        "fft_cols": f * (4 * n + 2 * n),                  # spectrum r+w, filter
+        "fft_rows_c2r": f * (2 * n + 4 * n),              # spectrum in, x r/w, x_old, x^T
+        "forward": f * (2 * n + n_strips * m),            # x, x^T in, strip partials out
+        "dual_update": f * (n_strips * m + 5 * m + 2 * n + 2 * g),
+        "survey_minimal": f * (4 * m + 3 * g + 12.5 * n),
+    }
+
+
+def setup_problem(cfg, nc, dev=0, angle_range=(0, 0)):
+    from paper_1810_13100_b200 import instances, ncsg
+
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=dev)
+    x_true, b = instances.make_instance(cfg, R.forward)
+    mask = instances.metric_mask(cfg)
+    return R, x_true, b, mask
+
+
+def cpu_reference_rate(cfg, b, mask, iters_hi=3, iters_lo=1):
+    """The reference's own ncs_solve (oracle/_ref, compiled unchanged) timed on
+    host cores: per-iteration time = (t(hi) - t(lo)) / (hi - lo), so solver
+    setup, Engine::init and the final recorded seminorm cancel."""
+    from oracle.oracle import REF_SO, Port, Prob, Ref
+
+    prob = Prob(0, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, b)
+    if os.path.exists(REF_SO):
+        impl, kind, cores = Ref(), "reference", 1
+        run = lambda k: impl.solve(prob, cfg.gamma, mask, k)
+    else:
+        impl, kind = Port(), "port"
+        cores = max(1, len(os.sched_getaffinity(0)))
+        run = lambda k: impl.solve(prob, cfg.gamma, mask, k, threads=cores)
+    t = time.perf_counter()
+    run(iters_lo)
+    t_lo = time.perf_counter() - t
+    t = time.perf_counter()
+    run(iters_hi)
+    t_hi = time.perf_counter() - t
+    per = max(1e-9, (t_hi - t_lo) / (iters_hi - iters_lo))
+    return {"value": 1.0 / per, "unit": "it/s", "cores": cores, "kind": kind,
+            "sample": f"{cfg.name} ncs_solve {iters_hi} vs {iters_lo} iterations, "
+                      f"difference of wall times ({t_hi:.1f}s, {t_lo:.1f}s), same b and mask"}
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from paper_1810_13100_b200 import instances
+    from oracle.oracle import Port
+
+    P = Port()
+    x_true, b = instances.make_instance(cfg, lambda im: P.radon_forward(im, cfg.angles, cfg.det))
+    mask = instances.metric_mask(cfg)
+    k = max(2, min(args.steps, 4))
+    cb = cpu_reference_rate(cfg, b, mask, iters_hi=k, iters_lo=1)
+    line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "it/s",
+            "n_gpus": args.gpus, "steps": k - 1, "warmup": 0, "ms_per_step": 1000.0 / cb["value"],
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload(cfg), "cpu_baseline": cb,
+            "e2e": {"value": cb["value"], "unit": "it/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload(cfg):
+    return {"workload": f"{cfg.name}: {cfg.description}", "n": cfg.n, "angles": cfg.angles,
+            "detectors": cfg.det, "lambda": cfg.lam, "alpha": cfg.alpha, "beta": cfg.beta,
+            "gamma": cfg.gamma, "dc": cfg.dc, "mask_scale": cfg.mask_scale, "batch": cfg.batch,
+            "l2": "flushed (256 MiB write) between timed steps, outside the events",
+            "parallelism": "angle-sharded" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "1 GPU"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    from paper_1810_13100_b200 import configs
+
+    cfg = configs.get(args.config)
+    if args.impl == "reference":
+        run_reference(args, cfg)
+        return
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        from paper_1810_13100_b200 import multigpu
+
+        multigpu.bench_sharded(args, cfg, METRIC, workload(cfg))
+        return
+    bench_single(args, cfg)
+
+
+def bench_single(args, cfg):
+    import torch
+
+    from paper_1810_13100_b200 import instances, ncsg
+
+    torch.cuda.set_device(0)
+    R, x_true, b, mask = setup_problem(cfg, None)
+    prob = ncsg.ct_problem(cfg, b, mask=mask) if cfg.kind == "ct" else ncsg.denoise_problem(
+        cfg, b, mask=mask)
+    prob.set_state()
+    prob.step(args.warmup)
+    prob.sync()
+    stream = torch.cuda.ExternalStream(prob.stream)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    launches0 = ncsg.launch_count()
+    with ClockSampler(0) as clk:
+        time.sleep(0.3)
+        prob.profile_begin()
+        with torch.cuda.stream(stream):
+            for k in range(args.steps):
+                flush.fill_(float(k))
+                starts[k].record(stream)
+                prob.step(1)
+                ends[k].record(stream)
+        phase_ms, nprof = prob.profile_end()
+        torch.cuda.synchronize()
+    launches = ncsg.launch_count() - launches0
+    prob.sync()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = sum(step_ms) / len(step_ms)
+    value = 1000.0 / ms * cfg.batch if cfg.batch > 1 else 1000.0 / ms
+    phase_avg = {k: v / max(1, nprof) for k, v in phase_ms.items()}
+
+    pk, pk_kind = peaks()
+    n_strips = (cfg.n + 127) // 128
+    n_parts = 0
+    nb = algorithmic_bytes(cfg, n_strips, 8)
+    dom = max(phase_avg, key=phase_avg.get)
+    dom_ms = phase_avg[dom]
+    achieved = nb[dom] / (dom_ms * 1e-3) / 1e9
+    clocks = clk.summary()
+    S = R.sample_count()
+    sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
+    smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # TB/s at the measured clock
+    gather = {}
+    if dom in ("adjoint", "forward"):
+        gather = {"bytes_per_launch": 16 * S, "achieved_tbs": 16 * S / (dom_ms * 1e-3) / 1e12,
+                  "peak_tbs": smem_peak, "frac": 16 * S / (dom_ms * 1e-3) / 1e12 / smem_peak,
+                  "note": "bilinear gathers (4 fp32 texels per sample) against shared-memory "
+                          "bandwidth 148 SM x 128 B/clk at the sampled SM clock"}
+    roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
+                "peak_kind": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
+                "traffic": None, "algorithmic_bytes_per_launch": nb[dom],
+                "launch_ms": dom_ms, "gather_roofline": gather}
+
+    line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": workload(cfg), "roofline": roofline,
+            "phases_ms": phase_avg, "gpu_launches": launches, "clocks": clocks,
+            "samples_per_projection": S}
+    if not args.no_e2e:
+        line["e2e"] = e2e_rate(cfg, b, mask, args.steps)
+    if not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_reference_rate(cfg, b, mask)
+        except Exception as e:  # the baseline is reported, never required
+            line["cpu_baseline"] = {"value": None, "error": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+def e2e_rate(cfg, b, mask, steps):
+    """Public API end to end: host b + mask -> problem (H2D), K steps, objective
+    and x/u back to host (D2H)."""
+    from paper_1810_13100_b200 import ncsg
+
+    t = time.perf_counter()
+    prob = ncsg.ct_problem(cfg, b, mask=mask)
+    prob.set_state()
+    prob.step(steps, graph=False)
+    f = prob.objective()
+    x, u, _ = prob.get_state()
+    dt = time.perf_counter() - t
+    h2d = 4 * b.size + 2 * 8 * cfg.n * (cfg.n // 2 + 1)
+    d2h = 8 * cfg.batch + 4 * (x.size + u.size)
+    assert np.all(np.isfinite(f))
+    return {"value": steps / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / steps,
+            "d2h_bytes_per_step": d2h / steps,
+            "note": "ncsg.Problem create (geometry replay, mask pinv, uploads) + set_state + "
+                    f"{steps} steps + objective + get_state, wall clock"}
+
+
+if __name__ == "__main__":
+    main()

@@ -193,7 +193,21 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
  * updates x, projects the own angles and updates the own dual blocks. */
 ncsg_status ncsg_step_phase_a(ncsg_problem* p);
 float* ncsg_atu_buffer(ncsg_problem* p);
+/* Use a caller-owned device buffer (batch*N*N floats, e.g. a torch tensor that
+ * NCCL all-reduces) as the A^T u exchange buffer; NULL reverts to internal. */
+ncsg_status ncsg_set_atu_buffer(ncsg_problem* p, float* dev_ptr);
 ncsg_status ncsg_step_phase_b(ncsg_problem* p);
+
+/* ------------------------------------------------------------ measurement
+ * Phase timing for bench.py: while profiling, every step records CUDA events
+ * on the handle's stream between its phases (adjoint, FFT rows r2c + combine,
+ * FFT columns, FFT rows c2r + x update, forward, dual update);
+ * ncsg_profile_end synchronises and returns the summed milliseconds per phase
+ * and the number of profiled steps. */
+ncsg_status ncsg_profile_begin(ncsg_problem* p);
+ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int* steps);
+/* Kernel launches issued by this library since load. */
+int64_t ncsg_launch_count(void);
 
 #ifdef __cplusplus
 }

@@ -17,7 +17,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["radon_kernels.cu", "fft_kernels.cu", "ncs_kernels.cu", "capi.cu"]
 CPP_SRCS = ["geometry.cpp"]
-HDRS = ["ncsg_internal.cuh", "ncs_kernels.cuh"]
+HDRS = ["ncsg_internal.cuh", "ncs_kernels.cuh", "ncs_device.cuh"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <climits>
 #include <cmath>
@@ -24,6 +25,11 @@ namespace {
 thread_local std::string g_err;
 }
 void set_error(const std::string& msg) { g_err = msg; }
+namespace {
+std::atomic<int64_t> g_launches{0};
+}
+int64_t launch_count() { return g_launches.load(); }
+void count_launch(int k) { g_launches += k; }
 
 template <class F>
 ncsg_status guard(F&& f) {
@@ -120,9 +126,16 @@ struct ncsg_problem {
   int64_t iter = 0;
   size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
   bool rank0 = true;              // adds the replicated blocks to A^T u
+  float* atu_ext = nullptr;       // caller-owned A^T u buffer (sharded phases)
+  DevBuf<float> atu_own;
   std::map<int, cudaGraphExec_t> graphs;
+  // phase profiling (bench.py): events recorded between the phases of do_step
+  bool profiling = false;
+  std::vector<cudaEvent_t> events;  // kPhases + 1 per profiled step
+  size_t ev_used = 0;
   ~ncsg_problem() {
     for (auto& kv : graphs) cudaGraphExecDestroy(kv.second);
+    for (auto e : events) cudaEventDestroy(e);
   }
 };
 
@@ -152,7 +165,20 @@ AtuTerms atu_terms(ncsg_problem* p) {
   return T;
 }
 
+constexpr int kPhases = 6;  // adjoint, fft rows r2c, fft cols, fft rows c2r, forward, dual
+
+void mark(ncsg_problem* p) {
+  if (!p->profiling) return;
+  if (p->ev_used == p->events.size()) {
+    cudaEvent_t e;
+    NCSG_CUDA_CHECK(cudaEventCreate(&e));
+    p->events.push_back(e);
+  }
+  NCSG_CUDA_CHECK(cudaEventRecord(p->events[p->ev_used++], p->stream.s));
+}
+
 void phase_a(ncsg_problem* p) {
+  mark(p);
   if (p->d.kind == NCSG_CT) {
     // u_s is the first m0 entries of each problem's dual (stride range).
     launch_radon_adjoint_partial(*p->radon, p->u.p, p->range, p->bp_part.p, p->batch,
@@ -160,11 +186,19 @@ void phase_a(ncsg_problem* p) {
   }
 }
 
-void phase_b(ncsg_problem* p) {
+// plain != nullptr: A^T u was assembled (and all-reduced) into `plain`.
+void phase_b(ncsg_problem* p, const float* plain = nullptr) {
   cudaStream_t s = p->stream.s;
   AtuTerms T = atu_terms(p);
+  if (plain) {
+    T = AtuTerms();
+    T.n = p->d.n;
+    T.plain = plain;
+  }
   T.counter = step_counter(p);
+  mark(p);
   launch_fft_rows_r2c(p->fft, T, p->spec.p, p->batch, s);
+  mark(p);
   launch_fft_cols_filter(p->fft, p->spec.p, p->maskT.p, p->batch, s);
   XUpdate xu;
   xu.x = p->x.p;
@@ -172,9 +206,12 @@ void phase_b(ncsg_problem* p) {
   xu.xT = (p->d.kind == NCSG_CT && !p->radon->geo.cls[1].empty()) ? p->xT.p : nullptr;
   xu.subtract = 1;
   xu.flag = p->flag.p;
+  mark(p);
   launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
+  mark(p);
   if (p->d.kind == NCSG_CT)
     launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
+  mark(p);
   DualArgs a;
   a.kind = p->d.kind;
   a.n = p->d.n;
@@ -198,6 +235,7 @@ void phase_b(ncsg_problem* p) {
   a.x_old = p->x_old.p;
   a.flag = p->flag.p;
   launch_dual_update(a, p->batch, s);
+  mark(p);
 }
 
 void do_step(ncsg_problem* p) {
@@ -700,7 +738,15 @@ size_t ncsg_problem_range_size(const ncsg_problem* p) { return p->range; }
 void* ncsg_problem_stream(const ncsg_problem* p) { return p->stream.s; }
 float* ncsg_state_x(ncsg_problem* p) { return p->x.p; }
 float* ncsg_state_u(ncsg_problem* p) { return p->u.p; }
-float* ncsg_atu_buffer(ncsg_problem* p) { return p->bp_part.p; }
+float* ncsg_atu_buffer(ncsg_problem* p) {
+  if (p->atu_ext) return p->atu_ext;
+  if (!p->atu_own.n) p->atu_own.alloc(p->nn * p->batch);
+  return p->atu_own.p;
+}
+
+ncsg_status ncsg_set_atu_buffer(ncsg_problem* p, float* dev_ptr) {
+  return guard([&] { p->atu_ext = dev_ptr; });
+}
 
 ncsg_status ncsg_set_state(ncsg_problem* p, const double* x, const double* u, int64_t iter) {
   return guard([&] {
@@ -794,13 +840,45 @@ ncsg_status ncsg_last_seminorm(ncsg_problem* p, double* out) {
   });
 }
 
+ncsg_status ncsg_profile_begin(ncsg_problem* p) {
+  return guard([&] {
+    p->profiling = true;
+    p->ev_used = 0;
+  });
+}
+
+ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int* steps) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+    p->profiling = false;
+    const size_t per = kPhases + 1;
+    const size_t ns = p->ev_used / per;
+    for (int k = 0; k < n_phase; ++k) phase_ms[k] = 0.0;
+    for (size_t st = 0; st < ns; ++st)
+      for (int k = 0; k < kPhases && k < n_phase; ++k) {
+        float ms = 0.f;
+        NCSG_CUDA_CHECK(cudaEventElapsedTime(&ms, p->events[st * per + k], p->events[st * per + k + 1]));
+        phase_ms[k] += ms;
+      }
+    if (steps) *steps = static_cast<int>(ns);
+    p->ev_used = 0;
+  });
+}
+
+int64_t ncsg_launch_count(void) { return ncsg::launch_count(); }
+
 ncsg_status ncsg_step_phase_a(ncsg_problem* p) {
-  return guard([&] { phase_a(p); });
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    phase_a(p);
+    launch_atu_assemble(atu_terms(p), ncsg_atu_buffer(p), p->batch, p->stream.s);
+  });
 }
 
 ncsg_status ncsg_step_phase_b(ncsg_problem* p) {
   return guard([&] {
-    phase_b(p);
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    phase_b(p, ncsg_atu_buffer(p));
     p->iter += 1;
   });
 }

@@ -21,6 +21,7 @@
 #include <cmath>
 #include <vector>
 
+#include "ncs_device.cuh"
 #include "ncsg_internal.cuh"
 
 namespace ncsg {
@@ -88,35 +89,6 @@ __device__ void fft_dif(float2* z, int nfft, int n, int logn, const float2* __re
     }
   }
   __syncthreads();
-}
-
-// A^T u (or a plain image) at (y, x) from the row-major terms.  The
-// transposed class-H partials are added separately (coalesced by columns).
-__device__ __forceinline__ float atu_rowmajor(const AtuTerms& T, int b, int y, int x) {
-  const int n = T.n;
-  const size_t nn = static_cast<size_t>(n) * n;
-  const size_t i = static_cast<size_t>(y) * n + x;
-  if (T.plain) return T.plain[b * nn + i];
-  float v = 0.f;
-  if (T.bp_part) {
-    const float* p = T.bp_part + b * T.part_stride + i;
-    for (int c = 0; c < T.nV; ++c) v += p[c * nn];
-  }
-  if (T.ident) v += T.ident[b * T.ident_stride + i];
-  if (T.ident2) v += T.ident2[b * T.ident_stride + i];
-  if (T.ug) {
-    // D^T g (grad.cpp:66-84): h block N x (N-1), then v block (N-1) x N.
-    const float* g = T.ug + b * T.ug_stride;
-    const float* hb = g;
-    const float* vb = g + static_cast<size_t>(n) * (n - 1);
-    float d = 0.f;
-    if (x < n - 1) d += hb[static_cast<size_t>(y) * (n - 1) + x];
-    if (x > 0) d -= hb[static_cast<size_t>(y) * (n - 1) + x - 1];
-    if (y < n - 1) d += vb[static_cast<size_t>(y) * n + x];
-    if (y > 0) d -= vb[static_cast<size_t>(y - 1) * n + x];
-    v += T.wd * d;
-  }
-  return v;
 }
 
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
@@ -314,6 +286,7 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
   fft_rows_r2c_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 2), smem, s>>>(
       terms, specT, f.tw.p, log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
@@ -324,6 +297,7 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
   fft_cols_filter_kernel<<<grid, fft_threads(n / 2), smem, s>>>(specT, maskT, f.tw.p, n,
                                                                 log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
@@ -337,6 +311,7 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
   fft_rows_c2r_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 2), smem, s>>>(
       specT, xu, f.tw.p, n, log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace ncsg

@@ -120,6 +120,8 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     a.inv_dY16 = static_cast<float>(65536.0 / static_cast<double>(a.dY));
     a.inv_adX16 =
         a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
+    a.dXq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dX), -9)));
+    a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }
   return g;

@@ -6,6 +6,7 @@
 
 #include <algorithm>
 
+#include "ncs_device.cuh"
 #include "ncs_kernels.cuh"
 
 namespace ncsg {
@@ -300,6 +301,7 @@ void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
   dim3 grid(grid_for(big, 256, 148 * 4), a.positivity ? 3 : 2, batch);
   dual_update_kernel<<<grid, 256, 0, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 int objective_blocks() { return 148; }
@@ -308,51 +310,60 @@ void launch_objective(const ObjArgs& a, int batch, cudaStream_t s) {
   dim3 grid(objective_blocks(), batch);
   objective_kernel<<<grid, 256, 0, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_grad_forward(const float* x, float* out, int n, int batch, cudaStream_t s) {
   size_t total = 2 * static_cast<size_t>(n) * (n - 1) * batch;
   grad_forward_kernel<<<grid_for(total, 256), 256, 0, s>>>(x, out, n, batch);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_grad_adjoint(const float* g, float* out, int n, int batch, cudaStream_t s) {
   size_t total = static_cast<size_t>(n) * n * batch;
   grad_adjoint_kernel<<<grid_for(total, 256), 256, 0, s>>>(g, out, n, batch);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_transpose(const float* in, float* out, int n, int batch, cudaStream_t s) {
   dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
   transpose_kernel<<<grid, dim3(32, 8), 0, s>>>(in, out, n, batch);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_f64_to_f32(const double* in, float* out, size_t count, cudaStream_t s) {
   f64_to_f32_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, out, count);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_f32_to_f64(const float* in, double* out, size_t count, cudaStream_t s) {
   f32_to_f64_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, out, count);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_sub(const float* a, const float* b, float* out, size_t count, cudaStream_t s) {
   sub_kernel<<<grid_for(count, 256), 256, 0, s>>>(a, b, out, count);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_seminorm(const SemArgs& a, int batch, cudaStream_t s) {
   dim3 grid(objective_blocks(), batch);
   seminorm_kernel<<<grid, 256, 0, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_stacked_rest(const StackArgs& a, int batch, cudaStream_t s) {
   dim3 grid(grid_for(a.range, 256), batch);
   stacked_rest_kernel<<<grid, 256, 0, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace ncsg
@@ -389,5 +400,41 @@ void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, i
   dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
   sum_partials_kernel<<<grid, dim3(32, 8), 0, s>>>(part, nV, nH, out, n);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+}  // namespace ncsg
+
+namespace ncsg {
+namespace {
+// A^T u as one image: class-V partials + transposed class-H partials (through
+// a shared-memory tile) + identity blocks + w D^T u_g (linear_map.cpp:47-55).
+__global__ void atu_assemble_kernel(AtuTerms T, float* out) {
+  __shared__ float t[32][33];
+  const int n = T.n;
+  const size_t nn = static_cast<size_t>(n) * n;
+  const int b = blockIdx.z;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const float* ph = T.bp_part ? T.bp_part + b * T.part_stride + T.nV * nn : nullptr;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = bx + k, x = by + threadIdx.x;  // transposed coordinates
+    float v = 0.f;
+    if (ph && y < n && x < n)
+      for (int c = 0; c < T.nH; ++c) v += ph[c * nn + static_cast<size_t>(y) * n + x];
+    t[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = by + k, x = bx + threadIdx.x;
+    if (y >= n || x >= n) continue;
+    out[b * nn + static_cast<size_t>(y) * n + x] = atu_rowmajor(T, b, y, x) + t[threadIdx.x][k];
+  }
+}
+}  // namespace
+
+void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t s) {
+  dim3 grid((T.n + 31) / 32, (T.n + 31) / 32, batch);
+  atu_assemble_kernel<<<grid, dim3(32, 8), 0, s>>>(T, out);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 }  // namespace ncsg

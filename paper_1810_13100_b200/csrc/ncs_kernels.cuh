@@ -66,3 +66,8 @@ void launch_f32_to_f64(const float* in, double* out, size_t count, cudaStream_t 
 void launch_sub(const float* a, const float* b, float* out, size_t count, cudaStream_t s);
 
 }  // namespace ncsg
+
+namespace ncsg {
+// out[batch][n*n] = A^T u assembled from `T` (sharded multi-GPU path).
+void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t s);
+}  // namespace ncsg

@@ -13,6 +13,9 @@ namespace ncsg {
 
 // ----------------------------------------------------------------- errors
 void set_error(const std::string& msg);
+// Kernel launches issued by this library (bench.py's gpu_launches).
+int64_t launch_count();
+void count_launch(int k = 1);
 struct Error {
   ncsg_status code;
   std::string msg;
@@ -44,6 +47,7 @@ struct AngleGeom {
   float aXf, aYf;    // aX, aY as floats in pixel units (range estimates)
   float inv_dY16;    // 65536 / dY  (step estimates on (diff >> 16))
   float inv_adX16;   // 65536 / |dX| (0 when dX == 0)
+  int dXq, dYq;      // dX, dY rounded to Q9.23 (tile-local stepping)
 };
 
 struct RayRange {  // valid tau interval [first, last] of one ray (empty: first > last)
@@ -92,9 +96,9 @@ struct DevBuf {
 // Tiling constants of the projector kernels.
 constexpr int kFpW = 128;    // forward strip width (pixels)
 constexpr int kFpT = 32;     // forward tile-row height
-constexpr int kFpWarps = 8;  // forward: warps per CTA = angles per CTA
+constexpr int kFpWarps = 4;  // forward: warps per CTA = angles per CTA
 constexpr int kBpW = 128;    // adjoint tile width
-constexpr int kBpT = 32;     // adjoint tile height
+constexpr int kBpT = 28;     // adjoint tile height (3 CTAs/SM of 4 accumulators)
 constexpr int kBpWarps = 4;  // adjoint: warps per CTA (private accumulators)
 
 struct RadonDev {

@@ -35,11 +35,6 @@ namespace {
 
 constexpr int kBpStride = 5;  // ray stride between lanes of one adjoint phase
 
-__device__ __forceinline__ float frac_q32(long long v) {
-  // low 32 bits are the fraction in units of 2^-32; keep the top 23 bits.
-  unsigned lo = static_cast<unsigned>(v);
-  return __uint_as_float(0x3f800000u | (lo >> 9)) - 1.0f;
-}
 
 // Smallest q with base + q*step >= target (step > 0), exact; inv16 = 65536/step.
 __device__ __forceinline__ int first_ge(long long base, long long step, long long target,
@@ -104,42 +99,70 @@ __device__ __forceinline__ void ray_range(const AngleGeom& g, float c, float x0,
   hi = min(s_mid, static_cast<int>(ceilf(mx)) + 1);
 }
 
+// Tile-local Q9.23 positions: value * 2^-23 pixels relative to the staged
+// region's origin (X0 - 2, Y0 - 2).  The start of every lane's run is exact
+// (converted from Q32); the per-step increments are Q32 rounded to Q23, so a
+// run of <= 64 steps drifts by < 4e-6 px -- continuous in the bilinear
+// weights, and the two-pixel margin of the staged region absorbs cell flips.
+__device__ __forceinline__ int to_local_q23(long long v, long long origin_q32) {
+  return static_cast<int>((v - origin_q32) >> 9);
+}
+// (v & mask) | one in a single LOP3 with register operands (the immediate
+// form needs two instructions): the Q23 fraction as a float in [1, 2).
+__device__ __forceinline__ float frac1_q23(int v, unsigned mask, unsigned one) {
+  unsigned r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xEA;" : "=r"(r) : "r"(v), "r"(mask), "r"(one));
+  return __uint_as_float(r);
+}
+__device__ __forceinline__ float lds(unsigned a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts(unsigned a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
+}
+
 struct FpArgs {
-  const AngleGeom* ang;
-  int n_ang;
+  const AngleGeom* ang[2];
+  int n_ang[2];
+  int chunks0;              // grid.y blocks of class 0; class 1 follows
+  const int2* strip_range[2];  // [angle][strip] s-range
   const RayRange* rays;
-  const int2* strip_range;  // [n_ang][n_strips] s-range per (angle, strip)
-  const float* img;
+  const float* img[2];      // class 0: x, class 1: x^T
   float* part;
   int n, det, s_mid, n_strips, rmax;
   long long P0;
   size_t nn, m;
 };
 
-template <int W, int T, int NW>
+template <int W, int T, int P, int NW>
 __global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
   extern __shared__ float sm[];
-  constexpr int P = W + 2;
+  constexpr int ROWS = T + 4;
   float* tile = sm;
-  float* racc = sm + (T + 2) * P;
+  float* racc = sm + ROWS * P;
+  const int cls = blockIdx.y < a.chunks0 ? 0 : 1;
+  const int chunk = cls == 0 ? blockIdx.y : blockIdx.y - a.chunks0;
   const int strip = blockIdx.x;
   const int X0 = strip * W;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int ai = blockIdx.y * NW + warp;
-  const bool has_angle = ai < a.n_ang;
+  const int ai = chunk * NW + warp;
+  const bool has_angle = ai < (cls ? a.n_ang[1] : a.n_ang[0]);
   const int b = blockIdx.z;
   const int n = a.n;
-  const float* img = a.img + static_cast<size_t>(b) * a.nn;
+  const float* img = (cls ? a.img[1] : a.img[0]) + static_cast<size_t>(b) * a.nn;
   const float c = 0.5f * (n - 1);
   const int n_rows = (n + T - 1) / T;
   const long long Xlo = strip == 0 ? -(2LL << 32) : (static_cast<long long>(X0) << 32);
   const long long Xhi = strip == a.n_strips - 1 ? (static_cast<long long>(n + 1) << 32)
                                                  : (static_cast<long long>(X0 + W) << 32);
+  const long long OX = static_cast<long long>(X0 - 2) << 32;
   AngleGeom g{};
   int slo = 0, shi = -1;
   if (has_angle) {
-    g = a.ang[ai];
-    int2 sr = a.strip_range[static_cast<size_t>(ai) * a.n_strips + strip];
+    g = (cls ? a.ang[1] : a.ang[0])[ai];
+    int2 sr = (cls ? a.strip_range[1] : a.strip_range[0])[static_cast<size_t>(ai) * a.n_strips + strip];
     slo = sr.x;
     shi = sr.y;
   }
@@ -150,48 +173,54 @@ __global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
   for (int r = 0; r < n_rows; ++r) {
     const int Y0 = r * T;
     __syncthreads();
-    for (int i = threadIdx.x; i < (T + 2) * P; i += NW * 32) {
-      int ry = i / P, rx = i - ry * P;
-      int gy = Y0 - 1 + ry, gx = X0 - 1 + rx;
-      tile[i] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
-                    ? __ldg(img + static_cast<size_t>(gy) * n + gx)
-                    : 0.f;
+    for (int i = threadIdx.x; i < ROWS * (W + 4); i += NW * 32) {
+      const int ry = i / (W + 4), rx = i - ry * (W + 4);
+      const int gy = Y0 - 2 + ry, gx = X0 - 2 + rx;
+      tile[ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
+                              ? __ldg(img + static_cast<size_t>(gy) * n + gx)
+                              : 0.f;
     }
     __syncthreads();
     if (!has_angle) continue;
     const long long Ylo = r == 0 ? -(2LL << 32) : (static_cast<long long>(Y0) << 32);
     const long long Yhi = r == n_rows - 1 ? (static_cast<long long>(n + 1) << 32)
                                           : (static_cast<long long>(Y0 + T) << 32);
+    const long long OY = static_cast<long long>(Y0 - 2) << 32;
     int tlo, thi;
     ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
     tlo = max(tlo, slo);
     thi = min(thi, shi);
-    const long long offX = static_cast<long long>(X0 - 1) << 32;
-    const long long offY = static_cast<long long>(Y0 - 1) << 32;
     for (int sb = tlo; sb <= thi; sb += 32) {
       const int s = sb + lane;
       const bool act = s <= thi;
-      LaneRun run{0, 0, 0, 0};
+      LaneRun run{OX, OY, 0, 0};
       if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
-      if (run.jhi <= run.jlo) run.jlo = 0x7fffffff, run.jhi = 0;
-      const int J0 = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(run.jlo));
+      const bool empty = run.jhi <= run.jlo;
+      if (empty) run.jlo = run.jhi = 0;
+      const int J0 = __reduce_min_sync(0xffffffffu, empty ? 0x7fffffffu : static_cast<unsigned>(run.jlo));
       const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
       if (J0 >= J1) continue;
-      long long X = run.X - offX + static_cast<long long>(J0) * g.dX;
-      long long Y = run.Y - offY + static_cast<long long>(J0) * g.dY;
+      int X = to_local_q23(run.X + static_cast<long long>(J0) * g.dX, OX);
+      int Y = to_local_q23(run.Y + static_cast<long long>(J0) * g.dY, OY);
+      if (empty) X = Y = 0;
+      const unsigned span = static_cast<unsigned>(run.jhi - run.jlo);
+      const unsigned tbase = static_cast<unsigned>(__cvta_generic_to_shared(tile));
+      unsigned mask = 0x7fffffu, one = 0x3f800000u;
       float acc = 0.f;
+#pragma unroll 4
       for (int j = J0; j < J1; ++j) {
-        if (j >= run.jlo && j < run.jhi) {
-          const int cx = static_cast<int>(X >> 32), cy = static_cast<int>(Y >> 32);
-          const float fx = frac_q32(X), fy = frac_q32(Y);
-          const float* p = tile + cy * P + cx;
-          const float v00 = p[0], v01 = p[1], v10 = p[P], v11 = p[P + 1];
-          const float v0 = fmaf(fx, v01 - v00, v00);
-          const float v1 = fmaf(fx, v11 - v10, v10);
-          acc += fmaf(fy, v1 - v0, v0);
-        }
-        X += g.dX;
-        Y += g.dY;
+        const bool on = static_cast<unsigned>(j - run.jlo) < span;
+        const int idx = on ? (Y >> 23) * P + (X >> 23) : 0;
+        const unsigned ad = tbase + 4u * static_cast<unsigned>(idx);
+        const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+        const float v00 = lds(ad), v01 = lds(ad + 4);
+        const float v10 = lds(ad + 4 * P), v11 = lds(ad + 4 * P + 4);
+        const float v0 = fmaf(fx, v01 - v00, v00);
+        const float v1 = fmaf(fx, v11 - v10, v10);
+        const float v = fmaf(fy, v1 - v0, v0);
+        acc += on ? v : 0.f;
+        X += g.dXq;
+        Y += g.dYq;
       }
       if (act) myacc[s - slo] += acc;
     }
@@ -205,29 +234,31 @@ __global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
 }
 
 struct BpArgs {
-  const AngleGeom* ang;
-  int ang_begin;     // first angle of chunk 0 in the class list
-  int n_ang;         // angles of this class
-  int chunk_len;
-  int n_chunks;
+  const AngleGeom* ang[2];
+  int n_ang[2];
+  int chunk_len[2];
+  int n_chunks[2];
   const RayRange* rays;
-  const float* u;    // [batch][m]
-  float* out;        // [batch][n_parts][nn] (this class's first part at part_off)
-  int part_off, n_parts;
+  const float* u;    // [batch][u_stride], sinogram dual first
+  float* out;        // [batch][n_parts][nn]; class 1 partials follow class 0's, transposed
   int n, det, s_mid;
   long long P0;
   size_t nn, m, u_stride;
 };
 
-template <int W, int T, int NW>
+template <int W, int T, int P, int NW>
 __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
   extern __shared__ float sm[];
-  constexpr int P = W + 2;
-  constexpr int ACC = (T + 2) * P;
+  constexpr int ROWS = T + 4;
+  constexpr int DUMMY = ROWS * P;               // scratch cell for masked lanes
+  constexpr int ACC = ((ROWS + 1) * P + 2 + 31) / 32 * 32;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int X0 = blockIdx.x * W, Y0 = blockIdx.y * T;
-  const int chunk = blockIdx.z % a.n_chunks;
-  const int b = blockIdx.z / a.n_chunks;
+  const int nparts = a.n_chunks[0] + a.n_chunks[1];
+  const int b = blockIdx.z / nparts;
+  const int part = blockIdx.z - b * nparts;
+  const int cls = part < a.n_chunks[0] ? 0 : 1;
+  const int chunk = cls == 0 ? part : part - a.n_chunks[0];
   const int n = a.n;
   const float c = 0.5f * (n - 1);
   float* acc = sm + warp * ACC;
@@ -237,12 +268,15 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
   const long long Xhi = static_cast<long long>(X0 + W) << 32;
   const long long Ylo = static_cast<long long>(Y0 - 1) << 32;
   const long long Yhi = static_cast<long long>(Y0 + T) << 32;
-  const int a_begin = chunk * a.chunk_len;
-  const int a_end = min(a.n_ang, a_begin + a.chunk_len);
+  const long long OX = static_cast<long long>(X0 - 2) << 32;
+  const long long OY = static_cast<long long>(Y0 - 2) << 32;
+  const int a_begin = chunk * (cls ? a.chunk_len[1] : a.chunk_len[0]);
+  const int a_end = min((cls ? a.n_ang[1] : a.n_ang[0]), a_begin + (cls ? a.chunk_len[1] : a.chunk_len[0]));
   const float* ub = a.u + static_cast<size_t>(b) * a.u_stride;
+  const AngleGeom* angs = (cls ? a.ang[1] : a.ang[0]);
 
   for (int ai = a_begin + warp; ai < a_end; ai += NW) {
-    const AngleGeom g = a.ang[ai];
+    const AngleGeom g = angs[ai];
     int tlo, thi;
     ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
     const float* urow = ub + static_cast<size_t>(g.t) * a.det + a.s_mid;
@@ -251,32 +285,40 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
       for (int ph = 0; ph < kBpStride; ++ph) {
         const int s = sb + kBpStride * lane + ph;
         bool act = s <= thi;
-        float w = act ? __ldg(urow + s) : 0.f;
+        const float w = act ? __ldg(urow + s) : 0.f;
         act = act && (w != 0.f);  // the reference skips rays with w == 0 (radon.cpp:110)
-        LaneRun run{0, 0, 0, 0};
+        LaneRun run{OX, OY, 0, 0};
         if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
-        if (run.jhi <= run.jlo) run.jlo = 0x7fffffff, run.jhi = 0;
-        const int J0 = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(run.jlo));
+        const bool empty = run.jhi <= run.jlo;
+        if (empty) run.jlo = run.jhi = 0;
+        const int J0 = __reduce_min_sync(0xffffffffu, empty ? 0x7fffffffu : static_cast<unsigned>(run.jlo));
         const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
         if (J0 >= J1) continue;
-        long long X = run.X - Xlo + static_cast<long long>(J0) * g.dX;
-        long long Y = run.Y - Ylo + static_cast<long long>(J0) * g.dY;
+        int X = to_local_q23(run.X + static_cast<long long>(J0) * g.dX, OX);
+        int Y = to_local_q23(run.Y + static_cast<long long>(J0) * g.dY, OY);
+        if (empty) X = Y = 0;
+        const unsigned span = static_cast<unsigned>(run.jhi - run.jlo);
+        const unsigned abase = static_cast<unsigned>(__cvta_generic_to_shared(acc));
+        unsigned mask = 0x7fffffu, one = 0x3f800000u;
+#pragma unroll 2
         for (int j = J0; j < J1; ++j) {
-          if (j >= run.jlo && j < run.jhi) {
-            const int cx = static_cast<int>(X >> 32), cy = static_cast<int>(Y >> 32);
-            const float fx = frac_q32(X), fy = frac_q32(Y);
-            float* p = acc + cy * P + cx;
-            const float wy1 = w * fy;
-            const float wy0 = w - wy1;
-            const float t0 = wy0 * fx;
-            const float t1 = wy1 * fx;
-            p[0] += wy0 - t0;
-            p[1] += t0;
-            p[P] += wy1 - t1;
-            p[P + 1] += t1;
-          }
-          X += g.dX;
-          Y += g.dY;
+          const bool on = static_cast<unsigned>(j - run.jlo) < span;
+          const int idx = on ? (Y >> 23) * P + (X >> 23) : DUMMY;
+          const unsigned ad = abase + 4u * static_cast<unsigned>(idx);
+          const float we = on ? w : 0.f;
+          const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+          const float wy1 = we * fy;
+          const float wy0 = we - wy1;
+          const float t0 = wy0 * fx;
+          const float t1 = wy1 * fx;
+          const float a00 = lds(ad), a01 = lds(ad + 4);
+          const float a10 = lds(ad + 4 * P), a11 = lds(ad + 4 * P + 4);
+          sts(ad, a00 + (wy0 - t0));
+          sts(ad + 4, a01 + t0);
+          sts(ad + 4 * P, a10 + (wy1 - t1));
+          sts(ad + 4 * P + 4, a11 + t1);
+          X += g.dXq;
+          Y += g.dYq;
           __syncwarp();
         }
       }
@@ -284,12 +326,12 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
   }
   __syncthreads();
   // Reduce the warps' accumulators over the owned pixels and store.
-  float* out = a.out + (static_cast<size_t>(b) * a.n_parts + a.part_off + chunk) * a.nn;
+  float* out = a.out + (static_cast<size_t>(b) * nparts + part) * a.nn;
   for (int i = threadIdx.x; i < T * W; i += NW * 32) {
     const int ry = i / W, rx = i - ry * W;
     const int gy = Y0 + ry, gx = X0 + rx;
     if (gy >= n || gx >= n) continue;
-    const int li = (ry + 1) * P + rx + 1;
+    const int li = (ry + 2) * P + rx + 2;
     float v = 0.f;
 #pragma unroll
     for (int w2 = 0; w2 < NW; ++w2) v += sm[w2 * ACC + li];
@@ -362,54 +404,73 @@ void RadonDev::upload() {
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
   const int tiles = ((n + kBpW - 1) / kBpW) * ((n + kBpT - 1) / kBpT);
-  // Target roughly six resident CTA waves over 148 SMs (3 CTAs per SM).
-  const long target = 148L * 3 * 2;
+  // Aim for about four waves of 3 resident CTAs per SM over 148 SMs.
+  const long target = 148L * 3 * 4;
+  const int na0 = static_cast<int>(geo.cls[0].size()), na1 = static_cast<int>(geo.cls[1].size());
+  const int na = na0 + na1;
+  long per = static_cast<long>(tiles) * batch;
+  int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
+  chunks = std::min(chunks, std::max(1, na / (kBpWarps * 3)));
   for (int k = 0; k < 2; ++k) {
-    int na = static_cast<int>(geo.cls[k].size());
-    if (na == 0) {
+    int nk = k == 0 ? na0 : na1;
+    if (nk == 0) {
       bp_chunks[k] = 0;
       bp_chunk_len[k] = 1;
       continue;
     }
-    long per = static_cast<long>(tiles) * batch * 2;
-    int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
-    chunks = std::min(chunks, std::max(1, na / (kBpWarps * 4)));
-    int len = (na + chunks - 1) / chunks;
-    bp_chunks[k] = (na + len - 1) / len;
+    int ck = std::max(1, static_cast<int>(std::lround(static_cast<double>(chunks) * nk / na)));
+    int len = (nk + ck - 1) / ck;
+    bp_chunks[k] = (nk + len - 1) / len;
     bp_chunk_len[k] = len;
   }
   bp_batch_planned = batch;
 }
 
+namespace {
+constexpr int kFpP = kFpW + 4;
+constexpr int kBpP = kBpW + 4;
+size_t fp_smem(int rmax) { return sizeof(float) * ((kFpT + 4) * kFpP + kFpWarps * rmax); }
+size_t bp_smem() {
+  return sizeof(float) * kBpWarps * ((((kBpT + 5) * kBpP + 2) + 31) / 32 * 32);
+}
+void set_smem(const void* fn, size_t bytes) {
+  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(bytes)));
+}
+}  // namespace
+
 void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
                                   float* fp_partial, int batch, cudaStream_t s) {
   const Geometry& g = r.geo;
+  FpArgs a;
+  int chunks[2];
   for (int k = 0; k < 2; ++k) {
-    int na = static_cast<int>(g.cls[k].size());
-    if (!na) continue;
-    FpArgs a;
-    a.ang = r.angles[k].p;
-    a.n_ang = na;
-    a.rays = r.rays.p;
-    a.strip_range = r.strip_range[k].p;
-    a.img = k == 0 ? img : imgT;
-    a.part = fp_partial;
-    a.n = g.n;
-    a.det = g.n_det;
-    a.s_mid = g.s_mid;
-    a.n_strips = r.n_strips;
-    a.rmax = r.fp_rmax[k];
-    a.P0 = g.P0;
-    a.nn = static_cast<size_t>(g.n) * g.n;
-    a.m = static_cast<size_t>(g.n_angles) * g.n_det;
-    size_t smem = sizeof(float) * ((kFpT + 2) * (kFpW + 2) + kFpWarps * a.rmax);
-    auto kern = fp_strip_kernel<kFpW, kFpT, kFpWarps>;
-    NCSG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    dim3 grid(r.n_strips, (na + kFpWarps - 1) / kFpWarps, batch);
-    kern<<<grid, kFpWarps * 32, smem, s>>>(a);
-    NCSG_CUDA_CHECK(cudaGetLastError());
+    a.ang[k] = r.angles[k].p;
+    a.n_ang[k] = static_cast<int>(g.cls[k].size());
+    a.strip_range[k] = r.strip_range[k].p;
+    chunks[k] = (a.n_ang[k] + kFpWarps - 1) / kFpWarps;
   }
+  if (chunks[0] + chunks[1] == 0) return;
+  a.chunks0 = chunks[0];
+  a.img[0] = img;
+  a.img[1] = imgT;
+  a.rays = r.rays.p;
+  a.part = fp_partial;
+  a.n = g.n;
+  a.det = g.n_det;
+  a.s_mid = g.s_mid;
+  a.n_strips = r.n_strips;
+  a.rmax = std::max(r.fp_rmax[0], r.fp_rmax[1]);
+  a.P0 = g.P0;
+  a.nn = static_cast<size_t>(g.n) * g.n;
+  a.m = static_cast<size_t>(g.n_angles) * g.n_det;
+  const size_t smem = fp_smem(a.rmax);
+  auto kern = fp_strip_kernel<kFpW, kFpT, kFpP, kFpWarps>;
+  set_smem(reinterpret_cast<const void*>(kern), smem);
+  dim3 grid(r.n_strips, chunks[0] + chunks[1], batch);
+  kern<<<grid, kFpWarps * 32, smem, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, int batch,
@@ -418,41 +479,38 @@ void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, in
   strip_sum_kernel<<<grid_for(m * batch, 256), 256, 0, s>>>(fp_partial, out, r.n_strips, m,
                                                           batch);
   NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_stride,
                                   float* bp_part, int batch, cudaStream_t s) {
   const Geometry& g = r.geo;
   const int n = g.n;
+  if (r.n_partials() == 0) return;
+  BpArgs a;
   for (int k = 0; k < 2; ++k) {
-    int na = static_cast<int>(g.cls[k].size());
-    if (!na) continue;
-    BpArgs a;
-    a.ang = r.angles[k].p;
-    a.ang_begin = 0;
-    a.n_ang = na;
-    a.chunk_len = r.bp_chunk_len[k];
-    a.n_chunks = r.bp_chunks[k];
-    a.rays = r.rays.p;
-    a.u = u;
-    a.out = bp_part;
-    a.part_off = k == 0 ? 0 : r.bp_chunks[0];
-    a.n_parts = r.n_partials();
-    a.n = n;
-    a.det = g.n_det;
-    a.s_mid = g.s_mid;
-    a.P0 = g.P0;
-    a.nn = static_cast<size_t>(n) * n;
-    a.m = static_cast<size_t>(g.n_angles) * g.n_det;
-    a.u_stride = u_stride ? u_stride : a.m;
-    size_t smem = sizeof(float) * kBpWarps * (kBpT + 2) * (kBpW + 2);
-    auto kern = bp_tile_kernel<kBpW, kBpT, kBpWarps>;
-    NCSG_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem)));
-    dim3 grid((n + kBpW - 1) / kBpW, (n + kBpT - 1) / kBpT, a.n_chunks * batch);
-    kern<<<grid, kBpWarps * 32, smem, s>>>(a);
-    NCSG_CUDA_CHECK(cudaGetLastError());
+    a.ang[k] = r.angles[k].p;
+    a.n_ang[k] = static_cast<int>(g.cls[k].size());
+    a.chunk_len[k] = r.bp_chunk_len[k];
+    a.n_chunks[k] = r.bp_chunks[k];
   }
+  a.rays = r.rays.p;
+  a.u = u;
+  a.out = bp_part;
+  a.n = n;
+  a.det = g.n_det;
+  a.s_mid = g.s_mid;
+  a.P0 = g.P0;
+  a.nn = static_cast<size_t>(n) * n;
+  a.m = static_cast<size_t>(g.n_angles) * g.n_det;
+  a.u_stride = u_stride ? u_stride : a.m;
+  const size_t smem = bp_smem();
+  auto kern = bp_tile_kernel<kBpW, kBpT, kBpP, kBpWarps>;
+  set_smem(reinterpret_cast<const void*>(kern), smem);
+  dim3 grid((n + kBpW - 1) / kBpW, (n + kBpT - 1) / kBpT, r.n_partials() * batch);
+  kern<<<grid, kBpWarps * 32, smem, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
 }
 
 }  // namespace ncsg

@@ -1,0 +1,119 @@
+"""Angle-sharded NCS over several GPUs of one node.
+
+Each rank owns a contiguous block of projection angles: its rows of R, of the
+sinogram dual u_s, of b and of the cached R x.  One step is
+
+    phase A   partial A^T u = R_r^T u_s,r (+ w D^T u_g on rank 0)      [local]
+    exchange  all-reduce of the N x N partial over NVLink (NCCL)
+    phase B   replicated circulant solve + x update (identical on every rank),
+              R_r x for the own angles, dual update of the own rays and of the
+              replicated u_g                                            [local]
+
+The gradient dual u_g and x are replicated and updated identically on every
+rank, so they never need to move; the only collective per step is one
+all-reduce of N^2 floats (1 MiB at 512^2) -- the "one all-reduce + replicated
+FFT solve" variant of SURVEY.md §8f rank 3, which at 512^2 costs less than
+reduce-scatter + 2 all-to-all + all-gather latencies.
+"""
+from __future__ import annotations
+
+import json
+import os
+import time
+
+
+def shard_angles(n_angles: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced angle block [begin, end) of `rank`."""
+    base, rem = divmod(n_angles, world)
+    begin = rank * base + min(rank, rem)
+    return begin, begin + base + (1 if rank < rem else 0)
+
+
+class ShardedSolver:
+    """One rank's share of an angle-sharded CT problem."""
+
+    def __init__(self, cfg, b, mask, rank, world, device):
+        import torch
+
+        from . import ncsg
+
+        self.rank, self.world = rank, world
+        self.range = shard_angles(cfg.angles, world, rank)
+        self.prob = ncsg.ct_problem(cfg, b, mask=mask, angle_range=self.range, device=device)
+        self.prob.set_state()
+        self.atu = torch.zeros(cfg.batch * cfg.n * cfg.n, dtype=torch.float32,
+                               device=f"cuda:{device}")
+        self.prob.bind_atu(self.atu)
+        self.stream = torch.cuda.ExternalStream(self.prob.stream, device=f"cuda:{device}")
+
+    def step(self, iters: int = 1):
+        import torch
+        import torch.distributed as dist
+
+        with torch.cuda.stream(self.stream):
+            for _ in range(iters):
+                self.prob.phase_a()
+                if self.world > 1:
+                    dist.all_reduce(self.atu)
+                self.prob.phase_b()
+
+    def objective(self):
+        import torch
+        import torch.distributed as dist
+
+        f = torch.tensor(self.prob.objective(), dtype=torch.float64)
+        if self.world > 1:
+            f = f.cuda()
+            dist.all_reduce(f)
+            f = f.cpu()
+        return f.numpy()
+
+
+def bench_sharded(args, cfg, metric, workload):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import instances, ncsg
+
+    rank = int(os.environ["RANK"])
+    world = int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=local)
+    x_true, b = instances.make_instance(cfg, R.forward)
+    mask = instances.metric_mask(cfg)
+    s = ShardedSolver(cfg, b, mask, rank, world, local)
+    s.step(args.warmup)
+    torch.cuda.synchronize()
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = ncsg.launch_count()
+    with torch.cuda.stream(s.stream):
+        for k in range(args.steps):
+            flush.fill_(float(k))
+            starts[k].record(s.stream)
+            s.step(1)
+            ends[k].record(s.stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    launches = ncsg.launch_count() - launches0
+    ms_local = sum(a.elapsed_time(e) for a, e in zip(starts, ends)) / args.steps
+    t = torch.tensor([ms_local], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    f = s.objective()
+    if rank == 0:
+        line = {"metric": metric, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": "f32", "data": "synthetic", "config": workload,
+                "gpu_launches": launches, "objective_after": float(np.sum(f)),
+                "collective": "NCCL all_reduce of the partial A^T u (N^2 fp32) per step"}
+        print(json.dumps(line), flush=True)
+    dist.barrier()
+    dist.destroy_process_group()

@@ -64,7 +64,9 @@ SYMBOLS = [
     "ncsg_problem_stream", "ncsg_set_state", "ncsg_get_state", "ncsg_state_x", "ncsg_state_u",
     "ncsg_step", "ncsg_step_graph", "ncsg_sync", "ncsg_objective", "ncsg_last_seminorm",
     "ncsg_solve", "ncsg_step_phase_a", "ncsg_atu_buffer", "ncsg_step_phase_b",
+    "ncsg_profile_begin", "ncsg_profile_end", "ncsg_launch_count", "ncsg_set_atu_buffer",
 ]
+PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
 
 
 def lib():
@@ -111,8 +113,11 @@ def lib():
     L.ncsg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                              C.POINTER(RecordRow), C.c_int, C.POINTER(C.c_int),
                              C.POINTER(C.c_double)]
-    for name in ("ncsg_step_phase_a", "ncsg_step_phase_b"):
+    for name in ("ncsg_step_phase_a", "ncsg_step_phase_b", "ncsg_profile_begin"):
         getattr(L, name).argtypes = [C.c_void_p]
+    L.ncsg_set_atu_buffer.argtypes = [C.c_void_p, C.c_void_p]
+    L.ncsg_profile_end.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(C.c_int)]
+    L.ncsg_launch_count.restype = C.c_int64
     _lib = L
     return L
 
@@ -126,6 +131,10 @@ def _check(status: int, what: str = ""):
     if status == 2:
         raise ValueError(msg)
     raise NcsgError(status, f"{what}: {msg}" if what else msg)
+
+
+def launch_count() -> int:
+    return lib().ncsg_launch_count()
 
 
 def device_count() -> int:
@@ -310,6 +319,27 @@ class Problem:
         if st == 4:
             raise DivergenceError(st, lib().ncsg_last_error().decode(), it.value)
         _check(st, "sync")
+
+    # -- angle-sharded step (multi-GPU): phase A, exchange A^T u, phase B --
+    def bind_atu(self, tensor):
+        """Use a caller-owned CUDA tensor (batch*N*N fp32) as the A^T u buffer."""
+        self._atu = tensor
+        _check(lib().ncsg_set_atu_buffer(self._h, C.c_void_p(tensor.data_ptr())), "bind_atu")
+
+    def phase_a(self):
+        _check(lib().ncsg_step_phase_a(self._h), "phase_a")
+
+    def phase_b(self):
+        _check(lib().ncsg_step_phase_b(self._h), "phase_b")
+
+    def profile_begin(self):
+        _check(lib().ncsg_profile_begin(self._h), "profile_begin")
+
+    def profile_end(self) -> tuple[dict, int]:
+        out = np.zeros(len(PHASES))
+        steps = C.c_int()
+        _check(lib().ncsg_profile_end(self._h, out, len(PHASES), C.byref(steps)), "profile_end")
+        return dict(zip(PHASES, out.tolist())), steps.value
 
     def objective(self) -> np.ndarray:
         out = np.zeros(self.batch)

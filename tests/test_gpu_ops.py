@@ -1,0 +1,148 @@
+"""Per-operator parity of the CUDA path against the oracle (north_star: relative
+L2 error <= 1e-5 for R, R^T, D and the FFT solve), through the C ABI."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def rel(a, b):
+    a, b = np.ravel(a), np.ravel(b)
+    return float(np.linalg.norm(a - b) / max(1e-300, np.linalg.norm(b)))
+
+
+GEOMS = [
+    (16, 12, 25),    # python smoke geometry (test_smoke.py:36-49)
+    (32, 30, 47),
+    (64, 48, 93),    # impulse geometry (test_ops.cpp:37-47)
+    (64, 60, 93),    # adjoint-probe geometry (test_ops.cpp:32-35)
+    (100, 37, 143),  # non power of two, odd angle count
+    (17, 9, 27),     # odd N (half-integer centre is integer)
+    (64, 1, 93),     # single angle
+    (64, 4, 95),     # angles exactly 0, 45, 90, 135 degrees
+    (200, 8, 301),   # wide detector, N not a multiple of the tile sizes
+]
+
+
+@pytest.mark.parametrize("n,A,D", GEOMS)
+def test_radon_forward_adjoint_small(ncsg, port, n, A, D):
+    rng = np.random.default_rng(n * 1000 + A)
+    x = rng.standard_normal((n, n))
+    u = rng.standard_normal((A, D))
+    R = ncsg.RadonMap(n, A, D)
+    assert R.sample_count() == port.radon_valid_counts(n, A, D).sum()
+    assert rel(R.forward(x), port.radon_forward(x, A, D)) <= TOL
+    assert rel(R.adjoint(u), port.radon_adjoint(u, n)) <= TOL
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c5"])
+def test_radon_config_sizes(ncsg, port, name):
+    from paper_1810_13100_b200 import configs
+
+    cfg = configs.get(name)
+    rng = np.random.default_rng(7)
+    x = rng.standard_normal((cfg.n, cfg.n))
+    u = rng.standard_normal((cfg.angles, cfg.det))
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det)
+    assert R.sample_count() == port.radon_valid_counts(cfg.n, cfg.angles, cfg.det).sum()
+    assert rel(R.forward(x), port.radon_forward(x, cfg.angles, cfg.det)) <= TOL
+    assert rel(R.adjoint(u), port.radon_adjoint(u, cfg.n)) <= TOL
+
+
+@pytest.mark.slow
+def test_radon_c4_size(ncsg, port):
+    """C4 (2048^2, 2048 x 2897): forward on a ray sample, adjoint in full."""
+    from paper_1810_13100_b200 import configs
+
+    cfg = configs.base("c4")
+    rng = np.random.default_rng(11)
+    x = rng.standard_normal((cfg.n, cfg.n))
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det)
+    y = R.forward(x).ravel()
+    rays = rng.choice(cfg.angles * cfg.det, 20000, replace=False)
+    assert rel(y[rays], port.radon_forward_rays(x, cfg.angles, cfg.det, rays)) <= TOL
+    u = rng.standard_normal((cfg.angles, cfg.det))
+    assert rel(R.adjoint(u), port.radon_adjoint(u, cfg.n)) <= TOL
+    assert R.sample_count() == 8581547248  # SURVEY.md §8 sizes table
+
+
+def test_adjoint_identity_and_determinism(ncsg):
+    n, A, D = 128, 180, 185
+    rng = np.random.default_rng(3)
+    x, u = rng.standard_normal((n, n)), rng.standard_normal((A, D))
+    R = ncsg.RadonMap(n, A, D)
+    y1, y2 = R.forward(x), R.forward(x)
+    z1, z2 = R.adjoint(u), R.adjoint(u)
+    np.testing.assert_array_equal(y1, y2)  # bitwise reproducible (test_ops.cpp:49-58)
+    np.testing.assert_array_equal(z1, z2)
+    lhs, rhs = np.vdot(y1, u), np.vdot(x, z1)
+    assert abs(lhs - rhs) / abs(lhs) <= 1e-5
+
+
+def test_batched_projector_equals_single(ncsg):
+    n, A, D = 64, 48, 93
+    rng = np.random.default_rng(4)
+    xs = rng.standard_normal((3, n, n))
+    us = rng.standard_normal((3, A, D))
+    R = ncsg.RadonMap(n, A, D)
+    yb, zb = R.forward(xs), R.adjoint(us)
+    for k in range(3):
+        np.testing.assert_array_equal(yb[k], R.forward(xs[k]))
+        np.testing.assert_array_equal(zb[k], R.adjoint(us[k]))
+
+
+def test_impulse_projects_to_one_per_angle(ncsg):
+    # test_ops.cpp:37-47
+    n = 64
+    x = np.zeros((n, n))
+    x[32, 32] = 1.0
+    s = ncsg.RadonMap(n, 48).forward(x)
+    np.testing.assert_allclose(s.sum(axis=1), 1.0, rtol=0.05)
+
+
+def test_zero_in_zero_out(ncsg):
+    R = ncsg.RadonMap(32, 30)
+    assert not R.forward(np.zeros((32, 32))).any()
+    assert not R.adjoint(np.zeros((30, 47))).any()
+
+
+def test_grad_parity(ncsg, port):
+    for n in (2, 3, 17, 64):
+        rng = np.random.default_rng(n)
+        x = rng.standard_normal((n, n))
+        g = rng.standard_normal(2 * n * (n - 1))
+        G = ncsg.GradMap(n)
+        assert rel(G.forward(x), port.grad_forward(x)) <= TOL
+        assert rel(G.adjoint(g), port.grad_adjoint(g, n)) <= TOL
+    # 3x3 hand values (test_ops.cpp:60-79)
+    x = np.array([1, 2, 4, 8, 16, 32, 64, 128, 256], float).reshape(3, 3)
+    g = ncsg.GradMap(3).forward(x)
+    assert g[0] == -1 and g[2] == -8 and g[6] == 1 - 8 and g[11] == 32 - 256
+
+
+@pytest.mark.parametrize("n", [8, 16, 128, 512, 1024, 2048])
+def test_mask_apply_parity(ncsg, port, n):
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n))
+    h = port.radon_mask(n, 3.0, 7.0) + port.laplacian_mask(n)
+    assert rel(ncsg.mask_apply(h, x), port.mask_apply(h, x)) <= TOL
+    if n <= 512:  # a general complex mask (Hermitian part taken, circulant.cpp:36)
+        hc = h + 0.5j * rng.standard_normal((n, n))
+        assert rel(ncsg.mask_apply(hc, x), port.mask_apply(hc, x)) <= TOL
+
+
+def test_mask_apply_identity_and_constants(ncsg):
+    # SPEC.md apply_circulant examples: h == 1 -> x; Laplacian kills constants
+    n = 16
+    x = np.random.default_rng(1).standard_normal((n, n))
+    np.testing.assert_allclose(ncsg.mask_apply(np.ones((n, n)), x), x, atol=1e-6)
+    from paper_1810_13100_b200.instances import laplacian_mask
+
+    assert np.abs(ncsg.mask_apply(laplacian_mask(n), np.full((n, n), 3.0))).max() < 1e-5
+
+
+def test_fft_needs_power_of_two(ncsg):
+    with pytest.raises(ValueError, match="power-of-two"):
+        ncsg.mask_apply(np.ones((12, 12)), np.ones((12, 12)))

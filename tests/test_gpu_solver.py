@@ -1,0 +1,268 @@
+"""NCS iteration parity of the CUDA path against the oracle: iterate and
+objective relative error <= 1e-4 after the configured iteration counts
+(north_star), plus the reference's solver KATs and equivalences."""
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import Prob
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def rel(a, b):
+    a, b = np.ravel(a), np.ravel(b)
+    return float(np.linalg.norm(a - b) / max(1e-300, np.linalg.norm(b)))
+
+
+def small_ct(port, n=32, A=36, seed=5, lam=0.01):
+    from paper_1810_13100_b200 import datagen
+
+    D = port.default_detector_count(n)
+    x = datagen.phantom(n, 6, seed)
+    clean = port.radon_forward(x, A, D)
+    b, _ = datagen.add_sinogram_noise(clean, 0.01, seed + 1)
+    dc = float((port.radon_forward(np.ones((n, n)), A, D) ** 2).sum() / n ** 2)
+    scale = port.calibrate_scale(n, A, D, 8, 0)
+    alpha = 0.1
+    mask = port.radon_mask(n, scale, dc) + port.laplacian_mask(n)
+    prob = Prob(0, n, A, D, alpha, alpha, lam, b)
+    gamma = 1.2 * port.screen(prob, 0.0, mask, iters=40)
+    return prob, mask, gamma
+
+
+def gpu_problem(ncsg, prob, gamma, mask, batch_b=None, **kw):
+    b = prob.b if batch_b is None else batch_b
+    batch = 1 if batch_b is None else len(batch_b)
+    kind = ncsg.CT if prob.kind == 0 else ncsg.DENOISE
+    p = ncsg.Problem(kind, prob.n, prob.alpha, prob.beta, prob.lam, gamma, b, mask=mask,
+                     n_angles=prob.angles, n_det=prob.det, batch=batch,
+                     positivity=prob.positivity, **kw)
+    p.set_state()
+    return p
+
+
+def check_run(gres, ores, q=0, tol=TOL):
+    assert rel(gres.x[q], ores.x) <= tol, rel(gres.x[q], ores.x)
+    assert rel(gres.u[q], ores.u) <= tol, rel(gres.u[q], ores.u)
+    go, oo = gres.rows[q][:, 1], ores.rows[:, 1]
+    assert len(go) == len(oo)
+    np.testing.assert_array_equal(gres.rows[q][:, 0], ores.rows[:, 0])
+    assert np.max(np.abs(go - oo) / np.abs(oo)) <= tol
+
+
+def test_first_step_kat(ncsg, port):
+    # test_solvers.cpp:192-203: from zeros, x stays 0, u_s = -alpha b/(1+alpha), u_g = 0
+    prob, mask, gamma = small_ct(port)
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    p.step(1)
+    p.sync()
+    x, u, it = p.get_state()
+    assert it == 1
+    assert not x.any()
+    want = -prob.alpha * prob.b.ravel() / (1 + prob.alpha)
+    assert rel(u[0, : prob.m0], want) <= 1e-6
+    assert not u[0, prob.m0:].any()
+
+
+def test_solve_equals_repeated_step_bitwise(ncsg, port):
+    # test_solvers.cpp:607-625 on the device: ncs_solve(5) == 5 x step, bitwise,
+    # and two identical runs are bitwise identical (deterministic kernels)
+    prob, mask, gamma = small_ct(port)
+    a = gpu_problem(ncsg, prob, gamma, mask).solve(5, record_every=2)
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    for _ in range(5):
+        p.step(1)
+    x, u, _ = p.get_state()
+    np.testing.assert_array_equal(a.x, x)
+    np.testing.assert_array_equal(a.u, u)
+    b = gpu_problem(ncsg, prob, gamma, mask).solve(5, record_every=2)
+    np.testing.assert_array_equal(a.x, b.x)
+    np.testing.assert_array_equal(a.rows[..., :4], b.rows[..., :4])
+
+
+def test_graph_replay_equals_eager(ncsg, port):
+    prob, mask, gamma = small_ct(port)
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    p.step(7)
+    q = gpu_problem(ncsg, prob, gamma, mask)
+    q.step(7, graph=True)
+    np.testing.assert_array_equal(p.get_state()[0], q.get_state()[0])
+
+
+def test_small_ct_parity_with_records(ncsg, port):
+    prob, mask, gamma = small_ct(port)
+    o = port.solve(prob, gamma, mask, 200, record_every=20)
+    g = gpu_problem(ncsg, prob, gamma, mask).solve(200, record_every=20)
+    check_run(g, o)
+    # seminorm rows (solvers.cpp:166-177) -- differences of iterates, fp32
+    sem_g, sem_o = g.rows[0][1:, 3], o.rows[1:, 3]
+    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= 1e-3
+
+
+def test_pdhg_parity(ncsg, port):
+    prob, mask, gamma = small_ct(port, n=32, A=24)
+    gp = 1.2 * port.screen(prob, 0.0, None, iters=40) + 1.0  # gamma >= alpha lambda_max(A^T A)
+    o = port.solve(prob, gp, None, 100, record_every=25, pdhg=True)
+    g = gpu_problem(ncsg, prob, gp, None).solve(100, record_every=25)
+    check_run(g, o)
+
+
+def test_positivity_parity(ncsg, port):
+    prob, mask, gamma = small_ct(port, n=32, A=24)
+    prob.positivity = True
+    mask = mask + 1.0
+    gamma = 1.2 * port.screen(prob, 0.0, mask, iters=40)
+    o = port.solve(prob, gamma, mask, 100, record_every=25)
+    g = gpu_problem(ncsg, prob, gamma, mask).solve(100, record_every=25)
+    check_run(g, o)
+
+
+def test_denoise_small_parity(ncsg, port):
+    from paper_1810_13100_b200 import datagen
+
+    n = 64
+    x = datagen.phantom(n, 5, 3)
+    b = x + 0.1 * datagen.stream_noise(x.shape, 4)
+    prob = Prob(1, n, 0, 0, 1.0, 1.0, 0.05, b)
+    mask = np.ones((n, n)) + port.laplacian_mask(n)
+    o = port.solve(prob, 1e-3, mask, 200, record_every=50)
+    g = gpu_problem(ncsg, prob, 1e-3, mask).solve(200, record_every=50)
+    check_run(g, o)
+
+
+def test_divergence_raises(ncsg, port):
+    # test_solvers.cpp:627-644: far too small gamma diverges -> DivergenceError
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    p = gpu_problem(ncsg, prob, 1e-6, None)
+    with pytest.raises(ncsg.DivergenceError, match="diverged at iteration"):
+        p.solve(3000, record_every=500)
+
+
+def test_invalid_arguments(ncsg, port):
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    with pytest.raises(ValueError):
+        gpu_problem(ncsg, prob, 0.0, None)  # gamma must be positive without a mask
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    with pytest.raises(ValueError):
+        p.solve(5, record_every=0)
+
+
+def config_case(name, port):
+    from paper_1810_13100_b200 import configs, instances
+
+    cfg = configs.get(name)
+    if cfg.kind == "ct":
+        x, b = instances.make_instance(cfg, lambda im: port.radon_forward(im, cfg.angles, cfg.det))
+    else:
+        x, b = instances.make_instance(cfg)
+    mask = instances.metric_mask(cfg)
+    prob = Prob(cfg.kind_id, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, b)
+    return cfg, prob, mask
+
+
+def test_c1_full_parity(ncsg, port):
+    cfg, prob, mask = config_case("c1", port)
+    o = port.solve(prob, cfg.gamma, mask, cfg.iters, record_every=50)
+    g = gpu_problem(ncsg, prob, cfg.gamma, mask).solve(cfg.iters, record_every=50)
+    check_run(g, o)
+
+
+@pytest.mark.slow
+def test_c2_full_parity(ncsg, port):
+    cfg, prob, mask = config_case("c2", port)
+    o = port.solve(prob, cfg.gamma, mask, cfg.iters, record_every=250)
+    g = gpu_problem(ncsg, prob, cfg.gamma, mask).solve(cfg.iters, record_every=250)
+    check_run(g, o)
+
+
+def test_c3_parity_100(ncsg, port):
+    cfg, prob, mask = config_case("c3", port)
+    o = port.solve(prob, cfg.gamma, mask, 100, record_every=50)
+    g = gpu_problem(ncsg, prob, cfg.gamma, mask).solve(100, record_every=50)
+    check_run(g, o)
+
+
+@pytest.mark.slow
+def test_c3_full_against_golden(ncsg, port):
+    path = os.path.join(GOLDEN, "c3_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("c3 golden not generated")
+    gd = np.load(path)
+    cfg, prob, mask = config_case("c3", port)
+    assert rel(prob.b, gd["b_head"]) == 0 or np.allclose(prob.b.ravel()[: gd["b_head"].size],
+                                                          gd["b_head"], rtol=1e-12)
+    g = gpu_problem(ncsg, prob, cfg.gamma, mask).solve(cfg.iters, record_every=cfg.iters // 4)
+    assert rel(g.x[0], gd["x"]) <= TOL
+    idx = gd["u_idx"]
+    assert rel(g.u[0][idx], gd["u_sample"]) <= TOL
+    oo = gd["rows"][:, 1]
+    assert np.max(np.abs(g.rows[0][:, 1] - oo) / np.abs(oo)) <= TOL
+
+
+@pytest.mark.slow
+def test_c5_batched_parity(ncsg, port):
+    from paper_1810_13100_b200 import configs, instances
+
+    cfg = configs.get("c5")
+    mask = instances.metric_mask(cfg)
+    bs = []
+    for q in range(cfg.batch):
+        _, b = instances.make_instance(cfg, lambda im: port.radon_forward(im, cfg.angles, cfg.det),
+                                       problem=q)
+        bs.append(b)
+    proto = Prob(0, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, bs[0])
+    g = gpu_problem(ncsg, proto, cfg.gamma, mask, batch_b=np.stack(bs)).solve(
+        cfg.iters, record_every=cfg.iters)
+    for q in (0, cfg.batch - 1):
+        prob = Prob(0, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, bs[q])
+        o = port.solve(prob, cfg.gamma, mask, cfg.iters, record_every=cfg.iters)
+        check_run(g, o, q=q)
+
+
+@pytest.mark.slow
+def test_c4_few_iterations(ncsg, port):
+    cfg, prob, mask = config_case("c4", port)
+    if not cfg.pinned:
+        pytest.skip("c4 not pinned")
+    o = port.solve(prob, cfg.gamma, mask, 3, record_every=3)
+    g = gpu_problem(ncsg, prob, cfg.gamma, mask).solve(3, record_every=3)
+    check_run(g, o)
+
+
+def test_sharded_phases_on_one_gpu(ncsg, port):
+    """The multi-GPU step (phase A, sum of the ranks' A^T u, phase B) emulated
+    with two angle shards on one device -- sequential, no cross-rank waits --
+    matches the unsharded engine."""
+    prob, mask, gamma = small_ct(port, n=64, A=40)
+    full = gpu_problem(ncsg, prob, gamma, mask)
+    full.step(30)
+    xf, uf, _ = full.get_state()
+    import torch
+
+    shards = [gpu_problem(ncsg, prob, gamma, mask, angle_range=r) for r in ((0, 20), (20, 40))]
+    bufs = [torch.zeros(prob.n * prob.n, device="cuda") for _ in shards]
+    for s, bf in zip(shards, bufs):
+        s.bind_atu(bf)
+    for _ in range(30):
+        for s in shards:
+            s.phase_a()
+        torch.cuda.synchronize()
+        tot = bufs[0] + bufs[1]
+        for bf in bufs:
+            bf.copy_(tot)
+        torch.cuda.synchronize()
+        for s in shards:
+            s.phase_b()
+        torch.cuda.synchronize()
+    x0, u0, _ = shards[0].get_state()
+    x1, u1, _ = shards[1].get_state()
+    np.testing.assert_array_equal(x0, x1)
+    assert rel(x0, xf) <= 1e-5
+    m0 = 20 * prob.det
+    us = np.concatenate([u0[0, :m0], u1[0, m0:prob.m0]])
+    assert rel(us, uf[0, : prob.m0]) <= 1e-5
+    assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 1e-5

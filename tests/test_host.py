@@ -1,0 +1,198 @@
+"""CPU-only checks of the host side: the C-ABI library and its exports, the
+synthetic-input generators, the pinned configs and mask formulas, and the
+angle-sharding decomposition of the multi-GPU path (gloo, world size 2)."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1810_13100_b200 import configs, datagen, instances
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ncsg.h")).read()
+    return sorted(set(re.findall(r"\b(ncsg_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(ncsg):
+    lib = ncsg.lib()
+    decl = declared_symbols()
+    assert len(decl) >= 30
+    for name in decl:
+        assert hasattr(lib, name), name
+    assert set(ncsg.SYMBOLS) <= set(decl)
+
+
+def test_library_has_sm100a_code():
+    from paper_1810_13100_b200 import _build
+
+    out = os.popen(f"/usr/local/cuda/bin/cuobjdump --list-elf {_build.LIB}").read()
+    assert "sm_100a" in out
+
+
+def test_no_gpu_means_loud_failure(ncsg):
+    if ncsg.device_count() > 0:
+        pytest.skip("a GPU is present")
+    with pytest.raises(ncsg.NcsgError, match="no CUDA device"):
+        ncsg.RadonMap(32, 30)
+
+
+def test_geometry_validation_matches_reference(ncsg):
+    # radon.cpp:37-42 messages and test_ops.cpp:26-30 cases
+    for args, msg in [((64, 60, 92), "odd"), ((64, 60, 89), "cover"), ((64, 0, 93), "angle"),
+                      ((1, 4, 3), ">= 2")]:
+        with pytest.raises(ValueError, match=msg):
+            ncsg.RadonMap(*args)
+
+
+def test_default_detector_count(ncsg, port):
+    for n in (2, 16, 64, 100, 128, 512, 2048):
+        assert ncsg.default_detector_count(n) == port.default_detector_count(n)
+
+
+def test_rng_streams_match_oracle(port):
+    for seed, stream in [(0, 0), (7, 123), (2**40 + 3, 99)]:
+        np.testing.assert_array_equal(datagen.normals(seed, stream, 9),
+                                      port.rng_normals(seed, stream, 9))
+    first = datagen.Streams(11, np.arange(50)).first_normal()
+    want = np.array([port.rng_normals(11, i, 1)[0] for i in range(50)])
+    np.testing.assert_allclose(first, want, rtol=1e-15, atol=1e-15)
+
+
+def test_phantom_matches_make_phantom(port):
+    for n in (32, 128):
+        ell = datagen.random_ellipses(n, 10, 5)
+        np.testing.assert_array_equal(datagen.make_phantom(n, ell), port.make_phantom(n, ell))
+        p = datagen.phantom(n, 10, 5)
+        assert p.min() >= 0.0 and p.max() <= 1.0 and p.max() > 0.0
+
+
+def test_random_ellipse_distribution():
+    n = 512
+    e = datagen.random_ellipses(n, 400, 9)
+    cx = (e[:, 1] * n + (n - 1)) / 2
+    a_px = e[:, 3] * n / 2
+    assert np.all((cx >= 0.1 * n - 1) & (cx <= 0.9 * n + 1))
+    assert np.all((a_px >= 5) & (a_px <= 40))
+    assert np.all((e[:, 5] >= 0) & (e[:, 5] < 180))
+    assert np.all((e[:, 0] >= 0) & (e[:, 0] < 1))
+
+
+def test_noise_matches_simulate_ct(port):
+    n, A = 24, 10
+    D = port.default_detector_count(n)
+    x = datagen.phantom(n, 4, 3)
+    clean = port.radon_forward(x, A, D)
+    b, sigma = datagen.add_sinogram_noise(clean, 0.01, 77)
+    want = port.simulate_ct(x, A, D, sigma, 77)
+    np.testing.assert_allclose(b, want, rtol=1e-14, atol=1e-14)
+
+
+def test_masks_match_oracle(port):
+    for n in (8, 64):
+        np.testing.assert_array_equal(instances.laplacian_mask(n), port.laplacian_mask(n))
+        np.testing.assert_allclose(instances.radon_mask(n, 3.5, 7.0), port.radon_mask(n, 3.5, 7.0),
+                                   rtol=1e-15)
+
+
+def test_metric_mask_composition(ref):
+    # test_pipeline.cpp:180-194: metric = meas + (beta/alpha)^2 Lap (+1)
+    cfg = configs.get("c1")
+    meas = instances.radon_mask(cfg.n, cfg.mask_scale, cfg.dc)
+    want = ref.metric_mask(meas, cfg.alpha, cfg.beta)
+    np.testing.assert_allclose(instances.metric_mask(cfg), want, rtol=1e-15)
+    want_p = ref.metric_mask(meas, cfg.alpha, cfg.beta, positivity=True)
+    np.testing.assert_allclose(instances.metric_mask(cfg, positivity=True), want_p, rtol=1e-15)
+
+
+def test_measurement_mask_matches_reference_recipe(ref):
+    # test_pipeline.cpp:158-178: measurement_mask == radon_mask(calibrate_scale(...))
+    n, A = 32, 30
+    D = ref.lib.ref_default_detector_count(n)
+    scale = ref.calibrate_scale(n, A, D, 8, 0)
+    full = ref.ct_metric_mask(n, A, D, 1.0, 1.0, dc=5.0, samples=8, seed=0)
+    np.testing.assert_array_equal(full, ref.metric_mask(ref.radon_mask(n, scale, 5.0), 1.0, 1.0))
+
+
+def test_pinned_configs_complete():
+    for cfg in configs.all_configs():
+        if cfg.name == "c4" and not cfg.pinned:
+            pytest.skip("c4 pinning still running")
+        assert cfg.alpha > 0 and cfg.beta > 0 and cfg.gamma > 0
+        if cfg.kind == "ct":
+            assert cfg.dc > 0 and cfg.mask_scale > 0
+            assert cfg.det % 2 == 1
+
+
+def test_pinned_c1_against_oracle(port):
+    # re-derive the C1 pins (cheap) with the oracle: dc and mask scale
+    cfg = configs.get("c1")
+    one = np.ones((cfg.n, cfg.n))
+    r1 = port.radon_forward(one, cfg.angles, cfg.det)
+    assert float((r1 * r1).sum() / cfg.n ** 2) == cfg.dc
+    assert port.calibrate_scale(cfg.n, cfg.angles, cfg.det, 8, 0) == pytest.approx(
+        cfg.mask_scale, rel=1e-12)
+
+
+def test_angle_shards_cover_and_balance():
+    from paper_1810_13100_b200.multigpu import shard_angles
+
+    for A in (180, 720, 2048, 7):
+        for world in (1, 2, 3, 4, 8):
+            shards = [shard_angles(A, world, r) for r in range(world)]
+            assert shards[0][0] == 0 and shards[-1][1] == A
+            for (a0, a1), (b0, b1) in zip(shards, shards[1:]):
+                assert a1 == b0
+            sizes = [b - a for a, b in shards]
+            assert max(sizes) - min(sizes) <= 1
+
+
+def _sharded_atu_worker(rank, world, port_so, out_q):
+    import torch.distributed as dist
+
+    from oracle.oracle import Port
+    from paper_1810_13100_b200.multigpu import shard_angles
+
+    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29533", rank=rank,
+                            world_size=world)
+    P = Port(port_so)
+    rng = np.random.default_rng(1)
+    n, A = 24, 16
+    D = P.default_detector_count(n)
+    us = rng.standard_normal((A, D))
+    ug = rng.standard_normal(2 * n * (n - 1))
+    w = 0.7
+    a0, a1 = shard_angles(A, world, rank)
+    own = np.zeros_like(us)
+    own[a0:a1] = us[a0:a1]
+    part = P.radon_adjoint(own, n, threads=1)
+    if rank == 0:  # the replicated blocks are contributed once
+        part = part + w * P.grad_adjoint(ug, n)
+    import torch
+
+    t = torch.from_numpy(part.copy())
+    dist.all_reduce(t)
+    full = P.radon_adjoint(us, n, threads=1) + w * P.grad_adjoint(ug, n)
+    out_q.put((rank, float(np.abs(t.numpy() - full).max() / np.abs(full).max())))
+    dist.destroy_process_group()
+
+
+def test_sharded_adjoint_allreduce_gloo():
+    """The N>1 decomposition: per-rank partial A^T u over own angles (+ the
+    replicated D^T u_g on rank 0) all-reduced equals the full A^T u."""
+    import multiprocessing as mp
+
+    from oracle.oracle import PORT_SO
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_atu_worker, args=(r, 2, PORT_SO, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(err < 1e-13 for _, err in res), res
