@@ -22,10 +22,12 @@
 //     with plain read-modify-write; lanes take rays 5 apart in 5 phases, so
 //     two lanes of one instruction never touch the same pixel.  Warps are
 //     reduced once per CTA into a partial image per angle chunk.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "ncsg_internal.cuh"
 
@@ -37,12 +39,15 @@ constexpr int kBpStride = 5;  // ray stride between lanes of one adjoint phase
 
 
 // Smallest q with base + q*step >= target (step > 0), exact; inv16 = 65536/step.
+// The float estimate is within one step of the answer (|diff| < 2^47), so one
+// exact correction in each direction suffices.
 __device__ __forceinline__ int first_ge(long long base, long long step, long long target,
                                         float inv16) {
-  long long diff = target - base;
+  const long long diff = target - base;
   int q = static_cast<int>(ceilf(static_cast<float>(static_cast<int>(diff >> 16)) * inv16));
-  while (base + static_cast<long long>(q) * step < target) ++q;
-  while (base + static_cast<long long>(q - 1) * step >= target) --q;
+  const long long r = static_cast<long long>(q) * step - diff;  // >= 0 iff q satisfies
+  q += r < 0 ? 1 : 0;
+  q -= (r >= step) ? 1 : 0;
   return q;
 }
 
@@ -123,6 +128,31 @@ __device__ __forceinline__ void sts(unsigned a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
 }
 
+// ---- TMA (cp.async.bulk.tensor) + mbarrier helpers ----
+__device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+
 struct FpArgs {
   const AngleGeom* ang[2];
   int n_ang[2];
@@ -136,12 +166,41 @@ struct FpArgs {
   size_t nn, m;
 };
 
-template <int W, int T, int P, int NW>
-__global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
-  extern __shared__ float sm[];
+// Tile staging of the forward strip sweep: rows [Y0-2, Y0+T+2) x columns
+// [X0-4, X0+W+4) of the class's image (zero outside), pitch P.  The 4-column
+// left margin keeps the TMA box start 16-byte aligned (a misaligned innermost
+// start coordinate is an illegal instruction on sm_100a, scripts/tma_probe.cu).
+template <int W, int T, int P>
+__device__ __forceinline__ void stage_tile_manual(float* tile, const float* img, int n, int X0,
+                                                  int Y0) {
   constexpr int ROWS = T + 4;
-  float* tile = sm;
-  float* racc = sm + ROWS * P;
+  for (int i = threadIdx.x; i < ROWS * (W + 8); i += blockDim.x) {
+    const int ry = i / (W + 8), rx = i - ry * (W + 8);
+    const int gy = Y0 - 2 + ry, gx = X0 - 4 + rx;
+    tile[ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
+                            ? __ldg(img + static_cast<size_t>(gy) * n + gx)
+                            : 0.f;
+  }
+}
+
+// R (radon.cpp:82-102): strip sweep.  USE_TMA: the (T+4) x (W+8) tiles are
+// fetched by one elected thread with cp.async.bulk.tensor (zero fill outside
+// the image) into a two-stage ring guarded by mbarriers, so tile r+1 streams
+// in while the warps integrate tile r; P must equal W+8 (dense TMA box).
+template <int W, int T, int P, int NW, bool USE_TMA>
+__global__ void __launch_bounds__(NW * 32)
+    fp_strip_kernel(FpArgs a, const __grid_constant__ CUtensorMap map0,
+                    const __grid_constant__ CUtensorMap map1) {
+  extern __shared__ __align__(128) float sm[];
+  constexpr int ROWS = T + 4;
+  constexpr int TILE = (ROWS * P + 31) / 32 * 32;  // floats, 128-B multiple
+  constexpr int NBUF = USE_TMA ? 2 : 1;
+  __shared__ __align__(8) unsigned long long bars[2];
+  // 128-B aligned tile ring (TMA destination), then the per-warp ray sums.
+  const unsigned sm_addr = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+  const unsigned pad = ((sm_addr + 127u) & ~127u) - sm_addr;
+  float* tiles = sm + pad / 4;
+  float* racc = tiles + NBUF * TILE;
   const int cls = blockIdx.y < a.chunks0 ? 0 : 1;
   const int chunk = cls == 0 ? blockIdx.y : blockIdx.y - a.chunks0;
   const int strip = blockIdx.x;
@@ -151,13 +210,33 @@ __global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
   const bool has_angle = ai < (cls ? a.n_ang[1] : a.n_ang[0]);
   const int b = blockIdx.z;
   const int n = a.n;
-  const float* img = (cls ? a.img[1] : a.img[0]) + static_cast<size_t>(b) * a.nn;
   const float c = 0.5f * (n - 1);
   const int n_rows = (n + T - 1) / T;
+  const CUtensorMap* map = cls ? &map1 : &map0;
+  const float* img = (cls ? a.img[1] : a.img[0]) + static_cast<size_t>(b) * a.nn;
+  const unsigned bar0 = static_cast<unsigned>(__cvta_generic_to_shared(&bars[0]));
+  const unsigned tile0 = sm_addr + pad;
+  constexpr unsigned kTileBytes = ROWS * (W + 8) * 4;
+  // TMA needs non-negative, 16-byte aligned box starts (scripts/tma_probe.cu),
+  // so the left strip and the first tile row of every strip are staged by the
+  // threads; every other tile streams in by TMA.
+  const bool tma_cta = USE_TMA && X0 >= 4;
+  if (tma_cta) {
+    if (threadIdx.x == 0) {
+      mbar_init(bar0, 1);
+      mbar_init(bar0 + 8, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      if (n_rows > 1) {
+        mbar_expect_tx(bar0 + 8, kTileBytes);
+        tma_load_3d(tile0 + TILE * 4, map, X0 - 4, T - 2, b, bar0 + 8);
+      }
+    }
+    __syncthreads();  // barrier init visible before anyone waits on it
+  }
   const long long Xlo = strip == 0 ? -(2LL << 32) : (static_cast<long long>(X0) << 32);
   const long long Xhi = strip == a.n_strips - 1 ? (static_cast<long long>(n + 1) << 32)
                                                  : (static_cast<long long>(X0 + W) << 32);
-  const long long OX = static_cast<long long>(X0 - 2) << 32;
+  const long long OX = static_cast<long long>(X0 - 4) << 32;
   AngleGeom g{};
   int slo = 0, shi = -1;
   if (has_angle) {
@@ -169,60 +248,69 @@ __global__ void __launch_bounds__(NW * 32) fp_strip_kernel(FpArgs a) {
   float* myacc = racc + warp * a.rmax;
   for (int i = lane; i < a.rmax; i += 32) myacc[i] = 0.f;
   const RayRange* rays = a.rays + static_cast<size_t>(g.t) * a.det + a.s_mid;
+  const unsigned mask = 0x7fffffu, one = 0x3f800000u;
 
   for (int r = 0; r < n_rows; ++r) {
     const int Y0 = r * T;
-    __syncthreads();
-    for (int i = threadIdx.x; i < ROWS * (W + 4); i += NW * 32) {
-      const int ry = i / (W + 4), rx = i - ry * (W + 4);
-      const int gy = Y0 - 2 + ry, gx = X0 - 2 + rx;
-      tile[ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
-                              ? __ldg(img + static_cast<size_t>(gy) * n + gx)
-                              : 0.f;
+    const int buf = USE_TMA ? (r & 1) : 0;
+    const unsigned tbase = tile0 + buf * TILE * 4;
+    if (tma_cta && r > 0) {
+      mbar_wait(bar0 + 8 * buf, ((r - 1) >> 1) & 1);
+    } else {
+      __syncthreads();
+      stage_tile_manual<W, T, P>(tiles + buf * TILE, img, n, X0, Y0);
+      __syncthreads();
     }
-    __syncthreads();
-    if (!has_angle) continue;
-    const long long Ylo = r == 0 ? -(2LL << 32) : (static_cast<long long>(Y0) << 32);
-    const long long Yhi = r == n_rows - 1 ? (static_cast<long long>(n + 1) << 32)
-                                          : (static_cast<long long>(Y0 + T) << 32);
-    const long long OY = static_cast<long long>(Y0 - 2) << 32;
-    int tlo, thi;
-    ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
-    tlo = max(tlo, slo);
-    thi = min(thi, shi);
-    for (int sb = tlo; sb <= thi; sb += 32) {
-      const int s = sb + lane;
-      const bool act = s <= thi;
-      LaneRun run{OX, OY, 0, 0};
-      if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
-      const bool empty = run.jhi <= run.jlo;
-      if (empty) run.jlo = run.jhi = 0;
-      const int J0 = __reduce_min_sync(0xffffffffu, empty ? 0x7fffffffu : static_cast<unsigned>(run.jlo));
-      const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
-      if (J0 >= J1) continue;
-      int X = to_local_q23(run.X + static_cast<long long>(J0) * g.dX, OX);
-      int Y = to_local_q23(run.Y + static_cast<long long>(J0) * g.dY, OY);
-      if (empty) X = Y = 0;
-      const unsigned span = static_cast<unsigned>(run.jhi - run.jlo);
-      const unsigned tbase = static_cast<unsigned>(__cvta_generic_to_shared(tile));
-      unsigned mask = 0x7fffffu, one = 0x3f800000u;
-      float acc = 0.f;
+    if (has_angle) {
+      const long long Ylo = r == 0 ? -(2LL << 32) : (static_cast<long long>(Y0) << 32);
+      const long long Yhi = r == n_rows - 1 ? (static_cast<long long>(n + 1) << 32)
+                                            : (static_cast<long long>(Y0 + T) << 32);
+      const long long OY = static_cast<long long>(Y0 - 2) << 32;
+      int tlo, thi;
+      ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
+      tlo = max(tlo, slo);
+      thi = min(thi, shi);
+      for (int sb = tlo; sb <= thi; sb += 32) {
+        const int s = sb + lane;
+        const bool act = s <= thi;
+        LaneRun run{OX, OY, 0, 0};
+        if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
+        const bool empty = run.jhi <= run.jlo;
+        if (empty) run.jlo = run.jhi = 0;
+        const int J0 =
+            __reduce_min_sync(0xffffffffu, empty ? 0x7fffffffu : static_cast<unsigned>(run.jlo));
+        const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(run.jhi));
+        if (J0 >= J1) continue;
+        int X = to_local_q23(run.X + static_cast<long long>(J0) * g.dX, OX);
+        int Y = to_local_q23(run.Y + static_cast<long long>(J0) * g.dY, OY);
+        if (empty) X = Y = 0;
+        const unsigned span = static_cast<unsigned>(run.jhi - run.jlo);
+        float acc = 0.f;
 #pragma unroll 4
-      for (int j = J0; j < J1; ++j) {
-        const bool on = static_cast<unsigned>(j - run.jlo) < span;
-        const int idx = on ? (Y >> 23) * P + (X >> 23) : 0;
-        const unsigned ad = tbase + 4u * static_cast<unsigned>(idx);
-        const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
-        const float v00 = lds(ad), v01 = lds(ad + 4);
-        const float v10 = lds(ad + 4 * P), v11 = lds(ad + 4 * P + 4);
-        const float v0 = fmaf(fx, v01 - v00, v00);
-        const float v1 = fmaf(fx, v11 - v10, v10);
-        const float v = fmaf(fy, v1 - v0, v0);
-        acc += on ? v : 0.f;
-        X += g.dXq;
-        Y += g.dYq;
+        for (int j = J0; j < J1; ++j) {
+          const bool on = static_cast<unsigned>(j - run.jlo) < span;
+          const int idx = on ? (Y >> 23) * P + (X >> 23) : 0;
+          const unsigned ad = tbase + 4u * static_cast<unsigned>(idx);
+          const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+          const float v00 = lds(ad), v01 = lds(ad + 4);
+          const float v10 = lds(ad + 4 * P), v11 = lds(ad + 4 * P + 4);
+          const float v0 = fmaf(fx, v01 - v00, v00);
+          const float v1 = fmaf(fx, v11 - v10, v10);
+          const float v = fmaf(fy, v1 - v0, v0);
+          acc += on ? v : 0.f;
+          X += g.dXq;
+          Y += g.dYq;
+        }
+        if (act) myacc[s - slo] += acc;
       }
-      if (act) myacc[s - slo] += acc;
+    }
+    if (tma_cta) {
+      __syncthreads();  // every warp is done with this buffer
+      if (threadIdx.x == 0 && r + 2 < n_rows) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(bar0 + 8 * buf, kTileBytes);
+        tma_load_3d(tbase, map, X0 - 4, (r + 2) * T - 2, b, bar0 + 8 * buf);
+      }
     }
   }
   __syncwarp();
@@ -281,9 +369,12 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
     ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
     const float* urow = ub + static_cast<size_t>(g.t) * a.det + a.s_mid;
     const RayRange* rays = a.rays + static_cast<size_t>(g.t) * a.det + a.s_mid;
-    for (int sb = tlo; sb <= thi; sb += 32 * kBpStride) {
-      for (int ph = 0; ph < kBpStride; ++ph) {
-        const int s = sb + kBpStride * lane + ph;
+    // Lanes of one phase take rays `stride` apart (>= 3 keeps the scatter
+    // race-free); 4 when the tile's rays fit in 128 lane slots, else 5.
+    const int stride = (thi - tlo + 1) <= 32 * 4 ? 4 : kBpStride;
+    for (int sb = tlo; sb <= thi; sb += 32 * stride) {
+      for (int ph = 0; ph < stride; ++ph) {
+        const int s = sb + stride * lane + ph;
         bool act = s <= thi;
         const float w = act ? __ldg(urow + s) : 0.f;
         act = act && (w != 0.f);  // the reference skips rays with w == 0 (radon.cpp:110)
@@ -427,9 +518,46 @@ void RadonDev::plan_adjoint(int batch) {
 }
 
 namespace {
-constexpr int kFpP = kFpW + 4;
+constexpr int kFpP = kFpW + 8;
 constexpr int kBpP = kBpW + 4;
-size_t fp_smem(int rmax) { return sizeof(float) * ((kFpT + 4) * kFpP + kFpWarps * rmax); }
+size_t fp_smem(int rmax, bool tma) {
+  const size_t tile = ((kFpT + 4) * kFpP + 31) / 32 * 32;
+  return sizeof(float) * ((tma ? 2 : 1) * tile + kFpWarps * rmax) + 128;
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                   const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                   const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      p = nullptr;
+    return reinterpret_cast<EncodeTiledFn>(p);
+  }();
+  return fn;
+}
+
+// 3-D (N, N, batch) fp32 map with a (W+8) x (T+4) x 1 box for the strip sweep.
+bool make_tile_map(CUtensorMap* m, const float* img, int n, int batch) {
+  static const bool disabled = getenv("NCSG_NO_TMA") != nullptr;
+  EncodeTiledFn fn = encode_fn();
+  if (disabled || !fn || !img || (n % 4) != 0 || (reinterpret_cast<uintptr_t>(img) & 15)) return false;
+  cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n),
+                        static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 4,
+                           static_cast<cuuint64_t>(n) * n * 4};
+  cuuint32_t box[3] = {kFpW + 8, kFpT + 4, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(img), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 size_t bp_smem() {
   return sizeof(float) * kBpWarps * ((((kBpT + 5) * kBpP + 2) + 31) / 32 * 32);
 }
@@ -464,11 +592,21 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
   a.P0 = g.P0;
   a.nn = static_cast<size_t>(g.n) * g.n;
   a.m = static_cast<size_t>(g.n_angles) * g.n_det;
-  const size_t smem = fp_smem(a.rmax);
-  auto kern = fp_strip_kernel<kFpW, kFpT, kFpP, kFpWarps>;
-  set_smem(reinterpret_cast<const void*>(kern), smem);
+  CUtensorMap m0{}, m1{};
+  bool tma = make_tile_map(&m0, img, g.n, batch);
+  if (tma && chunks[1] > 0) tma = make_tile_map(&m1, imgT, g.n, batch);
+  if (chunks[1] == 0) m1 = m0;
+  const size_t smem = fp_smem(a.rmax, tma);
   dim3 grid(r.n_strips, chunks[0] + chunks[1], batch);
-  kern<<<grid, kFpWarps * 32, smem, s>>>(a);
+  if (tma) {
+    auto kern = fp_strip_kernel<kFpW, kFpT, kFpP, kFpWarps, true>;
+    set_smem(reinterpret_cast<const void*>(kern), smem);
+    kern<<<grid, kFpWarps * 32, smem, s>>>(a, m0, m1);
+  } else {
+    auto kern = fp_strip_kernel<kFpW, kFpT, kFpP, kFpWarps, false>;
+    set_smem(reinterpret_cast<const void*>(kern), smem);
+    kern<<<grid, kFpWarps * 32, smem, s>>>(a, m0, m1);
+  }
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

@@ -348,8 +348,9 @@ class Problem:
 
     def solve(self, max_iters: int, record_every: int | None = None, f_star=None,
               check_step_condition: bool = False) -> SolveResult:
-        record_every = record_every or max(1, max_iters)
-        max_rows = max_iters // record_every + 3
+        if record_every is None:
+            record_every = max(1, max_iters)
+        max_rows = max_iters // max(1, record_every) + 3
         rows = (RecordRow * (max_rows * self.batch))()
         nr = C.c_int()
         est = C.c_double()
