@@ -1,0 +1,135 @@
+// C++ API checks of ncstomo_gpu.hpp, restating reference doctest cases
+// (proj/tests/unit/test_ops.cpp, test_circulant.cpp, test_solvers.cpp) against
+// the GPU path.  Prints one line per case; exit code = number of failures.
+#include <cmath>
+#include <cstdio>
+#include <numeric>
+#include <random>
+#include <vector>
+
+#include "ncstomo_gpu.hpp"
+
+using namespace ncstomo_gpu;
+
+static int failures = 0;
+#define CHECK(cond, name)                                      \
+  do {                                                         \
+    bool ok_ = (cond);                                         \
+    std::printf("%s %s\n", ok_ ? "PASS" : "FAIL", name);       \
+    if (!ok_) ++failures;                                      \
+  } while (0)
+
+static std::vector<double> randn(std::size_t n, unsigned seed) {
+  std::mt19937_64 g(seed);
+  std::normal_distribution<double> d;
+  std::vector<double> v(n);
+  for (auto& x : v) x = d(g);
+  return v;
+}
+
+int main() {
+  // test_ops.cpp:16-24
+  CHECK(default_detector_count(64) == 93 && default_detector_count(512) == 727,
+        "default_detector_count");
+  // test_ops.cpp:26-30
+  bool threw = false;
+  try {
+    RadonMap bad(64, 60, 92);
+  } catch (const std::invalid_argument&) {
+    threw = true;
+  }
+  CHECK(threw, "RadonMap rejects even detector count");
+  // test_ops.cpp:32-35 (fp32 device arithmetic: 1e-5)
+  {
+    RadonMap r(64, 60, 93);
+    auto x = randn(r.domain_size(), 123), u = randn(r.range_size(), 124);
+    std::vector<double> ax(r.range_size()), atu(r.domain_size());
+    r.forward(x, ax);
+    r.adjoint(u, atu);
+    double l = std::inner_product(ax.begin(), ax.end(), u.begin(), 0.0);
+    double rr = std::inner_product(x.begin(), x.end(), atu.begin(), 0.0);
+    CHECK(std::abs(l - rr) / std::max(1.0, std::abs(l)) <= 1e-5, "Radon adjoint probe");
+  }
+  // test_ops.cpp:37-47
+  {
+    RadonMap r(64, 48, 93);
+    std::vector<double> x(r.domain_size(), 0.0), s(r.range_size());
+    x[32 * 64 + 32] = 1.0;
+    r.forward(x, s);
+    bool ok = true;
+    for (int t = 0; t < 48; ++t) {
+      double tot = 0;
+      for (int d = 0; d < 93; ++d) tot += s[t * 93 + d];
+      ok = ok && std::abs(tot - 1.0) <= 0.05;
+    }
+    CHECK(ok, "impulse projects to ~1 per angle");
+  }
+  // test_ops.cpp:60-79
+  {
+    GradMap gm(3);
+    std::vector<double> x = {1, 2, 4, 8, 16, 32, 64, 128, 256}, g(gm.range_size());
+    gm.forward(x, g);
+    CHECK(g[0] == -1 && g[1] == -2 && g[2] == -8 && g[5] == -128 && g[6] == -7 &&
+              g[11] == 32 - 256,
+          "gradient hand values");
+  }
+  // test_circulant.cpp:55-64: identity mask
+  {
+    int n = 16;
+    SpectralMask one(n);
+    for (auto& h : one.h) h = 1.0;
+    auto x = randn(n * n, 5);
+    std::vector<double> y(n * n);
+    MaskApplier(n).apply(one, x, y);
+    double e = 0;
+    for (int i = 0; i < n * n; ++i) e = std::max(e, std::abs(y[i] - x[i]));
+    CHECK(e < 1e-5, "identity mask");
+  }
+  // test_solvers.cpp:192-203 and 607-625 on a 32^2 CT problem
+  {
+    int n = 32, A = 24, D = default_detector_count(n);
+    RadonMap geom(n, A, D);
+    auto truth = randn(geom.domain_size(), 9);
+    for (auto& v : truth) v = std::max(0.0, v);
+    std::vector<double> sino(geom.range_size());
+    geom.forward(truth, sino);
+    ModelParams p;
+    p.alpha = p.beta = 0.1;
+    p.lambda = 0.01;
+    SplitProblem prob = assemble_problem(sino, geom, p);
+    SolverConfig cfg;
+    cfg.alpha = p.alpha;
+    cfg.gamma = 400.0;
+    cfg.mask = metric_mask(radon_mask(n, 100.0, 400.0), p);
+    SolverState s = make_state(prob);
+    ncs_step(s, prob, cfg);
+    bool ok = true;
+    for (double v : s.x) ok = ok && v == 0.0;
+    for (std::size_t i = 0; i < sino.size(); ++i)
+      ok = ok && std::abs(s.u[i] + p.alpha * sino[i] / (1 + p.alpha)) <=
+                     1e-6 * (1 + std::abs(sino[i]));
+    CHECK(ok, "first step KAT");
+    SolverState a = make_state(prob);
+    for (int k = 0; k < 5; ++k) ncs_step(a, prob, cfg);
+    cfg.max_iters = 5;
+    cfg.record_every = 5;
+    SolveResult r = ncs_solve(prob, cfg);
+    CHECK(r.state.x == a.x && r.state.u == a.u, "ncs_solve(5) == 5 x ncs_step (bitwise)");
+    CHECK(r.record.rows.size() == 2 && r.record.rows.back().iter == 5, "record rows");
+    // divergence (test_solvers.cpp:627-644)
+    SolverConfig bad;
+    bad.alpha = p.alpha;
+    bad.gamma = 1e-6;
+    bad.max_iters = 3000;
+    bad.record_every = 500;
+    bool div = false;
+    try {
+      pdhg_solve(prob, bad);
+    } catch (const DivergenceError& e) {
+      div = e.iter > 0;
+    }
+    CHECK(div, "DivergenceError with iteration");
+  }
+  std::printf("%d failure(s)\n", failures);
+  return failures;
+}
