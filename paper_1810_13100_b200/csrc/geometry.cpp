@@ -6,6 +6,7 @@
 // -ffp-contract=off so the fp64 expressions round like the reference's
 // (x86-64, no FMA) build.
 #include <cmath>
+#include <algorithm>
 #include <cstdlib>
 #include <numbers>
 
@@ -32,6 +33,54 @@ Interval axis_interval(double a, double b, double lo, double hi) {
 }
 
 long long q32(double v) { return std::llround(std::ldexp(v, 32)); }
+
+// Shared-memory cost model of the adjoint scatter for one angle: lanes take
+// rays `stride` apart, start y-aligned at a tile's top row and read-modify-
+// write the 4 pixels of their sample.  Cost = average wavefronts per access
+// (bank-conflict degree over the accumulator pitch) / fraction of useful
+// lanes.  The stride with the lowest cost is used by bp_tile_kernel.
+double scatter_cost(double aX, double aY, double bX, double bY, int stride, int W, int T,
+                    int pitch) {
+  const int rays = static_cast<int>(W * std::fabs(aX) + T * std::fabs(aY)) + 3;
+  const int groups = (rays + 32 * stride - 1) / (32 * stride);
+  const double util = static_cast<double>(rays) / (32.0 * stride * groups);
+  double tot = 0.0;
+  int cnt = 0;
+  for (int trial = 0; trial < 8; ++trial) {
+    const double x0 = 1.0 + 0.37 * trial, y0 = 2.0 + 0.11 * trial;
+    for (int ph = 0; ph < stride; ++ph) {
+      int nl = 0;
+      double px[32], py[32];
+      for (int l = 0; l < 32; ++l) {
+        const int s = ph + stride * l;
+        if (s >= rays) break;
+        double x = x0 + s * aX, y = y0 + s * aY;
+        const double k = std::ceil((y0 - y) / bY);
+        px[nl] = x + k * bX;
+        py[nl] = y + k * bY;
+        ++nl;
+      }
+      if (!nl) continue;
+      for (int step = 0; step < 3; ++step)
+        for (int corner = 0; corner < 4; ++corner) {
+          int bank_n[32] = {0};
+          long addr[32];
+          int worst = 0;
+          for (int l = 0; l < nl; ++l) {
+            const long cy = static_cast<long>(std::floor(py[l] + step * bY)) + (corner >> 1);
+            const long cx = static_cast<long>(std::floor(px[l] + step * bX)) + (corner & 1);
+            addr[l] = cy * pitch + cx;
+            bool dup = false;
+            for (int q = 0; q < l; ++q) dup = dup || addr[q] == addr[l];
+            if (!dup) worst = std::max(worst, ++bank_n[((addr[l] % 32) + 32) % 32]);
+          }
+          tot += worst;
+          ++cnt;
+        }
+    }
+  }
+  return (tot / std::max(1, cnt)) / util;
+}
 
 }  // namespace
 
@@ -121,6 +170,18 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     a.inv_adX16 =
         a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
     a.dXq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dX), -9)));
+    {
+      const double fax = std::ldexp(static_cast<double>(aX), -32);
+      const double fay = std::ldexp(static_cast<double>(aY), -32);
+      const double fbx = std::ldexp(static_cast<double>(a.dX), -32);
+      const double fby = std::ldexp(static_cast<double>(a.dY), -32);
+      double best = 1e300;
+      a.bp_stride = 5;
+      for (int st = 3; st <= 7; ++st) {
+        const double cst = scatter_cost(fax, fay, fbx, fby, st, kBpW, kBpT, kBpW + 4);
+        if (cst < best) best = cst, a.bp_stride = st;
+      }
+    }
     a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }

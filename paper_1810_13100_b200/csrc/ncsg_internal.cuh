@@ -48,6 +48,7 @@ struct AngleGeom {
   float inv_dY16;    // 65536 / dY  (step estimates on (diff >> 16))
   float inv_adX16;   // 65536 / |dX| (0 when dX == 0)
   int dXq, dYq;      // dX, dY rounded to Q9.23 (tile-local stepping)
+  int bp_stride;     // adjoint lane ray stride (>= 3), chosen per angle on the host
 };
 
 struct RayRange {  // valid tau interval [first, last] of one ray (empty: first > last)

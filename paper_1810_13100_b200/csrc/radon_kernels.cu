@@ -35,7 +35,6 @@ namespace ncsg {
 
 namespace {
 
-constexpr int kBpStride = 5;  // ray stride between lanes of one adjoint phase
 
 
 // Smallest q with base + q*step >= target (step > 0), exact; inv16 = 65536/step.
@@ -94,14 +93,18 @@ __device__ __forceinline__ LaneRun setup_run(const AngleGeom& g, long long P0, i
 
 // Conservative integer s-range of rays that can touch the real-coordinate box
 // [x0, x1] x [y0, y1] (kernel frame), clamped to the detector.
+// s_lo = -s_mid comes from the host: ptxas (CUDA 12.9, sm_100a) folds
+// max(max(-a, x), y) into one VIMNMX3 and drops the negation of a uniform `a`
+// (scripts/vimnmx3_probe.cu), so no bound is negated in device code.
 __device__ __forceinline__ void ray_range(const AngleGeom& g, float c, float x0, float x1,
-                                          float y0, float y1, int s_mid, int& lo, int& hi) {
+                                          float y0, float y1, int s_lo, int s_mid, float eps,
+                                          int& lo, int& hi) {
   float a = (x0 - c) * g.aXf, b = (x1 - c) * g.aXf;
   float e = (y0 - c) * g.aYf, f = (y1 - c) * g.aYf;
   float mn = fminf(a, b) + fminf(e, f);
   float mx = fmaxf(a, b) + fmaxf(e, f);
-  lo = max(-s_mid, static_cast<int>(floorf(mn)) - 1);
-  hi = min(s_mid, static_cast<int>(ceilf(mx)) + 1);
+  lo = max(s_lo, static_cast<int>(floorf(mn - eps)));
+  hi = min(s_mid, static_cast<int>(ceilf(mx + eps)));
 }
 
 // Tile-local Q9.23 positions: value * 2^-23 pixels relative to the staged
@@ -161,7 +164,7 @@ struct FpArgs {
   const RayRange* rays;
   const float* img[2];      // class 0: x, class 1: x^T
   float* part;
-  int n, det, s_mid, n_strips, rmax;
+  int n, det, s_mid, s_lo, n_strips, rmax;
   long long P0;
   size_t nn, m;
 };
@@ -267,7 +270,7 @@ __global__ void __launch_bounds__(NW * 32)
                                             : (static_cast<long long>(Y0 + T) << 32);
       const long long OY = static_cast<long long>(Y0 - 2) << 32;
       int tlo, thi;
-      ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
+      ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_lo, a.s_mid, 1.0f, tlo, thi);
       tlo = max(tlo, slo);
       thi = min(thi, shi);
       for (int sb = tlo; sb <= thi; sb += 32) {
@@ -329,7 +332,7 @@ struct BpArgs {
   const RayRange* rays;
   const float* u;    // [batch][u_stride], sinogram dual first
   float* out;        // [batch][n_parts][nn]; class 1 partials follow class 0's, transposed
-  int n, det, s_mid;
+  int n, det, s_mid, s_lo;
   long long P0;
   size_t nn, m, u_stride;
 };
@@ -366,12 +369,13 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
   for (int ai = a_begin + warp; ai < a_end; ai += NW) {
     const AngleGeom g = angs[ai];
     int tlo, thi;
-    ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_mid, tlo, thi);
+    ray_range(g, c, X0 - 1.f, X0 + W + 0.f, Y0 - 1.f, Y0 + T + 0.f, a.s_lo, a.s_mid, 0.01f, tlo, thi);
     const float* urow = ub + static_cast<size_t>(g.t) * a.det + a.s_mid;
     const RayRange* rays = a.rays + static_cast<size_t>(g.t) * a.det + a.s_mid;
     // Lanes of one phase take rays `stride` apart (>= 3 keeps the scatter
-    // race-free); 4 when the tile's rays fit in 128 lane slots, else 5.
-    const int stride = (thi - tlo + 1) <= 32 * 4 ? 4 : kBpStride;
+    // race-free); the stride per angle minimises the host's bank-conflict /
+    // idle-lane cost model (geometry.cpp scatter_cost).
+    const int stride = g.bp_stride;
     for (int sb = tlo; sb <= thi; sb += 32 * stride) {
       for (int ph = 0; ph < stride; ++ph) {
         const int s = sb + stride * lane + ph;
@@ -587,6 +591,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
   a.n = g.n;
   a.det = g.n_det;
   a.s_mid = g.s_mid;
+  a.s_lo = -g.s_mid;
   a.n_strips = r.n_strips;
   a.rmax = std::max(r.fp_rmax[0], r.fp_rmax[1]);
   a.P0 = g.P0;
@@ -638,6 +643,7 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
   a.n = n;
   a.det = g.n_det;
   a.s_mid = g.s_mid;
+  a.s_lo = -g.s_mid;
   a.P0 = g.P0;
   a.nn = static_cast<size_t>(n) * n;
   a.m = static_cast<size_t>(g.n_angles) * g.n_det;
