@@ -143,6 +143,18 @@ namespace {
 
 int* step_counter(ncsg_problem* p) { return p->flag.p; }
 
+// Second input of the forward: x^T for class-H angles, or the symmetry
+// planes in orbit mode.
+float* prepare_forward_aux(const RadonDev& r, const float* img, float* aux, int batch,
+                           cudaStream_t s) {
+  if (r.orbit_mode) {
+    launch_make_planes(img, aux, r.geo.n, batch, s);
+    return aux;
+  }
+  if (!r.geo.cls[1].empty()) launch_transpose(img, aux, r.geo.n, batch, s);
+  return aux;
+}
+
 AtuTerms atu_terms(ncsg_problem* p) {
   AtuTerms T;
   T.n = p->d.n;
@@ -203,14 +215,18 @@ void phase_b(ncsg_problem* p, const float* plain = nullptr) {
   XUpdate xu;
   xu.x = p->x.p;
   xu.x_old = p->x_old.p;
-  xu.xT = (p->d.kind == NCSG_CT && !p->radon->geo.cls[1].empty()) ? p->xT.p : nullptr;
+  xu.xT = (p->d.kind == NCSG_CT && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
+              ? p->xT.p
+              : nullptr;
   xu.subtract = 1;
   xu.flag = p->flag.p;
   mark(p);
   launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
   mark(p);
-  if (p->d.kind == NCSG_CT)
+  if (p->d.kind == NCSG_CT) {
+    if (p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
     launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
+  }
   mark(p);
   DualArgs a;
   a.kind = p->d.kind;
@@ -221,7 +237,7 @@ void phase_b(ncsg_problem* p, const float* plain = nullptr) {
   a.wd = p->wd;
   a.bound = p->bound;
   a.fp_part = p->fp_part.p;
-  a.n_strips = p->radon ? p->radon->n_strips : 0;
+  a.n_strips = p->radon ? p->radon->fp_slots() : 0;
   a.m = p->m0;
   a.m_begin = p->m_begin;
   a.m_end = p->m_end;
@@ -248,7 +264,7 @@ void do_step(ncsg_problem* p) {
 void engine_init(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   if (p->d.kind == NCSG_CT) {
-    if (!p->radon->geo.cls[1].empty()) launch_transpose(p->x.p, p->xT.p, p->d.n, p->batch, s);
+    prepare_forward_aux(*p->radon, p->x.p, p->xT.p, p->batch, s);
     launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
     launch_strip_sum(*p->radon, p->fp_part.p, p->axs.p, p->batch, s);
   }
@@ -322,7 +338,7 @@ void ensure_scratch(ncsg_problem* p) {
   p->du.alloc(us);
   p->adx.alloc(us);
   p->mdx.alloc(xs);
-  p->dxT.alloc(xs);
+  p->dxT.alloc(3 * xs);
 }
 
 // Stacked forward of an image into a range vector (StackedMap::forward,
@@ -330,13 +346,13 @@ void ensure_scratch(ncsg_problem* p) {
 void stacked_forward(ncsg_problem* p, const float* img, float* imgT, float* out) {
   cudaStream_t s = p->stream.s;
   if (p->d.kind == NCSG_CT) {
-    if (!p->radon->geo.cls[1].empty()) launch_transpose(img, imgT, p->d.n, p->batch, s);
+    prepare_forward_aux(*p->radon, img, imgT, p->batch, s);
     launch_radon_forward_partial(*p->radon, img, imgT, p->fp_part.p, p->batch, s);
   }
   StackArgs a;
   a.kind = p->d.kind;
   a.n = p->d.n;
-  a.n_strips = p->radon ? p->radon->n_strips : 0;
+  a.n_strips = p->radon ? p->radon->fp_slots() : 0;
   a.wd = p->wd;
   a.fp_part = p->fp_part.p;
   a.x = img;
@@ -480,11 +496,9 @@ ncsg_status ncsg_radon_forward(const ncsg_radon* r, const float* x, float* out, 
     const Geometry& g = r->dev.geo;
     size_t nn = static_cast<size_t>(g.n) * g.n, m = static_cast<size_t>(g.n_angles) * g.n_det;
     DevBuf<float> xT, part;
-    if (!g.cls[1].empty()) {
-      xT.alloc(nn * batch);
-      launch_transpose(x, xT.p, g.n, batch, s);
-    }
-    part.alloc(m * r->dev.n_strips * batch);
+    xT.alloc(3 * nn * batch);
+    prepare_forward_aux(r->dev, x, xT.p, batch, s);
+    part.alloc(m * r->dev.fp_slots() * batch);
     part.zero(s);
     launch_radon_forward_partial(r->dev, x, xT.p, part.p, batch, s);
     launch_strip_sum(r->dev, part.p, out, batch, s);
@@ -705,13 +719,13 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     size_t xs = p->nn * p->batch;
     p->x.alloc(xs);
     p->x_old.alloc(xs);
-    p->xT.alloc(xs);
+    p->xT.alloc(3 * xs);  // x^T, or the 3 symmetry planes in orbit mode
     p->u.alloc(p->range * p->batch);
     p->b.alloc(p->m0 * p->batch);
     upload_f64(p.get(), desc->b, p->b.p, p->m0 * p->batch);
     if (d.kind == NCSG_CT) {
       p->axs.alloc(p->m0 * p->batch);
-      p->fp_part.alloc(p->m0 * p->radon->n_strips * p->batch);
+      p->fp_part.alloc(p->m0 * p->radon->fp_slots() * p->batch);
       p->fp_part.zero(s);
       p->bp_part.alloc(p->nn * p->radon->n_partials() * p->batch);
       p->axs.zero(s);

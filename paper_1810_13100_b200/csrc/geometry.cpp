@@ -185,6 +185,20 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }
+  // Dihedral orbits (only for a full, unsharded angle set divisible by 4).
+  if (n_angles % 4 == 0 && angle_begin == 0 && angle_end == n_angles) {
+    const int q = n_angles / 4;
+    for (const AngleGeom& a : g.cls[0]) {
+      if (a.t > q) continue;  // reps: theta in [0, 45 deg]
+      OrbitGeom o{};
+      o.rep = a;
+      o.t[0] = a.t;
+      o.t[1] = a.t + 2 * q;
+      o.t[2] = (a.t == 0 || a.t == q) ? -1 : n_angles - a.t;
+      o.t[3] = (a.t == 0 || a.t == q) ? -1 : 2 * q - a.t;
+      g.orbits.push_back(o);
+    }
+  }
   return g;
 }
 

@@ -55,12 +55,26 @@ struct RayRange {  // valid tau interval [first, last] of one ray (empty: first 
   int first, last;
 };
 
+// Dihedral orbit of an angle theta in [0, 45 deg] (n_angles % 4 == 0): the
+// members theta, theta+90, 180-theta, 90-theta sample the image at the
+// images of theta's lattice under the grid symmetries, so R for all four is
+// theta's lattice walk over four transformed copies of x (planes):
+//   plane 0: x,  plane 1: x1[r][c] = x[N-1-c][r],  plane 2: x2[r][c] = x[r][N-1-c],
+//   plane 3: x3[r][c] = x[N-1-c][N-1-r].
+// Members 2 and 3 walk tau in the opposite direction (neg).  t[k] < 0: the
+// member coincides with another one (theta = 0 or 45 deg).
+struct OrbitGeom {
+  AngleGeom rep;  // theta's class-V geometry (kernel frame = image frame)
+  int t[4];
+};
+
 struct Geometry {
   int n = 0, n_angles = 0, n_det = 0;
   int s_mid = 0;
   long long P0 = 0;
   std::vector<AngleGeom> cls[2];   // class 0 = V, class 1 = H
   std::vector<RayRange> rays;      // [t][d]
+  std::vector<OrbitGeom> orbits;   // filled when every angle belongs to an orbit
   int64_t samples = 0;
 };
 
@@ -114,14 +128,26 @@ struct RadonDev {
   int bp_batch_planned = 0;
   DevBuf<int2> strip_range[2];                // [angle][strip] s-range (forward)
   std::vector<int2> strip_range_host[2];
+  // Orbit-mode forward (fp_orbit_kernel): strips x segments of rows; each
+  // ray's partial sums land in the slot of its monotone staircase path.
+  bool orbit_mode = false;
+  int n_segs = 1;
+  int orb_rmax = 0;
+  DevBuf<OrbitGeom> orbits;
+  DevBuf<int2> orb_range;                     // [orbit][strip][seg] s-range
   void upload();
   void plan_adjoint(int batch);
   int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }
+  // Forward partial slots per ray (fp_partial[batch][slots][m]).
+  int fp_slots() const { return orbit_mode ? n_strips + n_segs - 1 : n_strips; }
 };
+// Symmetry planes 1..3 of the orbit-mode forward, [batch][3][n][n].
+void launch_make_planes(const float* x, float* planes, int n, int batch, cudaStream_t s);
 
 // Projector launches.  img / imgT: batch images (stride n*n), imgT may be
 // null when class H is empty.  fp_partial: [batch][n_strips][m] (zeros where
 // a strip has no rays; written entries overwritten each call).
+// Orbit mode: imgT = the symmetry planes buffer [batch][3][n][n].
 void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
                                   float* fp_partial, int batch, cudaStream_t s);
 // Sums partial strips into out[batch][m] (stand-alone forward).

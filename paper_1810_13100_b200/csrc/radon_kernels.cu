@@ -53,6 +53,7 @@ __device__ __forceinline__ int first_ge(long long base, long long step, long lon
 struct LaneRun {
   long long X, Y;  // position at local step 0
   int jlo, jhi;    // active local steps [jlo, jhi)
+  int k0;          // global step index of local step 0 (tau = dir * (k0 + j))
 };
 
 // Samples of ray s with Y in [Ylo, Yhi), X in [Xlo, Xhi) and tau inside the
@@ -88,6 +89,7 @@ __device__ __forceinline__ LaneRun setup_run(const AngleGeom& g, long long P0, i
   }
   r.jlo = jlo;
   r.jhi = jhi;
+  r.k0 = k0;
   return r;
 }
 
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(NW * 32)
       for (int sb = tlo; sb <= thi; sb += 32) {
         const int s = sb + lane;
         const bool act = s <= thi;
-        LaneRun run{OX, OY, 0, 0};
+        LaneRun run{OX, OY, 0, 0, 0};
         if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
         const bool empty = run.jhi <= run.jlo;
         if (empty) run.jlo = run.jhi = 0;
@@ -321,6 +323,268 @@ __global__ void __launch_bounds__(NW * 32)
     float* out = a.part + (static_cast<size_t>(b) * a.n_strips + strip) * a.m +
                  static_cast<size_t>(g.t) * a.det + a.s_mid;
     for (int s = slo + lane; s <= shi; s += 32) out[s] = myacc[s - slo];
+  }
+}
+
+// ------------------------------------------------------------ orbit forward
+constexpr int kOrbW = 128;   // strip width
+constexpr int kOrbT = 16;    // tile-row height
+constexpr int kOrbSeg = 128; // rows per segment (one CTA sweeps one segment)
+constexpr int kOrbWarps = 4; // orbits per CTA (one per warp)
+constexpr int kOrbP = kOrbW + 8;
+
+struct OrbArgs {
+  const OrbitGeom* orb;
+  int n_orb;
+  int n_chunks;               // orbit chunks per batch problem
+  const int2* range;          // [orbit][strip][seg]
+  const RayRange* rays;
+  const float* img;           // plane 0 (x), [batch][n][n]
+  const float* planes;        // planes 1..3, [batch][3][n][n]
+  float* part;                // [batch][slots][m]
+  int n, det, s_mid, s_lo, n_strips, n_segs, slots, rmax;
+  long long P0;
+  size_t nn, m;
+};
+
+// Validity of member ray (t, s) in the representative's step index j, where
+// tau_rep = dir * (k0 + j) and members 2, 3 run tau the other way.
+__device__ __forceinline__ void member_range(const RayRange* rays, int det, int s_mid, int t,
+                                             int s, bool neg, int dir, int k0, int jlo0,
+                                             int jhi0, int& jlo, int& jhi) {
+  if (t < 0) {
+    jlo = jhi = 0;
+    return;
+  }
+  const RayRange rr = rays[static_cast<size_t>(t) * det + s + s_mid];
+  // valid tau_rep interval
+  const int f = neg ? -rr.last : rr.first;
+  const int l = neg ? -rr.first : rr.last;
+  int lo, hi;
+  if (dir > 0) {
+    lo = f - k0;
+    hi = l - k0 + 1;
+  } else {
+    lo = -l - k0;
+    hi = -f - k0 + 1;
+  }
+  jlo = max(jlo0, lo);
+  jhi = min(jhi0, hi);
+  if (jhi <= jlo) jlo = jhi = 0;
+}
+
+// R for the four members of an orbit in one lattice walk (see OrbitGeom).
+// CTA = (strip, segment, 4 orbits); the segment's 16-row tiles of all four
+// planes are staged (one TMA box of depth 1 for x, one of depth 3 for the
+// other planes); each warp integrates its orbit's rays and keeps per-member
+// per-ray sums in shared memory.  Each (ray, strip, segment) partial goes to
+// the slot of the ray's staircase path (strip index along the ray's x
+// direction + segment index), so a ray's slots never collide and a plain sum
+// over all slots is its projection -- deterministic, no atomics.
+size_t orbit_smem(int rmax) {
+  constexpr int D = (2 * kOrbP + 4 + 31) / 32 * 32;
+  constexpr int PLANE = (D + (kOrbT + 4) * kOrbP + 63) / 32 * 32;
+  return sizeof(float) * (4 * PLANE + kOrbWarps * 5 * rmax) + 128;
+}
+
+struct OrbMaps {
+  CUtensorMap m[4];  // plane k over (n, n, batch), box (W+8, T+4, 1)
+};
+
+template <bool USE_TMA>
+__global__ void __launch_bounds__(kOrbWarps * 32)
+    fp_orbit_kernel(OrbArgs a, const __grid_constant__ OrbMaps maps) {
+  constexpr int W = kOrbW, T = kOrbT, P = kOrbP, NW = kOrbWarps;
+  constexpr int ROWS = T + 4;
+  // Each plane: D floats of zeroed slack, then the (T+4) x P tile. TMA box
+  // starts must be >= 0 and 16-byte aligned and destinations 128-byte aligned
+  // (scripts/tma_probe.cu), so the left strip / first tile row load their box
+  // at image col / row 0 into the same place and the tile's linear base moves
+  // back by 4 cols / 2 rows instead. Cells left of / above the image then read
+  // slack zeros or (col -1 of the left strip) the previous row's last column,
+  // always with bilinear weight < 1e-8 (valid samples have px, py >= -eps).
+  constexpr int D = (2 * P + 4 + 31) / 32 * 32;
+  constexpr int PLANE = (D + ROWS * P + 63) / 32 * 32;
+  extern __shared__ __align__(128) float sm[];
+  __shared__ __align__(8) unsigned long long bar;
+  const unsigned sm_addr = static_cast<unsigned>(__cvta_generic_to_shared(sm));
+  const unsigned pad = ((sm_addr + 127u) & ~127u) - sm_addr;
+  float* tiles = sm + pad / 4;
+  float* racc = tiles + 4 * PLANE;
+  unsigned* rflag = reinterpret_cast<unsigned*>(racc + NW * 4 * a.rmax);
+  const int strip = blockIdx.x, seg = blockIdx.y;
+  const int b = blockIdx.z / a.n_chunks;
+  const int chunk = blockIdx.z - b * a.n_chunks;
+  const int X0 = strip * W;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int oi = chunk * NW + warp;
+  const bool has = oi < a.n_orb;
+  const int n = a.n;
+  const float c = 0.5f * (n - 1);
+  const int n_rows = (n + T - 1) / T;
+  const int r_begin = seg * (kOrbSeg / T);
+  const int r_end = min(n_rows, r_begin + kOrbSeg / T);
+  const float* img = a.img + static_cast<size_t>(b) * a.nn;
+  const float* pl = a.planes + static_cast<size_t>(b) * 3 * a.nn;
+  const unsigned barA = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
+  const unsigned tile0 = sm_addr + pad;
+  constexpr unsigned kBytes = ROWS * (W + 8) * 4;
+  if (USE_TMA) {
+    for (int i = threadIdx.x; i < 4 * PLANE; i += NW * 32) tiles[i] = 0.f;
+    if (threadIdx.x == 0) {
+      mbar_init(barA, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+  }
+  const long long Xlo = strip == 0 ? -(2LL << 32) : (static_cast<long long>(X0) << 32);
+  const long long Xhi = strip == a.n_strips - 1 ? (static_cast<long long>(n + 1) << 32)
+                                                 : (static_cast<long long>(X0 + W) << 32);
+  const long long OX = static_cast<long long>(X0 - 4) << 32;
+  OrbitGeom o{};
+  int slo = 0, shi = -1;
+  if (has) {
+    o = a.orb[oi];
+    const int2 sr = a.range[(static_cast<size_t>(oi) * a.n_strips + strip) * a.n_segs + seg];
+    slo = sr.x;
+    shi = sr.y;
+  }
+  const AngleGeom& g = o.rep;
+  float* myacc = racc + warp * 4 * a.rmax;
+  unsigned* myflag = rflag + warp * a.rmax;
+  for (int i = lane; i < 4 * a.rmax; i += 32) myacc[i] = 0.f;
+  for (int i = lane; i < a.rmax; i += 32) myflag[i] = 0u;
+  const unsigned mask = 0x7fffffu, one = 0x3f800000u;
+  unsigned phase = 0;
+
+  for (int r = r_begin; r < r_end; ++r) {
+    const int Y0 = r * T;
+    __syncthreads();  // previous tile fully consumed
+    if (USE_TMA) {
+      if (threadIdx.x == 0) {
+        // clamp the box start to >= 0 and shift the destination instead
+        const int dx = X0 >= 4 ? 0 : 4, dy = Y0 >= 2 ? 0 : 2;
+        const unsigned dst = tile0 + 4u * D;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(barA, 4 * kBytes);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          tma_load_3d(dst + 4u * k * PLANE, &maps.m[k], X0 - 4 + dx, Y0 - 2 + dy, b, barA);
+      }
+      mbar_wait(barA, phase);
+      phase ^= 1u;
+    } else {
+      for (int i = threadIdx.x; i < 4 * ROWS * (W + 8); i += NW * 32) {
+        const int k = i / (ROWS * (W + 8));
+        const int rem = i - k * ROWS * (W + 8);
+        const int ry = rem / (W + 8), rx = rem - ry * (W + 8);
+        const int gy = Y0 - 2 + ry, gx = X0 - 4 + rx;
+        const float* src = k == 0 ? img : pl + static_cast<size_t>(k - 1) * a.nn;
+        tiles[k * PLANE + D + ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
+                                             ? __ldg(src + static_cast<size_t>(gy) * n + gx)
+                                             : 0.f;
+      }
+      __syncthreads();
+    }
+    const int base = D - ((USE_TMA && X0 < 4) ? 4 : 0) - ((USE_TMA && Y0 < 2) ? 2 * P : 0);
+    if (has) {
+      const long long Ylo = r == 0 ? -(2LL << 32) : (static_cast<long long>(Y0) << 32);
+      const long long Yhi = r == n_rows - 1 ? (static_cast<long long>(n + 1) << 32)
+                                            : (static_cast<long long>(Y0 + T) << 32);
+      const long long OY = static_cast<long long>(Y0 - 2) << 32;
+      int tlo, thi;
+      ray_range(g, c, X0 - 1.f, X0 + W + 1.f, Y0 - 1.f, Y0 + T + 1.f, a.s_lo, a.s_mid, 1.0f,
+                tlo, thi);
+      tlo = max(tlo, slo);
+      thi = min(thi, shi);
+      for (int sb = tlo; sb <= thi; sb += 32) {
+        const int s = sb + lane;
+        const bool act = s <= thi;
+        // shared run: ownership of the rep's lattice (x strip, y tile row)
+        const RayRange all{-0x3fffffff, 0x3fffffff};
+        LaneRun run{OX, OY, 0, 0, 0};
+        if (act) run = setup_run(g, a.P0, s, all, Xlo, Xhi, Ylo, Yhi);
+        const int k0 = run.k0;
+        int jl[4], jh[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (act && run.jhi > run.jlo)
+            member_range(a.rays, a.det, a.s_mid, o.t[k], s, k >= 2, g.dir, k0, run.jlo, run.jhi,
+                         jl[k], jh[k]);
+          else
+            jl[k] = jh[k] = 0;
+        }
+        int lo_all = 0x7fffffff, hi_all = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (jh[k] > jl[k]) lo_all = min(lo_all, jl[k]), hi_all = max(hi_all, jh[k]);
+        const int J0 = __reduce_min_sync(0xffffffffu, static_cast<unsigned>(lo_all));
+        const int J1 = __reduce_max_sync(0xffffffffu, static_cast<unsigned>(hi_all));
+        if (J0 >= J1) continue;
+        int X = to_local_q23(run.X + static_cast<long long>(J0) * g.dX, OX);
+        int Y = to_local_q23(run.Y + static_cast<long long>(J0) * g.dY, OY);
+        const unsigned span_xy = static_cast<unsigned>(max(0, hi_all - lo_all));
+        const int lo_xy = lo_all;
+        unsigned sp[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) sp[k] = static_cast<unsigned>(jh[k] - jl[k]);
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll 2
+        for (int j = J0; j < J1; ++j) {
+          const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
+          const int idx = on ? base + (Y >> 23) * P + (X >> 23) : 0;
+          const unsigned ad = tile0 + 4u * static_cast<unsigned>(idx);
+          const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const unsigned ak = ad + 4u * k * PLANE;
+            const float v00 = lds(ak), v01 = lds(ak + 4);
+            const float v10 = lds(ak + 4 * P), v11 = lds(ak + 4 * P + 4);
+            const float v0 = fmaf(fx, v01 - v00, v00);
+            const float v1 = fmaf(fx, v11 - v10, v10);
+            const float v = fmaf(fy, v1 - v0, v0);
+            acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v : 0.f;
+          }
+          X += g.dXq;
+          Y += g.dYq;
+        }
+        if (act) {
+          unsigned fl = 0;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            myacc[k * a.rmax + (s - slo)] += acc[k];
+            fl |= (jh[k] > jl[k]) ? (1u << k) : 0u;
+          }
+          myflag[s - slo] |= fl;
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (has) {
+    const int slot = (g.dX >= 0 ? strip : a.n_strips - 1 - strip) + seg;
+    float* out = a.part + (static_cast<size_t>(b) * a.slots + slot) * a.m + a.s_mid;
+    for (int s = slo + lane; s <= shi; s += 32) {
+      const unsigned fl = myflag[s - slo];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((fl >> k) & 1u)
+          out[static_cast<size_t>(o.t[k]) * a.det + s] = myacc[k * a.rmax + (s - slo)];
+    }
+  }
+}
+
+__global__ void make_planes_kernel(const float* x, float* planes, int n) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  const int b = blockIdx.z;
+  const float* xb = x + b * nn;
+  float* p = planes + static_cast<size_t>(b) * 3 * nn;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nn;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int r = static_cast<int>(i / n), cc = static_cast<int>(i - static_cast<size_t>(r) * n);
+    p[i] = xb[static_cast<size_t>(n - 1 - cc) * n + r];                      // x1
+    p[nn + i] = xb[static_cast<size_t>(r) * n + (n - 1 - cc)];               // x2
+    p[2 * nn + i] = xb[static_cast<size_t>(n - 1 - cc) * n + (n - 1 - r)];   // x3
   }
 }
 
@@ -382,7 +646,7 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
         bool act = s <= thi;
         const float w = act ? __ldg(urow + s) : 0.f;
         act = act && (w != 0.f);  // the reference skips rays with w == 0 (radon.cpp:110)
-        LaneRun run{OX, OY, 0, 0};
+        LaneRun run{OX, OY, 0, 0, 0};
         if (act) run = setup_run(g, a.P0, s, rays[s], Xlo, Xhi, Ylo, Yhi);
         const bool empty = run.jhi <= run.jlo;
         if (empty) run.jlo = run.jhi = 0;
@@ -494,6 +758,40 @@ void RadonDev::upload() {
       NCSG_CUDA_CHECK(cudaMemcpy(strip_range[k].p, sr.data(), sr.size() * sizeof(int2),
                                  cudaMemcpyHostToDevice));
   }
+  // Orbit-mode forward: (strip, segment) ray ranges of every orbit's rep.
+  orbit_mode = false;
+  if (!geo.orbits.empty() && !getenv("NCSG_NO_ORBIT")) {
+    const int ns = (n + kOrbW - 1) / kOrbW;
+    n_segs = (n + kOrbSeg - 1) / kOrbSeg;
+    std::vector<int2> orr(geo.orbits.size() * ns * n_segs);
+    int rmax = 1;
+    for (size_t oi = 0; oi < geo.orbits.size(); ++oi) {
+      const AngleGeom& g = geo.orbits[oi].rep;
+      double ax = std::ldexp(static_cast<double>(g.aX), -32);
+      double ay = std::ldexp(static_cast<double>(g.aY), -32);
+      for (int st = 0; st < ns; ++st)
+        for (int sg = 0; sg < n_segs; ++sg) {
+          double x0 = st * kOrbW - 3.0, x1 = st * kOrbW + kOrbW + 3.0;
+          double y0 = sg * kOrbSeg - 3.0, y1 = sg * kOrbSeg + kOrbSeg + 3.0;
+          double p = (x0 - c) * ax, q = (x1 - c) * ax, e = (y0 - c) * ay, f = (y1 - c) * ay;
+          int lo = std::max(-geo.s_mid, static_cast<int>(std::floor(std::min(p, q) + std::min(e, f))) - 2);
+          int hi = std::min(geo.s_mid, static_cast<int>(std::ceil(std::max(p, q) + std::max(e, f))) + 2);
+          orr[(oi * ns + st) * n_segs + sg] = make_int2(lo, hi);
+          rmax = std::max(rmax, hi - lo + 1);
+        }
+    }
+    const size_t smem = orbit_smem(rmax);
+    if (ns == n_strips && smem <= 112 * 1024) {
+      orbit_mode = true;
+      orb_rmax = rmax;
+      orbits.alloc(geo.orbits.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(orbits.p, geo.orbits.data(),
+                                 geo.orbits.size() * sizeof(OrbitGeom), cudaMemcpyHostToDevice));
+      orb_range.alloc(orr.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(orb_range.p, orr.data(), orr.size() * sizeof(int2),
+                                 cudaMemcpyHostToDevice));
+    }
+  }
 }
 
 void RadonDev::plan_adjoint(int batch) {
@@ -547,16 +845,19 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 3-D (N, N, batch) fp32 map with a (W+8) x (T+4) x 1 box for the strip sweep.
-bool make_tile_map(CUtensorMap* m, const float* img, int n, int batch) {
+// 3-D (N, N, depth) fp32 map with a box_w x box_h x box_d box.
+bool make_tile_map(CUtensorMap* m, const float* img, int n, int batch, int box_w = kFpW + 8,
+                   int box_h = kFpT + 4, int box_d = 1, size_t batch_stride = 0) {
   static const bool disabled = getenv("NCSG_NO_TMA") != nullptr;
   EncodeTiledFn fn = encode_fn();
   if (disabled || !fn || !img || (n % 4) != 0 || (reinterpret_cast<uintptr_t>(img) & 15)) return false;
   cuuint64_t dims[3] = {static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n),
                         static_cast<cuuint64_t>(batch)};
   cuuint64_t strides[2] = {static_cast<cuuint64_t>(n) * 4,
-                           static_cast<cuuint64_t>(n) * n * 4};
-  cuuint32_t box[3] = {kFpW + 8, kFpT + 4, 1};
+                           static_cast<cuuint64_t>(batch_stride ? batch_stride
+                                                                : static_cast<size_t>(n) * n) * 4};
+  cuuint32_t box[3] = {static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h),
+                       static_cast<cuuint32_t>(box_d)};
   cuuint32_t estr[3] = {1, 1, 1};
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(img), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -574,6 +875,46 @@ void set_smem(const void* fn, size_t bytes) {
 void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
                                   float* fp_partial, int batch, cudaStream_t s) {
   const Geometry& g = r.geo;
+  if (r.orbit_mode) {
+    OrbArgs a;
+    a.orb = r.orbits.p;
+    a.n_orb = static_cast<int>(g.orbits.size());
+    a.n_chunks = (a.n_orb + kOrbWarps - 1) / kOrbWarps;
+    a.range = r.orb_range.p;
+    a.rays = r.rays.p;
+    a.img = img;
+    a.planes = imgT;
+    a.part = fp_partial;
+    a.n = g.n;
+    a.det = g.n_det;
+    a.s_mid = g.s_mid;
+    a.s_lo = -g.s_mid;
+    a.n_strips = r.n_strips;
+    a.n_segs = r.n_segs;
+    a.slots = r.fp_slots();
+    a.rmax = r.orb_rmax;
+    a.P0 = g.P0;
+    a.nn = static_cast<size_t>(g.n) * g.n;
+    a.m = static_cast<size_t>(g.n_angles) * g.n_det;
+    OrbMaps maps{};
+    const size_t nn = static_cast<size_t>(g.n) * g.n;
+    bool tma = make_tile_map(&maps.m[0], img, g.n, batch, kOrbW + 8, kOrbT + 4, 1);
+    for (int k = 1; k < 4 && tma; ++k)
+      tma = make_tile_map(&maps.m[k], imgT + (k - 1) * nn, g.n, batch, kOrbW + 8, kOrbT + 4, 1,
+                          3 * nn);
+    const size_t smem = orbit_smem(a.rmax);
+    dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
+    if (tma) {
+      set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<true>), smem);
+      fp_orbit_kernel<true><<<grid, kOrbWarps * 32, smem, s>>>(a, maps);
+    } else {
+      set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<false>), smem);
+      fp_orbit_kernel<false><<<grid, kOrbWarps * 32, smem, s>>>(a, maps);
+    }
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   FpArgs a;
   int chunks[2];
   for (int k = 0; k < 2; ++k) {
@@ -619,7 +960,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
 void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, int batch,
                       cudaStream_t s) {
   size_t m = static_cast<size_t>(r.geo.n_angles) * r.geo.n_det;
-  strip_sum_kernel<<<grid_for(m * batch, 256), 256, 0, s>>>(fp_partial, out, r.n_strips, m,
+  strip_sum_kernel<<<grid_for(m * batch, 256), 256, 0, s>>>(fp_partial, out, r.fp_slots(), m,
                                                           batch);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -653,6 +994,14 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
   set_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((n + kBpW - 1) / kBpW, (n + kBpT - 1) / kBpT, r.n_partials() * batch);
   kern<<<grid, kBpWarps * 32, smem, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_make_planes(const float* x, float* planes, int n, int batch, cudaStream_t s) {
+  const size_t nn = static_cast<size_t>(n) * n;
+  dim3 grid(grid_for(nn, 256), 1, batch);
+  make_planes_kernel<<<grid, 256, 0, s>>>(x, planes, n);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
