@@ -328,9 +328,18 @@ __global__ void __launch_bounds__(NW * 32)
 
 // ------------------------------------------------------------ orbit forward
 constexpr int kOrbW = 128;   // strip width
-constexpr int kOrbT = 16;    // tile-row height
-constexpr int kOrbSeg = 128; // rows per segment (one CTA sweeps one segment)
-constexpr int kOrbWarps = 4; // orbits per CTA (one per warp)
+#ifndef NCSG_ORB_T
+#define NCSG_ORB_T 16
+#endif
+#ifndef NCSG_ORB_SEG
+#define NCSG_ORB_SEG 64
+#endif
+#ifndef NCSG_ORB_WARPS
+#define NCSG_ORB_WARPS 8
+#endif
+constexpr int kOrbT = NCSG_ORB_T;          // tile-row height
+constexpr int kOrbSeg = NCSG_ORB_SEG;      // rows per segment (one CTA sweeps one segment)
+constexpr int kOrbWarps = NCSG_ORB_WARPS;  // orbits per CTA (one per warp)
 constexpr int kOrbP = kOrbW + 8;
 
 struct OrbArgs {

@@ -74,9 +74,12 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(_build.LIB):
-        _build.build()
-    L = C.CDLL(_build.LIB)
+    path = os.environ.get("NCSG_LIB")  # experiment builds (scripts/build_variant.py)
+    if not path:
+        path = _build.LIB
+        if not os.path.exists(path):
+            _build.build()
+    L = C.CDLL(path)
     L.ncsg_last_error.restype = C.c_char_p
     L.ncsg_version.restype = C.c_char_p
     for name in ("ncsg_radon_domain_size", "ncsg_radon_range_size", "ncsg_problem_domain_size",
