@@ -176,9 +176,11 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
       const double fbx = std::ldexp(static_cast<double>(a.dX), -32);
       const double fby = std::ldexp(static_cast<double>(a.dY), -32);
       double best = 1e300;
+      int bpW, bpT;
+      bp_tile_shape(n, bpW, bpT);
       a.bp_stride = 5;
       for (int st = 3; st <= 7; ++st) {
-        const double cst = scatter_cost(fax, fay, fbx, fby, st, kBpW, kBpT, kBpW + 4);
+        const double cst = scatter_cost(fax, fay, fbx, fby, st, bpW, bpT, bpW + 4);
         if (cst < best) best = cst, a.bp_stride = st;
       }
     }

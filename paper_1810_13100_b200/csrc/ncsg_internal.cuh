@@ -112,9 +112,27 @@ struct DevBuf {
 constexpr int kFpW = 128;    // forward strip width (pixels)
 constexpr int kFpT = 32;     // forward tile-row height
 constexpr int kFpWarps = 4;  // forward: warps per CTA = angles per CTA
-constexpr int kBpW = 128;    // adjoint tile width
-constexpr int kBpT = 28;     // adjoint tile height (3 CTAs/SM of 4 accumulators)
-constexpr int kBpWarps = 4;  // adjoint: warps per CTA (private accumulators)
+#ifndef NCSG_BP_WARPS
+#define NCSG_BP_WARPS 4
+#endif
+#ifndef NCSG_BP_WAVES
+#define NCSG_BP_WAVES 4
+#endif
+// Adjoint output tile (W x T): 172 x 20 where 172-wide tiles cover n with
+// <= 5% waste (n = 512: 3 tiles), else 128 x 28. Both keep 4 accumulators of
+// (T + 5) x (W + 4) floats under 75 KB so 3 CTAs fit per SM; the wider tile
+// packs more rays per lane group (sweep in profiles/r1_summary.md).
+inline void bp_tile_shape(int n, int& W, int& T) {
+  if ((n + 171) / 172 * 172 <= n + n / 20) {
+    W = 172;
+    T = 20;
+  } else {
+    W = 128;
+    T = 28;
+  }
+}
+constexpr int kBpWarps = NCSG_BP_WARPS;  // adjoint: warps per CTA (private accumulators)
+constexpr int kBpWaves = NCSG_BP_WAVES;  // adjoint: target CTAs = 148 * 3 * waves
 
 struct RadonDev {
   Geometry geo;

@@ -16,7 +16,7 @@
 //     radon.cpp:91-98) and accumulates per-ray sums in shared memory; the
 //     strip's partial ray sums go to part[strip][ray] and are summed in strip
 //     order by the consumer (deterministic, no atomics).
-// R^T (bp_tile_kernel):  CTA = (kBpW x kBpT output tile, chunk of angles).
+// R^T (bp_tile_kernel):  CTA = (W x T output tile, chunk of angles).
 //     Each warp owns a private shared-memory accumulator of the tile plus a
 //     one-pixel halo and scatters w * bilinear weights (radon.cpp:116-125)
 //     with plain read-modify-write; lanes take rays 5 apart in 5 phases, so
@@ -805,9 +805,11 @@ void RadonDev::upload() {
 
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
-  const int tiles = ((n + kBpW - 1) / kBpW) * ((n + kBpT - 1) / kBpT);
+  int bw, bt;
+  bp_tile_shape(n, bw, bt);
+  const int tiles = ((n + bw - 1) / bw) * ((n + bt - 1) / bt);
   // Aim for about four waves of 3 resident CTAs per SM over 148 SMs.
-  const long target = 148L * 3 * 4;
+  const long target = 148L * 3 * kBpWaves;
   const int na0 = static_cast<int>(geo.cls[0].size()), na1 = static_cast<int>(geo.cls[1].size());
   const int na = na0 + na1;
   long per = static_cast<long>(tiles) * batch;
@@ -830,7 +832,6 @@ void RadonDev::plan_adjoint(int batch) {
 
 namespace {
 constexpr int kFpP = kFpW + 8;
-constexpr int kBpP = kBpW + 4;
 size_t fp_smem(int rmax, bool tma) {
   const size_t tile = ((kFpT + 4) * kFpP + 31) / 32 * 32;
   return sizeof(float) * ((tma ? 2 : 1) * tile + kFpWarps * rmax) + 128;
@@ -872,8 +873,8 @@ bool make_tile_map(CUtensorMap* m, const float* img, int n, int batch, int box_w
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-size_t bp_smem() {
-  return sizeof(float) * kBpWarps * ((((kBpT + 5) * kBpP + 2) + 31) / 32 * 32);
+size_t bp_smem(int W, int T) {
+  return sizeof(float) * kBpWarps * ((((T + 5) * (W + 4) + 2) + 31) / 32 * 32);
 }
 void set_smem(const void* fn, size_t bytes) {
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -998,10 +999,13 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
   a.nn = static_cast<size_t>(n) * n;
   a.m = static_cast<size_t>(g.n_angles) * g.n_det;
   a.u_stride = u_stride ? u_stride : a.m;
-  const size_t smem = bp_smem();
-  auto kern = bp_tile_kernel<kBpW, kBpT, kBpP, kBpWarps>;
+  int W, T;
+  bp_tile_shape(n, W, T);
+  const size_t smem = bp_smem(W, T);
+  auto kern = W == 172 ? bp_tile_kernel<172, 20, 176, kBpWarps>
+                       : bp_tile_kernel<128, 28, 132, kBpWarps>;
   set_smem(reinterpret_cast<const void*>(kern), smem);
-  dim3 grid((n + kBpW - 1) / kBpW, (n + kBpT - 1) / kBpT, r.n_partials() * batch);
+  dim3 grid((n + W - 1) / W, (n + T - 1) / T, r.n_partials() * batch);
   kern<<<grid, kBpWarps * 32, smem, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();

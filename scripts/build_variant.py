@@ -14,11 +14,12 @@ os.makedirs(out, exist_ok=True)
 B.build()
 objs = []
 for src in B.CU_SRCS + B.CPP_SRCS:
-    o = os.path.join(B.OBJ, src + ".o")
-    if src == "radon_kernels.cu":
-        o = os.path.join(out, src + ".o")
-        subprocess.run([B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-                        *defs, "-c", os.path.join(B.CSRC, src), "-o", o], check=True)
+    o = os.path.join(out, src + ".o")
+    if src.endswith(".cu"):
+        cmd = [B.NVCC, *B.ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC"]
+    else:
+        cmd = ["g++", "-std=c++20", "-O2", "-fPIC", "-ffp-contract=off", f"-I{B.CUDA}/include"]
+    subprocess.run([*cmd, *defs, "-c", os.path.join(B.CSRC, src), "-o", o], check=True)
     objs.append(o)
 subprocess.run([B.NVCC, *B.ARCH, "-shared", "-o", os.path.join(out, "libncsg.so"), *objs,
                 "-cudart", "static"], check=True)
