@@ -329,7 +329,7 @@ __global__ void __launch_bounds__(NW * 32)
 // ------------------------------------------------------------ orbit forward
 constexpr int kOrbW = 128;   // strip width
 #ifndef NCSG_ORB_T
-#define NCSG_ORB_T 16
+#define NCSG_ORB_T 32
 #endif
 #ifndef NCSG_ORB_SEG
 #define NCSG_ORB_SEG 64
