@@ -178,11 +178,38 @@ typedef struct {
  * and at the end.  rows: capacity max_rows per problem, problem-major
  * (row r of problem q at rows[q*max_rows + r]); *n_rows = rows per problem.
  * f_star (nullable, one per problem) anchors rel_subopt as in the reference.
- * check_step_condition runs the 40-step power-method screen
- * (solvers.cpp:206-245) and writes its estimate into *screen_est (nullable). */
+ * check_step_condition runs the 40-step power-method screen with `seed`
+ * (SolverConfig::seed; solvers.cpp:206-245, 278) and writes its estimate into
+ * *screen_est (nullable; NaN when not run).  As in the reference a positive
+ * estimate is a warning for the caller, not an error. */
 ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
-                       int check_step_condition, const double* f_star, ncsg_record_row* rows,
-                       int max_rows, int* n_rows, double* screen_est);
+                       int check_step_condition, uint64_t seed, const double* f_star,
+                       ncsg_record_row* rows, int max_rows, int* n_rows, double* screen_est);
+
+/* ------------------------------------------------------------- setup path
+ * (the GPU versions of the reference's CPU setup.) */
+
+/* calibrate_scale(NormalMap(R), radon_mask(N, 1, 1), n_samples, seed)
+ * (circulant.cpp:142-169) -- the least-squares scale of the R^T R template
+ * that measurement_mask (pipeline.cpp:100-110) passes to radon_mask for
+ * parallel-beam geometry.  Probes are the reference's RngStream(seed, s)
+ * normals (circulant.cpp:89-94), drawn on the host bit-for-bit. */
+ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t seed,
+                                 double* scale);
+
+/* DC response of R^T R, <1, R^T R 1>/N^2: the dc value of radon_mask under the
+ * rule the configs pin. */
+ncsg_status ncsg_radon_dc_response(const ncsg_radon* r, double* dc);
+
+/* Engine::screen_step_condition (solvers.cpp:206-245): `iters` steps of
+ * power_method (solvers.cpp:466-484, start vector RngStream(seed, 0)) on
+ * alpha A^T A - M + shift I, shift = gamma + alpha max|h| (gamma without a
+ * mask).  *est = the estimated largest eigenvalue of alpha A^T A - M (the
+ * reference warns when est > 1e-8 max(1, shift)); *shift (nullable).  With
+ * gamma = 0 this is alpha * lambda_max(A^T A - C), the gamma rule of the
+ * configs.  Unsharded problems only. */
+ncsg_status ncsg_screen_step_condition(ncsg_problem* p, uint64_t seed, int iters, double* est,
+                                       double* shift);
 
 /* -------------------------------------------------------- multi-GPU phases
  * One NCS step split at its exchange points for angle-sharded execution

@@ -17,12 +17,14 @@
 // device failures (there is no CPU fallback).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
 #include <memory>
 #include <optional>
 #include <span>
+#include <sstream>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -86,6 +88,7 @@ class RadonMap final : public ProjectionMap {
   int n() const { return n_; }
   /// Valid bilinear samples per application (the reference's sum of R(1)).
   std::int64_t sample_count() const { return ncsg_radon_sample_count(h_.get()); }
+  const ncsg_radon* handle() const { return h_.get(); }
 
  private:
   int n_, n_angles_, n_det_;
@@ -198,6 +201,28 @@ struct ModelParams {
   bool positivity = false;
 };
 
+/// calibrate_scale(NormalMap(geometry), radon_mask(n, 1, 1), n_samples, seed)
+/// (circulant.cpp:142-169), computed on the GPU.
+inline double calibrate_scale(const RadonMap& geometry, int n_samples, std::uint64_t seed) {
+  double scale = 0.0;
+  detail::check(ncsg_calibrate_scale(geometry.handle(), n_samples, seed, &scale));
+  return scale;
+}
+
+/// <1, R^T R 1> / N^2, the dc value the configs pin for radon_mask.
+inline double dc_response(const RadonMap& geometry) {
+  double dc = 0.0;
+  detail::check(ncsg_radon_dc_response(geometry.handle(), &dc));
+  return dc;
+}
+
+/// measurement_mask for parallel-beam geometry (pipeline.cpp:100-110).
+inline SpectralMask measurement_mask(const RadonMap& geometry, double dc, int samples,
+                                     std::uint64_t seed) {
+  if (samples < 1) throw std::invalid_argument("mask estimation needs samples >= 1");
+  return radon_mask(geometry.n(), calibrate_scale(geometry, samples, seed), dc);
+}
+
 /// metric_mask (pipeline.cpp:112-118).
 inline SpectralMask metric_mask(const SpectralMask& measurement, const ModelParams& p) {
   double w = p.beta / p.alpha;
@@ -268,7 +293,9 @@ struct SolverConfig {
   int record_every = 1;
   double pinv_rel_tol = 1e-12;
   std::uint64_t seed = 0;
-  bool check_step_condition = false;
+  /// Power-method screen of M >= alpha A^T A at solve start (solvers.hpp:67-69);
+  /// a violation becomes a warning in the record, as in the reference.
+  bool check_step_condition = true;
   int device = 0;
 };
 
@@ -365,11 +392,25 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
   int nr = 0;
   double est = 0.0;
   ncsg_status st = ncsg_solve(eng.get(), cfg.max_iters, cfg.record_every,
-                              cfg.check_step_condition ? 1 : 0, f_star, rows.data(), max_rows,
-                              &nr, &est);
+                              cfg.check_step_condition ? 1 : 0, cfg.seed, f_star, rows.data(),
+                              max_rows, &nr, &est);
   if (st == NCSG_DIVERGED) throw_divergence();
   check(st);
   SolveResult res;
+  if (cfg.check_step_condition) {  // screen_step_condition (solvers.cpp:238-244)
+    double shift = cfg.gamma;
+    if (!pdhg && cfg.mask) {
+      double hmax = 0.0;
+      for (const auto& z : cfg.mask->h) hmax = std::max(hmax, std::abs(z));
+      shift = cfg.gamma + cfg.alpha * hmax;
+    }
+    if (est > 1e-8 * std::max(1.0, shift)) {
+      std::ostringstream os;
+      os << "step condition M >= alpha A^T A appears violated "
+            "(largest eigenvalue of alpha A^T A - M is about " << est << ")";
+      res.record.warnings.push_back(os.str());
+    }
+  }
   res.state = std::move(s);
   check(ncsg_get_state(eng.get(), res.state.x.data(), res.state.u.data(), nullptr));
   res.state.iter = 0;

@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "host_rng.hpp"
 #include "ncs_kernels.cuh"
 #include "ncsg_internal.cuh"
 
@@ -155,7 +156,11 @@ float* prepare_forward_aux(const RadonDev& r, const float* img, float* aux, int 
   return aux;
 }
 
-AtuTerms atu_terms(ncsg_problem* p) {
+AtuTerms atu_terms_for(ncsg_problem* p, float* u);
+AtuTerms atu_terms(ncsg_problem* p) { return atu_terms_for(p, p->u.p); }
+
+// Terms of A^T u for an arbitrary dual vector u laid out like the state's.
+AtuTerms atu_terms_for(ncsg_problem* p, float* u) {
   AtuTerms T;
   T.n = p->d.n;
   if (p->d.kind == NCSG_CT) {
@@ -163,14 +168,14 @@ AtuTerms atu_terms(ncsg_problem* p) {
     T.nV = p->radon->bp_chunks[0];
     T.nH = p->radon->bp_chunks[1];
     T.part_stride = static_cast<size_t>(p->radon->n_partials()) * p->nn;
-    if (p->rank0 && p->d.positivity) T.ident = p->u.p + p->m0 + p->g;
+    if (p->rank0 && p->d.positivity) T.ident = u + p->m0 + p->g;
   } else if (p->rank0) {
-    T.ident = p->u.p;
-    if (p->d.positivity) T.ident2 = p->u.p + p->m0 + p->g;
+    T.ident = u;
+    if (p->d.positivity) T.ident2 = u + p->m0 + p->g;
   }
   T.ident_stride = p->range;
   if (p->rank0) {
-    T.ug = p->u.p + p->m0;
+    T.ug = u + p->m0;
     T.ug_stride = p->range;
     T.wd = p->wd;
   }
@@ -329,6 +334,21 @@ std::vector<double> objective_values(ncsg_problem* p) {
   return f;
 }
 
+// Sum of per-block [a.b, c.d] partials of batch entry b (dot_pair_blocks per entry).
+std::vector<double> read_dot_pairs(double* dev, int batch, cudaStream_t s) {
+  const int nb = dot_pair_blocks();
+  std::vector<double> h(static_cast<size_t>(batch) * nb * 2);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), dev, h.size() * sizeof(double), cudaMemcpyDeviceToHost, s));
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<double> out(2 * static_cast<size_t>(batch), 0.0);
+  for (int b = 0; b < batch; ++b)
+    for (int k = 0; k < nb; ++k) {
+      out[2 * b] += h[(static_cast<size_t>(b) * nb + k) * 2];
+      out[2 * b + 1] += h[(static_cast<size_t>(b) * nb + k) * 2 + 1];
+    }
+  return out;
+}
+
 void ensure_scratch(ncsg_problem* p) {
   if (p->x_prev.n) return;
   size_t xs = p->nn * p->batch, us = p->range * p->batch;
@@ -425,6 +445,64 @@ std::vector<double> seminorm_values(ncsg_problem* p) {
     out[b] = std::sqrt(rad);
   }
   return out;
+}
+
+// Engine::screen_step_condition (solvers.cpp:206-245) in Mask / Scaled mode:
+// 40-step power_method (solvers.cpp:466-484) of alpha A^T A - M + shift I
+// with shift = gamma + alpha max|h| (gamma without a mask); returns the
+// estimate of the largest eigenvalue of alpha A^T A - M.  Runs on batch
+// entry 0 (the operator is shared by the batch).
+double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_out) {
+  cudaStream_t s = p->stream.s;
+  ensure_scratch(p);
+  struct BatchOne {
+    ncsg_problem* p;
+    int saved;
+    ~BatchOne() { p->batch = saved; }
+  } guard_batch{p, p->batch};
+  p->batch = 1;
+  double shift = p->d.gamma;
+  if (p->has_mask) {
+    double hmax = 0.0;
+    for (const auto& z : p->mask_full) hmax = std::max(hmax, std::abs(z));
+    shift = p->d.gamma + p->d.alpha * hmax;
+  }
+  if (shift_out) *shift_out = shift;
+  const size_t nn = p->nn;
+  std::vector<double> hv(nn);
+  HostRng rng(seed, 0);
+  double nv = 0.0;
+  for (auto& z : hv) z = rng.next_normal();
+  for (double z : hv) nv += z * z;
+  nv = std::sqrt(nv);
+  if (nv == 0.0) return -shift;
+  std::vector<float> hf(nn);
+  for (size_t i = 0; i < nn; ++i) hf[i] = static_cast<float>(hv[i] / nv);
+  float* v = p->dx.p;      // current vector
+  float* w = p->x_prev.p;  // operator output
+  float* atav = p->mdx.p;  // A^T A v
+  float* cv = p->has_mask ? ncsg_atu_buffer(p) : nullptr;  // C v
+  float* av = p->adx.p;    // A v (range)
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(v, hf.data(), nn * 4, cudaMemcpyHostToDevice, s));
+  DevBuf<double> red;
+  red.alloc(static_cast<size_t>(dot_pair_blocks()) * 2);
+  double lambda = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    stacked_forward(p, v, p->dxT.p, av);
+    if (p->d.kind == NCSG_CT)
+      launch_radon_adjoint_partial(*p->radon, av, p->range, p->bp_part.p, 1, s);
+    launch_atu_assemble(atu_terms_for(p, av), atav, 1, s);
+    if (cv) apply_filter(p, v, p->maskT_orig.p, cv);
+    launch_screen_combine(v, atav, cv, static_cast<float>(p->d.alpha),
+                          static_cast<float>(p->d.gamma), static_cast<float>(shift), w, nn, s);
+    launch_dot_pair(v, w, w, w, nn, 1, red.p, s);
+    auto d = read_dot_pairs(red.p, 1, s);
+    lambda = d[0];
+    const double nw = std::sqrt(d[1]);
+    if (nw == 0.0) return -shift;
+    launch_scale(w, static_cast<float>(1.0 / nw), v, nn, s);
+  }
+  return lambda - shift;
 }
 
 void upload_f64(ncsg_problem* p, const double* h, float* d, size_t count) {
@@ -898,8 +976,8 @@ ncsg_status ncsg_step_phase_b(ncsg_problem* p) {
 }
 
 ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
-                       int check_step_condition, const double* f_star, ncsg_record_row* rows,
-                       int max_rows, int* n_rows, double* screen_est) {
+                       int check_step_condition, uint64_t seed, const double* f_star,
+                       ncsg_record_row* rows, int max_rows, int* n_rows, double* screen_est) {
   return guard([&] {
     // solve_template (solvers.cpp:267-337)
     if (max_iters < 0) throw Error{NCSG_INVALID, "max_iters must be nonnegative"};
@@ -909,7 +987,13 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
     p->iter = 0;
     engine_init(p);
     reset_flag(p);
-    if (check_step_condition && screen_est) *screen_est = NAN;  // see ncsg_screen (Python/C++)
+    if (screen_est) *screen_est = NAN;
+    if (check_step_condition) {  // solvers.cpp:278 (warning, not an error)
+      if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
+        throw Error{NCSG_INVALID, "the step-condition screen needs the unsharded problem"};
+      double e = screen_estimate(p, seed, 40, nullptr);
+      if (screen_est) *screen_est = e;
+    }
     const int B = p->batch;
     std::vector<std::vector<ncsg_record_row>> rec(B);
     auto t0 = std::chrono::steady_clock::now();
@@ -953,6 +1037,128 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
       for (int i = 0; i < std::min(nr, max_rows); ++i) rows[static_cast<size_t>(b) * max_rows + i] = rec[b][i];
     }
     if (n_rows) *n_rows = std::min(nr, max_rows);
+  });
+}
+
+
+/* ---------------------------------------------------------------- setup path */
+
+ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t seed,
+                                 double* scale) {
+  return guard([&] {
+    // calibrate_scale(NormalMap(R), radon_mask(n, 1, 1), n_samples, seed)
+    // (circulant.cpp:142-169, called by measurement_mask, pipeline.cpp:100-110).
+    // With T = F^-1 diag(t) F (t = template, DC bin excluded; real and even),
+    //   num = sum_bins Re(conj(t Fv) F(R^T R v)) = N^2 <T v, R^T R v>,
+    //   den = sum_bins |t Fv|^2                  = N^2 <T v, T v>,
+    // so each probe needs R, R^T and one real filter pass.
+    if (!r || !scale) throw Error{NCSG_INVALID, "bad calibrate_scale arguments"};
+    if (n_samples < 1) throw Error{NCSG_INVALID, "n_samples must be positive"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    RadonDev& dev = const_cast<RadonDev&>(r->dev);
+    const Geometry& g = dev.geo;
+    const int n = g.n;
+    if (n & (n - 1)) throw Error{NCSG_INVALID, "GPU FFT sizes are powers of two"};
+    cudaStream_t s = r->stream.s;
+    const size_t nn = static_cast<size_t>(n) * n, m = static_cast<size_t>(g.n_angles) * g.n_det;
+    std::vector<std::complex<double>> t(nn);
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) {
+        const double mj = std::min(j, n - j), mk = std::min(k, n - k);
+        t[static_cast<size_t>(j) * n + k] = (j == 0 && k == 0) ? 0.0 : 1.0 / std::sqrt(mj * mj + mk * mk);
+      }
+    FftPlan f;
+    f.init(n, s);
+    auto hm = half_mask(n, t, 1.0 / static_cast<double>(nn));
+    DevBuf<float2> mT;
+    mT.alloc(hm.size());
+    NCSG_CUDA_CHECK(cudaMemcpy(mT.p, hm.data(), hm.size() * sizeof(float2), cudaMemcpyHostToDevice));
+    const int B = std::min(n_samples, 8);
+    dev.plan_adjoint(B);
+    DevBuf<float> v, av, y, aux, sino, fpart, bpart;
+    DevBuf<float2> spec;
+    DevBuf<double> red;
+    v.alloc(nn * B);
+    av.alloc(nn * B);
+    y.alloc(nn * B);
+    aux.alloc(3 * nn * B);
+    sino.alloc(m * B);
+    fpart.alloc(m * dev.fp_slots() * B);
+    fpart.zero(s);
+    bpart.alloc(nn * dev.n_partials() * B);
+    spec.alloc(static_cast<size_t>(n / 2 + 1) * n * B);
+    red.alloc(static_cast<size_t>(dot_pair_blocks()) * 2 * B);
+    std::vector<float> hv(nn * B);
+    double num = 0.0, den = 0.0;
+    for (int s0 = 0; s0 < n_samples; s0 += B) {
+      const int nb = std::min(B, n_samples - s0);
+      for (int b = 0; b < nb; ++b) {  // probe_image (circulant.cpp:89-94)
+        HostRng rng(seed, static_cast<uint64_t>(s0 + b));
+        for (size_t i = 0; i < nn; ++i) hv[b * nn + i] = static_cast<float>(rng.next_normal());
+      }
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(v.p, hv.data(), nb * nn * 4, cudaMemcpyHostToDevice, s));
+      prepare_forward_aux(dev, v.p, aux.p, nb, s);
+      launch_radon_forward_partial(dev, v.p, aux.p, fpart.p, nb, s);
+      launch_strip_sum(dev, fpart.p, sino.p, nb, s);
+      launch_radon_adjoint_partial(dev, sino.p, 0, bpart.p, nb, s);
+      launch_sum_partials(bpart.p, dev.bp_chunks[0], dev.bp_chunks[1], av.p, n, nb, s);
+      AtuTerms T;
+      T.n = n;
+      T.plain = v.p;
+      launch_fft_rows_r2c(f, T, spec.p, nb, s);
+      launch_fft_cols_filter(f, spec.p, mT.p, nb, s);
+      XUpdate xu;
+      xu.x = y.p;
+      xu.subtract = 0;
+      launch_fft_rows_c2r(f, spec.p, xu, nb, s);
+      launch_dot_pair(y.p, av.p, y.p, y.p, nn, nb, red.p, s);
+      auto sums = read_dot_pairs(red.p, nb, s);
+      for (int b = 0; b < nb; ++b) {
+        num += sums[2 * b];
+        den += sums[2 * b + 1];
+      }
+    }
+    if (den == 0.0) throw Error{NCSG_INVALID, "calibrate_scale: template response is zero"};
+    *scale = num / den;
+  });
+}
+
+ncsg_status ncsg_radon_dc_response(const ncsg_radon* r, double* dc) {
+  return guard([&] {
+    // <1, R^T R 1> / N^2 = ||R 1||^2 / N^2: the DC bin of radon_mask.
+    if (!r || !dc) throw Error{NCSG_INVALID, "bad dc_response arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(r->dev.device));
+    const RadonDev& dev = r->dev;
+    cudaStream_t s = r->stream.s;
+    const size_t nn = static_cast<size_t>(dev.geo.n) * dev.geo.n;
+    const size_t m = static_cast<size_t>(dev.geo.n_angles) * dev.geo.n_det;
+    DevBuf<float> one, aux, sino, fpart;
+    DevBuf<double> red;
+    one.alloc(nn);
+    std::vector<float> h(nn, 1.0f);
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(one.p, h.data(), nn * 4, cudaMemcpyHostToDevice, s));
+    aux.alloc(3 * nn);
+    sino.alloc(m);
+    fpart.alloc(m * dev.fp_slots());
+    fpart.zero(s);
+    red.alloc(static_cast<size_t>(dot_pair_blocks()) * 2);
+    prepare_forward_aux(dev, one.p, aux.p, 1, s);
+    launch_radon_forward_partial(dev, one.p, aux.p, fpart.p, 1, s);
+    launch_strip_sum(dev, fpart.p, sino.p, 1, s);
+    launch_dot_pair(sino.p, sino.p, sino.p, sino.p, m, 1, red.p, s);
+    *dc = read_dot_pairs(red.p, 1, s)[0] / static_cast<double>(nn);
+  });
+}
+
+ncsg_status ncsg_screen_step_condition(ncsg_problem* p, uint64_t seed, int iters, double* est,
+                                       double* shift_out) {
+  return guard([&] {
+    if (!p || !est) throw Error{NCSG_INVALID, "bad screen arguments"};
+    if (iters < 1) throw Error{NCSG_INVALID, "iters must be positive"};
+    if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
+      throw Error{NCSG_INVALID, "the step-condition screen needs the unsharded problem"};
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    *est = screen_estimate(p, seed, iters, shift_out);
   });
 }
 

@@ -408,6 +408,44 @@ namespace ncsg {
 namespace {
 // A^T u as one image: class-V partials + transposed class-H partials (through
 // a shared-memory tile) + identity blocks + w D^T u_g (linear_map.cpp:47-55).
+// Per-block partial sums [sum a*b, sum c*d] in fp64 for the setup path
+// (power_method dots, calibrate_scale sums); block partials are added on the
+// host in block order, so results are deterministic.
+__global__ void dot_pair_kernel(const float* a, const float* b, const float* c, const float* d,
+                                size_t count, double* out) {
+  __shared__ double sh[32];
+  const size_t off = static_cast<size_t>(blockIdx.y) * count;
+  double s0 = 0.0, s1 = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    s0 += static_cast<double>(a[off + i]) * b[off + i];
+    s1 += static_cast<double>(c[off + i]) * d[off + i];
+  }
+  double* o = out + (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 2;
+  const double t0 = block_sum(s0, sh);
+  if (threadIdx.x == 0) o[0] = t0;
+  const double t1 = block_sum(s1, sh);
+  if (threadIdx.x == 0) o[1] = t1;
+}
+
+// The shifted screen operator (solvers.cpp:228-237):
+//   w = alpha * A^T A v - M v + shift * v,  M v = gamma v + alpha * (C v).
+__global__ void screen_combine_kernel(const float* v, const float* atav, const float* cv,
+                                      float alpha, float gamma, float shift, float* w,
+                                      size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float mv = gamma * v[i] + (cv ? alpha * cv[i] : 0.f);
+    w[i] = alpha * atav[i] - mv + shift * v[i];
+  }
+}
+
+__global__ void scale_kernel(const float* in, float s, float* out, size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    out[i] = s * in[i];
+}
+
 __global__ void atu_assemble_kernel(AtuTerms T, float* out) {
   __shared__ float t[32][33];
   const int n = T.n;
@@ -437,4 +475,28 @@ void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t 
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
+int dot_pair_blocks() { return 148; }
+
+void launch_dot_pair(const float* a, const float* b, const float* c, const float* d, size_t count,
+                     int batch, double* out, cudaStream_t s) {
+  dim3 grid(dot_pair_blocks(), batch);
+  dot_pair_kernel<<<grid, 256, 0, s>>>(a, b, c, d, count, out);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_screen_combine(const float* v, const float* atav, const float* cv, float alpha,
+                           float gamma, float shift, float* w, size_t count, cudaStream_t s) {
+  screen_combine_kernel<<<grid_for(count, 256), 256, 0, s>>>(v, atav, cv, alpha, gamma, shift, w,
+                                                             count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_scale(const float* in, float sc, float* out, size_t count, cudaStream_t s) {
+  scale_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, sc, out, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
 }  // namespace ncsg

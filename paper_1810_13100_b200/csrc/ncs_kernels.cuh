@@ -70,4 +70,13 @@ void launch_sub(const float* a, const float* b, float* out, size_t count, cudaSt
 namespace ncsg {
 // out[batch][n*n] = A^T u assembled from `T` (sharded multi-GPU path).
 void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t s);
+
+// Setup path (calibrate_scale, power-method screen): out[batch][blocks][2] =
+// per-block [sum a*b, sum c*d] over `count` elements of each batch entry.
+int dot_pair_blocks();
+void launch_dot_pair(const float* a, const float* b, const float* c, const float* d, size_t count,
+                     int batch, double* out, cudaStream_t s);
+void launch_screen_combine(const float* v, const float* atav, const float* cv, float alpha,
+                           float gamma, float shift, float* w, size_t count, cudaStream_t s);
+void launch_scale(const float* in, float sc, float* out, size_t count, cudaStream_t s);
 }  // namespace ncsg

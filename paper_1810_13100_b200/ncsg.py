@@ -65,6 +65,7 @@ SYMBOLS = [
     "ncsg_step", "ncsg_step_graph", "ncsg_sync", "ncsg_objective", "ncsg_last_seminorm",
     "ncsg_solve", "ncsg_step_phase_a", "ncsg_atu_buffer", "ncsg_step_phase_b",
     "ncsg_profile_begin", "ncsg_profile_end", "ncsg_launch_count", "ncsg_set_atu_buffer",
+    "ncsg_calibrate_scale", "ncsg_radon_dc_response", "ncsg_screen_step_condition",
 ]
 PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
 
@@ -113,9 +114,13 @@ def lib():
     L.ncsg_sync.argtypes = [C.c_void_p, C.POINTER(C.c_int64)]
     L.ncsg_objective.argtypes = [C.c_void_p, _dp]
     L.ncsg_last_seminorm.argtypes = [C.c_void_p, _dp]
-    L.ncsg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+    L.ncsg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
                              C.POINTER(RecordRow), C.c_int, C.POINTER(C.c_int),
                              C.POINTER(C.c_double)]
+    L.ncsg_calibrate_scale.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
+    L.ncsg_radon_dc_response.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
+    L.ncsg_screen_step_condition.argtypes = [C.c_void_p, C.c_uint64, C.c_int,
+                                             C.POINTER(C.c_double), C.POINTER(C.c_double)]
     for name in ("ncsg_step_phase_a", "ncsg_step_phase_b", "ncsg_profile_begin"):
         getattr(L, name).argtypes = [C.c_void_p]
     L.ncsg_set_atu_buffer.argtypes = [C.c_void_p, C.c_void_p]
@@ -189,6 +194,30 @@ class RadonMap:
         _check(lib().ncsg_radon_adjoint_host(self._h, u.ravel(), out.ravel(), batch), "adjoint")
         return out.reshape(u.shape[:-2] + (self.n, self.n))
 
+    def calibrate_scale(self, n_samples: int = 8, seed: int = 0) -> float:
+        """calibrate_scale(NormalMap(R), radon_mask(n, 1, 1), n_samples, seed)
+        (circulant.cpp:142-169) on the GPU."""
+        out = C.c_double()
+        _check(lib().ncsg_calibrate_scale(self._h, n_samples, seed, C.byref(out)),
+               "calibrate_scale")
+        return out.value
+
+    def dc_response(self) -> float:
+        """<1, R^T R 1> / n^2 (the dc rule of the pinned configs)."""
+        out = C.c_double()
+        _check(lib().ncsg_radon_dc_response(self._h, C.byref(out)), "dc_response")
+        return out.value
+
+    def measurement_mask(self, samples: int = 8, seed: int = 0, dc: float | None = None):
+        """measurement_mask for parallel-beam geometry (pipeline.cpp:100-110):
+        radon_mask(n, calibrate_scale(...), dc) as an (n, n) complex array."""
+        from .instances import radon_mask
+
+        scale = self.calibrate_scale(samples, seed)
+        if dc is None:
+            dc = self.dc_response()
+        return radon_mask(self.n, scale, dc)
+
     def forward_device(self, x_ptr: int, out_ptr: int, batch: int = 1, stream=None):
         _check(lib().ncsg_radon_forward(self._h, x_ptr, out_ptr, batch, stream), "forward")
 
@@ -246,6 +275,7 @@ class SolveResult:
     u: np.ndarray
     rows: np.ndarray  # (batch, k, 5): iter, objective, rel_subopt, seminorm, wall_ms
     objective: np.ndarray
+    screen_est: float = float("nan")  # step-condition screen estimate (check_step_condition)
 
 
 class Problem:
@@ -349,8 +379,16 @@ class Problem:
         _check(lib().ncsg_objective(self._h, out), "objective")
         return out
 
+    def screen(self, seed: int = 0, iters: int = 40) -> tuple[float, float]:
+        """Engine::screen_step_condition (solvers.cpp:206-245): (estimate of the
+        largest eigenvalue of alpha A^T A - M, shift)."""
+        est, shift = C.c_double(), C.c_double()
+        _check(lib().ncsg_screen_step_condition(self._h, seed, iters, C.byref(est),
+                                                C.byref(shift)), "screen")
+        return est.value, shift.value
+
     def solve(self, max_iters: int, record_every: int | None = None, f_star=None,
-              check_step_condition: bool = False) -> SolveResult:
+              check_step_condition: bool = False, seed: int = 0) -> SolveResult:
         if record_every is None:
             record_every = max(1, max_iters)
         max_rows = max_iters // max(1, record_every) + 3
@@ -362,12 +400,12 @@ class Problem:
             fs = np.ascontiguousarray(np.broadcast_to(np.asarray(f_star, np.float64),
                                                       (self.batch,)))
         _check(lib().ncsg_solve(self._h, max_iters, record_every, int(check_step_condition),
-                                None if fs is None else fs.ctypes.data, rows, max_rows,
+                                seed, None if fs is None else fs.ctypes.data, rows, max_rows,
                                 C.byref(nr), C.byref(est)), "solve")
         arr = np.array([[r.iter, r.objective, r.rel_subopt, r.seminorm_step, r.wall_ms]
                         for r in rows]).reshape(self.batch, max_rows, 5)[:, : nr.value]
         x, u, _ = self.get_state()
-        return SolveResult(x, u, arr, arr[:, -1, 1].copy())
+        return SolveResult(x, u, arr, arr[:, -1, 1].copy(), est.value)
 
 
 def ct_problem(cfg, b, mask=None, batch=None, **kw) -> Problem:
