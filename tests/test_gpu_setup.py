@@ -126,3 +126,26 @@ def test_screen_gamma_rule(ncsg, port):
     est, _ = gpu_problem(ncsg, prob, 0.0, mask).screen(0, 40)
     want = port.screen(prob, 0.0, mask, iters=40)
     assert abs(est - want) <= 1e-5 * abs(want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c3", "c5", "c4", "c2"])
+def test_pinned_setup_values_full_size(ncsg, name):
+    # oracle/pin_configs.py computed dc, the mask scale and the gamma = 0
+    # screen estimate of every BASELINE config with the oracle (fp64, CPU);
+    # the GPU setup path reproduces them at full size.
+    from paper_1810_13100_b200 import configs, instances
+
+    cfg = configs.get(name)
+    if cfg.kind == "ct":
+        r = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det)
+        assert abs(r.dc_response() - cfg.dc) <= 1e-5 * cfg.dc
+        scale = r.calibrate_scale(cfg.pinned["mask_samples"], cfg.pinned["mask_seed"])
+        assert abs(scale - cfg.mask_scale) <= 1e-5 * cfg.mask_scale, (scale, cfg.mask_scale)
+        del r
+    mask = instances.metric_mask(cfg)
+    kind = ncsg.CT if cfg.kind == "ct" else ncsg.DENOISE
+    p = ncsg.Problem(kind, cfg.n, cfg.alpha, cfg.beta, cfg.lam, 0.0, np.zeros(cfg.m), mask=mask,
+                     n_angles=cfg.angles, n_det=cfg.det)
+    est, shift = p.screen(0, 40)
+    _check_screen(est, shift, cfg.pinned["screen_lmax"])
