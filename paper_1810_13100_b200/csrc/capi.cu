@@ -358,7 +358,7 @@ void ensure_scratch(ncsg_problem* p) {
   p->du.alloc(us);
   p->adx.alloc(us);
   p->mdx.alloc(xs);
-  p->dxT.alloc(3 * xs);
+  p->dxT.alloc(4 * xs);
 }
 
 // Stacked forward of an image into a range vector (StackedMap::forward,
@@ -574,7 +574,7 @@ ncsg_status ncsg_radon_forward(const ncsg_radon* r, const float* x, float* out, 
     const Geometry& g = r->dev.geo;
     size_t nn = static_cast<size_t>(g.n) * g.n, m = static_cast<size_t>(g.n_angles) * g.n_det;
     DevBuf<float> xT, part;
-    xT.alloc(3 * nn * batch);
+    xT.alloc(4 * nn * batch);
     prepare_forward_aux(r->dev, x, xT.p, batch, s);
     part.alloc(m * r->dev.fp_slots() * batch);
     part.zero(s);
@@ -797,7 +797,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     size_t xs = p->nn * p->batch;
     p->x.alloc(xs);
     p->x_old.alloc(xs);
-    p->xT.alloc(3 * xs);  // x^T, or the 3 symmetry planes in orbit mode
+    p->xT.alloc(4 * xs);  // x^T, or the interleaved orbit member images
     p->u.alloc(p->range * p->batch);
     p->b.alloc(p->m0 * p->batch);
     upload_f64(p.get(), desc->b, p->b.p, p->m0 * p->batch);
@@ -1081,7 +1081,7 @@ ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t se
     v.alloc(nn * B);
     av.alloc(nn * B);
     y.alloc(nn * B);
-    aux.alloc(3 * nn * B);
+    aux.alloc(4 * nn * B);
     sino.alloc(m * B);
     fpart.alloc(m * dev.fp_slots() * B);
     fpart.zero(s);
@@ -1137,7 +1137,7 @@ ncsg_status ncsg_radon_dc_response(const ncsg_radon* r, double* dc) {
     one.alloc(nn);
     std::vector<float> h(nn, 1.0f);
     NCSG_CUDA_CHECK(cudaMemcpyAsync(one.p, h.data(), nn * 4, cudaMemcpyHostToDevice, s));
-    aux.alloc(3 * nn);
+    aux.alloc(4 * nn);
     sino.alloc(m);
     fpart.alloc(m * dev.fp_slots());
     fpart.zero(s);

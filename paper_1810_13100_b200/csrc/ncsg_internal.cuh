@@ -159,7 +159,8 @@ struct RadonDev {
   // Forward partial slots per ray (fp_partial[batch][slots][m]).
   int fp_slots() const { return orbit_mode ? n_strips + n_segs - 1 : n_strips; }
 };
-// Symmetry planes 1..3 of the orbit-mode forward, [batch][3][n][n].
+// Orbit-mode forward input: the four dihedral member images interleaved per
+// pixel, [batch][n][n][4] floats (4*n*n per problem).
 void launch_make_planes(const float* x, float* planes, int n, int batch, cudaStream_t s);
 
 // Projector launches.  img / imgT: batch images (stride n*n), imgT may be

@@ -348,8 +348,7 @@ struct OrbArgs {
   int n_chunks;               // orbit chunks per batch problem
   const int2* range;          // [orbit][strip][seg]
   const RayRange* rays;
-  const float* img;           // plane 0 (x), [batch][n][n]
-  const float* planes;        // planes 1..3, [batch][3][n][n]
+  const float4* quad;         // [batch][n][n] (x, x1, x2, x3) per pixel (make_quad_kernel)
   float* part;                // [batch][slots][m]
   int n, det, s_mid, s_lo, n_strips, n_segs, slots, rmax;
   long long P0;
@@ -382,44 +381,61 @@ __device__ __forceinline__ void member_range(const RayRange* rays, int det, int 
   if (jhi <= jlo) jlo = jhi = 0;
 }
 
-// R for the four members of an orbit in one lattice walk (see OrbitGeom).
-// CTA = (strip, segment, 4 orbits); the segment's 16-row tiles of all four
-// planes are staged (one TMA box of depth 1 for x, one of depth 3 for the
-// other planes); each warp integrates its orbit's rays and keeps per-member
-// per-ray sums in shared memory.  Each (ray, strip, segment) partial goes to
-// the slot of the ray's staircase path (strip index along the ray's x
-// direction + segment index), so a ray's slots never collide and a plain sum
-// over all slots is its projection -- deterministic, no atomics.
-size_t orbit_smem(int rmax) {
-  constexpr int D = (2 * kOrbP + 4 + 31) / 32 * 32;
-  constexpr int PLANE = (D + (kOrbT + 4) * kOrbP + 63) / 32 * 32;
-  return sizeof(float) * (4 * PLANE + kOrbWarps * 5 * rmax) + 128;
+__device__ __forceinline__ float4 lds4(unsigned a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(a));
+  return v;
 }
 
-struct OrbMaps {
-  CUtensorMap m[4];  // plane k over (n, n, batch), box (W+8, T+4, 1)
-};
+__device__ __forceinline__ void tma_load_4d(unsigned dst, const CUtensorMap* map, int c0, int c1,
+                                            int c2, int c3, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+      "l"(reinterpret_cast<unsigned long long>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3),
+      "r"(bar)
+      : "memory");
+}
+
+// R for the four members of an orbit in one lattice walk (see OrbitGeom).
+// The four member images are interleaved per pixel (x, x1, x2, x3: one
+// 16-byte cell), so a sample's 2x2 neighbourhood for all four members is four
+// 128-bit shared loads; a quarter-warp of consecutive rays spans 8-12 cells,
+// which keeps the 128-bit accesses close to conflict-free.
+// CTA = (strip, segment, kOrbWarps orbits); the segment's tiles (cells of the
+// strip plus a 4-column / 2-row margin) arrive by one TMA box each; each warp
+// integrates its orbit's rays and keeps per-member per-ray sums in shared
+// memory.  Each (ray, strip, segment) partial goes to the slot of the ray's
+// staircase path (strip index along the ray's x direction + segment index),
+// so a ray's slots never collide and a plain sum over all slots is its
+// projection -- deterministic, no atomics.
+constexpr int kOrbD = (2 * kOrbP + 4 + 7) / 8 * 8;                        // slack cells
+constexpr int kOrbTile = (kOrbD + (kOrbT + 4) * kOrbP + 8 + 7) / 8 * 8;  // cells
+size_t orbit_smem(int rmax) {
+  return sizeof(float) * (4 * kOrbTile + kOrbWarps * 5 * rmax) + 128;
+}
 
 template <bool USE_TMA>
 __global__ void __launch_bounds__(kOrbWarps * 32)
-    fp_orbit_kernel(OrbArgs a, const __grid_constant__ OrbMaps maps) {
+    fp_orbit_kernel(OrbArgs a, const __grid_constant__ CUtensorMap map) {
   constexpr int W = kOrbW, T = kOrbT, P = kOrbP, NW = kOrbWarps;
   constexpr int ROWS = T + 4;
-  // Each plane: D floats of zeroed slack, then the (T+4) x P tile. TMA box
-  // starts must be >= 0 and 16-byte aligned and destinations 128-byte aligned
-  // (scripts/tma_probe.cu), so the left strip / first tile row load their box
-  // at image col / row 0 into the same place and the tile's linear base moves
-  // back by 4 cols / 2 rows instead. Cells left of / above the image then read
-  // slack zeros or (col -1 of the left strip) the previous row's last column,
-  // always with bilinear weight < 1e-8 (valid samples have px, py >= -eps).
-  constexpr int D = (2 * P + 4 + 31) / 32 * 32;
-  constexpr int PLANE = (D + ROWS * P + 63) / 32 * 32;
+  // D cells of zeroed slack, then the (T+4) x P tile of cells. TMA box starts
+  // must be >= 0 (scripts/tma_probe.cu), so the left strip / first tile row
+  // load their box at image col / row 0 into the same place and the tile's
+  // linear base moves back by 4 cols / 2 rows instead. Cells left of / above
+  // the image then read slack zeros or (col -1 of the left strip) the previous
+  // row's last cell, always with bilinear weight < 1e-8 (valid samples have
+  // px, py >= -eps).
+  constexpr int D = kOrbD;
   extern __shared__ __align__(128) float sm[];
   __shared__ __align__(8) unsigned long long bar;
   const unsigned sm_addr = static_cast<unsigned>(__cvta_generic_to_shared(sm));
   const unsigned pad = ((sm_addr + 127u) & ~127u) - sm_addr;
   float* tiles = sm + pad / 4;
-  float* racc = tiles + 4 * PLANE;
+  float* racc = tiles + 4 * kOrbTile;
   unsigned* rflag = reinterpret_cast<unsigned*>(racc + NW * 4 * a.rmax);
   const int strip = blockIdx.x, seg = blockIdx.y;
   const int b = blockIdx.z / a.n_chunks;
@@ -433,13 +449,12 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
   const int n_rows = (n + T - 1) / T;
   const int r_begin = seg * (kOrbSeg / T);
   const int r_end = min(n_rows, r_begin + kOrbSeg / T);
-  const float* img = a.img + static_cast<size_t>(b) * a.nn;
-  const float* pl = a.planes + static_cast<size_t>(b) * 3 * a.nn;
+  const float4* quad = a.quad + static_cast<size_t>(b) * a.nn;
   const unsigned barA = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
   const unsigned tile0 = sm_addr + pad;
-  constexpr unsigned kBytes = ROWS * (W + 8) * 4;
+  constexpr unsigned kBytes = ROWS * (W + 8) * 16;
   if (USE_TMA) {
-    for (int i = threadIdx.x; i < 4 * PLANE; i += NW * 32) tiles[i] = 0.f;
+    for (int i = threadIdx.x; i < 4 * kOrbTile; i += NW * 32) tiles[i] = 0.f;
     if (threadIdx.x == 0) {
       mbar_init(barA, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -471,27 +486,22 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
     __syncthreads();  // previous tile fully consumed
     if (USE_TMA) {
       if (threadIdx.x == 0) {
-        // clamp the box start to >= 0 and shift the destination instead
+        // clamp the box start to >= 0 and shift the tile's base instead
         const int dx = X0 >= 4 ? 0 : 4, dy = Y0 >= 2 ? 0 : 2;
-        const unsigned dst = tile0 + 4u * D;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_expect_tx(barA, 4 * kBytes);
-#pragma unroll
-        for (int k = 0; k < 4; ++k)
-          tma_load_3d(dst + 4u * k * PLANE, &maps.m[k], X0 - 4 + dx, Y0 - 2 + dy, b, barA);
+        mbar_expect_tx(barA, kBytes);
+        tma_load_4d(tile0 + 16u * D, &map, 0, X0 - 4 + dx, Y0 - 2 + dy, b, barA);
       }
       mbar_wait(barA, phase);
       phase ^= 1u;
     } else {
-      for (int i = threadIdx.x; i < 4 * ROWS * (W + 8); i += NW * 32) {
-        const int k = i / (ROWS * (W + 8));
-        const int rem = i - k * ROWS * (W + 8);
-        const int ry = rem / (W + 8), rx = rem - ry * (W + 8);
+      float4* t4 = reinterpret_cast<float4*>(tiles);
+      for (int i = threadIdx.x; i < ROWS * (W + 8); i += NW * 32) {
+        const int ry = i / (W + 8), rx = i - ry * (W + 8);
         const int gy = Y0 - 2 + ry, gx = X0 - 4 + rx;
-        const float* src = k == 0 ? img : pl + static_cast<size_t>(k - 1) * a.nn;
-        tiles[k * PLANE + D + ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
-                                             ? __ldg(src + static_cast<size_t>(gy) * n + gx)
-                                             : 0.f;
+        t4[D + ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
+                                  ? quad[static_cast<size_t>(gy) * n + gx]
+                                  : make_float4(0.f, 0.f, 0.f, 0.f);
       }
       __syncthreads();
     }
@@ -542,15 +552,18 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
         for (int j = J0; j < J1; ++j) {
           const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
           const int idx = on ? base + (Y >> 23) * P + (X >> 23) : 0;
-          const unsigned ad = tile0 + 4u * static_cast<unsigned>(idx);
+          const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
           const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+          const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
+          const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
+          const float v00[4] = {q00.x, q00.y, q00.z, q00.w};
+          const float v01[4] = {q01.x, q01.y, q01.z, q01.w};
+          const float v10[4] = {q10.x, q10.y, q10.z, q10.w};
+          const float v11[4] = {q11.x, q11.y, q11.z, q11.w};
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
-            const unsigned ak = ad + 4u * k * PLANE;
-            const float v00 = lds(ak), v01 = lds(ak + 4);
-            const float v10 = lds(ak + 4 * P), v11 = lds(ak + 4 * P + 4);
-            const float v0 = fmaf(fx, v01 - v00, v00);
-            const float v1 = fmaf(fx, v11 - v10, v10);
+            const float v0 = fmaf(fx, v01[k] - v00[k], v00[k]);
+            const float v1 = fmaf(fx, v11[k] - v10[k], v10[k]);
             const float v = fmaf(fy, v1 - v0, v0);
             acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v : 0.f;
           }
@@ -583,17 +596,37 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
   }
 }
 
-__global__ void make_planes_kernel(const float* x, float* planes, int n) {
+// The four dihedral member images interleaved per pixel:
+//   quad[r][c] = (x[r][c], x[N-1-c][r], x[r][N-1-c], x[N-1-c][N-1-r]).
+// 32 x 32 output blocks; the three transposed/flipped sources are staged
+// through shared memory so every global read and write is coalesced.
+__global__ void make_quad_kernel(const float* x, float4* quad, int n) {
+  __shared__ float t1[32][33], t3[32][33];
   const size_t nn = static_cast<size_t>(n) * n;
   const int b = blockIdx.z;
   const float* xb = x + b * nn;
-  float* p = planes + static_cast<size_t>(b) * 3 * nn;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < nn;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int r = static_cast<int>(i / n), cc = static_cast<int>(i - static_cast<size_t>(r) * n);
-    p[i] = xb[static_cast<size_t>(n - 1 - cc) * n + r];                      // x1
-    p[nn + i] = xb[static_cast<size_t>(r) * n + (n - 1 - cc)];               // x2
-    p[2 * nn + i] = xb[static_cast<size_t>(n - 1 - cc) * n + (n - 1 - r)];   // x3
+  float4* qb = quad + b * nn;
+  const int r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  // t1[cc][rr] = x[N-1-(c0+cc)][r0+rr]  (rows N-1-c0-31 .. N-1-c0 of x, cols r0..)
+  // t3[cc][rr] = x[N-1-(c0+cc)][N-1-(r0+rr)]
+  for (int k = ty; k < 32; k += 8) {
+    const int src_row = n - 1 - (c0 + k);
+    const bool ok = src_row >= 0 && r0 + tx < n;
+    t1[k][tx] = ok ? xb[static_cast<size_t>(src_row) * n + r0 + tx] : 0.f;
+    const int col3 = n - 1 - (r0 + tx);
+    t3[k][tx] = (src_row >= 0 && col3 >= 0) ? xb[static_cast<size_t>(src_row) * n + col3] : 0.f;
+  }
+  __syncthreads();
+  for (int k = ty; k < 32; k += 8) {
+    const int r = r0 + k, cc = c0 + tx;
+    if (r >= n || cc >= n) continue;
+    float4 q;
+    q.x = xb[static_cast<size_t>(r) * n + cc];
+    q.y = t1[tx][k];
+    q.z = xb[static_cast<size_t>(r) * n + (n - 1 - cc)];
+    q.w = t3[tx][k];
+    qb[static_cast<size_t>(r) * n + cc] = q;
   }
 }
 
@@ -873,6 +906,22 @@ bool make_tile_map(CUtensorMap* m, const float* img, int n, int batch, int box_w
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
+// (4, n, n, batch) float32 view of the interleaved member images, box
+// (4, box_w, box_h, 1): one TMA load brings a whole orbit tile.
+bool make_quad_map(CUtensorMap* m, const float* quad, int n, int batch, int box_w, int box_h) {
+  static const bool disabled = getenv("NCSG_NO_TMA") != nullptr;
+  EncodeTiledFn fn = encode_fn();
+  if (disabled || !fn || !quad || (reinterpret_cast<uintptr_t>(quad) & 15)) return false;
+  cuuint64_t dims[4] = {4, static_cast<cuuint64_t>(n), static_cast<cuuint64_t>(n),
+                        static_cast<cuuint64_t>(batch)};
+  cuuint64_t strides[3] = {16, static_cast<cuuint64_t>(n) * 16,
+                           static_cast<cuuint64_t>(n) * n * 16};
+  cuuint32_t box[4] = {4, static_cast<cuuint32_t>(box_w), static_cast<cuuint32_t>(box_h), 1};
+  cuuint32_t estr[4] = {1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(quad), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 size_t bp_smem(int W, int T) {
   return sizeof(float) * kBpWarps * ((((T + 5) * (W + 4) + 2) + 31) / 32 * 32);
 }
@@ -892,8 +941,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     a.n_chunks = (a.n_orb + kOrbWarps - 1) / kOrbWarps;
     a.range = r.orb_range.p;
     a.rays = r.rays.p;
-    a.img = img;
-    a.planes = imgT;
+    a.quad = reinterpret_cast<const float4*>(imgT);  // orbit mode: aux = make_quad output
     a.part = fp_partial;
     a.n = g.n;
     a.det = g.n_det;
@@ -906,20 +954,16 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     a.P0 = g.P0;
     a.nn = static_cast<size_t>(g.n) * g.n;
     a.m = static_cast<size_t>(g.n_angles) * g.n_det;
-    OrbMaps maps{};
-    const size_t nn = static_cast<size_t>(g.n) * g.n;
-    bool tma = make_tile_map(&maps.m[0], img, g.n, batch, kOrbW + 8, kOrbT + 4, 1);
-    for (int k = 1; k < 4 && tma; ++k)
-      tma = make_tile_map(&maps.m[k], imgT + (k - 1) * nn, g.n, batch, kOrbW + 8, kOrbT + 4, 1,
-                          3 * nn);
+    CUtensorMap map{};
+    const bool tma = make_quad_map(&map, imgT, g.n, batch, kOrbW + 8, kOrbT + 4);
     const size_t smem = orbit_smem(a.rmax);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     if (tma) {
       set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<true>), smem);
-      fp_orbit_kernel<true><<<grid, kOrbWarps * 32, smem, s>>>(a, maps);
+      fp_orbit_kernel<true><<<grid, kOrbWarps * 32, smem, s>>>(a, map);
     } else {
       set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<false>), smem);
-      fp_orbit_kernel<false><<<grid, kOrbWarps * 32, smem, s>>>(a, maps);
+      fp_orbit_kernel<false><<<grid, kOrbWarps * 32, smem, s>>>(a, map);
     }
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
@@ -1012,9 +1056,8 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
 }
 
 void launch_make_planes(const float* x, float* planes, int n, int batch, cudaStream_t s) {
-  const size_t nn = static_cast<size_t>(n) * n;
-  dim3 grid(grid_for(nn, 256), 1, batch);
-  make_planes_kernel<<<grid, 256, 0, s>>>(x, planes, n);
+  dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
+  make_quad_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<float4*>(planes), n);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
