@@ -355,16 +355,23 @@ struct OrbArgs {
   size_t nn, m;
 };
 
+// Valid tau interval of member ray (t, s) (an empty range for absent members
+// t < 0 or lanes past the group end); loaded one group ahead of its use.
+__device__ __forceinline__ RayRange member_rays(const RayRange* rays, int det, int s_mid, int t,
+                                                int s, bool ok) {
+  if (t < 0 || !ok) return RayRange{1, 0};
+  const int2 v = __ldg(reinterpret_cast<const int2*>(rays) + static_cast<size_t>(t) * det + s + s_mid);
+  return RayRange{v.x, v.y};
+}
+
 // Validity of member ray (t, s) in the representative's step index j, where
 // tau_rep = dir * (k0 + j) and members 2, 3 run tau the other way.
-__device__ __forceinline__ void member_range(const RayRange* rays, int det, int s_mid, int t,
-                                             int s, bool neg, int dir, int k0, int jlo0,
-                                             int jhi0, int& jlo, int& jhi) {
+__device__ __forceinline__ void member_range(RayRange rr, int t, bool neg, int dir, int k0,
+                                             int jlo0, int jhi0, int& jlo, int& jhi) {
   if (t < 0) {
     jlo = jhi = 0;
     return;
   }
-  const RayRange rr = rays[static_cast<size_t>(t) * det + s + s_mid];
   // valid tau_rep interval
   const int f = neg ? -rr.last : rr.first;
   const int l = neg ? -rr.first : rr.last;
@@ -516,9 +523,19 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
                 tlo, thi);
       tlo = max(tlo, slo);
       thi = min(thi, shi);
+      RayRange nxt[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], tlo + lane, tlo + lane <= thi);
       for (int sb = tlo; sb <= thi; sb += 32) {
         const int s = sb + lane;
         const bool act = s <= thi;
+        RayRange cur[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {  // prefetch the next group's ray ranges
+          cur[k] = nxt[k];
+          nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], s + 32, s + 32 <= thi);
+        }
         // shared run: ownership of the rep's lattice (x strip, y tile row)
         const RayRange all{-0x3fffffff, 0x3fffffff};
         LaneRun run{OX, OY, 0, 0, 0};
@@ -528,8 +545,7 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           if (act && run.jhi > run.jlo)
-            member_range(a.rays, a.det, a.s_mid, o.t[k], s, k >= 2, g.dir, k0, run.jlo, run.jhi,
-                         jl[k], jh[k]);
+            member_range(cur[k], o.t[k], k >= 2, g.dir, k0, run.jlo, run.jhi, jl[k], jh[k]);
           else
             jl[k] = jh[k] = 0;
         }
