@@ -281,24 +281,28 @@ def bench_single(args, cfg):
 
 
 def e2e_rate(cfg, b, mask, steps):
-    """Public API end to end: host b + mask -> problem (H2D), K steps, objective
-    and x/u back to host (D2H)."""
+    """Public API end to end, the call a user makes for this config: host b +
+    mask -> ncsg.Problem (geometry replay, pinv filter, H2D uploads), one
+    ncs_solve of the config's iteration count (record_every = max_iters, the
+    reference's bench protocol), objective + x/u back to host
+    (D2H).  Wall clock around all of it."""
     from paper_1810_13100_b200 import ncsg
 
+    iters = cfg.iters
     t = time.perf_counter()
     prob = ncsg.ct_problem(cfg, b, mask=mask)
     prob.set_state()
-    prob.step(steps, graph=False)
-    f = prob.objective()
-    x, u, _ = prob.get_state()
+    res = prob.solve(iters, record_every=iters)
     dt = time.perf_counter() - t
-    h2d = 4 * b.size + 2 * 8 * cfg.n * (cfg.n // 2 + 1)
-    d2h = 8 * cfg.batch + 4 * (x.size + u.size)
-    assert np.all(np.isfinite(f))
-    return {"value": steps / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / steps,
-            "d2h_bytes_per_step": d2h / steps,
-            "note": "ncsg.Problem create (geometry replay, mask pinv, uploads) + set_state + "
-                    f"{steps} steps + objective + get_state, wall clock"}
+    nk = cfg.n // 2 + 1
+    m = cfg.angles * cfg.det
+    h2d = 4 * b.size + 2 * 8 * nk * cfg.n + 8 * m  # b, two half-spectrum filters, ray table
+    d2h = 4 * (res.x.size + res.u.size) + res.rows.size * 8
+    assert np.all(np.isfinite(res.objective))
+    return {"value": iters / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / iters,
+            "d2h_bytes_per_step": d2h / iters, "iters": iters, "seconds": dt,
+            "note": f"ncsg.Problem create + set_state + solve({iters}) + state/records download, "
+                    "wall clock"}
 
 
 if __name__ == "__main__":

@@ -9,6 +9,8 @@
 #include <algorithm>
 #include <cstdlib>
 #include <numbers>
+#include <thread>
+#include <vector>
 
 #include "ncsg_internal.cuh"
 
@@ -66,13 +68,12 @@ double scatter_cost(double aX, double aY, double bX, double bY, int stride, int 
           int bank_n[32] = {0};
           long addr[32];
           int worst = 0;
+          // lanes' footprints are disjoint (stride >= 3), so addresses are distinct
           for (int l = 0; l < nl; ++l) {
             const long cy = static_cast<long>(std::floor(py[l] + step * bY)) + (corner >> 1);
             const long cx = static_cast<long>(std::floor(px[l] + step * bX)) + (corner & 1);
             addr[l] = cy * pitch + cx;
-            bool dup = false;
-            for (int q = 0; q < l; ++q) dup = dup || addr[q] == addr[l];
-            if (!dup) worst = std::max(worst, ++bank_n[((addr[l] % 32) + 32) % 32]);
+            worst = std::max(worst, ++bank_n[((addr[l] % 32) + 32) % 32]);
           }
           tot += worst;
           ++cnt;
@@ -80,6 +81,39 @@ double scatter_cost(double aX, double aY, double bX, double bY, int stride, int 
     }
   }
   return (tot / std::max(1, cnt)) / util;
+}
+
+// Adjoint lane stride of every angle: the stride in 3..7 with the lowest
+// scatter_cost, evaluated on all host cores (the model is ~1 ms per angle).
+void choose_strides(Geometry& g) {
+  int bpW, bpT;
+  bp_tile_shape(g.n, bpW, bpT);
+  std::vector<AngleGeom*> all;
+  for (auto& cls : g.cls)
+    for (auto& a : cls) all.push_back(&a);
+  auto work = [&](size_t i0, size_t i1) {
+    for (size_t i = i0; i < i1; ++i) {
+      AngleGeom& a = *all[i];
+      const double fax = std::ldexp(static_cast<double>(a.aX), -32);
+      const double fay = std::ldexp(static_cast<double>(a.aY), -32);
+      const double fbx = std::ldexp(static_cast<double>(a.dX), -32);
+      const double fby = std::ldexp(static_cast<double>(a.dY), -32);
+      double best = 1e300;
+      a.bp_stride = 5;
+      for (int st = 3; st <= 7; ++st) {
+        const double cst = scatter_cost(fax, fay, fbx, fby, st, bpW, bpT, bpW + 4);
+        if (cst < best) best = cst, a.bp_stride = st;
+      }
+    }
+  };
+  const size_t nt = std::max<size_t>(1, std::min<size_t>(16, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  const size_t per = (all.size() + nt - 1) / nt;
+  for (size_t t = 0; t < nt; ++t) {
+    const size_t i0 = t * per, i1 = std::min(all.size(), i0 + per);
+    if (i0 < i1) th.emplace_back(work, i0, i1);
+  }
+  for (auto& t : th) t.join();
 }
 
 }  // namespace
@@ -170,23 +204,11 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     a.inv_adX16 =
         a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
     a.dXq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dX), -9)));
-    {
-      const double fax = std::ldexp(static_cast<double>(aX), -32);
-      const double fay = std::ldexp(static_cast<double>(aY), -32);
-      const double fbx = std::ldexp(static_cast<double>(a.dX), -32);
-      const double fby = std::ldexp(static_cast<double>(a.dY), -32);
-      double best = 1e300;
-      int bpW, bpT;
-      bp_tile_shape(n, bpW, bpT);
-      a.bp_stride = 5;
-      for (int st = 3; st <= 7; ++st) {
-        const double cst = scatter_cost(fax, fay, fbx, fby, st, bpW, bpT, bpW + 4);
-        if (cst < best) best = cst, a.bp_stride = st;
-      }
-    }
+    a.bp_stride = 5;  // chosen below (choose_strides)
     a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }
+  choose_strides(g);
   // Dihedral orbits (only for a full, unsharded angle set divisible by 4).
   if (n_angles % 4 == 0 && angle_begin == 0 && angle_end == n_angles) {
     const int q = n_angles / 4;
