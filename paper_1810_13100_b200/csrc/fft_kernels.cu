@@ -28,7 +28,10 @@ namespace ncsg {
 
 namespace {
 
-constexpr int kRowsPerBlock = 8;  // rows per row-pass CTA (4 packed pairs)
+#ifndef NCSG_FFT_ROWS
+#define NCSG_FFT_ROWS 4
+#endif
+constexpr int kRowsPerBlock = NCSG_FFT_ROWS;  // rows per row-pass CTA (packed pairs)
 
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
   return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
