@@ -259,9 +259,16 @@ def bench_single(args, cfg):
                   "peak_tbs": smem_peak, "frac": 16 * S / (dom_ms * 1e-3) / 1e12 / smem_peak,
                   "note": "bilinear gathers (4 fp32 texels per sample) against shared-memory "
                           "bandwidth 148 SM x 128 B/clk at the sampled SM clock"}
+    traffic = None
+    try:  # DRAM bytes per launch of the same kernel from the committed ncu capture
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh)["dram_bytes_per_launch"].get(dom)
+    except (OSError, ValueError, KeyError):
+        pass
     roofline = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
                 "peak_kind": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-                "traffic": None, "algorithmic_bytes_per_launch": nb[dom],
+                "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
+                "algorithmic_bytes_per_launch": nb[dom],
                 "launch_ms": dom_ms, "gather_roofline": gather}
 
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1,
