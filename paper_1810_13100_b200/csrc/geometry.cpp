@@ -86,8 +86,8 @@ double scatter_cost(double aX, double aY, double bX, double bY, int stride, int 
 // Adjoint lane stride of every angle: the stride in 3..7 with the lowest
 // scatter_cost, evaluated on all host cores (the model is ~1 ms per angle).
 void choose_strides(Geometry& g) {
-  int bpW, bpT;
-  bp_tile_shape(g.n, bpW, bpT);
+  int bpW, bpT, bpP;
+  bp_tile_shape(g.n, bpW, bpT, bpP);
   std::vector<AngleGeom*> all;
   for (auto& cls : g.cls)
     for (auto& a : cls) all.push_back(&a);
@@ -101,7 +101,7 @@ void choose_strides(Geometry& g) {
       double best = 1e300;
       a.bp_stride = 5;
       for (int st = 3; st <= 7; ++st) {
-        const double cst = scatter_cost(fax, fay, fbx, fby, st, bpW, bpT, bpW + 4);
+        const double cst = scatter_cost(fax, fay, fbx, fby, st, bpW, bpT, bpP);
         if (cst < best) best = cst, a.bp_stride = st;
       }
     }

@@ -122,13 +122,22 @@ constexpr int kFpWarps = 4;  // forward: warps per CTA = angles per CTA
 // <= 5% waste (n = 512: 3 tiles), else 128 x 28. Both keep 4 accumulators of
 // (T + 5) x (W + 4) floats under 75 KB so 3 CTAs fit per SM; the wider tile
 // packs more rays per lane group (sweep in profiles/r1_summary.md).
-inline void bp_tile_shape(int n, int& W, int& T) {
+#ifndef NCSG_BP_WIDE_T
+#define NCSG_BP_WIDE_T 20
+#endif
+#ifndef NCSG_BP_WIDE_P
+#define NCSG_BP_WIDE_P 176
+#endif
+constexpr int kBpWideT = NCSG_BP_WIDE_T, kBpWideP = NCSG_BP_WIDE_P;
+inline void bp_tile_shape(int n, int& W, int& T, int& P) {
   if ((n + 171) / 172 * 172 <= n + n / 20) {
     W = 172;
-    T = 20;
+    T = kBpWideT;
+    P = kBpWideP;
   } else {
     W = 128;
     T = 28;
+    P = 132;
   }
 }
 constexpr int kBpWarps = NCSG_BP_WARPS;  // adjoint: warps per CTA (private accumulators)

@@ -854,8 +854,8 @@ void RadonDev::upload() {
 
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
-  int bw, bt;
-  bp_tile_shape(n, bw, bt);
+  int bw, bt, bpitch;
+  bp_tile_shape(n, bw, bt, bpitch);
   const int tiles = ((n + bw - 1) / bw) * ((n + bt - 1) / bt);
   // Aim for about four waves of 3 resident CTAs per SM over 148 SMs.
   const long target = 148L * 3 * kBpWaves;
@@ -938,8 +938,8 @@ bool make_quad_map(CUtensorMap* m, const float* quad, int n, int batch, int box_
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
-size_t bp_smem(int W, int T) {
-  return sizeof(float) * kBpWarps * ((((T + 5) * (W + 4) + 2) + 31) / 32 * 32);
+size_t bp_smem(int T, int P) {
+  return sizeof(float) * kBpWarps * ((((T + 5) * P + 2) + 31) / 32 * 32);
 }
 void set_smem(const void* fn, size_t bytes) {
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1059,10 +1059,10 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
   a.nn = static_cast<size_t>(n) * n;
   a.m = static_cast<size_t>(g.n_angles) * g.n_det;
   a.u_stride = u_stride ? u_stride : a.m;
-  int W, T;
-  bp_tile_shape(n, W, T);
-  const size_t smem = bp_smem(W, T);
-  auto kern = W == 172 ? bp_tile_kernel<172, 20, 176, kBpWarps>
+  int W, T, P;
+  bp_tile_shape(n, W, T, P);
+  const size_t smem = bp_smem(T, P);
+  auto kern = W == 172 ? bp_tile_kernel<172, kBpWideT, kBpWideP, kBpWarps>
                        : bp_tile_kernel<128, 28, 132, kBpWarps>;
   set_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((n + W - 1) / W, (n + T - 1) / T, r.n_partials() * batch);
