@@ -57,6 +57,13 @@ class ShardedSolver:
                     dist.all_reduce(self.atu)
                 self.prob.phase_b()
 
+    def profile(self, steps: int):
+        """Per-phase CUDA-event times (ms) of this rank over `steps` steps; the
+        all-reduce falls between the adjoint and FFT phases."""
+        self.prob.profile_begin()
+        self.step(steps)
+        return self.prob.profile_end()
+
     def objective(self):
         import torch
         import torch.distributed as dist
@@ -67,53 +74,3 @@ class ShardedSolver:
             dist.all_reduce(f)
             f = f.cpu()
         return f.numpy()
-
-
-def bench_sharded(args, cfg, metric, workload):
-    import numpy as np
-    import torch
-    import torch.distributed as dist
-
-    from . import instances, ncsg
-
-    rank = int(os.environ["RANK"])
-    world = int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
-    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=local)
-    x_true, b = instances.make_instance(cfg, R.forward)
-    mask = instances.metric_mask(cfg)
-    s = ShardedSolver(cfg, b, mask, rank, world, local)
-    s.step(args.warmup)
-    torch.cuda.synchronize()
-    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    dist.barrier()
-    torch.cuda.synchronize()
-    launches0 = ncsg.launch_count()
-    with torch.cuda.stream(s.stream):
-        for k in range(args.steps):
-            flush.fill_(float(k))
-            starts[k].record(s.stream)
-            s.step(1)
-            ends[k].record(s.stream)
-    torch.cuda.synchronize()
-    dist.barrier()
-    launches = ncsg.launch_count() - launches0
-    ms_local = sum(a.elapsed_time(e) for a, e in zip(starts, ends)) / args.steps
-    t = torch.tensor([ms_local], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    f = s.objective()
-    if rank == 0:
-        line = {"metric": metric, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": world,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic", "config": workload,
-                "gpu_launches": launches, "objective_after": float(np.sum(f)),
-                "collective": "NCCL all_reduce of the partial A^T u (N^2 fp32) per step"}
-        print(json.dumps(line), flush=True)
-    dist.barrier()
-    dist.destroy_process_group()
