@@ -116,12 +116,15 @@ def algorithmic_bytes(cfg, n_strips, n_parts):
 
 
 def setup_problem(cfg, nc, dev=0, angle_range=(0, 0)):
+    """Seeded instances for every problem of the config (C5: 64 problems, one
+    phantom/noise seed each), the GPU forward synthesising the sinograms."""
     from paper_1810_13100_b200 import instances, ncsg
 
-    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=dev)
-    x_true, b = instances.make_instance(cfg, R.forward)
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=dev) if cfg.kind == "ct" else None
+    fwd = R.forward if R is not None else None
+    xs, bs = zip(*[instances.make_instance(cfg, fwd, problem=q) for q in range(cfg.batch)])
     mask = instances.metric_mask(cfg)
-    return R, x_true, b, mask
+    return R, np.stack(xs), np.stack(bs), mask
 
 
 def cpu_reference_rate(cfg, b, mask, iters_hi=3, iters_lo=1):
@@ -130,7 +133,8 @@ def cpu_reference_rate(cfg, b, mask, iters_hi=3, iters_lo=1):
     setup, Engine::init and the final recorded seminorm cancel."""
     from oracle.oracle import REF_SO, Port, Prob, Ref
 
-    prob = Prob(0, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, b)
+    b0 = np.asarray(b).reshape(cfg.batch, -1)[0]  # one problem (C5: the first of 64)
+    prob = Prob(cfg.kind_id, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, b0)
     if os.path.exists(REF_SO):
         impl, kind, cores = Ref(), "reference", 1
         run = lambda k: impl.solve(prob, cfg.gamma, mask, k)
@@ -357,8 +361,8 @@ def bench_single(args, cfg):
     phase_avg = {k: v / max(1, nprof) for k, v in phase_ms.items()}
 
     clocks = clk.summary()
-    roofline = roofline_of(cfg, phase_avg, R.sample_count(), clocks)
-    S = R.sample_count()
+    S = R.sample_count() if R is not None else 0
+    roofline = roofline_of(cfg, phase_avg, S, clocks)
 
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -386,7 +390,8 @@ def e2e_rate(cfg, b, mask, steps):
 
     iters = cfg.iters
     t = time.perf_counter()
-    prob = ncsg.ct_problem(cfg, b, mask=mask)
+    make = ncsg.ct_problem if cfg.kind == "ct" else ncsg.denoise_problem
+    prob = make(cfg, b, mask=mask)
     prob.set_state()
     res = prob.solve(iters, record_every=iters)
     dt = time.perf_counter() - t
@@ -395,7 +400,7 @@ def e2e_rate(cfg, b, mask, steps):
     h2d = 4 * b.size + 2 * 8 * nk * cfg.n + 8 * m  # b, two half-spectrum filters, ray table
     d2h = 4 * (res.x.size + res.u.size) + res.rows.size * 8
     assert np.all(np.isfinite(res.objective))
-    return {"value": iters / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / iters,
+    return {"value": iters * cfg.batch / dt, "unit": "it/s", "h2d_bytes_per_step": h2d / iters,
             "d2h_bytes_per_step": d2h / iters, "iters": iters, "seconds": dt,
             "note": f"ncsg.Problem create + set_state + solve({iters}) + state/records download, "
                     "wall clock"}

@@ -295,6 +295,11 @@ class Problem:
         self.alpha, self.beta, self.lam, self.gamma = alpha, beta, lam, gamma
         self.positivity = positivity
         b = np.ascontiguousarray(b, np.float64).ravel()
+        m = n_angles * n_det if kind == CT else n * n
+        if b.size != batch * m:  # the C ABI reads batch * m offsets from b
+            raise ValueError(f"offset size mismatch: got {b.size}, need batch*m = {batch * m}")
+        if mask is not None and np.asarray(mask).size != n * n:
+            raise ValueError(f"mask must have N*N = {n * n} entries")
         self._b = b
         d = ProblemDesc()
         d.kind, d.n, d.n_angles, d.n_det = kind, n, n_angles, n_det

@@ -266,3 +266,29 @@ def test_sharded_phases_on_one_gpu(ncsg, port):
     us = np.concatenate([u0[0, :m0], u1[0, m0:prob.m0]])
     assert rel(us, uf[0, : prob.m0]) <= 1e-5
     assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 1e-5
+
+
+@pytest.mark.parametrize("name", ["ct16", "ct32", "ct32_pos", "tv32"])
+def test_gpu_matches_reference_golden(ncsg, name):
+    # Fixtures computed by the reference's own build (oracle/gen_golden.py):
+    # per-operator R / R^T at 1e-5 and the solve's iterate, dual and record
+    # objectives at the 1e-4 bar -- no oracle involved at run time.
+    g = np.load(os.path.join(GOLDEN, f"ref_{name}.npz"))
+    kind = ncsg.CT if int(g["kind"]) == 0 else ncsg.DENOISE
+    n, A, D = int(g["n"]), int(g["angles"]), int(g["det"])
+    if "radon_x" in g:
+        R = ncsg.RadonMap(n, A, D)
+        assert rel(R.forward(g["radon_x"]), g["radon_fwd"]) <= 1e-5
+        assert rel(R.adjoint(g["radon_u"]), g["radon_adj"]) <= 1e-5
+    p = ncsg.Problem(kind, n, float(g["alpha"]), float(g["beta"]), float(g["lam"]),
+                     float(g["gamma"]), g["b"], mask=g["mask"], n_angles=A, n_det=D,
+                     positivity=bool(int(g["positivity"])))
+    p.set_state()
+    r = p.solve(int(g["iters"]), record_every=int(g["record_every"]))
+    assert rel(r.x[0], g["x"]) <= TOL, rel(r.x[0], g["x"])
+    assert rel(r.u[0], g["u"]) <= TOL, rel(r.u[0], g["u"])
+    np.testing.assert_array_equal(r.rows[0][:, 0], g["rows"][:, 0])
+    go, oo = r.rows[0][:, 1], g["rows"][:, 1]
+    fin = np.isfinite(oo)
+    np.testing.assert_array_equal(np.isfinite(go), fin)  # NonnegConj: +inf rows match
+    assert np.max(np.abs(go[fin] - oo[fin]) / np.abs(oo[fin])) <= TOL

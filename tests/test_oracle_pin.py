@@ -7,7 +7,8 @@ Two anchors:
     their file:line (the doctest suites themselves need Eigen/doctest, absent
     from this image, so they cannot be built).
 Also checks the committed golden vectors in tests/golden/ (generated from the
-reference build by oracle/gen_golden.py).
+reference build by oracle/gen_golden.py; c3_full.npz comes from the oracle,
+tests/golden/make_c3_golden.py).
 """
 import glob
 import math
@@ -304,8 +305,9 @@ def test_port_matches_reference_positivity(port, ref):
 
 
 # ------------------------------------------------------------- golden files
-@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "*.npz"))))
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLDEN, "ref_*.npz"))))
 def test_port_matches_golden(port, path):
+    # fixtures computed by the reference build itself (oracle/gen_golden.py)
     g = np.load(path, allow_pickle=False)
     kind = int(g["kind"])
     n, A, D = int(g["n"]), int(g["angles"]), int(g["det"])
@@ -313,7 +315,8 @@ def test_port_matches_golden(port, path):
         np.testing.assert_array_equal(port.radon_forward(g["radon_x"], A, D), g["radon_fwd"])
         np.testing.assert_allclose(port.radon_adjoint(g["radon_u"], n, threads=1), g["radon_adj"],
                                    rtol=0, atol=0)
-    prob = Prob(kind, n, A, D, float(g["alpha"]), float(g["beta"]), float(g["lam"]), g["b"])
+    prob = Prob(kind, n, A, D, float(g["alpha"]), float(g["beta"]), float(g["lam"]), g["b"],
+                positivity=bool(int(g["positivity"])))
     r = port.solve(prob, float(g["gamma"]), g["mask"], int(g["iters"]),
                    record_every=int(g["record_every"]), threads=1)
     np.testing.assert_array_equal(r.x, g["x"])
