@@ -222,18 +222,24 @@ def roofline_of(cfg, phase_avg, S, clocks):
     achieved = nb[dom] / (dom_ms * 1e-3) / 1e9
     sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # TB/s at the measured clock
-    gather = {}
-    if dom in ("adjoint", "forward"):
-        gather = {"bytes_per_launch": 16 * S, "achieved_tbs": 16 * S / (dom_ms * 1e-3) / 1e12,
-                  "peak_tbs": smem_peak, "frac": 16 * S / (dom_ms * 1e-3) / 1e12 / smem_peak,
-                  "note": "bilinear gathers (4 fp32 texels per sample) against shared-memory "
-                          "bandwidth 148 SM x 128 B/clk at the sampled SM clock"}
-    traffic = None
-    try:  # DRAM bytes per launch of the same kernel from the committed ncu capture
+    traffic, wf_frac = None, None
+    try:  # DRAM bytes / smem wavefront use of the same kernel from the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh)["dram_bytes_per_launch"].get(dom)
+            prof = json.load(fh)
+        traffic = prof["dram_bytes_per_launch"].get(dom)
+        wf_frac = prof.get("smem_wavefront_frac", {}).get(dom)
     except (OSError, ValueError, KeyError):
         pass
+    gather = {}
+    if dom in ("adjoint", "forward"):
+        # R reads 4 texels per sample (16 B); R^T read-modify-writes them (32 B)
+        per = 32 if dom == "adjoint" else 16
+        gather = {"bytes_per_launch": per * S, "achieved_tbs": per * S / (dom_ms * 1e-3) / 1e12,
+                  "peak_tbs": smem_peak, "frac": per * S / (dom_ms * 1e-3) / 1e12 / smem_peak,
+                  "ncu_smem_wavefront_frac": wf_frac,
+                  "note": f"{per} B of shared-memory texel traffic per bilinear sample against "
+                          "148 SM x 128 B/clk at the sampled SM clock; ncu_smem_wavefront_frac "
+                          "= measured share of the wavefront peak (bank conflicts included)"}
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
             "peak_kind": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
             "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
