@@ -4,7 +4,8 @@
 // For real input the reference's c2c transform followed by Re() equals a
 // real-to-half-spectrum transform with the Hermitian part of h, so the work is
 // three passes over an N x (N/2+1) half spectrum stored column-major
-// (specT[k][j], k = 0..N/2), each pass a batch of shared-memory radix-2 FFTs:
+// (specT[k][j], k = 0..N/2), each pass a batch of shared-memory Stockham FFTs
+// (radix-8 stages in registers, one radix-2/4 stage when log2 N % 3 != 0):
 //   1. rows, real -> half spectrum (two real rows packed per complex FFT);
 //      the row loader assembles a = A^T u on the fly (adjoint partial images,
 //      transposed class-H partials, D^T u_g, identity blocks): the "combine"
@@ -39,59 +40,109 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 
-__device__ __forceinline__ unsigned bitrev(unsigned v, int logn) { return __brev(v) >> (32 - logn); }
-
-// In-place radix-2 DIT over `nfft` contiguous length-n sequences (bit-reversed
-// input, natural output).  sign: -1 forward, +1 inverse (unnormalised).
-__device__ void fft_dit(float2* z, int nfft, int n, int logn, const float2* __restrict__ tw,
-                        int sign) {
-  const int half = n >> 1;
-  const int total = nfft * half;
-  for (int lh = 0; lh < logn; ++lh) {
-    const int h = 1 << lh;
-    const int tstride = half >> lh;  // n / (2h)
-    __syncthreads();
-    for (int bi = threadIdx.x; bi < total; bi += blockDim.x) {
-      const int q = bi / half;
-      const int t = bi - q * half;
-      const int j = t & (h - 1);
-      const int i0 = ((t >> lh) << (lh + 1)) + j;
-      float2 w = __ldg(tw + j * tstride);
-      if (sign > 0) w.y = -w.y;
-      float2* zq = z + q * n;
-      const float2 u = zq[i0];
-      const float2 v = cmul(zq[i0 + h], w);
-      zq[i0] = cadd(u, v);
-      zq[i0 + h] = csub(u, v);
-    }
+// ---- Stockham autosort FFT (natural order in and out) -------------------
+// Stage with radix R and span Ns (Ns = product of the previous radices): for
+// j < n/R, k = j mod Ns, the R inputs in[j + r n/R] are twiddled by
+// w_{Ns R}^{r k}, transformed by an R-point DFT in registers and written to
+// out[(j - k) R + k + r Ns].  tw[i] = exp(-2 pi i i / n), i < n (fp64-derived).
+template <int SIGN>
+__device__ __forceinline__ float2 mul_i(float2 a) {  // * (-i) forward, * (+i) inverse
+  return SIGN < 0 ? make_float2(a.y, -a.x) : make_float2(-a.y, a.x);
+}
+template <int SIGN>
+__device__ __forceinline__ void dft2(float2* v) {
+  const float2 t = v[0];
+  v[0] = cadd(t, v[1]);
+  v[1] = csub(t, v[1]);
+}
+template <int SIGN>
+__device__ __forceinline__ void dft4(float2* v) {
+  const float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
+  const float2 a2 = cadd(v[1], v[3]), a3 = mul_i<SIGN>(csub(v[1], v[3]));
+  v[0] = cadd(a0, a2);
+  v[2] = csub(a0, a2);
+  v[1] = cadd(a1, a3);
+  v[3] = csub(a1, a3);
+}
+template <int SIGN>
+__device__ __forceinline__ void dft8(float2* v) {
+  float2 e[4] = {v[0], v[2], v[4], v[6]}, o[4] = {v[1], v[3], v[5], v[7]};
+  dft4<SIGN>(e);
+  dft4<SIGN>(o);
+  const float c = 0.70710678118654752440f;
+  o[1] = SIGN < 0 ? make_float2(c * (o[1].x + o[1].y), c * (o[1].y - o[1].x))
+                  : make_float2(c * (o[1].x - o[1].y), c * (o[1].x + o[1].y));
+  o[2] = mul_i<SIGN>(o[2]);
+  o[3] = SIGN < 0 ? make_float2(c * (o[3].y - o[3].x), -c * (o[3].x + o[3].y))
+                  : make_float2(-c * (o[3].x + o[3].y), c * (o[3].x - o[3].y));
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    v[k] = cadd(e[k], o[k]);
+    v[k + 4] = csub(e[k], o[k]);
   }
-  __syncthreads();
+}
+template <int R, int SIGN>
+__device__ __forceinline__ void dftR(float2* v) {
+  if (R == 2) dft2<SIGN>(v);
+  if (R == 4) dft4<SIGN>(v);
+  if (R == 8) dft8<SIGN>(v);
 }
 
-// In-place radix-2 DIF (natural input, bit-reversed output).
-__device__ void fft_dif(float2* z, int nfft, int n, int logn, const float2* __restrict__ tw,
-                        int sign) {
-  const int half = n >> 1;
-  const int total = nfft * half;
-  for (int lh = logn - 1; lh >= 0; --lh) {
-    const int h = 1 << lh;
-    const int tstride = half >> lh;
-    __syncthreads();
-    for (int bi = threadIdx.x; bi < total; bi += blockDim.x) {
-      const int q = bi / half;
-      const int t = bi - q * half;
-      const int j = t & (h - 1);
-      const int i0 = ((t >> lh) << (lh + 1)) + j;
-      float2 w = __ldg(tw + j * tstride);
-      if (sign > 0) w.y = -w.y;
-      float2* zq = z + q * n;
-      const float2 u = zq[i0];
-      const float2 v = zq[i0 + h];
-      zq[i0] = cadd(u, v);
-      zq[i0 + h] = cmul(csub(u, v), w);
+template <int R, int SIGN>
+__device__ void stockham_stage(const float2* in, float2* out, int nfft, int n, int logn, int Ns,
+                               int lns, const float2* __restrict__ tw) {
+  constexpr int LR = R == 2 ? 1 : R == 4 ? 2 : 3;
+  const int lm = logn - LR;  // log2(n / R)
+  const int m = 1 << lm;
+  const int lstep = logn - lns - LR;  // log2(n / (Ns R))
+  for (int bi = threadIdx.x; bi < (nfft << lm); bi += blockDim.x) {
+    const int q = bi >> lm, j = bi & (m - 1);
+    const float2* src = in + (q << logn);
+    float2* dst = out + (q << logn);
+    const int k = j & (Ns - 1);
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[j + r * m];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 w = __ldg(tw + ((r * k) << lstep));
+      if (SIGN > 0) w.y = -w.y;
+      v[r] = cmul(v[r], w);
     }
+    dftR<R, SIGN>(v);
+    const int idx = ((j - k) << LR) + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[idx + r * Ns] = v[r];
+  }
+}
+
+// nfft contiguous length-n transforms held in `a`; `b` is scratch of the same
+// size.  Returns the buffer holding the (natural-order) result.
+template <int SIGN>
+__device__ float2* fft_stockham(float2* a, float2* b, int nfft, int n, int logn,
+                                const float2* __restrict__ tw) {
+  int lns = 0;
+  const int rem = logn % 3;
+  if (rem) {
+    __syncthreads();
+    if (rem == 1)
+      stockham_stage<2, SIGN>(a, b, nfft, n, logn, 1, 0, tw);
+    else
+      stockham_stage<4, SIGN>(a, b, nfft, n, logn, 1, 0, tw);
+    lns = rem;
+    float2* t = a;
+    a = b;
+    b = t;
+  }
+  for (; lns < logn; lns += 3) {
+    __syncthreads();
+    stockham_stage<8, SIGN>(a, b, nfft, n, logn, 1 << lns, lns, tw);
+    float2* t = a;
+    a = b;
+    b = t;
   }
   __syncthreads();
+  return a;
 }
 
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
@@ -101,6 +152,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
   const int y0 = blockIdx.x * kRowsPerBlock;
   const int b = blockIdx.y;
   const int npair = kRowsPerBlock / 2;
+  float2* zb = zs + npair * n;  // Stockham scratch
   if (T.counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
     atomicAdd(T.counter + 1, 1);
   // Phase 1: row-major terms, coalesced along x.
@@ -108,7 +160,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
     const float v = y < n ? atu_rowmajor(T, b, y, x) : 0.f;
-    float2* slot = zs + (r >> 1) * n + bitrev(x, logn);
+    float2* slot = zs + (r >> 1) * n + x;
     if (r & 1)
       slot->y = v;
     else
@@ -126,14 +178,14 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
       float v = 0.f;
       const float* p = base + static_cast<size_t>(x) * n + y;
       for (int c = 0; c < T.nH; ++c) v += p[c * nn];
-      float2* slot = zs + (r >> 1) * n + bitrev(x, logn);
+      float2* slot = zs + (r >> 1) * n + x;
       if (r & 1)
         slot->y += v;
       else
         slot->x += v;
     }
   }
-  fft_dit(zs, npair, n, logn, tw, -1);
+  const float2* z = fft_stockham<-1>(zs, zb, npair, n, logn, tw);
   // Unpack the two real rows of each pair: A = (Z_k + conj Z_-k)/2,
   // B = (Z_k - conj Z_-k)/(2i); write specT[k][y] (k = 0..n/2).
   const int nk = n / 2 + 1;
@@ -142,7 +194,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
     const int y = y0 + r;
     if (y >= n) continue;
-    const float2* zq = zs + (r >> 1) * n;
+    const float2* zq = z + (r >> 1) * n;
     const float2 zk = zq[k];
     const float2 zm = zq[(n - k) & (n - 1)];
     float2 v;
@@ -162,11 +214,12 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   const int nk = n / 2 + 1;
   float2* col = specT + (static_cast<size_t>(b) * nk + k) * n;
   const float2* mk = maskT + static_cast<size_t>(k) * n;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) zs[bitrev(j, logn)] = col[j];
-  fft_dit(zs, 1, n, logn, tw, -1);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) zs[j] = cmul(zs[j], __ldg(mk + j));
-  fft_dif(zs, 1, n, logn, tw, +1);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) col[j] = zs[bitrev(j, logn)];
+  float2* zb = zs + n;
+  for (int j = threadIdx.x; j < n; j += blockDim.x) zs[j] = col[j];
+  float2* z = fft_stockham<-1>(zs, zb, 1, n, logn, tw);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
+  z = fft_stockham<+1>(z, z == zs ? zb : zs, 1, n, logn, tw);
+  for (int j = threadIdx.x; j < n; j += blockDim.x) col[j] = z[j];
 }
 
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
@@ -177,14 +230,15 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   const int nk = n / 2 + 1;
   const size_t nn = static_cast<size_t>(n) * n;
   const float2* in = specT + static_cast<size_t>(b) * nk * n;
+  float2* zb = zs + (kRowsPerBlock / 2) * n;  // Stockham scratch
   // Build Z = G_a + i G_b with Hermitian extension (G_r[n-k] = conj G_r[k]).
   for (int i = threadIdx.x; i < nk * kRowsPerBlock; i += blockDim.x) {
     const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
     const int y = y0 + r;
     const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
     float2* zq = zs + (r >> 1) * n;
-    const unsigned ik = bitrev(k, logn);
-    const unsigned im = bitrev((n - k) & (n - 1), logn);
+    const unsigned ik = k;
+    const unsigned im = (n - k) & (n - 1);
     if ((r & 1) == 0) {
       // a part: Z[k] += G_a[k], Z[n-k] += conj(G_a[k])
       zq[ik].x = g.x;
@@ -202,8 +256,8 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     if ((r & 1) == 0) continue;
     const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
     float2* zq = zs + (r >> 1) * n;
-    const unsigned ik = bitrev(k, logn);
-    const unsigned im = bitrev((n - k) & (n - 1), logn);
+    const unsigned ik = k;
+    const unsigned im = (n - k) & (n - 1);
     // b part: Z[k] += i G_b[k], Z[n-k] += i conj(G_b[k])
     zq[ik].x -= g.y;
     zq[ik].y += g.x;
@@ -212,15 +266,15 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
       zq[im].y += g.x;
     }
   }
-  fft_dit(zs, kRowsPerBlock / 2, n, logn, tw, +1);
+  float2* z = fft_stockham<+1>(zs, zb, kRowsPerBlock / 2, n, logn, tw);
   // x update, row-major.
   int bad = 0;
   for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
     if (y >= n) continue;
-    const float2 z = zs[(r >> 1) * n + x];
-    const float w = (r & 1) ? z.y : z.x;
+    const float2 zz = z[(r >> 1) * n + x];
+    const float w = (r & 1) ? zz.y : zz.x;
     const size_t gi = b * nn + static_cast<size_t>(y) * n + x;
     float xn;
     if (xu.subtract) {
@@ -234,9 +288,9 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     bad |= !isfinite(xn);
     if (xu.xT) {
       if (r & 1)
-        zs[(r >> 1) * n + x].y = xn;
+        z[(r >> 1) * n + x].y = xn;
       else
-        zs[(r >> 1) * n + x].x = xn;
+        z[(r >> 1) * n + x].x = xn;
     }
   }
   if (xu.flag && __syncthreads_or(bad) && threadIdx.x == 0)
@@ -247,8 +301,8 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
       const int x = i / kRowsPerBlock, r = i - x * kRowsPerBlock;
       const int y = y0 + r;
       if (y >= n) continue;
-      const float2 z = zs[(r >> 1) * n + x];
-      xu.xT[b * nn + static_cast<size_t>(x) * n + y] = (r & 1) ? z.y : z.x;
+      const float2 zz = z[(r >> 1) * n + x];
+      xu.xT[b * nn + static_cast<size_t>(x) * n + y] = (r & 1) ? zz.y : zz.x;
     }
   }
 }
@@ -259,7 +313,7 @@ int log2i(int n) {
   return l;
 }
 
-int fft_threads(int work) { return std::max(32, std::min(512, work)); }
+int fft_threads(int work) { return std::max(64, std::min(512, work)); }
 
 }  // namespace
 
@@ -267,8 +321,8 @@ void FftPlan::init(int n_, cudaStream_t s) {
   if (n_ < 8 || (n_ & (n_ - 1)))
     throw Error{NCSG_INVALID, "GPU circulant solve needs a power-of-two image size >= 8"};
   n = n_;
-  std::vector<float2> h(n / 2);
-  for (int k = 0; k < n / 2; ++k) {
+  std::vector<float2> h(n);
+  for (int k = 0; k < n; ++k) {
     double ang = -2.0 * 3.14159265358979323846 * k / n;
     h[k] = make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
   }
@@ -281,12 +335,13 @@ void FftPlan::init(int n_, cudaStream_t s) {
 void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT, int batch,
                          cudaStream_t s) {
   const int n = f.n;
-  size_t smem = sizeof(float2) * (kRowsPerBlock / 2) * n;
+  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_rows_r2c_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
-  fft_rows_r2c_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 2), smem, s>>>(
+  // the loader (sums of adjoint partial images) wants more threads than the FFT
+  fft_rows_r2c_kernel<<<grid, fft_threads(kRowsPerBlock * n / 4), smem, s>>>(
       terms, specT, f.tw.p, log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -295,9 +350,12 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
                             cudaStream_t s) {
   const int n = f.n;
-  size_t smem = sizeof(float2) * n;
+  size_t smem = 2 * sizeof(float2) * n;
+  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_cols_filter_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
   dim3 grid(n / 2 + 1, batch);
-  fft_cols_filter_kernel<<<grid, fft_threads(n / 2), smem, s>>>(specT, maskT, f.tw.p, n,
+  fft_cols_filter_kernel<<<grid, fft_threads(n / 8), smem, s>>>(specT, maskT, f.tw.p, n,
                                                                 log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -306,12 +364,12 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s) {
   const int n = f.n;
-  size_t smem = sizeof(float2) * (kRowsPerBlock / 2) * n;
+  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_rows_c2r_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
-  fft_rows_c2r_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 2), smem, s>>>(
+  fft_rows_c2r_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 4), smem, s>>>(
       specT, xu, f.tw.p, n, log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();

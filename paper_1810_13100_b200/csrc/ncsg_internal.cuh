@@ -192,7 +192,7 @@ void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, i
 // ------------------------------------------------------------------ FFT
 struct FftPlan {
   int n = 0;
-  DevBuf<float2> tw;  // exp(-2 pi i k / n), k < n/2
+  DevBuf<float2> tw;  // exp(-2 pi i k / n), k < n
   void init(int n_, cudaStream_t s);
 };
 // Spectrum layout: specT[batch][n/2+1][n] complex (column-major half spectrum).
