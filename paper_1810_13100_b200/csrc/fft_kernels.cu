@@ -206,20 +206,26 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
   }
 }
 
+#ifndef NCSG_FFT_COLS
+#define NCSG_FFT_COLS 4
+#endif
+constexpr int kColsPerBlock = NCSG_FFT_COLS;  // columns per column-pass CTA
+
 __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2* __restrict__ maskT,
                                        const float2* __restrict__ tw, int n, int logn) {
   extern __shared__ float2 zs[];
-  const int k = blockIdx.x;
+  const int k0 = blockIdx.x * kColsPerBlock;
   const int b = blockIdx.y;
   const int nk = n / 2 + 1;
-  float2* col = specT + (static_cast<size_t>(b) * nk + k) * n;
-  const float2* mk = maskT + static_cast<size_t>(k) * n;
-  float2* zb = zs + n;
-  for (int j = threadIdx.x; j < n; j += blockDim.x) zs[j] = col[j];
-  float2* z = fft_stockham<-1>(zs, zb, 1, n, logn, tw);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
-  z = fft_stockham<+1>(z, z == zs ? zb : zs, 1, n, logn, tw);
-  for (int j = threadIdx.x; j < n; j += blockDim.x) col[j] = z[j];
+  const int nc = min(kColsPerBlock, nk - k0);
+  float2* col = specT + (static_cast<size_t>(b) * nk + k0) * n;  // nc contiguous columns
+  const float2* mk = maskT + static_cast<size_t>(k0) * n;
+  float2* zb = zs + kColsPerBlock * n;
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) zs[j] = col[j];
+  float2* z = fft_stockham<-1>(zs, zb, nc, n, logn, tw);
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
+  z = fft_stockham<+1>(z, z == zs ? zb : zs, nc, n, logn, tw);
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
@@ -350,12 +356,12 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
                             cudaStream_t s) {
   const int n = f.n;
-  size_t smem = 2 * sizeof(float2) * n;
+  size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_cols_filter_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
-  dim3 grid(n / 2 + 1, batch);
-  fft_cols_filter_kernel<<<grid, fft_threads(n / 8), smem, s>>>(specT, maskT, f.tw.p, n,
+  dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
+  fft_cols_filter_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, maskT, f.tw.p, n,
                                                                 log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
