@@ -340,7 +340,10 @@ constexpr int kOrbW = 128;   // strip width
 constexpr int kOrbT = NCSG_ORB_T;          // tile-row height
 constexpr int kOrbSeg = NCSG_ORB_SEG;      // rows per segment (one CTA sweeps one segment)
 constexpr int kOrbWarps = NCSG_ORB_WARPS;  // orbits per CTA (one per warp)
-constexpr int kOrbP = kOrbW + 8;
+#ifndef NCSG_ORB_P
+#define NCSG_ORB_P (kOrbW + 8)
+#endif
+constexpr int kOrbP = NCSG_ORB_P;  // tile pitch in cells (= TMA box width, >= W + 8)
 
 struct OrbArgs {
   const OrbitGeom* orb;
@@ -459,7 +462,7 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
   const float4* quad = a.quad + static_cast<size_t>(b) * a.nn;
   const unsigned barA = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
   const unsigned tile0 = sm_addr + pad;
-  constexpr unsigned kBytes = ROWS * (W + 8) * 16;
+  constexpr unsigned kBytes = ROWS * P * 16;
   if (USE_TMA) {
     for (int i = threadIdx.x; i < 4 * kOrbTile; i += NW * 32) tiles[i] = 0.f;
     if (threadIdx.x == 0) {
@@ -503,8 +506,8 @@ __global__ void __launch_bounds__(kOrbWarps * 32)
       phase ^= 1u;
     } else {
       float4* t4 = reinterpret_cast<float4*>(tiles);
-      for (int i = threadIdx.x; i < ROWS * (W + 8); i += NW * 32) {
-        const int ry = i / (W + 8), rx = i - ry * (W + 8);
+      for (int i = threadIdx.x; i < ROWS * P; i += NW * 32) {
+        const int ry = i / P, rx = i - ry * P;
         const int gy = Y0 - 2 + ry, gx = X0 - 4 + rx;
         t4[D + ry * P + rx] = (gy >= 0 && gy < n && gx >= 0 && gx < n)
                                   ? quad[static_cast<size_t>(gy) * n + gx]
@@ -971,7 +974,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     a.nn = static_cast<size_t>(g.n) * g.n;
     a.m = static_cast<size_t>(g.n_angles) * g.n_det;
     CUtensorMap map{};
-    const bool tma = make_quad_map(&map, imgT, g.n, batch, kOrbW + 8, kOrbT + 4);
+    const bool tma = make_quad_map(&map, imgT, g.n, batch, kOrbP, kOrbT + 4);
     const size_t smem = orbit_smem(a.rmax);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     if (tma) {
