@@ -21,6 +21,8 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
+#include <fstream>
 #include <memory>
 #include <optional>
 #include <span>
@@ -422,6 +424,22 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
 }
 
 }  // namespace detail
+
+/// write_record_csv (io.cpp:203-215): the reference's convergence CSV, same
+/// header and %.17g formatting.
+inline void write_record_csv(const std::string& path, const ConvergenceRecord& record) {
+  std::ofstream out(path, std::ios::trunc);
+  if (!out) throw std::runtime_error("cannot open " + path + " for writing");
+  out << "iter,objective,rel_subopt,seminorm_step,wall_ms\n";
+  char buf[256];
+  for (const auto& row : record.rows) {
+    std::snprintf(buf, sizeof buf, "%lld,%.17g,%.17g,%.17g,%.17g\n",
+                  static_cast<long long>(row.iter), row.objective, row.rel_subopt,
+                  row.seminorm_step, row.wall_ms);
+    out << buf;
+  }
+  if (!out) throw std::runtime_error("short write to " + path);
+}
 
 /// ncs_step (solvers.cpp:417-421): one splitting iteration in place.
 inline void ncs_step(SolverState& state, const SplitProblem& prob, const SolverConfig& cfg) {

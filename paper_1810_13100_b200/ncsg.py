@@ -422,3 +422,13 @@ def ct_problem(cfg, b, mask=None, batch=None, **kw) -> Problem:
 def denoise_problem(cfg, b, mask=None, **kw) -> Problem:
     return Problem(DENOISE, cfg.n, cfg.alpha, cfg.beta, cfg.lam, cfg.gamma, b, mask=mask,
                    batch=cfg.batch, **kw)
+
+
+def write_record_csv(path: str, rows) -> None:
+    """write_record_csv (io.cpp:203-215) for one problem's record rows
+    (iter, objective, rel_subopt, seminorm_step, wall_ms): same header and
+    %.17g formatting as the reference."""
+    with open(path, "w") as f:
+        f.write("iter,objective,rel_subopt,seminorm_step,wall_ms\n")
+        for r in np.asarray(rows).reshape(-1, 5):
+            f.write("%d,%.17g,%.17g,%.17g,%.17g\n" % (int(r[0]), r[1], r[2], r[3], r[4]))

@@ -3,6 +3,8 @@
 // the GPU path.  Prints one line per case; exit code = number of failures.
 #include <cmath>
 #include <cstdio>
+#include <fstream>
+#include <string>
 #include <numeric>
 #include <random>
 #include <vector>
@@ -129,6 +131,46 @@ int main() {
       div = e.iter > 0;
     }
     CHECK(div, "DivergenceError with iteration");
+  }
+  // GPU setup path (circulant.cpp:142-169, pipeline.cpp:100-110) and the
+  // step-condition screen (solvers.cpp:206-245, 278).
+  {
+    int n = 32, A = 24, D = default_detector_count(n);
+    RadonMap geom(n, A, D);
+    const double dc = dc_response(geom);
+    const double scale = calibrate_scale(geom, 8, 0);
+    // SURVEY.md §8 probe: C_R ~ 0.25-0.28 angles*N and DC(R^T R) ~ 0.95 angles*N
+    CHECK(scale > 0.15 * A * n && scale < 0.4 * A * n, "calibrate_scale magnitude");
+    CHECK(dc > 0.5 * A * n && dc < 1.5 * A * n, "dc response magnitude");
+    SpectralMask meas = measurement_mask(geom, dc, 8, 0);
+    CHECK(std::abs(meas.h[0].real() - dc) < 1e-9 * dc &&
+              std::abs(meas.h[1].real() - scale) < 1e-9 * scale,
+          "measurement_mask = radon_mask(n, scale, dc)");
+    auto truth = randn(geom.domain_size(), 11);
+    std::vector<double> sino(geom.range_size());
+    geom.forward(truth, sino);
+    ModelParams p;
+    p.alpha = p.beta = 0.1;
+    p.lambda = 0.01;
+    SplitProblem prob = assemble_problem(sino, geom, p);
+    SolverConfig cfg;
+    cfg.alpha = p.alpha;
+    cfg.mask = metric_mask(meas, p);
+    cfg.max_iters = 3;
+    cfg.record_every = 1;
+    cfg.gamma = 1e-3;  // far below alpha lambda_max(A^T A - C): the screen warns
+    SolveResult small = ncs_solve(prob, cfg);
+    CHECK(!small.record.warnings.empty(), "screen warns on a violated step condition");
+    cfg.gamma = 10.0 * A * n;  // comfortably above
+    SolveResult big = ncs_solve(prob, cfg);
+    CHECK(big.record.warnings.empty() && big.record.rows.size() == 4, "no warning when it holds");
+    write_record_csv("/tmp/ncsg_record_test.csv", big.record);
+    std::ifstream in("/tmp/ncsg_record_test.csv");
+    std::string header, first;
+    std::getline(in, header);
+    std::getline(in, first);
+    CHECK(header == "iter,objective,rel_subopt,seminorm_step,wall_ms" && first.rfind("0,", 0) == 0,
+          "write_record_csv format (io.cpp:203-215)");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;

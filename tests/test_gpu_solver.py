@@ -292,3 +292,15 @@ def test_gpu_matches_reference_golden(ncsg, name):
     fin = np.isfinite(oo)
     np.testing.assert_array_equal(np.isfinite(go), fin)  # NonnegConj: +inf rows match
     assert np.max(np.abs(go[fin] - oo[fin]) / np.abs(oo[fin])) <= TOL
+
+
+def test_record_every_one_parity(ncsg, port):
+    # record_every = 1 -- an objective and a seminorm row
+    # after every step (solvers.cpp:281-332), each from device reductions.
+    prob, mask, gamma = small_ct(port, n=32, A=24)
+    o = port.solve(prob, gamma, mask, 20, record_every=1)
+    g = gpu_problem(ncsg, prob, gamma, mask).solve(20, record_every=1)
+    check_run(g, o)
+    sem_g, sem_o = g.rows[0][1:, 3], o.rows[1:, 3]
+    assert len(sem_g) == 20
+    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= 1e-3

@@ -196,3 +196,16 @@ def test_sharded_adjoint_allreduce_gloo():
     for p in procs:
         p.join(timeout=60)
     assert all(err < 1e-13 for _, err in res), res
+
+
+def test_write_record_csv_format(tmp_path):
+    # io.cpp:203-215: header and %lld,%.17g x4 rows
+    from paper_1810_13100_b200 import ncsg
+
+    rows = np.array([[0, 1.0, 0.5, 0.0, 0.1], [10, 0.1 + 0.2, 1e-20, 3.0, 12.25]])
+    path = tmp_path / "rec.csv"
+    ncsg.write_record_csv(str(path), rows)
+    lines = path.read_text().splitlines()
+    assert lines[0] == "iter,objective,rel_subopt,seminorm_step,wall_ms"
+    assert lines[1] == "0,1,0.5,0,0.10000000000000001"
+    assert lines[2] == "10,0.30000000000000004,9.9999999999999995e-21,3,12.25"
