@@ -626,6 +626,7 @@ static void prox_all(const Prob* p, double* r) {
 typedef struct {
   Prob* p;
   double alpha, gamma;
+  int n_cg;           /* > 0: admm_cg x-update (XMode::Cg) */
   const double* mask; /* cfg.mask (nullable) */
   double* m_pinv;     /* pinv(gamma + alpha*mask) */
   double *ax, *ax_new, *r, *atu, *w, *adx, *mdx, *tmp;
@@ -636,6 +637,7 @@ static void engine_init(Engine* e, Prob* p, double alpha, double gamma, const do
   e->p = p;
   e->alpha = alpha;
   e->gamma = gamma;
+  e->n_cg = 0;
   e->mask = mask;
   e->m_pinv = NULL;
   if (mask) {
@@ -681,12 +683,51 @@ static int check_finite(const Prob* p, const double* x, const double* u) {
   return 0;
 }
 
-/* Engine::step (solvers.cpp:124-161) in mask (NCS) or scaled (PDHG) mode.
- * Returns 0 or 1 on divergence.  (u, r swap handled by copying back.) */
+static double dotd(const double* a, const double* b, size_t n);
+
+/* cg (solvers.cpp:442-463) on NormalMap(stacked) (linear_map.cpp:57-61):
+ * n_iters conjugate-gradient steps from x = 0 for A^T A x = rhs. */
+static void cg_normal(Prob* p, const double* rhs, int n_iters, double* x, double* tmp) {
+  size_t n = p->nn;
+  double* r = (double*)malloc(sizeof(double) * n);
+  double* q = (double*)malloc(sizeof(double) * n);
+  double* ap = (double*)malloc(sizeof(double) * n);
+  double* mid = (double*)malloc(sizeof(double) * p->range);
+  memset(x, 0, sizeof(double) * n);
+  memcpy(r, rhs, sizeof(double) * n);
+  memcpy(q, rhs, sizeof(double) * n);
+  double rs = dotd(r, r, n);
+  for (int it = 0; it < n_iters; ++it) {
+    if (rs == 0.0) break;
+    stacked_forward(p, q, mid);
+    stacked_adjoint(p, mid, ap, tmp);
+    double pap = dotd(q, ap, n);
+    if (pap <= 0.0) break;
+    double a = rs / pap;
+    for (size_t j = 0; j < n; ++j) x[j] += a * q[j];
+    for (size_t j = 0; j < n; ++j) r[j] -= a * ap[j];
+    double rs_new = dotd(r, r, n);
+    double beta = rs_new / rs;
+    for (size_t j = 0; j < n; ++j) q[j] = r[j] + beta * q[j];
+    rs = rs_new;
+  }
+  free(r);
+  free(q);
+  free(ap);
+  free(mid);
+}
+
+/* Engine::step (solvers.cpp:124-161) in mask (NCS), scaled (PDHG) or Cg
+ * (ADMM-CG) mode.  Returns 0 or 1 on divergence.  (u, r swap handled by
+ * copying back.) */
 static int engine_step(Engine* e, double* x, double* u) {
   Prob* p = e->p;
   stacked_adjoint(p, u, e->atu, e->tmp);
-  if (e->m_pinv) {
+  if (e->n_cg > 0) {
+    cg_normal(p, e->atu, e->n_cg, e->w, e->tmp);
+    double inv = 1.0 / e->alpha;
+    for (size_t j = 0; j < p->nn; ++j) e->w[j] = inv * e->w[j];
+  } else if (e->m_pinv) {
     orc_mask_apply(p->n, e->m_pinv, e->atu, e->w);
   } else {
     double inv = 1.0 / e->gamma;
@@ -735,8 +776,13 @@ static double engine_seminorm(Engine* e, const double* dx, const double* du) {
     t1 += d * d;
   }
   double a_quad = e->alpha * e->alpha * dotd(e->adx, e->adx, p->range);
-  engine_apply_m(e, dx, e->mdx);
-  double m_quad = e->alpha * dotd(dx, e->mdx, p->nn);
+  double m_quad;
+  if (e->n_cg > 0) {
+    m_quad = a_quad; /* M = alpha A^T A (solvers.cpp:174) */
+  } else {
+    engine_apply_m(e, dx, e->mdx);
+    m_quad = e->alpha * dotd(dx, e->mdx, p->nn);
+  }
   double rad = t1 + m_quad - a_quad;
   if (rad < 0.0) {
     double mag = t1 + fabs(m_quad) + a_quad;
@@ -810,18 +856,21 @@ int orc_screen(int kind, int n, int angles, int det, double alpha, double beta, 
 /* solve_template (solvers.cpp:267-337) for ncs_solve (mask) / pdhg_solve
  * (mask == NULL).  rows: {iter, objective, rel_subopt, seminorm, wall_ms=0}.
  * Returns 0, 2 (bad input) or 4 (DivergenceError; *div_iter set). */
-int orc_solve(int kind, int n, int angles, int det, double alpha, double beta, double lambda,
-              int positivity, const double* b, double gamma, const double* mask, int max_iters,
-              int record_every, const double* x0, const double* u0, double* x_out,
-              double* u_out, double* rows, int max_rows, int* n_rows, double* objective,
-              int64_t* div_iter, int nthreads) {
+int orc_solve_ex(int kind, int n, int angles, int det, double alpha, double beta,
+                 double lambda, int positivity, const double* b, double gamma,
+                 const double* mask, int n_cg, int max_iters, int record_every,
+                 const double* x0, const double* u0, double* x_out, double* u_out, double* rows,
+                 int max_rows, int* n_rows, double* objective, int64_t* div_iter, int nthreads) {
   if (max_iters < 0 || record_every < 1 || alpha <= 0.0) return 2;
-  if (!mask && gamma <= 0.0) return 2;
+  if (!mask && n_cg <= 0 && gamma <= 0.0) return 2;
+  if (n_cg > 0 && mask) return 2; /* admm_cg uses M = alpha A^T A (solvers.cpp:437-438) */
   if (kind == 0 && orc_radon_check(n, angles, det)) return 2;
   Prob p;
   prob_init(&p, kind, n, angles, det, alpha, beta, lambda, positivity, b, nthreads);
   Engine e;
   engine_init(&e, &p, alpha, gamma, mask);
+  e.n_cg = n_cg;
+  const int64_t axis_scale = n_cg > 0 ? n_cg : 1; /* solvers.cpp:279 */
   double* x = x_out;
   double* u = u_out;
   if (x0)
@@ -838,7 +887,7 @@ int orc_solve(int kind, int n, int angles, int det, double alpha, double beta, d
   do {                                                        \
     if (k_rows < max_rows) {                                  \
       double* o = rows + 5 * k_rows;                          \
-      o[0] = (double)(K);                                     \
+      o[0] = (double)((K) * axis_scale);                      \
       o[1] = objective_from_ax(&p, e.ax);                     \
       o[2] = 0.0;                                             \
       o[3] = (SEM);                                           \
@@ -888,6 +937,16 @@ int orc_solve(int kind, int n, int angles, int det, double alpha, double beta, d
   free(du);
   engine_free(&e);
   return rc;
+}
+
+int orc_solve(int kind, int n, int angles, int det, double alpha, double beta, double lambda,
+              int positivity, const double* b, double gamma, const double* mask, int max_iters,
+              int record_every, const double* x0, const double* u0, double* x_out,
+              double* u_out, double* rows, int max_rows, int* n_rows, double* objective,
+              int64_t* div_iter, int nthreads) {
+  return orc_solve_ex(kind, n, angles, det, alpha, beta, lambda, positivity, b, gamma, mask, 0,
+                      max_iters, record_every, x0, u0, x_out, u_out, rows, max_rows, n_rows,
+                      objective, div_iter, nthreads);
 }
 
 /* ncs_step (solvers.cpp:417-421): fresh Engine + init + one step, `steps` times. */

@@ -98,6 +98,10 @@ class Port:
                                 C.c_double, C.c_int, _vp, C.c_double, _vp, C.c_int, C.c_int, _vp,
                                 _vp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int),
                                 C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
+        L.orc_solve_ex.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                   C.c_double, C.c_int, _vp, C.c_double, _vp, C.c_int, C.c_int,
+                                   C.c_int, _vp, _vp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int),
+                                   C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
         L.orc_ncs_step.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _vp, C.c_double, _vp, _dp, _dp, C.c_int,
                                    C.c_int]
@@ -213,10 +217,11 @@ class Port:
         return h, _ptr(h)
 
     def solve(self, prob, gamma, mask, max_iters, record_every=None, x0=None, u0=None,
-              threads=None, pdhg=False):
-        """ncs_solve (pdhg=False, mask required) / pdhg_solve (mask=None)."""
+              threads=None, pdhg=False, n_cg=0):
+        """ncs_solve (pdhg=False, mask required) / pdhg_solve (mask=None) /
+        admm_cg_solve (n_cg > 0, mask=None)."""
         p = prob
-        if pdhg:
+        if pdhg or n_cg:
             mask = None
         record_every = record_every or max(1, max_iters)
         b = np.ascontiguousarray(p.b, np.float64).ravel()
@@ -230,10 +235,11 @@ class Port:
         div = C.c_int64(-1)
         x0a = None if x0 is None else np.ascontiguousarray(x0, np.float64).ravel()
         u0a = None if u0 is None else np.ascontiguousarray(u0, np.float64).ravel()
-        rc = self.lib.orc_solve(p.kind, p.n, p.angles, p.det, p.alpha, p.beta, p.lam,
-                                int(p.positivity), _ptr(b), gamma, hp, max_iters, record_every,
-                                _ptr(x0a), _ptr(u0a), x, u, rows.ravel(), max_rows, C.byref(nr),
-                                C.byref(obj), C.byref(div), threads or default_threads())
+        rc = self.lib.orc_solve_ex(p.kind, p.n, p.angles, p.det, p.alpha, p.beta, p.lam,
+                                   int(p.positivity), _ptr(b), gamma, hp, n_cg, max_iters,
+                                   record_every, _ptr(x0a), _ptr(u0a), x, u, rows.ravel(),
+                                   max_rows, C.byref(nr), C.byref(obj), C.byref(div),
+                                   threads or default_threads())
         if rc == 4:
             raise OracleError(f"diverged at iteration {div.value}")
         _check(rc, "solve")
@@ -321,6 +327,10 @@ class Ref:
                                 C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.ref_ncs_step.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _dp, C.c_double, _vp, _dp, _dp, C.c_int]
+        L.ref_admm_cg_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
+                                        C.c_double, C.c_double, C.c_int, _dp, C.c_double,
+                                        C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int,
+                                        C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.ref_objective.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                     C.c_double, C.c_int, _dp, _dp, C.POINTER(C.c_double)]
 
@@ -442,6 +452,24 @@ class Ref:
                                      record_every, int(check_step), _ptr(x0a), _ptr(u0a),
                                      int(pdhg), x, u, rows.ravel(), max_rows, C.byref(nr),
                                      C.byref(obj)), "solve")
+        return SolveOut(x.reshape(p.n, p.n), u, rows[: nr.value].copy(), obj.value)
+
+    def admm_cg_solve(self, prob, gamma, n_cg, max_iters, record_every=None):
+        """admm_cg_solve (solvers.cpp:435-440) of the reference build."""
+        p = prob
+        record_every = record_every or max(1, max_iters)
+        b = np.ascontiguousarray(p.b, np.float64).ravel()
+        x = np.zeros(p.n * p.n)
+        u = np.zeros(p.range_size)
+        max_rows = max_iters // record_every + 3
+        rows = np.zeros((max_rows, 5))
+        nr = C.c_int()
+        obj = C.c_double()
+        self._chk(self.lib.ref_admm_cg_solve(p.kind, p.n, p.angles, p.det, p.alpha, p.beta,
+                                             p.lam, int(p.positivity), b, gamma, n_cg,
+                                             max_iters, record_every, x, u, rows.ravel(),
+                                             max_rows, C.byref(nr), C.byref(obj)),
+                  "admm_cg_solve")
         return SolveOut(x.reshape(p.n, p.n), u, rows[: nr.value].copy(), obj.value)
 
     def ncs_step(self, prob, gamma, mask, x, u, steps=1):

@@ -276,6 +276,40 @@ int ref_solve(int kind, int n, int angles, int det, double alpha, double beta, d
   });
 }
 
+// admm_cg_solve (solvers.cpp:435-440): the same engine with the x-update
+// w = (1/alpha) CG(A^T A, A^T u, n_cg); no mask.
+int ref_admm_cg_solve(int kind, int n, int angles, int det, double alpha, double beta,
+                      double lambda, int positivity, const double* b, double gamma, int n_cg,
+                      int max_iters, int record_every, double* x_out, double* u_out,
+                      double* rows, int max_rows, int* n_rows, double* objective) {
+  return guard([&] {
+    Desc d{kind, n, angles, det, alpha, beta, lambda, positivity};
+    SplitProblem prob = build_problem(d, b);
+    SolverConfig cfg;
+    cfg.alpha = alpha;
+    cfg.gamma = gamma;
+    cfg.max_iters = max_iters;
+    cfg.record_every = record_every;
+    cfg.check_step_condition = false;
+    SolveResult res = admm_cg_solve(prob, cfg, n_cg);
+    std::memcpy(x_out, res.state.x.v.data(), sizeof(double) * res.state.x.v.size());
+    std::memcpy(u_out, res.state.u.data(), sizeof(double) * res.state.u.size());
+    int k = 0;
+    for (const RecordRow& r : res.record.rows) {
+      if (k >= max_rows) break;
+      double* o = rows + 5 * k;
+      o[0] = static_cast<double>(r.iter);
+      o[1] = r.objective;
+      o[2] = r.rel_subopt;
+      o[3] = r.seminorm_step;
+      o[4] = r.wall_ms;
+      ++k;
+    }
+    *n_rows = k;
+    *objective = res.objective;
+  });
+}
+
 // ncs_step (solvers.cpp:417-421): fresh Engine per call, in place on (x, u).
 int ref_ncs_step(int kind, int n, int angles, int det, double alpha, double beta, double lambda,
                  int positivity, const double* b, double gamma, const double* mask, double* x,

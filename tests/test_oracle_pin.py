@@ -322,3 +322,20 @@ def test_port_matches_golden(port, path):
     np.testing.assert_array_equal(r.x, g["x"])
     np.testing.assert_array_equal(r.u, g["u"])
     np.testing.assert_array_equal(r.rows[:, :4], g["rows"][:, :4])
+
+
+@pytest.mark.parametrize("kind,positivity", [(0, False), (0, True), (1, False)])
+def test_admm_cg_matches_reference_bitwise(port, ref, kind, positivity):
+    # admm_cg_solve (solvers.cpp:435-463): x-update by n_cg CG steps on A^T A
+    # (NormalMap, linear_map.cpp:57-61); record axis scaled by n_cg.
+    n = 16
+    A, D = (12, port.default_detector_count(n)) if kind == 0 else (0, 0)
+    m = A * D if kind == 0 else n * n
+    b = rand(m, 31)
+    prob = Prob(kind, n, A, D, 0.5, 0.5, 0.02, b, positivity=positivity)
+    r1 = ref.admm_cg_solve(prob, 0.0, 4, 12, record_every=4)
+    r2 = port.solve(prob, 0.0, None, 12, record_every=4, threads=1, n_cg=4)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    np.testing.assert_array_equal(r1.u, r2.u)
+    np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
+    assert r1.rows[-1, 0] == 12 * 4
