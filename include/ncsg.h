@@ -186,6 +186,14 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
                        int check_step_condition, uint64_t seed, const double* f_star,
                        ncsg_record_row* rows, int max_rows, int* n_rows, double* screen_est);
 
+/* admm_cg_solve (solvers.cpp:435-440): n_cg > 0 switches the x-update to
+ * w = (1/alpha) cg(A^T A, A^T u, n_cg) (solvers.cpp:138-145, 442-463;
+ * NormalMap, linear_map.cpp:57-61) -- M = alpha A^T A, so the problem must
+ * have no mask; record iterations are scaled by n_cg (solvers.cpp:279) and
+ * the step-condition screen is skipped (solvers.cpp:207).  Batch 1,
+ * unsharded.  n_cg = 0 restores the circulant / PDHG x-update. */
+ncsg_status ncsg_set_cg(ncsg_problem* p, int n_cg);
+
 /* ------------------------------------------------------------- setup path
  * (the GPU versions of the reference's CPU setup.) */
 

@@ -11,7 +11,7 @@
 //   metric_mask ........................... pipeline.hpp:38-71
 //   SolverConfig, SolverState, RecordRow,
 //   SolveResult, DivergenceError,
-//   ncs_step, ncs_solve, pdhg_solve ....... solvers.hpp:59-121
+//   ncs_step, ncs_solve, pdhg_solve, admm_cg_solve ... solvers.hpp:59-121
 // Exceptions: std::invalid_argument for validation failures, DivergenceError
 // (a std::runtime_error with .iter) for divergence, std::runtime_error for
 // device failures (there is no CPU fallback).
@@ -342,8 +342,10 @@ namespace detail {
 /// Device-resident Engine for one (problem, config) pair.
 class Engine {
  public:
-  Engine(const SplitProblem& prob, const SolverConfig& cfg, bool pdhg) {
+  Engine(const SplitProblem& prob, const SolverConfig& cfg, bool pdhg, int n_cg = 0) {
     if (pdhg && cfg.mask) throw std::invalid_argument("pdhg uses M = gamma I; drop the mask");
+    if (n_cg > 0 && cfg.mask)
+      throw std::invalid_argument("admm_cg uses M = alpha A^T A; drop the mask/overrides");
     if (!(cfg.alpha > 0.0)) throw std::invalid_argument("alpha must be positive");
     if (cfg.mask && cfg.mask->n != prob.n)
       throw std::invalid_argument("mask/problem size mismatch");
@@ -359,7 +361,7 @@ class Engine {
     d.alpha = cfg.alpha;
     d.beta = prob.beta * cfg.alpha / prob.alpha;
     d.lambda = prob.lambda;
-    d.gamma = cfg.gamma;
+    d.gamma = (n_cg > 0 && !(cfg.gamma > 0.0)) ? 1.0 : cfg.gamma;  // unused by the CG update
     d.pinv_rel_tol = cfg.pinv_rel_tol;
     d.mask = (!pdhg && cfg.mask) ? reinterpret_cast<const double*>(cfg.mask->h.data()) : nullptr;
     d.b = prob.offset.data();
@@ -367,6 +369,7 @@ class Engine {
     ncsg_problem* h = nullptr;
     check(ncsg_problem_create(&d, &h));
     h_.reset(h, [](ncsg_problem* p) { ncsg_problem_destroy(p); });
+    if (n_cg > 0) check(ncsg_set_cg(h, n_cg));
   }
   ncsg_problem* get() const { return h_.get(); }
 
@@ -383,10 +386,11 @@ inline void throw_divergence() {
 }
 
 inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool pdhg,
-                         const double* f_star, const SolverState* init) {
+                         const double* f_star, const SolverState* init, int n_cg = 0) {
   if (cfg.max_iters < 0) throw std::invalid_argument("max_iters must be nonnegative");
   if (cfg.record_every < 1) throw std::invalid_argument("record_every must be >= 1");
-  Engine eng(prob, cfg, pdhg);
+  if (n_cg < 0) throw std::invalid_argument("n_cg must be >= 1");
+  Engine eng(prob, cfg, pdhg, n_cg);
   SolverState s = init ? *init : make_state(prob);
   check(ncsg_set_state(eng.get(), s.x.data(), s.u.data(), 0));
   int max_rows = cfg.max_iters / cfg.record_every + 3;
@@ -399,7 +403,7 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
   if (st == NCSG_DIVERGED) throw_divergence();
   check(st);
   SolveResult res;
-  if (cfg.check_step_condition) {  // screen_step_condition (solvers.cpp:238-244)
+  if (cfg.check_step_condition && n_cg == 0) {  // screen_step_condition (solvers.cpp:207-244)
     double shift = cfg.gamma;
     if (!pdhg && cfg.mask) {
       double hmax = 0.0;
@@ -466,6 +470,16 @@ inline SolveResult pdhg_solve(const SplitProblem& prob, const SolverConfig& cfg,
                               const double* f_star = nullptr,
                               const SolverState* init = nullptr) {
   return detail::solve(prob, cfg, true, f_star, init);
+}
+
+/// admm_cg_solve (solvers.cpp:435-440): x-update by n_cg conjugate-gradient
+/// steps on A^T A (M = alpha A^T A); record iterations count CG steps.
+inline SolveResult admm_cg_solve(const SplitProblem& prob, const SolverConfig& cfg, int n_cg,
+                                 const double* f_star = nullptr,
+                                 const SolverState* init = nullptr) {
+  if (cfg.mask) throw std::invalid_argument("admm_cg uses M = alpha A^T A; drop the mask/overrides");
+  if (n_cg < 1) throw std::invalid_argument("n_cg must be >= 1");
+  return detail::solve(prob, cfg, true, f_star, init, n_cg);
 }
 
 }  // namespace ncstomo_gpu

@@ -129,6 +129,11 @@ struct ncsg_problem {
   bool rank0 = true;              // adds the replicated blocks to A^T u
   float* atu_ext = nullptr;       // caller-owned A^T u buffer (sharded phases)
   DevBuf<float> atu_own;
+  // admm_cg_solve mode (solvers.cpp:435-440): n_cg > 0 replaces the circulant
+  // x-update by n_cg CG steps on A^T A (batch 1, unsharded, no mask)
+  int n_cg = 0;
+  DevBuf<double> cg_x, cg_r, cg_p;  // fp64 CG iterates
+  DevBuf<float> cg_p32, cg_ap;       // operator input / output
   std::map<int, cudaGraphExec_t> graphs;
   // phase profiling (bench.py): events recorded between the phases of do_step
   bool profiling = false;
@@ -203,8 +208,21 @@ void phase_a(ncsg_problem* p) {
   }
 }
 
+void x_update_cg(ncsg_problem* p);
+void phase_b_circulant(ncsg_problem* p, const float* plain);
+void forward_and_dual(ncsg_problem* p);
+
 // plain != nullptr: A^T u was assembled (and all-reduced) into `plain`.
 void phase_b(ncsg_problem* p, const float* plain = nullptr) {
+  if (p->n_cg > 0 && !plain) {
+    x_update_cg(p);
+  } else {
+    phase_b_circulant(p, plain);
+  }
+  forward_and_dual(p);
+}
+
+void phase_b_circulant(ncsg_problem* p, const float* plain) {
   cudaStream_t s = p->stream.s;
   AtuTerms T = atu_terms(p);
   if (plain) {
@@ -227,6 +245,12 @@ void phase_b(ncsg_problem* p, const float* plain = nullptr) {
   xu.flag = p->flag.p;
   mark(p);
   launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
+}
+
+// Engine::step after the x update (solvers.cpp:146-158): R x+ for the own
+// angles and the fused dual update.
+void forward_and_dual(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
   mark(p);
   if (p->d.kind == NCSG_CT) {
     if (p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
@@ -431,7 +455,7 @@ std::vector<double> seminorm_values(ncsg_problem* p) {
       mq += r[2];
     }
     double a_quad = p->d.alpha * p->d.alpha * aq;
-    double m_quad = p->d.alpha * mq;
+    double m_quad = p->n_cg > 0 ? a_quad : p->d.alpha * mq;  // Cg: M = alpha A^T A (solvers.cpp:174)
     // seminorm_from (solvers.cpp:35-50)
     double rad = t1 + m_quad - a_quad;
     if (rad < 0.0) {
@@ -503,6 +527,70 @@ double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_
     launch_scale(w, static_cast<float>(1.0 / nw), v, nn, s);
   }
   return lambda - shift;
+}
+
+// cg (solvers.cpp:442-463) on NormalMap(stacked) (linear_map.cpp:57-61) for
+// batch entry 0: x_out = n_iters CG steps from 0 for A^T A x = rhs.  The
+// scalars (r.r, p.Ap) are fp64 reductions read back each step, as the
+// reference's loop needs them on the host to decide its breaks.
+void cg_solve(ncsg_problem* p, const float* rhs, int n_iters, double* x_out) {
+  cudaStream_t s = p->stream.s;
+  const size_t nn = p->nn;
+  double* r = p->cg_r.p;
+  double* q = p->cg_p.p;
+  float* q32 = p->cg_p32.p;
+  float* ap = p->cg_ap.p;
+  const int nb = dot_pair_blocks();
+  auto sum_blocks = [&]() {
+    std::vector<double> h(nb);
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), p->red.p, nb * sizeof(double),
+                                    cudaMemcpyDeviceToHost, s));
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+    double acc = 0.0;
+    for (double v : h) acc += v;
+    return acc;
+  };
+  NCSG_CUDA_CHECK(cudaMemsetAsync(x_out, 0, nn * sizeof(double), s));
+  NCSG_CUDA_CHECK(cudaMemsetAsync(r, 0, nn * sizeof(double), s));
+  NCSG_CUDA_CHECK(cudaMemsetAsync(q, 0, nn * sizeof(double), s));
+  // r = rhs, p = rhs (fp64), p32 = rhs; r.r comes out of the same kernel
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(q32, rhs, nn * 4, cudaMemcpyDeviceToDevice, s));
+  launch_cg_update(r, r, q, q32, -1.0, nn, p->red.p, s);  // r = 0 + 1 * rhs
+  double rs = sum_blocks();
+  launch_cg_direction(q, r, 0.0, q32, nn, s);              // p = r
+  for (int it = 0; it < n_iters; ++it) {
+    if (rs == 0.0) break;
+    stacked_forward(p, q32, p->dxT.p, p->adx.p);
+    if (p->d.kind == NCSG_CT)
+      launch_radon_adjoint_partial(*p->radon, p->adx.p, p->range, p->bp_part.p, 1, s);
+    launch_atu_assemble(atu_terms_for(p, p->adx.p), ap, 1, s);
+    launch_cg_dot(q, ap, nn, p->red.p, s);
+    const double pap = sum_blocks();
+    if (pap <= 0.0) break;
+    const double a = rs / pap;
+    launch_cg_update(x_out, r, q, ap, a, nn, p->red.p, s);
+    const double rs_new = sum_blocks();
+    const double beta = rs_new / rs;
+    launch_cg_direction(q, r, beta, q32, nn, s);
+    rs = rs_new;
+  }
+}
+
+// Engine::step x-update in Cg mode (solvers.cpp:138-145): w = CG(A^T A, A^T u)
+// / alpha; x -= w (x_old kept for the extrapolation), finiteness flag.
+void x_update_cg(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  ensure_scratch(p);
+  float* atu = ncsg_atu_buffer(p);
+  AtuTerms T = atu_terms(p);
+  mark(p);
+  launch_atu_assemble(T, atu, 1, s);
+  mark(p);
+  cg_solve(p, atu, p->n_cg, p->cg_x.p);
+  mark(p);
+  launch_x_update(p->x.p, p->x_old.p, p->cg_x.p, 1.0 / p->d.alpha, p->nn, p->flag.p, s);
+  if (p->d.kind == NCSG_CT && !p->radon->orbit_mode)
+    prepare_forward_aux(*p->radon, p->x.p, p->xT.p, 1, s);  // x^T for class-H angles
 }
 
 void upload_f64(ncsg_problem* p, const double* h, float* d, size_t count) {
@@ -880,6 +968,11 @@ ncsg_status ncsg_step_graph(ncsg_problem* p, int iters) {
   return guard([&] {
     NCSG_CUDA_CHECK(cudaSetDevice(p->device));
     if (iters <= 0) return;
+    if (p->n_cg > 0) {  // CG reads its scalars back every step: not capturable
+      for (int k = 0; k < iters; ++k) do_step(p);
+      p->iter += iters;
+      return;
+    }
     auto it = p->graphs.find(iters);
     if (it == p->graphs.end()) {
       cudaGraph_t graph;
@@ -988,7 +1081,7 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
     engine_init(p);
     reset_flag(p);
     if (screen_est) *screen_est = NAN;
-    if (check_step_condition) {  // solvers.cpp:278 (warning, not an error)
+    if (check_step_condition && p->n_cg == 0) {  // solvers.cpp:207, 278 (warning only)
       if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
         throw Error{NCSG_INVALID, "the step-condition screen needs the unsharded problem"};
       double e = screen_estimate(p, seed, 40, nullptr);
@@ -1000,7 +1093,8 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
     auto emit = [&](int64_t k, const std::vector<double>& sem) {
       auto f = objective_values(p);
       double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
-      for (int b = 0; b < B; ++b) rec[b].push_back({k, f[b], 0.0, sem[b], ms});
+      const int64_t axis = p->n_cg > 0 ? p->n_cg : 1;  // solvers.cpp:279
+      for (int b = 0; b < B; ++b) rec[b].push_back({k * axis, f[b], 0.0, sem[b], ms});
     };
     emit(0, std::vector<double>(B, 0.0));
     ensure_scratch(p);
@@ -1040,6 +1134,29 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
   });
 }
 
+
+ncsg_status ncsg_set_cg(ncsg_problem* p, int n_cg) {
+  return guard([&] {
+    // admm_cg_solve (solvers.cpp:435-440) / Engine Cg mode (solvers.cpp:111-113)
+    if (n_cg < 0) throw Error{NCSG_INVALID, "n_cg must be >= 1"};
+    if (n_cg > 0) {
+      if (p->has_mask)
+        throw Error{NCSG_INVALID, "admm_cg uses M = alpha A^T A; drop the mask/overrides"};
+      if (p->batch != 1) throw Error{NCSG_INVALID, "the CG x-update runs one problem (batch 1)"};
+      if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
+        throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};
+      NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+      if (!p->cg_x.n) {
+        p->cg_x.alloc(p->nn);
+        p->cg_r.alloc(p->nn);
+        p->cg_p.alloc(p->nn);
+        p->cg_p32.alloc(p->nn);
+        p->cg_ap.alloc(p->nn);
+      }
+    }
+    p->n_cg = n_cg;
+  });
+}
 
 /* ---------------------------------------------------------------- setup path */
 

@@ -440,6 +440,63 @@ __global__ void screen_combine_kernel(const float* v, const float* atav, const f
   }
 }
 
+// CG step of cg (solvers.cpp:456-459) with fp64 iterates (the operator runs
+// in fp32): x += a p; r -= a ap; per-block partial sums of r.r into out[block].
+__global__ void cg_update_kernel(double* x, double* r, const double* p, const float* ap,
+                                 double a, size_t count, double* out) {
+  __shared__ double sh[32];
+  double rr = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    x[i] += a * p[i];
+    const double ri = r[i] - a * static_cast<double>(ap[i]);
+    r[i] = ri;
+    rr += ri * ri;
+  }
+  const double t = block_sum(rr, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
+// p = r + beta p (solvers.cpp:461), plus the fp32 copy the operator reads.
+__global__ void cg_direction_kernel(double* p, const double* r, double beta, float* p32,
+                                    size_t count) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const double v = r[i] + beta * p[i];
+    p[i] = v;
+    p32[i] = static_cast<float>(v);
+  }
+}
+
+// p.ap with fp64 p (power of the CG denominator) -- per-block partials.
+__global__ void cg_dot_kernel(const double* p, const float* ap, size_t count, double* out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    acc += p[i] * static_cast<double>(ap[i]);
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[blockIdx.x] = t;
+}
+
+// ADMM-CG x update (solvers.cpp:138-145): x_old = x; x -= inv_alpha * d; the
+// check_finite flag (solvers.cpp:248-255) and the step counter like c2r.
+__global__ void x_update_kernel(float* x, float* x_old, const double* d, double inv_alpha,
+                                size_t count, int* flag) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && flag) atomicAdd(flag + 1, 1);
+  int bad = 0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float xo = x[i];
+    x_old[i] = xo;
+    const float xn = static_cast<float>(xo - inv_alpha * d[i]);
+    x[i] = xn;
+    bad |= !isfinite(xn);
+  }
+  if (flag && __syncthreads_or(bad) && threadIdx.x == 0)
+    atomicMin(flag, *(volatile int*)(flag + 1));
+}
+
 __global__ void scale_kernel(const float* in, float s, float* out, size_t count) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -495,6 +552,33 @@ void launch_screen_combine(const float* v, const float* atav, const float* cv, f
 
 void launch_scale(const float* in, float sc, float* out, size_t count, cudaStream_t s) {
   scale_kernel<<<grid_for(count, 256), 256, 0, s>>>(in, sc, out, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_cg_update(double* x, double* r, const double* p, const float* ap, double a,
+                      size_t count, double* out, cudaStream_t s) {
+  cg_update_kernel<<<dot_pair_blocks(), 256, 0, s>>>(x, r, p, ap, a, count, out);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_cg_direction(double* p, const double* r, double beta, float* p32, size_t count,
+                         cudaStream_t s) {
+  cg_direction_kernel<<<grid_for(count, 256), 256, 0, s>>>(p, r, beta, p32, count);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_cg_dot(const double* p, const float* ap, size_t count, double* out, cudaStream_t s) {
+  cg_dot_kernel<<<dot_pair_blocks(), 256, 0, s>>>(p, ap, count, out);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_x_update(float* x, float* x_old, const double* d, double inv_alpha, size_t count,
+                     int* flag, cudaStream_t s) {
+  x_update_kernel<<<grid_for(count, 256), 256, 0, s>>>(x, x_old, d, inv_alpha, count, flag);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

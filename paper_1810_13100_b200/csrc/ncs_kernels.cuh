@@ -79,4 +79,14 @@ void launch_dot_pair(const float* a, const float* b, const float* c, const float
 void launch_screen_combine(const float* v, const float* atav, const float* cv, float alpha,
                            float gamma, float shift, float* w, size_t count, cudaStream_t s);
 void launch_scale(const float* in, float sc, float* out, size_t count, cudaStream_t s);
+
+// ADMM-CG x-update (admm_cg_solve, solvers.cpp:135-145, 442-463): fp64 CG
+// iterates, fp32 operator.  out[dot_pair_blocks()] = per-block partial sums.
+void launch_cg_update(double* x, double* r, const double* p, const float* ap, double a,
+                      size_t count, double* out, cudaStream_t s);
+void launch_cg_direction(double* p, const double* r, double beta, float* p32, size_t count,
+                         cudaStream_t s);
+void launch_cg_dot(const double* p, const float* ap, size_t count, double* out, cudaStream_t s);
+void launch_x_update(float* x, float* x_old, const double* d, double inv_alpha, size_t count,
+                     int* flag, cudaStream_t s);
 }  // namespace ncsg

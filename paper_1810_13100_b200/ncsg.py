@@ -66,6 +66,7 @@ SYMBOLS = [
     "ncsg_solve", "ncsg_step_phase_a", "ncsg_atu_buffer", "ncsg_step_phase_b",
     "ncsg_profile_begin", "ncsg_profile_end", "ncsg_launch_count", "ncsg_set_atu_buffer",
     "ncsg_calibrate_scale", "ncsg_radon_dc_response", "ncsg_screen_step_condition",
+    "ncsg_set_cg",
 ]
 PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
 
@@ -117,6 +118,7 @@ def lib():
     L.ncsg_solve.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_void_p,
                              C.POINTER(RecordRow), C.c_int, C.POINTER(C.c_int),
                              C.POINTER(C.c_double)]
+    L.ncsg_set_cg.argtypes = [C.c_void_p, C.c_int]
     L.ncsg_calibrate_scale.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
     L.ncsg_radon_dc_response.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     L.ncsg_screen_step_condition.argtypes = [C.c_void_p, C.c_uint64, C.c_int,
@@ -383,6 +385,11 @@ class Problem:
         out = np.zeros(self.batch)
         _check(lib().ncsg_objective(self._h, out), "objective")
         return out
+
+    def set_cg(self, n_cg: int) -> None:
+        """admm_cg_solve mode (solvers.cpp:435-440): x-update by n_cg CG steps
+        on A^T A (no mask, batch 1); n_cg = 0 restores the circulant solve."""
+        _check(lib().ncsg_set_cg(self._h, n_cg), "set_cg")
 
     def screen(self, seed: int = 0, iters: int = 40) -> tuple[float, float]:
         """Engine::screen_step_condition (solvers.cpp:206-245): (estimate of the

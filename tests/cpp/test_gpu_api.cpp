@@ -164,6 +164,22 @@ int main() {
     cfg.gamma = 10.0 * A * n;  // comfortably above
     SolveResult big = ncs_solve(prob, cfg);
     CHECK(big.record.warnings.empty() && big.record.rows.size() == 4, "no warning when it holds");
+    // admm_cg_solve (solvers.cpp:435-440): CG x-update, record axis in CG steps
+    SolverConfig acfg;
+    acfg.alpha = 0.5;
+    acfg.max_iters = 6;
+    acfg.record_every = 3;
+    SolveResult adm = admm_cg_solve(prob, acfg, 4);
+    CHECK(adm.record.rows.size() == 3 && adm.record.rows.back().iter == 24 &&
+              std::isfinite(adm.objective),
+          "admm_cg_solve runs, iterations counted in CG steps");
+    bool rejected = false;
+    try {
+      admm_cg_solve(prob, cfg, 4);  // cfg has a mask
+    } catch (const std::invalid_argument&) {
+      rejected = true;
+    }
+    CHECK(rejected, "admm_cg_solve rejects a mask");
     write_record_csv("/tmp/ncsg_record_test.csv", big.record);
     std::ifstream in("/tmp/ncsg_record_test.csv");
     std::string header, first;
