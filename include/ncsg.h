@@ -98,13 +98,16 @@ ncsg_status ncsg_mask_apply_host(int n, const double* mask, const double* x, dou
  *                 (pipeline.cpp:69-98)
  *   NCSG_DENOISE  blocks {1, I, QuadraticConj, b}, {beta/alpha, D, ...}
  *                 (the SplitProblem built in test_solvers.cpp:646-664)
+ *   NCSG_PET      blocks {1, R, PoissonConj(counts = b, alpha), 0},
+ *                 {beta/alpha, D, ...} -- assemble_problem with model "pet"
+ *                 (pipeline.cpp:84-89; prox.cpp:9-13, 47-74)
  * With positivity != 0 a third block {1, I, NonnegConj} is appended
  * (pipeline.cpp:93-96).  `mask` (nullable) is the SolverConfig::mask -- the
  * metric surrogate C; NULL selects M = gamma I, i.e. pdhg_solve
  * (solvers.cpp:428-433).  The engine applies pinv(gamma + alpha*C) with
  * cfg.pinv_rel_tol (solvers.cpp:93-99).  `b` holds `batch` offsets back to
  * back (m each). */
-typedef enum { NCSG_CT = 0, NCSG_DENOISE = 1 } ncsg_kind;
+typedef enum { NCSG_CT = 0, NCSG_DENOISE = 1, NCSG_PET = 2 } ncsg_kind;
 
 typedef struct {
   int kind;          /* ncsg_kind */

@@ -203,6 +203,22 @@ struct ModelParams {
   bool positivity = false;
 };
 
+/// default_model_params (pipeline.cpp:54-67).
+inline ModelParams default_model_params(const std::string& model) {
+  ModelParams p;
+  p.model = model;
+  if (model == "ct") return p;
+  if (model == "pet") {
+    p.alpha = 1e-3;
+    p.beta = 1e-3;
+    p.gamma = 1e-4;
+    p.lambda = 1e-3;
+    p.dc = 1e-2;
+    return p;
+  }
+  throw std::invalid_argument("unknown model \"" + model + "\"");
+}
+
 /// calibrate_scale(NormalMap(geometry), radon_mask(n, 1, 1), n_samples, seed)
 /// (circulant.cpp:142-169), computed on the GPU.
 inline double calibrate_scale(const RadonMap& geometry, int n_samples, std::uint64_t seed) {
@@ -253,14 +269,20 @@ struct SplitProblem {
 
 inline SplitProblem assemble_problem(std::span<const double> sino, const RadonMap& geometry,
                                      const ModelParams& p) {
-  if (p.model != "ct") throw std::invalid_argument("unknown model \"" + p.model + "\"");
+  if (p.model != "ct" && p.model != "pet")
+    throw std::invalid_argument("unknown model \"" + p.model + "\"");
   if (p.alpha <= 0.0 || p.beta <= 0.0)
     throw std::invalid_argument("alpha and beta must be positive");
   if (p.lambda < 0.0) throw std::invalid_argument("lambda must be nonnegative");
   if (geometry.range_size() != sino.size())
     throw std::invalid_argument("sinogram shape does not match the geometry");
   SplitProblem s;
-  s.kind = NCSG_CT;
+  // ct: {1, R, QuadraticConj, sino}; pet: {1, R, PoissonConj(sino, alpha), 0}
+  // (pipeline.cpp:84-89) -- the counts travel in the offset slot
+  s.kind = p.model == "pet" ? NCSG_PET : NCSG_CT;
+  if (s.kind == NCSG_PET)
+    for (double c : sino)
+      if (c < 0.0) throw std::invalid_argument("Poisson counts must be nonnegative");
   s.n = geometry.n();
   s.n_angles = geometry.n_angles();
   s.n_det = geometry.n_detectors();

@@ -537,7 +537,7 @@ static void prob_init(Prob* p, int kind, int n, int angles, int det, double alph
   p->beta = beta;
   p->lambda = lambda;
   p->nn = (size_t)n * n;
-  p->m0 = kind == 0 ? (size_t)angles * det : p->nn;
+  p->m0 = kind != 1 ? (size_t)angles * det : p->nn; /* CT (0) and PET (2) project */
   p->g = 2 * (size_t)n * (n - 1);
   p->range = p->m0 + p->g + (positivity ? p->nn : 0);
   p->w_d = beta / alpha;
@@ -547,7 +547,7 @@ static void prob_init(Prob* p, int kind, int n, int angles, int det, double alph
 
 /* StackedMap::forward (linear_map.cpp:39-45) */
 static void stacked_forward(const Prob* p, const double* x, double* out) {
-  if (p->kind == 0)
+  if (p->kind != 1)
     orc_radon_forward(p->n, p->angles, p->det, x, out, p->nthreads);
   else
     memcpy(out, x, sizeof(double) * p->nn);
@@ -565,7 +565,7 @@ static void stacked_forward(const Prob* p, const double* x, double* out) {
 /* StackedMap::adjoint (linear_map.cpp:47-55) */
 static void stacked_adjoint(const Prob* p, const double* u, double* out, double* tmp) {
   memset(out, 0, sizeof(double) * p->nn);
-  if (p->kind == 0)
+  if (p->kind != 1)
     orc_radon_adjoint(p->n, p->angles, p->det, u, tmp, p->nthreads);
   else
     memcpy(tmp, u, sizeof(double) * p->nn);
@@ -584,11 +584,26 @@ static void stacked_adjoint(const Prob* p, const double* u, double* out, double*
 static double objective_from_ax(const Prob* p, const double* ax) {
   double total = 0.0;
   double acc = 0.0;
-  for (size_t j = 0; j < p->m0; ++j) {
-    double z = ax[j] - p->b[j];
-    acc += z * z;
+  if (p->kind == 2) {
+    /* PoissonConj::objective (prox.cpp:62-74), counts in b */
+    for (size_t j = 0; j < p->m0; ++j) {
+      double y = ax[j], c = p->b[j];
+      if (c > 0.0) {
+        if (y <= 0.0) return INFINITY;
+        acc += y - c * log(y);
+      } else {
+        if (y < 0.0) return INFINITY;
+        acc += y;
+      }
+    }
+    total += acc;
+  } else {
+    for (size_t j = 0; j < p->m0; ++j) {
+      double z = ax[j] - p->b[j];
+      acc += z * z;
+    }
+    total += 0.5 * acc;
   }
-  total += 0.5 * acc;
   acc = 0.0;
   const double* g = ax + p->m0;
   for (size_t j = 0; j < p->g; ++j) acc += fabs(g[j]);
@@ -608,9 +623,20 @@ static double objective_from_ax(const Prob* p, const double* ax) {
 }
 
 /* prox evaluate per block (solvers.cpp:151-156; prox.cpp:21-44,103-105) */
+/* prox_conj_poisson (prox.cpp:9-13) */
+static double prox_conj_poisson(double u, double c) {
+  double d = u - 1.0;
+  return 1.0 + 0.5 * (d - sqrt(d * d + 4.0 * c));
+}
+
 static void prox_all(const Prob* p, double* r) {
-  double s = 1.0 / (1.0 + p->alpha);
-  for (size_t j = 0; j < p->m0; ++j) r[j] *= s;
+  if (p->kind == 2) {
+    /* PoissonConj::evaluate (prox.cpp:56-60): c = alpha * counts */
+    for (size_t j = 0; j < p->m0; ++j) r[j] = prox_conj_poisson(r[j], p->alpha * p->b[j]);
+  } else {
+    double s = 1.0 / (1.0 + p->alpha);
+    for (size_t j = 0; j < p->m0; ++j) r[j] *= s;
+  }
   double* g = r + p->m0;
   double bd = p->bound;
   for (size_t j = 0; j < p->g; ++j) {
@@ -736,7 +762,7 @@ static int engine_step(Engine* e, double* x, double* u) {
   for (size_t j = 0; j < p->nn; ++j) x[j] -= e->w[j];
   stacked_forward(p, x, e->ax_new);
   for (size_t i = 0; i < p->range; ++i) {
-    double bi = i < p->m0 ? p->b[i] : 0.0;
+    double bi = (i < p->m0 && p->kind != 2) ? p->b[i] : 0.0; /* PET block: offset {} */
     e->r[i] = u[i] + e->alpha * (2.0 * e->ax_new[i] - e->ax[i] - bi);
   }
   prox_all(p, e->r);
@@ -864,7 +890,7 @@ int orc_solve_ex(int kind, int n, int angles, int det, double alpha, double beta
   if (max_iters < 0 || record_every < 1 || alpha <= 0.0) return 2;
   if (!mask && n_cg <= 0 && gamma <= 0.0) return 2;
   if (n_cg > 0 && mask) return 2; /* admm_cg uses M = alpha A^T A (solvers.cpp:437-438) */
-  if (kind == 0 && orc_radon_check(n, angles, det)) return 2;
+  if (kind != 1 && orc_radon_check(n, angles, det)) return 2;
   Prob p;
   prob_init(&p, kind, n, angles, det, alpha, beta, lambda, positivity, b, nthreads);
   Engine e;

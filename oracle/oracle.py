@@ -510,7 +510,7 @@ class Prob:
 
     @property
     def m0(self):
-        return self.angles * self.det if self.kind == 0 else self.n * self.n
+        return self.angles * self.det if self.kind != 1 else self.n * self.n
 
     @property
     def g(self):

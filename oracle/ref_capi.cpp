@@ -70,12 +70,12 @@ struct Desc {
 };
 
 SplitProblem build_problem(const Desc& d, const double* b) {
-  if (d.kind == 0) {
+  if (d.kind == 0 || d.kind == 2) {  // CT-TV or PET-TV (assemble_problem, pipeline.cpp:69-98)
     auto geom = std::make_shared<RadonMap>(d.n, d.angles, d.det);
     Sinogram s(d.angles, d.det);
     std::memcpy(s.v.data(), b, sizeof(double) * s.v.size());
     ModelParams p;
-    p.model = "ct";
+    p.model = d.kind == 2 ? "pet" : "ct";
     p.alpha = d.alpha;
     p.beta = d.beta;
     p.lambda = d.lambda;
@@ -228,7 +228,7 @@ int ref_rng_normals(uint64_t seed, uint64_t stream, int count, double* out) {
 int ref_problem_sizes(int kind, int n, int angles, int det, int positivity, int64_t* range) {
   return guard([&] {
     Desc d{kind, n, angles, det, 1.0, 1.0, 1.0, positivity};
-    std::size_t m = kind == 0 ? static_cast<std::size_t>(angles) * det
+    std::size_t m = kind != 1 ? static_cast<std::size_t>(angles) * det
                               : static_cast<std::size_t>(n) * n;
     std::vector<double> b(m, 0.0);
     SplitProblem p = build_problem(d, b.data());

@@ -168,7 +168,7 @@ AtuTerms atu_terms(ncsg_problem* p) { return atu_terms_for(p, p->u.p); }
 AtuTerms atu_terms_for(ncsg_problem* p, float* u) {
   AtuTerms T;
   T.n = p->d.n;
-  if (p->d.kind == NCSG_CT) {
+  if (p->d.kind != NCSG_DENOISE) {
     T.bp_part = p->bp_part.p;
     T.nV = p->radon->bp_chunks[0];
     T.nH = p->radon->bp_chunks[1];
@@ -201,7 +201,7 @@ void mark(ncsg_problem* p) {
 
 void phase_a(ncsg_problem* p) {
   mark(p);
-  if (p->d.kind == NCSG_CT) {
+  if (p->d.kind != NCSG_DENOISE) {
     // u_s is the first m0 entries of each problem's dual (stride range).
     launch_radon_adjoint_partial(*p->radon, p->u.p, p->range, p->bp_part.p, p->batch,
                                  p->stream.s);
@@ -238,7 +238,7 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
   XUpdate xu;
   xu.x = p->x.p;
   xu.x_old = p->x_old.p;
-  xu.xT = (p->d.kind == NCSG_CT && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
+  xu.xT = (p->d.kind != NCSG_DENOISE && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
               ? p->xT.p
               : nullptr;
   xu.subtract = 1;
@@ -252,7 +252,7 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
 void forward_and_dual(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   mark(p);
-  if (p->d.kind == NCSG_CT) {
+  if (p->d.kind != NCSG_DENOISE) {
     if (p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
     launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
   }
@@ -292,7 +292,7 @@ void do_step(ncsg_problem* p) {
 // blocks are recomputed from x each step).
 void engine_init(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
-  if (p->d.kind == NCSG_CT) {
+  if (p->d.kind != NCSG_DENOISE) {
     prepare_forward_aux(*p->radon, p->x.p, p->xT.p, p->batch, s);
     launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
     launch_strip_sum(*p->radon, p->fp_part.p, p->axs.p, p->batch, s);
@@ -347,8 +347,8 @@ std::vector<double> objective_values(ncsg_problem* p) {
       mx = std::max(mx, r[2]);
       mn = std::min(mn, r[3]);
     }
-    // QuadraticConj::objective + ScaledL1Conj::objective (prox.cpp:26-44)
-    double total = 0.5 * q + static_cast<double>(p->bound) * l1;
+    // QuadraticConj / PoissonConj::objective + ScaledL1Conj::objective (prox.cpp:26-70)
+    double total = (p->d.kind == NCSG_PET ? q : 0.5 * q) + static_cast<double>(p->bound) * l1;
     if (p->d.positivity) {  // NonnegConj::objective (prox.cpp:107-114)
       double tol = 1e-9 * std::max(1.0, mx);
       if (mn < -tol) total = INFINITY;
@@ -389,7 +389,7 @@ void ensure_scratch(ncsg_problem* p) {
 // linear_map.cpp:39-45).
 void stacked_forward(ncsg_problem* p, const float* img, float* imgT, float* out) {
   cudaStream_t s = p->stream.s;
-  if (p->d.kind == NCSG_CT) {
+  if (p->d.kind != NCSG_DENOISE) {
     prepare_forward_aux(*p->radon, img, imgT, p->batch, s);
     launch_radon_forward_partial(*p->radon, img, imgT, p->fp_part.p, p->batch, s);
   }
@@ -513,7 +513,7 @@ double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_
   double lambda = 0.0;
   for (int it = 0; it < iters; ++it) {
     stacked_forward(p, v, p->dxT.p, av);
-    if (p->d.kind == NCSG_CT)
+    if (p->d.kind != NCSG_DENOISE)
       launch_radon_adjoint_partial(*p->radon, av, p->range, p->bp_part.p, 1, s);
     launch_atu_assemble(atu_terms_for(p, av), atav, 1, s);
     if (cv) apply_filter(p, v, p->maskT_orig.p, cv);
@@ -561,7 +561,7 @@ void cg_solve(ncsg_problem* p, const float* rhs, int n_iters, double* x_out) {
   for (int it = 0; it < n_iters; ++it) {
     if (rs == 0.0) break;
     stacked_forward(p, q32, p->dxT.p, p->adx.p);
-    if (p->d.kind == NCSG_CT)
+    if (p->d.kind != NCSG_DENOISE)
       launch_radon_adjoint_partial(*p->radon, p->adx.p, p->range, p->bp_part.p, 1, s);
     launch_atu_assemble(atu_terms_for(p, p->adx.p), ap, 1, s);
     launch_cg_dot(q, ap, nn, p->red.p, s);
@@ -589,7 +589,7 @@ void x_update_cg(ncsg_problem* p) {
   cg_solve(p, atu, p->n_cg, p->cg_x.p);
   mark(p);
   launch_x_update(p->x.p, p->x_old.p, p->cg_x.p, 1.0 / p->d.alpha, p->nn, p->flag.p, s);
-  if (p->d.kind == NCSG_CT && !p->radon->orbit_mode)
+  if (p->d.kind != NCSG_DENOISE && !p->radon->orbit_mode)
     prepare_forward_aux(*p->radon, p->x.p, p->xT.p, 1, s);  // x^T for class-H angles
 }
 
@@ -815,7 +815,8 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
   return guard([&] {
     if (!desc || !out) throw Error{NCSG_INVALID, "null problem descriptor"};
     const ncsg_problem_desc& d = *desc;
-    if (d.kind != NCSG_CT && d.kind != NCSG_DENOISE) throw Error{NCSG_INVALID, "unknown problem kind"};
+    if (d.kind != NCSG_CT && d.kind != NCSG_DENOISE && d.kind != NCSG_PET)
+      throw Error{NCSG_INVALID, "unknown problem kind"};
     if (d.n < 2) throw Error{NCSG_INVALID, "image size must be >= 2"};
     if (d.batch < 1) throw Error{NCSG_INVALID, "batch must be >= 1"};
     // assemble_problem / Engine validation (pipeline.cpp:74-77, solvers.cpp:91-106)
@@ -835,7 +836,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     p->g = 2 * static_cast<size_t>(d.n) * (d.n - 1);
     p->wd = static_cast<float>(d.beta / d.alpha);
     p->bound = static_cast<float>(d.lambda * d.alpha / d.beta);
-    if (d.kind == NCSG_CT) {
+    if (d.kind != NCSG_DENOISE) {
       Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end);
       p->m0 = static_cast<size_t>(d.n_angles) * d.n_det;
       int ab = d.angle_end > 0 ? d.angle_begin : 0;
@@ -889,7 +890,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     p->u.alloc(p->range * p->batch);
     p->b.alloc(p->m0 * p->batch);
     upload_f64(p.get(), desc->b, p->b.p, p->m0 * p->batch);
-    if (d.kind == NCSG_CT) {
+    if (d.kind != NCSG_DENOISE) {
       p->axs.alloc(p->m0 * p->batch);
       p->fp_part.alloc(p->m0 * p->radon->fp_slots() * p->batch);
       p->fp_part.zero(s);

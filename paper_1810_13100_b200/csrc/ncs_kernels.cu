@@ -62,6 +62,26 @@ __global__ void dual_update_kernel(DualArgs a) {
         ax[i] = rx;
         bad |= isnan(un);
       }
+    } else if (a.kind == NCSG_PET) {
+      // PoissonConj block (pipeline.cpp:86-88): offset 0, counts in b,
+      // u = prox_conj_poisson(r, alpha * counts) (prox.cpp:9-13, 56-60) in the
+      // cancellation-free form 1 + (d - sqrt(d^2 + 4c)) / 2 = 1 - 2c / (d + sqrt(...)).
+      const float* part = a.fp_part + b * a.n_strips * a.m;
+      float* us = a.u0 + b * a.u_stride;
+      float* ax = a.axs + b * a.m;
+      const float* cnt = a.b + b * a.m;
+      for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+        float rx = 0.f;
+        for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
+        const double r = static_cast<double>(us[i]) + alpha * (2.f * rx - ax[i]);
+        const double c = static_cast<double>(alpha) * cnt[i];
+        const double d = r - 1.0;
+        const double sq = sqrt(d * d + 4.0 * c);
+        const double un = d > 0.0 ? 1.0 - 2.0 * c / (d + sq) : 1.0 + 0.5 * (d - sq);
+        us[i] = static_cast<float>(un);
+        ax[i] = rx;
+        bad |= isnan(un);
+      }
     } else {
       float* ud = a.u0 + b * a.u_stride;
       const float* bb = a.b + b * nn;
@@ -137,6 +157,17 @@ __global__ void objective_kernel(ObjArgs a) {
     for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
       const double z = static_cast<double>(ax[i]) - static_cast<double>(bb[i]);
       q += z * z;
+    }
+  } else if (a.kind == NCSG_PET) {
+    // PoissonConj::objective (prox.cpp:62-74): sum y - c log y, +inf outside the domain
+    const float* ax = a.axs + b * a.m;
+    const float* cnt = a.b + b * a.m;
+    for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+      const double y = ax[i], c = cnt[i];
+      if (c > 0.0)
+        q += y <= 0.0 ? INFINITY : y - c * log(y);
+      else
+        q += y < 0.0 ? INFINITY : y;
     }
   } else {
     const float* bb = a.b + b * nn;
@@ -278,7 +309,7 @@ __global__ void stacked_rest_kernel(StackArgs a) {
        i += stride) {
     float v;
     if (i < a.m0) {
-      if (a.kind == NCSG_CT) {
+      if (a.kind != NCSG_DENOISE) {
         const float* part = a.fp_part + b * a.n_strips * a.m0 + i;
         v = 0.f;
         for (int k = 0; k < a.n_strips; ++k) v += part[k * a.m0];

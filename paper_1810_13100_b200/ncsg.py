@@ -268,7 +268,7 @@ def mask_apply(mask, x, device: int = 0) -> np.ndarray:
     return out
 
 
-CT, DENOISE = 0, 1
+CT, DENOISE, PET = 0, 1, 2
 
 
 @dataclass
@@ -297,7 +297,7 @@ class Problem:
         self.alpha, self.beta, self.lam, self.gamma = alpha, beta, lam, gamma
         self.positivity = positivity
         b = np.ascontiguousarray(b, np.float64).ravel()
-        m = n_angles * n_det if kind == CT else n * n
+        m = n_angles * n_det if kind != DENOISE else n * n
         if b.size != batch * m:  # the C ABI reads batch * m offsets from b
             raise ValueError(f"offset size mismatch: got {b.size}, need batch*m = {batch * m}")
         if mask is not None and np.asarray(mask).size != n * n:

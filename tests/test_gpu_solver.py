@@ -347,3 +347,36 @@ def test_admm_cg_rejects_mask_and_batch(ncsg, port):
     q = gpu_problem(ncsg, prob, gamma, None, batch_b=[prob.b, prob.b])
     with pytest.raises(ValueError):
         q.set_cg(4)
+
+
+@pytest.mark.parametrize("positivity", [False, True])
+def test_pet_parity(ncsg, port, positivity):
+    # PET-TV (assemble_problem model "pet", pipeline.cpp:84-89): the dual
+    # update applies prox_conj_poisson (prox.cpp:9-13) to the sinogram block,
+    # the objective is PoissonConj::objective (prox.cpp:62-74).
+    from paper_1810_13100_b200 import datagen
+
+    n, A = 32, 24
+    D = port.default_detector_count(n)
+    x = datagen.phantom(n, 5, 11)
+    y = port.radon_forward(x, A, D)
+    counts = np.random.default_rng(12).poisson(np.maximum(y, 0.0) * 10.0).astype(float)
+    alpha = 0.05
+    dc = float((port.radon_forward(np.ones((n, n)), A, D) ** 2).sum() / n ** 2)
+    mask = port.radon_mask(n, port.calibrate_scale(n, A, D, 8, 0), dc) + port.laplacian_mask(n)
+    if positivity:
+        mask = mask + 1.0
+    prob = Prob(2, n, A, D, alpha, alpha, 0.01, counts, positivity=positivity)
+    gamma = 1.2 * port.screen(prob, 0.0, mask, iters=40)
+    o = port.solve(prob, gamma, mask, 60, record_every=20)
+    p = ncsg.Problem(ncsg.PET, n, alpha, alpha, 0.01, gamma, counts, mask=mask, n_angles=A,
+                     n_det=D, positivity=positivity)
+    p.set_state()
+    g = p.solve(60, record_every=20)
+    assert rel(g.x[0], o.x) <= TOL, rel(g.x[0], o.x)
+    assert rel(g.u[0], o.u) <= TOL, rel(g.u[0], o.u)
+    go, oo = g.rows[0][:, 1], o.rows[:, 1]
+    fin = np.isfinite(oo)
+    np.testing.assert_array_equal(np.isfinite(go), fin)
+    if fin.any():  # NonnegConj makes rows +inf while x has negative pixels
+        assert np.max(np.abs(go[fin] - oo[fin]) / np.abs(oo[fin])) <= TOL

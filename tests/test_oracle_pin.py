@@ -339,3 +339,21 @@ def test_admm_cg_matches_reference_bitwise(port, ref, kind, positivity):
     np.testing.assert_array_equal(r1.u, r2.u)
     np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
     assert r1.rows[-1, 0] == 12 * 4
+
+
+@pytest.mark.parametrize("positivity", [False, True])
+def test_pet_model_matches_reference_bitwise(port, ref, positivity):
+    # assemble_problem with model "pet" (pipeline.cpp:84-89): PoissonConj data
+    # block (prox.cpp:9-13, 47-74) on Poisson counts, TV block as for CT.
+    n, A = 16, 12
+    D = port.default_detector_count(n)
+    x = ref.make_phantom(n, [[1.0, 0.1, -0.05, 0.7, 0.5, 0.0]])
+    y = ref.radon_forward(x, A, D)
+    counts = np.random.default_rng(5).poisson(np.maximum(y, 0.0) * 20.0).astype(float)
+    prob = Prob(2, n, A, D, 0.05, 0.05, 0.01, counts, positivity=positivity)
+    mask = ref.ct_metric_mask(n, A, D, 0.05, 0.05, dc=300.0, positivity=positivity)
+    r1 = ref.solve(prob, 3.0, mask, 12, record_every=4)
+    r2 = port.solve(prob, 3.0, mask, 12, record_every=4, threads=1)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    np.testing.assert_array_equal(r1.u, r2.u)
+    np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
