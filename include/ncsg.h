@@ -76,6 +76,36 @@ ncsg_status ncsg_radon_forward_host(const ncsg_radon* r, const double* x, double
 ncsg_status ncsg_radon_adjoint_host(const ncsg_radon* r, const double* u, double* out,
                                     int batch);
 
+/* ------------------------------------------------------- sparse / fan beam
+ * SparseMap (sparse.hpp:21-43): CSR over sinogram bins (view-major) with the
+ * stored transpose for the adjoint (deterministic, exact to the matrix). */
+typedef struct ncsg_sparse ncsg_sparse;
+
+/* build_fanbeam(n, FanBeamGeometry{views, rays, source_radius, fan_angle})
+ * (fanbeam.cpp:43-111, Siddon lengths in fp64 on the host), same validation
+ * messages; the matrix is uploaded as fp32 values / int32 indices. */
+ncsg_status ncsg_fanbeam_create(int n, int views, int rays, double source_radius,
+                                double fan_angle, int device, ncsg_sparse** out);
+/* FanBeamGeometry::defaults (fanbeam.cpp:10-17): radius n, fan covering the
+ * corner circle. */
+ncsg_status ncsg_fan_defaults(int n, double* source_radius, double* fan_angle);
+/* SparseMap(n, views, rays, triplets) (sparse.cpp:9-45) from COO triplets. */
+ncsg_status ncsg_sparse_create(int n, int views, int rays, int64_t nnz, const int64_t* rows,
+                               const int64_t* cols, const double* vals, int device,
+                               ncsg_sparse** out);
+ncsg_status ncsg_sparse_destroy(ncsg_sparse* a);
+int64_t ncsg_sparse_nnz(const ncsg_sparse* a);
+/* SparseMap::forward / adjoint (sparse.cpp:55-71) on device arrays (batch
+ * back to back) or fp64 host spans. */
+ncsg_status ncsg_sparse_forward(const ncsg_sparse* a, const float* x, float* out, int batch,
+                                void* stream);
+ncsg_status ncsg_sparse_adjoint(const ncsg_sparse* a, const float* u, float* out, int batch,
+                                void* stream);
+ncsg_status ncsg_sparse_forward_host(const ncsg_sparse* a, const double* x, double* out,
+                                     int batch);
+ncsg_status ncsg_sparse_adjoint_host(const ncsg_sparse* a, const double* u, double* out,
+                                     int batch);
+
 /* GradMap::forward / adjoint (grad.hpp:17-28, grad.cpp:53-84): range layout is
  * the N x (N-1) horizontal block followed by the (N-1) x N vertical block. */
 ncsg_status ncsg_grad_forward(int n, const float* x, float* out, int batch, void* stream);
@@ -126,6 +156,10 @@ typedef struct {
   int angle_begin;   /* angle shard [angle_begin, angle_end) of this rank; */
   int angle_end;     /* 0,0 = all angles (single GPU) */
   int device;
+  /* CT / PET data block on an explicit SparseMap (fan beam) instead of the
+   * parallel-beam RadonMap (nullable; n_angles / n_det then come from it).
+   * The handle must outlive the problem (the reference's shared_ptr). */
+  const struct ncsg_sparse* sparse;
 } ncsg_problem_desc;
 
 typedef struct ncsg_problem ncsg_problem;

@@ -510,19 +510,242 @@ int orc_simulate_ct(int n, int n_angles, int n_det, const double* x, double sigm
   return 0;
 }
 
+/* ------------------------------------------------ fan beam (SparseMap) */
+/* CSR system matrix with its stored transpose (SparseMap, sparse.cpp:9-45). */
+typedef struct {
+  int n, views, rays;
+  double radius, fan;
+  size_t rows, cols, nnz;
+  size_t *row_ptr, *col_idx, *t_row_ptr, *t_col_idx;
+  double *val, *t_val;
+} Csr;
+
+static double g_fan_radius = 0.0, g_fan_angle = 0.0; /* orc_set_fan */
+static Csr g_fan_csr = {0};                          /* single-entry cache */
+
+void orc_set_fan(double source_radius, double fan_angle) {
+  g_fan_radius = source_radius;
+  g_fan_angle = fan_angle;
+}
+
+/* FanBeamGeometry::defaults (fanbeam.cpp:10-17) */
+void orc_fan_defaults(int n, double* source_radius, double* fan_angle) {
+  *source_radius = n;
+  *fan_angle = 2.0 * asin(sqrt(2.0) * n / (2.0 * (double)n));
+}
+
+/* clip_axis (fanbeam.cpp:27-38) */
+static void clip_axis(double s0, double d, double h, double* enter, double* exit_, int* hit) {
+  if (d == 0.0) {
+    if (s0 < -h || s0 > h) *hit = 0;
+    return;
+  }
+  double t0 = (-h - s0) / d, t1 = (h - s0) / d;
+  if (t0 > t1) {
+    double t = t0;
+    t0 = t1;
+    t1 = t;
+  }
+  if (t0 > *enter) *enter = t0;
+  if (t1 < *exit_) *exit_ = t1;
+  if (*enter >= *exit_) *hit = 0;
+}
+
+/* build_fanbeam (fanbeam.cpp:43-111): Siddon intersection lengths, triplets
+ * in ray order; then SparseMap's CSR + counting-sort transpose. */
+static int fan_build(int n, int views, int rays, double R, double fan, Csr* A) {
+  if (n < 2 || views < 1 || rays < 1) return 2;
+  double h = 0.5 * n;
+  if (R <= h * sqrt(2.0)) return 2;
+  if (fan <= 0.0 || fan >= kPi) return 2;
+  size_t cap = (size_t)views * rays * 2 * n + 16, cnt = 0;
+  int64_t* tr = (int64_t*)malloc(sizeof(int64_t) * cap);
+  int64_t* tc = (int64_t*)malloc(sizeof(int64_t) * cap);
+  double* tv = (double*)malloc(sizeof(double) * cap);
+  double dpsi = rays > 1 ? fan / (rays - 1) : 0.0;
+  double psi0 = -0.5 * fan;
+  int64_t ray_index = 0;
+  for (int v = 0; v < views; ++v) {
+    double phi = 2.0 * kPi * v / views;
+    double sx = R * cos(phi), sy = R * sin(phi);
+    double cx = -cos(phi), cy = -sin(phi);
+    for (int r = 0; r < rays; ++r, ++ray_index) {
+      double psi = rays > 1 ? psi0 + r * dpsi : 0.0;
+      double cp = cos(psi), sp = sin(psi);
+      double dx = cp * cx - sp * cy;
+      double dy = sp * cx + cp * cy;
+      double enter = 0.0, exit_ = INFINITY;
+      int hit = 1;
+      clip_axis(sx, dx, h, &enter, &exit_, &hit);
+      clip_axis(sy, dy, h, &enter, &exit_, &hit);
+      if (!hit) continue;
+      double t = enter;
+      double px = sx + t * dx, py = sy + t * dy;
+      int ix = (int)floor(px + h), iy = (int)floor(py + h);
+      ix = ix < 0 ? 0 : (ix > n - 1 ? n - 1 : ix);
+      iy = iy < 0 ? 0 : (iy > n - 1 ? n - 1 : iy);
+      int step_x = dx > 0.0 ? 1 : -1, step_y = dy > 0.0 ? 1 : -1;
+      while (t < exit_ - 1e-12) {
+        double tx = dx != 0.0 ? ((ix + (step_x > 0 ? 1 : 0)) - h - sx) / dx : INFINITY;
+        double ty = dy != 0.0 ? ((iy + (step_y > 0 ? 1 : 0)) - h - sy) / dy : INFINITY;
+        double m = tx < ty ? tx : ty;
+        if (exit_ < m) m = exit_;
+        double t_next = m > t ? m : t;
+        double len = t_next - t;
+        if (len > 0.0) {
+          if (cnt == cap) {
+            cap *= 2;
+            tr = (int64_t*)realloc(tr, sizeof(int64_t) * cap);
+            tc = (int64_t*)realloc(tc, sizeof(int64_t) * cap);
+            tv = (double*)realloc(tv, sizeof(double) * cap);
+          }
+          tr[cnt] = ray_index;
+          tc[cnt] = (int64_t)(n - 1 - iy) * n + ix;
+          tv[cnt] = len;
+          ++cnt;
+        }
+        t = t_next;
+        if (t >= exit_ - 1e-12) break;
+        if (tx <= ty) {
+          ix += step_x;
+          if (ix < 0 || ix >= n) break;
+        } else {
+          iy += step_y;
+          if (iy < 0 || iy >= n) break;
+        }
+      }
+    }
+  }
+  A->n = n;
+  A->views = views;
+  A->rays = rays;
+  A->radius = R;
+  A->fan = fan;
+  A->rows = (size_t)views * rays;
+  A->cols = (size_t)n * n;
+  A->nnz = cnt;
+  /* rows are generated in increasing order, so the stable sort by row is the
+   * identity (sparse.cpp:19-20) */
+  A->row_ptr = (size_t*)calloc(A->rows + 1, sizeof(size_t));
+  A->col_idx = (size_t*)malloc(sizeof(size_t) * (cnt ? cnt : 1));
+  A->val = (double*)malloc(sizeof(double) * (cnt ? cnt : 1));
+  for (size_t i = 0; i < cnt; ++i) ++A->row_ptr[tr[i] + 1];
+  for (size_t r = 0; r < A->rows; ++r) A->row_ptr[r + 1] += A->row_ptr[r];
+  for (size_t i = 0; i < cnt; ++i) {
+    A->col_idx[i] = (size_t)tc[i];
+    A->val[i] = tv[i];
+  }
+  A->t_row_ptr = (size_t*)calloc(A->cols + 1, sizeof(size_t));
+  A->t_col_idx = (size_t*)malloc(sizeof(size_t) * (cnt ? cnt : 1));
+  A->t_val = (double*)malloc(sizeof(double) * (cnt ? cnt : 1));
+  for (size_t i = 0; i < cnt; ++i) ++A->t_row_ptr[A->col_idx[i] + 1];
+  for (size_t c = 0; c < A->cols; ++c) A->t_row_ptr[c + 1] += A->t_row_ptr[c];
+  size_t* cursor = (size_t*)malloc(sizeof(size_t) * (A->cols + 1));
+  memcpy(cursor, A->t_row_ptr, sizeof(size_t) * A->cols);
+  for (size_t r = 0; r < A->rows; ++r)
+    for (size_t i = A->row_ptr[r]; i < A->row_ptr[r + 1]; ++i) {
+      size_t dst = cursor[A->col_idx[i]]++;
+      A->t_col_idx[dst] = r;
+      A->t_val[dst] = A->val[i];
+    }
+  free(cursor);
+  free(tr);
+  free(tc);
+  free(tv);
+  return 0;
+}
+
+static void csr_free(Csr* A) {
+  free(A->row_ptr);
+  free(A->col_idx);
+  free(A->val);
+  free(A->t_row_ptr);
+  free(A->t_col_idx);
+  free(A->t_val);
+  memset(A, 0, sizeof(*A));
+}
+
+/* the cached fan-beam matrix for (n, views, rays) and the current orc_set_fan */
+static Csr* fan_matrix(int n, int views, int rays) {
+  Csr* A = &g_fan_csr;
+  if (A->row_ptr && A->n == n && A->views == views && A->rays == rays &&
+      A->radius == g_fan_radius && A->fan == g_fan_angle)
+    return A;
+  csr_free(A);
+  if (fan_build(n, views, rays, g_fan_radius, g_fan_angle, A)) return NULL;
+  return A;
+}
+
+/* SparseMap::forward (sparse.cpp:55-62); rows independent -> OpenMP-exact */
+static void csr_forward(const Csr* A, const double* x, double* out, int nthreads) {
+  set_threads(nthreads);
+#pragma omp parallel for schedule(static)
+  for (long long r = 0; r < (long long)A->rows; ++r) {
+    double acc = 0.0;
+    for (size_t i = A->row_ptr[r]; i < A->row_ptr[r + 1]; ++i) acc += A->val[i] * x[A->col_idx[i]];
+    out[r] = acc;
+  }
+}
+
+/* SparseMap::adjoint with the stored transpose (sparse.cpp:64-71) */
+static void csr_adjoint(const Csr* A, const double* u, double* out, int nthreads) {
+  set_threads(nthreads);
+#pragma omp parallel for schedule(static)
+  for (long long c = 0; c < (long long)A->cols; ++c) {
+    double acc = 0.0;
+    for (size_t i = A->t_row_ptr[c]; i < A->t_row_ptr[c + 1]; ++i)
+      acc += A->t_val[i] * u[A->t_col_idx[i]];
+    out[c] = acc;
+  }
+}
+
+int orc_fanbeam_triplets(int n, int views, int rays, double R, double fan, int64_t cap,
+                         int64_t* nnz, int64_t* row, int64_t* col, double* val) {
+  Csr A;
+  memset(&A, 0, sizeof(A));
+  if (fan_build(n, views, rays, R, fan, &A)) return 2;
+  *nnz = (int64_t)A.nnz;
+  if (cap >= (int64_t)A.nnz)
+    for (size_t r = 0; r < A.rows; ++r)
+      for (size_t i = A.row_ptr[r]; i < A.row_ptr[r + 1]; ++i) {
+        row[i] = (int64_t)r;
+        col[i] = (int64_t)A.col_idx[i];
+        val[i] = A.val[i];
+      }
+  csr_free(&A);
+  return 0;
+}
+
+int orc_fanbeam_apply(int n, int views, int rays, double R, double fan, int adjoint,
+                      const double* in, double* out, int nthreads) {
+  Csr A;
+  memset(&A, 0, sizeof(A));
+  if (fan_build(n, views, rays, R, fan, &A)) return 2;
+  if (adjoint)
+    csr_adjoint(&A, in, out, nthreads);
+  else
+    csr_forward(&A, in, out, nthreads);
+  csr_free(&A);
+  return 0;
+}
+
 /* ------------------------------------------------------- solvers.cpp NCS */
 /* Problem layouts of the hot path:
  *   kind 0  CT-TV:    blocks {1, R, QuadraticConj, b}, {beta/alpha, D,
  *                     ScaledL1Conj(lambda*alpha/beta)} [+ {1, I, NonnegConj}]
  *                     -- assemble_problem (pipeline.cpp:84-97)
  *   kind 1  denoise:  blocks {1, I, QuadraticConj, b}, {beta/alpha, D, ...}
- *                     [+ {1, I, NonnegConj}] (test_solvers.cpp:646-664). */
+ *                     [+ {1, I, NonnegConj}] (test_solvers.cpp:646-664).
+ *   kind 2  PET-TV:   kind 0 with {1, R, PoissonConj(b, alpha), 0}.
+ *   kind 3  fan-beam CT-TV: kind 0 on build_fanbeam's SparseMap (angles =
+ *                     views, det = rays; geometry from orc_set_fan). */
 typedef struct {
   int kind, n, angles, det, positivity, nthreads;
   double alpha, beta, lambda;
   size_t nn, m0, g, range;
   double w_d, bound;
   const double* b; /* block-0 offset, length m0 */
+  const Csr* fanA; /* kind 3 */
 } Prob;
 
 static void prob_init(Prob* p, int kind, int n, int angles, int det, double alpha, double beta,
@@ -543,11 +766,14 @@ static void prob_init(Prob* p, int kind, int n, int angles, int det, double alph
   p->w_d = beta / alpha;
   p->bound = lambda * alpha / beta;
   p->b = b;
+  p->fanA = kind == 3 ? fan_matrix(n, angles, det) : NULL;
 }
 
 /* StackedMap::forward (linear_map.cpp:39-45) */
 static void stacked_forward(const Prob* p, const double* x, double* out) {
-  if (p->kind != 1)
+  if (p->kind == 3)
+    csr_forward(p->fanA, x, out, p->nthreads);
+  else if (p->kind != 1)
     orc_radon_forward(p->n, p->angles, p->det, x, out, p->nthreads);
   else
     memcpy(out, x, sizeof(double) * p->nn);
@@ -565,7 +791,9 @@ static void stacked_forward(const Prob* p, const double* x, double* out) {
 /* StackedMap::adjoint (linear_map.cpp:47-55) */
 static void stacked_adjoint(const Prob* p, const double* u, double* out, double* tmp) {
   memset(out, 0, sizeof(double) * p->nn);
-  if (p->kind != 1)
+  if (p->kind == 3)
+    csr_adjoint(p->fanA, u, tmp, p->nthreads);
+  else if (p->kind != 1)
     orc_radon_adjoint(p->n, p->angles, p->det, u, tmp, p->nthreads);
   else
     memcpy(tmp, u, sizeof(double) * p->nn);
@@ -890,7 +1118,8 @@ int orc_solve_ex(int kind, int n, int angles, int det, double alpha, double beta
   if (max_iters < 0 || record_every < 1 || alpha <= 0.0) return 2;
   if (!mask && n_cg <= 0 && gamma <= 0.0) return 2;
   if (n_cg > 0 && mask) return 2; /* admm_cg uses M = alpha A^T A (solvers.cpp:437-438) */
-  if (kind != 1 && orc_radon_check(n, angles, det)) return 2;
+  if ((kind == 0 || kind == 2) && orc_radon_check(n, angles, det)) return 2;
+  if (kind == 3 && !fan_matrix(n, angles, det)) return 2;
   Prob p;
   prob_init(&p, kind, n, angles, det, alpha, beta, lambda, positivity, b, nthreads);
   Engine e;

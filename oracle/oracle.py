@@ -98,6 +98,12 @@ class Port:
                                 C.c_double, C.c_int, _vp, C.c_double, _vp, C.c_int, C.c_int, _vp,
                                 _vp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int),
                                 C.POINTER(C.c_double), C.POINTER(C.c_int64), C.c_int]
+        L.orc_set_fan.argtypes = [C.c_double, C.c_double]
+        L.orc_fan_defaults.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.orc_fanbeam_triplets.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                           C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp]
+        L.orc_fanbeam_apply.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                        C.c_int, _dp, _dp, C.c_int]
         L.orc_solve_ex.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _vp, C.c_double, _vp, C.c_int, C.c_int,
                                    C.c_int, _vp, _vp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int),
@@ -115,6 +121,34 @@ class Port:
     # -- operators -----------------------------------------------------
     def default_detector_count(self, n):
         return self.lib.orc_default_detector_count(n)
+
+    # -- fan beam (fanbeam.cpp, sparse.cpp) ------------------------------
+    def set_fan(self, radius, fan_angle):
+        """Geometry of kind-3 (fan-beam CT-TV) problems."""
+        self.lib.orc_set_fan(radius, fan_angle)
+
+    def fan_defaults(self, n):
+        r, f = C.c_double(), C.c_double()
+        self.lib.orc_fan_defaults(n, C.byref(r), C.byref(f))
+        return r.value, f.value
+
+    def fanbeam_triplets(self, n, views, rays, radius, fan_angle):
+        nnz = C.c_int64()
+        _check(self.lib.orc_fanbeam_triplets(n, views, rays, radius, fan_angle, 0,
+                                             C.byref(nnz), None, None, None), "fanbeam")
+        k = nnz.value
+        row, col, val = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k)
+        _check(self.lib.orc_fanbeam_triplets(n, views, rays, radius, fan_angle, k,
+                                             C.byref(nnz), row.ctypes.data, col.ctypes.data,
+                                             val.ctypes.data), "fanbeam")
+        return row, col, val
+
+    def fanbeam_apply(self, n, views, rays, radius, fan_angle, v, adjoint=False, threads=None):
+        v = np.ascontiguousarray(v, np.float64).ravel()
+        out = np.zeros(n * n if adjoint else views * rays)
+        _check(self.lib.orc_fanbeam_apply(n, views, rays, radius, fan_angle, int(adjoint), v,
+                                          out, threads or default_threads()), "fanbeam_apply")
+        return out
 
     def radon_forward(self, x, angles, det, threads=None):
         x = np.ascontiguousarray(x, np.float64)
@@ -327,6 +361,12 @@ class Ref:
                                 C.POINTER(C.c_int), C.POINTER(C.c_double)]
         L.ref_ncs_step.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _dp, C.c_double, _vp, _dp, _dp, C.c_int]
+        L.ref_set_fan.argtypes = [C.c_double, C.c_double]
+        L.ref_fan_defaults.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+        L.ref_fanbeam_triplets.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                           C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp]
+        L.ref_fanbeam_apply.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
+                                        C.c_int, _dp, _dp]
         L.ref_admm_cg_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                         C.c_double, C.c_double, C.c_int, _dp, C.c_double,
                                         C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int,
@@ -453,6 +493,32 @@ class Ref:
                                      int(pdhg), x, u, rows.ravel(), max_rows, C.byref(nr),
                                      C.byref(obj)), "solve")
         return SolveOut(x.reshape(p.n, p.n), u, rows[: nr.value].copy(), obj.value)
+
+    def set_fan(self, radius, fan_angle):
+        self.lib.ref_set_fan(radius, fan_angle)
+
+    def fan_defaults(self, n):
+        r, f = C.c_double(), C.c_double()
+        self.lib.ref_fan_defaults(n, C.byref(r), C.byref(f))
+        return r.value, f.value
+
+    def fanbeam_triplets(self, n, views, rays, radius, fan_angle):
+        nnz = C.c_int64()
+        self._chk(self.lib.ref_fanbeam_triplets(n, views, rays, radius, fan_angle, 0,
+                                                C.byref(nnz), None, None, None), "fanbeam")
+        k = nnz.value
+        row, col, val = np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k)
+        self._chk(self.lib.ref_fanbeam_triplets(n, views, rays, radius, fan_angle, k,
+                                                C.byref(nnz), row.ctypes.data, col.ctypes.data,
+                                                val.ctypes.data), "fanbeam")
+        return row, col, val
+
+    def fanbeam_apply(self, n, views, rays, radius, fan_angle, v, adjoint=False):
+        v = np.ascontiguousarray(v, np.float64).ravel()
+        out = np.zeros(n * n if adjoint else views * rays)
+        self._chk(self.lib.ref_fanbeam_apply(n, views, rays, radius, fan_angle, int(adjoint), v,
+                                             out), "fanbeam_apply")
+        return out
 
     def admm_cg_solve(self, prob, gamma, n_cg, max_iters, record_every=None):
         """admm_cg_solve (solvers.cpp:435-440) of the reference build."""

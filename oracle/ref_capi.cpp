@@ -16,6 +16,7 @@
 #include <vector>
 
 #include "ncstomo/circulant.hpp"
+#include "ncstomo/fanbeam.hpp"
 #include "ncstomo/grad.hpp"
 #include "ncstomo/linear_map.hpp"
 #include "ncstomo/phantom.hpp"
@@ -24,6 +25,7 @@
 #include "ncstomo/radon.hpp"
 #include "ncstomo/rng.hpp"
 #include "ncstomo/solvers.hpp"
+#include "ncstomo/sparse.hpp"
 
 using namespace ncstomo;
 
@@ -69,7 +71,26 @@ struct Desc {
   int positivity;
 };
 
+// Fan-beam geometry used by kind 3 (fan-beam CT-TV through SparseMap): set by
+// ref_set_fan before building problems (test infrastructure, not thread-safe).
+FanBeamGeometry g_fan{};
+
 SplitProblem build_problem(const Desc& d, const double* b) {
+  if (d.kind == 3) {  // CT-TV on build_fanbeam's SparseMap (fanbeam.cpp, sparse.cpp)
+    FanBeamGeometry g = g_fan;
+    g.n_views = d.angles;
+    g.n_rays = d.det;
+    auto geom = std::make_shared<SparseMap>(build_fanbeam(d.n, g));
+    Sinogram s(d.angles, d.det);
+    std::memcpy(s.v.data(), b, sizeof(double) * s.v.size());
+    ModelParams p;
+    p.model = "ct";
+    p.alpha = d.alpha;
+    p.beta = d.beta;
+    p.lambda = d.lambda;
+    p.positivity = d.positivity != 0;
+    return assemble_problem(s, geom, p);
+  }
   if (d.kind == 0 || d.kind == 2) {  // CT-TV or PET-TV (assemble_problem, pipeline.cpp:69-98)
     auto geom = std::make_shared<RadonMap>(d.n, d.angles, d.det);
     Sinogram s(d.angles, d.det);
@@ -100,6 +121,50 @@ SplitProblem build_problem(const Desc& d, const double* b) {
 extern "C" {
 
 const char* ref_last_error() { return g_err.c_str(); }
+
+// Fan-beam geometry (fanbeam.hpp FanBeamGeometry) for kind 3 problems.
+void ref_set_fan(double source_radius, double fan_angle) {
+  g_fan.source_radius = source_radius;
+  g_fan.fan_angle = fan_angle;
+}
+
+// FanBeamGeometry::defaults (fanbeam.cpp:10-17): radius and fan angle.
+void ref_fan_defaults(int n, double* source_radius, double* fan_angle) {
+  FanBeamGeometry g = FanBeamGeometry::defaults(n, 1, 1);
+  *source_radius = g.source_radius;
+  *fan_angle = g.fan_angle;
+}
+
+// build_fanbeam (fanbeam.cpp:43-111) as CSR-ordered triplets (to_triplets,
+// sparse.cpp:73-80).  Call with cap = 0 to get *nnz only.
+int ref_fanbeam_triplets(int n, int views, int rays, double source_radius, double fan_angle,
+                         int64_t cap, int64_t* nnz, int64_t* row, int64_t* col, double* val) {
+  return guard([&] {
+    FanBeamGeometry g{views, rays, source_radius, fan_angle};
+    SparseMap m = build_fanbeam(n, g);
+    auto t = m.to_triplets();
+    *nnz = static_cast<int64_t>(t.size());
+    if (cap >= static_cast<int64_t>(t.size()))
+      for (std::size_t i = 0; i < t.size(); ++i) {
+        row[i] = t[i].row;
+        col[i] = t[i].col;
+        val[i] = t[i].value;
+      }
+  });
+}
+
+// SparseMap::forward / adjoint (sparse.cpp:55-71) of the fan-beam matrix.
+int ref_fanbeam_apply(int n, int views, int rays, double source_radius, double fan_angle,
+                      int adjoint, const double* in, double* out) {
+  return guard([&] {
+    FanBeamGeometry g{views, rays, source_radius, fan_angle};
+    SparseMap m = build_fanbeam(n, g);
+    if (adjoint)
+      m.adjoint({in, m.range_size()}, {out, m.domain_size()});
+    else
+      m.forward({in, m.domain_size()}, {out, m.range_size()});
+  });
+}
 
 int ref_default_detector_count(int n) { return default_detector_count(n); }
 

@@ -15,8 +15,8 @@ ROOT = os.path.dirname(HERE)
 CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-CU_SRCS = ["radon_kernels.cu", "fft_kernels.cu", "ncs_kernels.cu", "capi.cu"]
-CPP_SRCS = ["geometry.cpp"]
+CU_SRCS = ["radon_kernels.cu", "fft_kernels.cu", "ncs_kernels.cu", "sparse_kernels.cu", "capi.cu"]
+CPP_SRCS = ["geometry.cpp", "fanbeam.cpp"]
 HDRS = ["ncsg_internal.cuh", "ncs_kernels.cuh", "ncs_device.cuh"]
 
 

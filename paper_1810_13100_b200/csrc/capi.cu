@@ -104,11 +104,18 @@ struct ncsg_radon {
   Stream stream;
 };
 
+struct ncsg_sparse {
+  SparseDev dev;
+  Stream stream;
+  int device = 0;
+};
+
 struct ncsg_problem {
   ncsg_problem_desc d{};
   int device = 0;
   Stream stream;
   std::unique_ptr<RadonDev> radon;
+  const SparseDev* sparse = nullptr;  // SparseMap projector (caller keeps the handle alive)
   FftPlan fft;
   bool has_mask = false;
   std::vector<std::complex<double>> mask_full;  // cfg.mask (apply_m)
@@ -149,6 +156,31 @@ namespace {
 
 int* step_counter(ncsg_problem* p) { return p->flag.p; }
 
+// ---- projector of the data block: the parallel-beam RadonMap kernels or an
+// explicit SparseMap (fan beam).  Both write R x as partial slots summed by
+// the dual update / strip_sum, and R^T u as partial images (class-V frame,
+// then class-H transposed) summed into A^T u by the FFT loader.
+bool has_projector(const ncsg_problem* p) { return p->radon || p->sparse; }
+int proj_slots(const ncsg_problem* p) {
+  return p->sparse ? 1 : (p->radon ? p->radon->fp_slots() : 0);
+}
+int proj_nV(const ncsg_problem* p) { return p->sparse ? 1 : p->radon->bp_chunks[0]; }
+int proj_nH(const ncsg_problem* p) { return p->sparse ? 0 : p->radon->bp_chunks[1]; }
+int proj_parts(const ncsg_problem* p) { return proj_nV(p) + proj_nH(p); }
+void proj_prepare(ncsg_problem* p, const float* img, float* aux, int batch);
+void proj_forward(ncsg_problem* p, const float* img, const float* aux, float* part, int batch) {
+  if (p->sparse)
+    launch_sparse_forward(*p->sparse, img, p->nn, part, p->m0, batch, p->stream.s);
+  else
+    launch_radon_forward_partial(*p->radon, img, aux, part, batch, p->stream.s);
+}
+void proj_adjoint(ncsg_problem* p, const float* u, size_t u_stride, float* part, int batch) {
+  if (p->sparse)
+    launch_sparse_adjoint(*p->sparse, u, u_stride, part, p->nn, batch, p->stream.s);
+  else
+    launch_radon_adjoint_partial(*p->radon, u, u_stride, part, batch, p->stream.s);
+}
+
 // Second input of the forward: x^T for class-H angles, or the symmetry
 // planes in orbit mode.
 float* prepare_forward_aux(const RadonDev& r, const float* img, float* aux, int batch,
@@ -161,6 +193,10 @@ float* prepare_forward_aux(const RadonDev& r, const float* img, float* aux, int 
   return aux;
 }
 
+void proj_prepare(ncsg_problem* p, const float* img, float* aux, int batch) {
+  if (p->radon) prepare_forward_aux(*p->radon, img, aux, batch, p->stream.s);
+}
+
 AtuTerms atu_terms_for(ncsg_problem* p, float* u);
 AtuTerms atu_terms(ncsg_problem* p) { return atu_terms_for(p, p->u.p); }
 
@@ -170,9 +206,9 @@ AtuTerms atu_terms_for(ncsg_problem* p, float* u) {
   T.n = p->d.n;
   if (p->d.kind != NCSG_DENOISE) {
     T.bp_part = p->bp_part.p;
-    T.nV = p->radon->bp_chunks[0];
-    T.nH = p->radon->bp_chunks[1];
-    T.part_stride = static_cast<size_t>(p->radon->n_partials()) * p->nn;
+    T.nV = proj_nV(p);
+    T.nH = proj_nH(p);
+    T.part_stride = static_cast<size_t>(proj_parts(p)) * p->nn;
     if (p->rank0 && p->d.positivity) T.ident = u + p->m0 + p->g;
   } else if (p->rank0) {
     T.ident = u;
@@ -203,8 +239,7 @@ void phase_a(ncsg_problem* p) {
   mark(p);
   if (p->d.kind != NCSG_DENOISE) {
     // u_s is the first m0 entries of each problem's dual (stride range).
-    launch_radon_adjoint_partial(*p->radon, p->u.p, p->range, p->bp_part.p, p->batch,
-                                 p->stream.s);
+    proj_adjoint(p, p->u.p, p->range, p->bp_part.p, p->batch);
   }
 }
 
@@ -238,7 +273,7 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
   XUpdate xu;
   xu.x = p->x.p;
   xu.x_old = p->x_old.p;
-  xu.xT = (p->d.kind != NCSG_DENOISE && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
+  xu.xT = (p->radon && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
               ? p->xT.p
               : nullptr;
   xu.subtract = 1;
@@ -253,8 +288,8 @@ void forward_and_dual(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   mark(p);
   if (p->d.kind != NCSG_DENOISE) {
-    if (p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
-    launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
+    if (p->radon && p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
+    proj_forward(p, p->x.p, p->xT.p, p->fp_part.p, p->batch);
   }
   mark(p);
   DualArgs a;
@@ -266,7 +301,7 @@ void forward_and_dual(ncsg_problem* p) {
   a.wd = p->wd;
   a.bound = p->bound;
   a.fp_part = p->fp_part.p;
-  a.n_strips = p->radon ? p->radon->fp_slots() : 0;
+  a.n_strips = proj_slots(p);
   a.m = p->m0;
   a.m_begin = p->m_begin;
   a.m_end = p->m_end;
@@ -293,9 +328,13 @@ void do_step(ncsg_problem* p) {
 void engine_init(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   if (p->d.kind != NCSG_DENOISE) {
-    prepare_forward_aux(*p->radon, p->x.p, p->xT.p, p->batch, s);
-    launch_radon_forward_partial(*p->radon, p->x.p, p->xT.p, p->fp_part.p, p->batch, s);
-    launch_strip_sum(*p->radon, p->fp_part.p, p->axs.p, p->batch, s);
+    proj_prepare(p, p->x.p, p->xT.p, p->batch);
+    proj_forward(p, p->x.p, p->xT.p, p->fp_part.p, p->batch);
+    if (p->radon)
+      launch_strip_sum(*p->radon, p->fp_part.p, p->axs.p, p->batch, s);
+    else
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(p->axs.p, p->fp_part.p, p->m0 * p->batch * 4,
+                                      cudaMemcpyDeviceToDevice, s));
   }
 }
 
@@ -390,13 +429,13 @@ void ensure_scratch(ncsg_problem* p) {
 void stacked_forward(ncsg_problem* p, const float* img, float* imgT, float* out) {
   cudaStream_t s = p->stream.s;
   if (p->d.kind != NCSG_DENOISE) {
-    prepare_forward_aux(*p->radon, img, imgT, p->batch, s);
-    launch_radon_forward_partial(*p->radon, img, imgT, p->fp_part.p, p->batch, s);
+    proj_prepare(p, img, imgT, p->batch);
+    proj_forward(p, img, imgT, p->fp_part.p, p->batch);
   }
   StackArgs a;
   a.kind = p->d.kind;
   a.n = p->d.n;
-  a.n_strips = p->radon ? p->radon->fp_slots() : 0;
+  a.n_strips = proj_slots(p);
   a.wd = p->wd;
   a.fp_part = p->fp_part.p;
   a.x = img;
@@ -514,7 +553,7 @@ double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_
   for (int it = 0; it < iters; ++it) {
     stacked_forward(p, v, p->dxT.p, av);
     if (p->d.kind != NCSG_DENOISE)
-      launch_radon_adjoint_partial(*p->radon, av, p->range, p->bp_part.p, 1, s);
+      proj_adjoint(p, av, p->range, p->bp_part.p, 1);
     launch_atu_assemble(atu_terms_for(p, av), atav, 1, s);
     if (cv) apply_filter(p, v, p->maskT_orig.p, cv);
     launch_screen_combine(v, atav, cv, static_cast<float>(p->d.alpha),
@@ -562,7 +601,7 @@ void cg_solve(ncsg_problem* p, const float* rhs, int n_iters, double* x_out) {
     if (rs == 0.0) break;
     stacked_forward(p, q32, p->dxT.p, p->adx.p);
     if (p->d.kind != NCSG_DENOISE)
-      launch_radon_adjoint_partial(*p->radon, p->adx.p, p->range, p->bp_part.p, 1, s);
+      proj_adjoint(p, p->adx.p, p->range, p->bp_part.p, 1);
     launch_atu_assemble(atu_terms_for(p, p->adx.p), ap, 1, s);
     launch_cg_dot(q, ap, nn, p->red.p, s);
     const double pap = sum_blocks();
@@ -589,8 +628,7 @@ void x_update_cg(ncsg_problem* p) {
   cg_solve(p, atu, p->n_cg, p->cg_x.p);
   mark(p);
   launch_x_update(p->x.p, p->x_old.p, p->cg_x.p, 1.0 / p->d.alpha, p->nn, p->flag.p, s);
-  if (p->d.kind != NCSG_DENOISE && !p->radon->orbit_mode)
-    prepare_forward_aux(*p->radon, p->x.p, p->xT.p, 1, s);  // x^T for class-H angles
+  if (p->radon && !p->radon->orbit_mode) proj_prepare(p, p->x.p, p->xT.p, 1);  // x^T for class H
 }
 
 void upload_f64(ncsg_problem* p, const double* h, float* d, size_t count) {
@@ -689,6 +727,106 @@ ncsg_status ncsg_radon_adjoint(const ncsg_radon* r, const float* u, float* out, 
     launch_sum_partials(part.p, dev.bp_chunks[0], dev.bp_chunks[1], out, g.n, batch, s);
     NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
   });
+}
+
+ncsg_status ncsg_fan_defaults(int n, double* source_radius, double* fan_angle) {
+  return guard([&] {
+    if (!source_radius || !fan_angle) throw Error{NCSG_INVALID, "null output"};
+    fan_defaults(n, *source_radius, *fan_angle);
+  });
+}
+
+static ncsg_status sparse_upload(SparseHost&& h, int device, ncsg_sparse** out) {
+  return guard([&] {
+    if (!out) throw Error{NCSG_INVALID, "null output handle"};
+    require_device(device);
+    NCSG_CUDA_CHECK(cudaSetDevice(device));
+    auto a = std::make_unique<ncsg_sparse>();
+    a->device = device;
+    a->dev.upload(h);
+    NCSG_CUDA_CHECK(cudaStreamCreateWithFlags(&a->stream.s, cudaStreamNonBlocking));
+    *out = a.release();
+  });
+}
+
+ncsg_status ncsg_fanbeam_create(int n, int views, int rays, double source_radius,
+                                double fan_angle, int device, ncsg_sparse** out) {
+  SparseHost h;
+  ncsg_status st = guard([&] { h = build_fanbeam(n, views, rays, source_radius, fan_angle); });
+  if (st != NCSG_OK) return st;
+  return sparse_upload(std::move(h), device, out);
+}
+
+ncsg_status ncsg_sparse_create(int n, int views, int rays, int64_t nnz, const int64_t* rows,
+                               const int64_t* cols, const double* vals, int device,
+                               ncsg_sparse** out) {
+  SparseHost h;
+  ncsg_status st = guard([&] {
+    if (n < 1 || views < 1 || rays < 1 || nnz < 0 || (nnz && (!rows || !cols || !vals)))
+      throw Error{NCSG_INVALID, "bad sparse map arguments"};
+    h = build_sparse(n, views, rays, std::vector<int64_t>(rows, rows + nnz),
+                     std::vector<int64_t>(cols, cols + nnz),
+                     std::vector<double>(vals, vals + nnz));
+  });
+  if (st != NCSG_OK) return st;
+  return sparse_upload(std::move(h), device, out);
+}
+
+ncsg_status ncsg_sparse_destroy(ncsg_sparse* a) {
+  return guard([&] { delete a; });
+}
+
+int64_t ncsg_sparse_nnz(const ncsg_sparse* a) { return a ? static_cast<int64_t>(a->dev.nnz) : 0; }
+
+ncsg_status ncsg_sparse_forward(const ncsg_sparse* a, const float* x, float* out, int batch,
+                                void* stream) {
+  return guard([&] {
+    if (!a || !x || !out || batch < 1) throw Error{NCSG_INVALID, "bad sparse_forward arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(a->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : a->stream.s;
+    launch_sparse_forward(a->dev, x, a->dev.cols, out, a->dev.rows, batch, s);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+ncsg_status ncsg_sparse_adjoint(const ncsg_sparse* a, const float* u, float* out, int batch,
+                                void* stream) {
+  return guard([&] {
+    if (!a || !u || !out || batch < 1) throw Error{NCSG_INVALID, "bad sparse_adjoint arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(a->device));
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : a->stream.s;
+    launch_sparse_adjoint(a->dev, u, a->dev.rows, out, a->dev.cols, batch, s);
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  });
+}
+
+static ncsg_status sparse_host(const ncsg_sparse* a, const double* in, double* out, int batch,
+                               bool adjoint) {
+  return guard([&] {
+    if (!a || !in || !out || batch < 1) throw Error{NCSG_INVALID, "bad sparse arguments"};
+    NCSG_CUDA_CHECK(cudaSetDevice(a->device));
+    const size_t ni = (adjoint ? a->dev.rows : a->dev.cols) * batch;
+    const size_t no = (adjoint ? a->dev.cols : a->dev.rows) * batch;
+    std::vector<float> hi(in, in + ni), ho(no);
+    DevBuf<float> di, dout;
+    di.alloc(ni);
+    dout.alloc(no);
+    NCSG_CUDA_CHECK(cudaMemcpy(di.p, hi.data(), ni * 4, cudaMemcpyHostToDevice));
+    ncsg_status st = adjoint ? ncsg_sparse_adjoint(a, di.p, dout.p, batch, nullptr)
+                             : ncsg_sparse_forward(a, di.p, dout.p, batch, nullptr);
+    if (st != NCSG_OK) throw Error{st, g_err};
+    NCSG_CUDA_CHECK(cudaMemcpy(ho.data(), dout.p, no * 4, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < no; ++i) out[i] = ho[i];
+  });
+}
+
+ncsg_status ncsg_sparse_forward_host(const ncsg_sparse* a, const double* x, double* out,
+                                     int batch) {
+  return sparse_host(a, x, out, batch, false);
+}
+ncsg_status ncsg_sparse_adjoint_host(const ncsg_sparse* a, const double* u, double* out,
+                                     int batch) {
+  return sparse_host(a, u, out, batch, true);
 }
 
 ncsg_status ncsg_radon_forward_host(const ncsg_radon* r, const double* x, double* out,
@@ -836,7 +974,22 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     p->g = 2 * static_cast<size_t>(d.n) * (d.n - 1);
     p->wd = static_cast<float>(d.beta / d.alpha);
     p->bound = static_cast<float>(d.lambda * d.alpha / d.beta);
-    if (d.kind != NCSG_DENOISE) {
+    if (d.kind != NCSG_DENOISE && d.sparse) {
+      // SparseMap data block (fan beam, sparse.cpp); the handle outlives the problem
+      const SparseDev& A = d.sparse->dev;
+      if (A.n != d.n) throw Error{NCSG_INVALID, "sparse map / image size mismatch"};
+      if (d.angle_end > 0) throw Error{NCSG_INVALID, "sparse projectors are not angle-sharded"};
+      require_device(d.device);
+      if (d.sparse->device != d.device)
+        throw Error{NCSG_INVALID, "sparse map lives on another device"};
+      p->sparse = &A;
+      p->d.n_angles = A.views;
+      p->d.n_det = A.rays;
+      p->m0 = A.rows;
+      p->m_begin = 0;
+      p->m_end = p->m0;
+      p->rank0 = true;
+    } else if (d.kind != NCSG_DENOISE) {
       Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end);
       p->m0 = static_cast<size_t>(d.n_angles) * d.n_det;
       int ab = d.angle_end > 0 ? d.angle_begin : 0;
@@ -892,9 +1045,9 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     upload_f64(p.get(), desc->b, p->b.p, p->m0 * p->batch);
     if (d.kind != NCSG_DENOISE) {
       p->axs.alloc(p->m0 * p->batch);
-      p->fp_part.alloc(p->m0 * p->radon->fp_slots() * p->batch);
+      p->fp_part.alloc(p->m0 * proj_slots(p.get()) * p->batch);
       p->fp_part.zero(s);
-      p->bp_part.alloc(p->nn * p->radon->n_partials() * p->batch);
+      p->bp_part.alloc(p->nn * proj_parts(p.get()) * p->batch);
       p->axs.zero(s);
     }
     p->spec.alloc(static_cast<size_t>(d.n / 2 + 1) * d.n * p->batch);

@@ -83,6 +83,21 @@ struct Geometry {
 // Throws Error{NCSG_INVALID} with the reference's messages.
 Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end);
 
+// Explicit sparse projector (SparseMap, sparse.cpp): CSR over sinogram rows
+// (view-major) and its stored transpose over image pixels, fp64 on the host.
+struct SparseHost {
+  int n = 0, views = 0, rays = 0;
+  std::vector<int64_t> row_ptr, t_row_ptr;
+  std::vector<int> col, t_col;
+  std::vector<double> val, t_val;
+};
+// SparseMap(n, views, rays, triplets) layout (sparse.cpp:9-45).
+SparseHost build_sparse(int n, int views, int rays, std::vector<int64_t> rows,
+                        std::vector<int64_t> cols, std::vector<double> vals);
+// build_fanbeam (fanbeam.cpp:43-111) and FanBeamGeometry::defaults (:10-17).
+SparseHost build_fanbeam(int n, int views, int rays, double source_radius, double fan_angle);
+void fan_defaults(int n, double& source_radius, double& fan_angle);
+
 // ------------------------------------------------------- device buffers
 template <class T>
 struct DevBuf {
@@ -142,6 +157,21 @@ inline void bp_tile_shape(int n, int& W, int& T, int& P) {
 }
 constexpr int kBpWarps = NCSG_BP_WARPS;  // adjoint: warps per CTA (private accumulators)
 constexpr int kBpWaves = NCSG_BP_WAVES;  // adjoint: target CTAs = 148 * 3 * waves
+
+// SparseMap on the device (sparse_kernels.cu): fp32 values, int32 indices.
+struct SparseDev {
+  int n = 0, views = 0, rays = 0;
+  size_t rows = 0, cols = 0, nnz = 0;
+  DevBuf<int64_t> row_ptr, t_row_ptr;
+  DevBuf<int> col, t_col;
+  DevBuf<float> val, t_val;
+  void upload(const SparseHost& h);
+};
+// y[b] = A x[b] (rows = sinogram bins) / y[b] = A^T u[b] (rows = pixels).
+void launch_sparse_forward(const SparseDev& A, const float* x, size_t x_stride, float* y,
+                           size_t y_stride, int batch, cudaStream_t s);
+void launch_sparse_adjoint(const SparseDev& A, const float* u, size_t u_stride, float* y,
+                           size_t y_stride, int batch, cudaStream_t s);
 
 struct RadonDev {
   Geometry geo;

@@ -45,6 +45,7 @@ class ProblemDesc(C.Structure):
         ("beta", C.c_double), ("lambda_", C.c_double), ("gamma", C.c_double),
         ("pinv_rel_tol", C.c_double), ("mask", C.c_void_p), ("b", C.c_void_p),
         ("angle_begin", C.c_int), ("angle_end", C.c_int), ("device", C.c_int),
+        ("sparse", C.c_void_p),
     ]
 
 
@@ -66,7 +67,9 @@ SYMBOLS = [
     "ncsg_solve", "ncsg_step_phase_a", "ncsg_atu_buffer", "ncsg_step_phase_b",
     "ncsg_profile_begin", "ncsg_profile_end", "ncsg_launch_count", "ncsg_set_atu_buffer",
     "ncsg_calibrate_scale", "ncsg_radon_dc_response", "ncsg_screen_step_condition",
-    "ncsg_set_cg",
+    "ncsg_set_cg", "ncsg_fanbeam_create", "ncsg_fan_defaults", "ncsg_sparse_create",
+    "ncsg_sparse_destroy", "ncsg_sparse_nnz", "ncsg_sparse_forward", "ncsg_sparse_adjoint",
+    "ncsg_sparse_forward_host", "ncsg_sparse_adjoint_host",
 ]
 PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
 
@@ -119,6 +122,18 @@ def lib():
                              C.POINTER(RecordRow), C.c_int, C.POINTER(C.c_int),
                              C.POINTER(C.c_double)]
     L.ncsg_set_cg.argtypes = [C.c_void_p, C.c_int]
+    L.ncsg_fanbeam_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double, C.c_int,
+                                      C.POINTER(C.c_void_p)]
+    L.ncsg_fan_defaults.argtypes = [C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.ncsg_sparse_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
+    L.ncsg_sparse_destroy.argtypes = [C.c_void_p]
+    L.ncsg_sparse_nnz.restype = C.c_int64
+    L.ncsg_sparse_nnz.argtypes = [C.c_void_p]
+    for name in ("ncsg_sparse_forward", "ncsg_sparse_adjoint"):
+        getattr(L, name).argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p]
+    for name in ("ncsg_sparse_forward_host", "ncsg_sparse_adjoint_host"):
+        getattr(L, name).argtypes = [C.c_void_p, _dp, _dp, C.c_int]
     L.ncsg_calibrate_scale.argtypes = [C.c_void_p, C.c_int, C.c_uint64, C.POINTER(C.c_double)]
     L.ncsg_radon_dc_response.argtypes = [C.c_void_p, C.POINTER(C.c_double)]
     L.ncsg_screen_step_condition.argtypes = [C.c_void_p, C.c_uint64, C.c_int,
@@ -280,6 +295,69 @@ class SolveResult:
     screen_est: float = float("nan")  # step-condition screen estimate (check_step_condition)
 
 
+def fan_defaults(n: int) -> tuple[float, float]:
+    """FanBeamGeometry::defaults (fanbeam.cpp:10-17): (source_radius, fan_angle)."""
+    r, f = C.c_double(), C.c_double()
+    _check(lib().ncsg_fan_defaults(n, C.byref(r), C.byref(f)), "fan_defaults")
+    return r.value, f.value
+
+
+class SparseMap:
+    """SparseMap (sparse.hpp:21-43) on the GPU: CSR + stored transpose.
+    FanBeam(...) builds build_fanbeam's matrix (fanbeam.cpp:43-111)."""
+
+    def __init__(self, handle, n, views, rays):
+        self._h = handle
+        self.n, self.n_angles, self.n_det = n, views, rays
+
+    @classmethod
+    def from_triplets(cls, n, views, rays, rows, cols, vals, device: int = 0):
+        rows = np.ascontiguousarray(rows, np.int64)
+        cols = np.ascontiguousarray(cols, np.int64)
+        vals = np.ascontiguousarray(vals, np.float64)
+        h = C.c_void_p()
+        _check(lib().ncsg_sparse_create(n, views, rays, rows.size, rows.ctypes.data,
+                                        cols.ctypes.data, vals.ctypes.data, device, C.byref(h)),
+               "SparseMap")
+        return cls(h, n, views, rays)
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ncsg_sparse_destroy(self._h)
+            self._h = None
+
+    def nnz(self) -> int:
+        return lib().ncsg_sparse_nnz(self._h)
+
+    def forward(self, x) -> np.ndarray:
+        x = np.ascontiguousarray(x, np.float64)
+        batch = x.size // (self.n * self.n)
+        out = np.zeros((batch, self.n_angles, self.n_det))
+        _check(lib().ncsg_sparse_forward_host(self._h, x.ravel(), out.ravel(), batch), "forward")
+        return out.reshape(x.shape[:-2] + (self.n_angles, self.n_det))
+
+    def adjoint(self, u) -> np.ndarray:
+        u = np.ascontiguousarray(u, np.float64)
+        batch = u.size // (self.n_angles * self.n_det)
+        out = np.zeros((batch, self.n, self.n))
+        _check(lib().ncsg_sparse_adjoint_host(self._h, u.ravel(), out.ravel(), batch), "adjoint")
+        return out.reshape(u.shape[:-2] + (self.n, self.n))
+
+
+class FanBeam(SparseMap):
+    """build_fanbeam(n, FanBeamGeometry{views, rays, source_radius, fan_angle})."""
+
+    def __init__(self, n: int, views: int, rays: int, source_radius: float | None = None,
+                 fan_angle: float | None = None, device: int = 0):
+        r0, f0 = fan_defaults(n)
+        self.source_radius = r0 if source_radius is None else source_radius
+        self.fan_angle = f0 if fan_angle is None else fan_angle
+        h = C.c_void_p()
+        _check(lib().ncsg_fanbeam_create(n, views, rays, self.source_radius, self.fan_angle,
+                                         device, C.byref(h)), "FanBeam")
+        super().__init__(h, n, views, rays)
+
+
 class Problem:
     """SplitProblem + SolverConfig + device Engine (solvers.hpp:24-78).
 
@@ -291,8 +369,12 @@ class Problem:
     def __init__(self, kind: int, n: int, alpha: float, beta: float, lam: float, gamma: float,
                  b, mask=None, n_angles: int = 0, n_det: int = 0, batch: int = 1,
                  positivity: bool = False, pinv_rel_tol: float = 1e-12,
-                 angle_range: tuple[int, int] = (0, 0), device: int = 0):
+                 angle_range: tuple[int, int] = (0, 0), device: int = 0,
+                 sparse: SparseMap | None = None):
         self.kind, self.n, self.batch = kind, n, batch
+        self._sparse = sparse  # keep the projector alive for the problem's lifetime
+        if sparse is not None:
+            n_angles, n_det = sparse.n_angles, sparse.n_det
         self.n_angles, self.n_det = n_angles, n_det
         self.alpha, self.beta, self.lam, self.gamma = alpha, beta, lam, gamma
         self.positivity = positivity
@@ -317,6 +399,7 @@ class Problem:
         d.b = b.ctypes.data
         d.angle_begin, d.angle_end = angle_range
         d.device = device
+        d.sparse = sparse._h if sparse is not None else None
         h = C.c_void_p()
         _check(lib().ncsg_problem_create(C.byref(d), C.byref(h)), "problem_create")
         self._h = h

@@ -146,3 +146,23 @@ def test_mask_apply_identity_and_constants(ncsg):
 def test_fft_needs_power_of_two(ncsg):
     with pytest.raises(ValueError, match="power-of-two"):
         ncsg.mask_apply(np.ones((12, 12)), np.ones((12, 12)))
+
+
+@pytest.mark.parametrize("n,views,rays", [(16, 12, 21), (32, 24, 45), (64, 40, 91)])
+def test_fanbeam_sparse_map(ncsg, port, n, views, rays):
+    # build_fanbeam + SparseMap::forward/adjoint (fanbeam.cpp, sparse.cpp:55-71)
+    R, fan = port.fan_defaults(n)
+    assert (R, fan) == ncsg.fan_defaults(n)
+    A = ncsg.FanBeam(n, views, rays)
+    rows, cols, vals = port.fanbeam_triplets(n, views, rays, R, fan)
+    assert A.nnz() == rows.size
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n))
+    u = rng.standard_normal((views, rays))
+    fx = port.fanbeam_apply(n, views, rays, R, fan, x)
+    au = port.fanbeam_apply(n, views, rays, R, fan, u, adjoint=True)
+    assert rel(A.forward(x), fx) <= 1e-5
+    assert rel(A.adjoint(u), au) <= 1e-5
+    # the same matrix from triplets
+    B = ncsg.SparseMap.from_triplets(n, views, rays, rows, cols, vals)
+    np.testing.assert_array_equal(B.forward(x), A.forward(x))

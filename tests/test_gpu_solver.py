@@ -380,3 +380,27 @@ def test_pet_parity(ncsg, port, positivity):
     np.testing.assert_array_equal(np.isfinite(go), fin)
     if fin.any():  # NonnegConj makes rows +inf while x has negative pixels
         assert np.max(np.abs(go[fin] - oo[fin]) / np.abs(oo[fin])) <= TOL
+
+
+def test_fanbeam_ct_parity(ncsg, port):
+    # CT-TV on build_fanbeam's SparseMap (assemble_problem with a SparseMap
+    # geometry): the NCS engine with the sparse projector against the oracle.
+    from paper_1810_13100_b200 import datagen
+
+    n, views, rays = 32, 36, 61
+    R, fan = port.fan_defaults(n)
+    port.set_fan(R, fan)
+    x = datagen.phantom(n, 5, 13)
+    b = port.fanbeam_apply(n, views, rays, R, fan, x).reshape(views, rays)
+    b = b + 0.01 * np.max(b) * np.random.default_rng(14).standard_normal(b.shape)
+    prob = Prob(3, n, views, rays, 0.1, 0.1, 0.01, b)
+    mask = np.ones((n, n)) * 0.5 * np.max(b) + port.laplacian_mask(n)
+    gamma = 1.2 * port.screen(prob, 0.0, mask, iters=40)
+    o = port.solve(prob, gamma, mask, 60, record_every=20)
+    A = ncsg.FanBeam(n, views, rays)
+    p = ncsg.Problem(ncsg.CT, n, 0.1, 0.1, 0.01, gamma, b, mask=mask, sparse=A)
+    p.set_state()
+    g = p.solve(60, record_every=20)
+    check_run(g, o)
+    est, shift = p.screen(0, 40)  # = alpha lambda_max(A^T A - C) - gamma
+    assert abs(est - (gamma / 1.2 - gamma)) <= 1e-4 * shift

@@ -357,3 +357,39 @@ def test_pet_model_matches_reference_bitwise(port, ref, positivity):
     np.testing.assert_array_equal(r1.x, r2.x)
     np.testing.assert_array_equal(r1.u, r2.u)
     np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
+
+
+# ------------------------------------------------------------- fan beam
+def test_fanbeam_matrix_matches_reference(port, ref):
+    # build_fanbeam (fanbeam.cpp:43-111) + SparseMap CSR order (sparse.cpp)
+    n = 24
+    R, fan = ref.fan_defaults(n)
+    assert (R, fan) == port.fan_defaults(n)
+    for views, rays, rad in [(16, 33, R), (9, 1, 2.5 * n), (20, 48, 1.2 * n)]:
+        a = ref.fanbeam_triplets(n, views, rays, rad, fan)
+        b = port.fanbeam_triplets(n, views, rays, rad, fan)
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
+        v = rand(views * rays, 3)
+        np.testing.assert_array_equal(ref.fanbeam_apply(n, views, rays, rad, fan, v, True),
+                                      port.fanbeam_apply(n, views, rays, rad, fan, v, True,
+                                                         threads=1))
+        x = rand(n * n, 4)
+        np.testing.assert_array_equal(ref.fanbeam_apply(n, views, rays, rad, fan, x),
+                                      port.fanbeam_apply(n, views, rays, rad, fan, x))
+
+
+def test_fanbeam_ct_solve_matches_reference_bitwise(port, ref):
+    n, views, rays = 16, 18, 31
+    R, fan = ref.fan_defaults(n)
+    ref.set_fan(R, fan)
+    port.set_fan(R, fan)
+    x = ref.make_phantom(n, [[1.0, 0.1, -0.05, 0.7, 0.5, 0.0]])
+    b = port.fanbeam_apply(n, views, rays, R, fan, x)
+    prob = Prob(3, n, views, rays, 0.1, 0.1, 0.01, b)
+    mask = port.laplacian_mask(n) + 1.0
+    r1 = ref.solve(prob, 2000.0, mask, 12, record_every=4)
+    r2 = port.solve(prob, 2000.0, mask, 12, record_every=4, threads=1)
+    np.testing.assert_array_equal(r1.x, r2.x)
+    np.testing.assert_array_equal(r1.u, r2.u)
+    np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
