@@ -242,6 +242,13 @@ ncsg_status ncsg_set_cg(ncsg_problem* p, int n_cg);
 ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t seed,
                                  double* scale);
 
+/* measurement_mask for a non-parallel geometry (pipeline.cpp:100-110):
+ * empirical_mask(NormalMap(A), N, n_samples, seed).mask
+ * (circulant.cpp:98-140) of a SparseMap, written as interleaved complex N*N
+ * (the SpectralMask layout); *n_dead (nullable) = bins no probe resolved. */
+ncsg_status ncsg_sparse_empirical_mask(const ncsg_sparse* a, int n_samples, uint64_t seed,
+                                       double* mask, int* n_dead);
+
 /* DC response of R^T R, <1, R^T R 1>/N^2: the dc value of radon_mask under the
  * rule the configs pin. */
 ncsg_status ncsg_radon_dc_response(const ncsg_radon* r, double* dc);

@@ -716,6 +716,76 @@ int orc_fanbeam_triplets(int n, int views, int rays, double R, double fan, int64
   return 0;
 }
 
+/* empirical_mask (circulant.cpp:98-140) of NormalMap(fan-beam SparseMap):
+ * per bin the mean of F(A^T A v)/F(v) over the probes whose |F v| clears
+ * 1e-12 * ||F v||; dead bins (never cleared) stay 0. */
+int orc_fanbeam_empirical_mask(int n, int views, int rays, double R, double fan, int samples,
+                               uint64_t seed, int nthreads, double* mask, int* n_dead) {
+  Csr A;
+  memset(&A, 0, sizeof(A));
+  if (samples < 1 || fan_build(n, views, rays, R, fan, &A)) return 2;
+  size_t nn = (size_t)n * n;
+  double* v = (double*)malloc(sizeof(double) * nn);
+  double* av = (double*)malloc(sizeof(double) * nn);
+  double* mid = (double*)malloc(sizeof(double) * A.rows);
+  double* cin = (double*)malloc(sizeof(double) * 2 * nn);
+  double* fv = (double*)malloc(sizeof(double) * 2 * nn);
+  double* fav = (double*)malloc(sizeof(double) * 2 * nn);
+  double* sum = (double*)calloc(2 * nn, sizeof(double));
+  int* hits = (int*)calloc(nn, sizeof(int));
+  for (int s = 0; s < samples; ++s) {
+    Rng r = rng_make(seed, (uint64_t)s);
+    for (size_t i = 0; i < nn; ++i) v[i] = rng_normal(&r);
+    for (size_t i = 0; i < nn; ++i) {
+      cin[2 * i] = v[i];
+      cin[2 * i + 1] = 0.0;
+    }
+    ncs_fft2d(cin, fv, n, n, -1);
+    csr_forward(&A, v, mid, nthreads);
+    csr_adjoint(&A, mid, av, nthreads);
+    for (size_t i = 0; i < nn; ++i) {
+      cin[2 * i] = av[i];
+      cin[2 * i + 1] = 0.0;
+    }
+    ncs_fft2d(cin, fav, n, n, -1);
+    double norm = 0.0;
+    for (size_t i = 0; i < nn; ++i) norm += fv[2 * i] * fv[2 * i] + fv[2 * i + 1] * fv[2 * i + 1];
+    norm = sqrt(norm);
+    double cutoff = 1e-12 * norm;
+    for (size_t i = 0; i < nn; ++i) {
+      double a = fv[2 * i], b = fv[2 * i + 1];
+      if (hypot(a, b) < cutoff) continue;
+      /* complex division fav / fv as std::complex<double> does (libstdc++) */
+      double c = fav[2 * i], d = fav[2 * i + 1];
+      double den = a * a + b * b;
+      sum[2 * i] += (c * a + d * b) / den;
+      sum[2 * i + 1] += (d * a - c * b) / den;
+      ++hits[i];
+    }
+  }
+  int dead = 0;
+  for (size_t i = 0; i < nn; ++i) {
+    if (hits[i] == 0) {
+      mask[2 * i] = mask[2 * i + 1] = 0.0;
+      ++dead;
+      continue;
+    }
+    mask[2 * i] = sum[2 * i] / (double)hits[i];
+    mask[2 * i + 1] = sum[2 * i + 1] / (double)hits[i];
+  }
+  *n_dead = dead;
+  free(v);
+  free(av);
+  free(mid);
+  free(cin);
+  free(fv);
+  free(fav);
+  free(sum);
+  free(hits);
+  csr_free(&A);
+  return 0;
+}
+
 int orc_fanbeam_apply(int n, int views, int rays, double R, double fan, int adjoint,
                       const double* in, double* out, int nthreads) {
   Csr A;

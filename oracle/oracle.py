@@ -104,6 +104,9 @@ class Port:
                                            C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp]
         L.orc_fanbeam_apply.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_int, _dp, _dp, C.c_int]
+        L.orc_fanbeam_empirical_mask.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double,
+                                                 C.c_double, C.c_int, C.c_uint64, C.c_int, _dp,
+                                                 C.POINTER(C.c_int)]
         L.orc_solve_ex.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                    C.c_double, C.c_int, _vp, C.c_double, _vp, C.c_int, C.c_int,
                                    C.c_int, _vp, _vp, _dp, _dp, _dp, C.c_int, C.POINTER(C.c_int),
@@ -142,6 +145,16 @@ class Port:
                                              C.byref(nnz), row.ctypes.data, col.ctypes.data,
                                              val.ctypes.data), "fanbeam")
         return row, col, val
+
+    def fanbeam_empirical_mask(self, n, views, rays, radius, fan_angle, samples=8, seed=0,
+                               threads=None):
+        out = np.zeros((n, n), np.complex128)
+        dead = C.c_int()
+        _check(self.lib.orc_fanbeam_empirical_mask(n, views, rays, radius, fan_angle, samples,
+                                                   seed, threads or default_threads(),
+                                                   out.view(np.float64).ravel(),
+                                                   C.byref(dead)), "empirical_mask")
+        return out, dead.value
 
     def fanbeam_apply(self, n, views, rays, radius, fan_angle, v, adjoint=False, threads=None):
         v = np.ascontiguousarray(v, np.float64).ravel()
@@ -367,6 +380,9 @@ class Ref:
                                            C.c_int64, C.POINTER(C.c_int64), _vp, _vp, _vp]
         L.ref_fanbeam_apply.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double, C.c_double,
                                         C.c_int, _dp, _dp]
+        L.ref_fanbeam_empirical_mask.argtypes = [C.c_int, C.c_int, C.c_int, C.c_double,
+                                                 C.c_double, C.c_int, C.c_uint64, _dp,
+                                                 C.POINTER(C.c_int)]
         L.ref_admm_cg_solve.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                         C.c_double, C.c_double, C.c_int, _dp, C.c_double,
                                         C.c_int, C.c_int, C.c_int, _dp, _dp, _dp, C.c_int,
@@ -512,6 +528,15 @@ class Ref:
                                                 C.byref(nnz), row.ctypes.data, col.ctypes.data,
                                                 val.ctypes.data), "fanbeam")
         return row, col, val
+
+    def fanbeam_empirical_mask(self, n, views, rays, radius, fan_angle, samples=8, seed=0):
+        out = np.zeros((n, n), np.complex128)
+        dead = C.c_int()
+        self._chk(self.lib.ref_fanbeam_empirical_mask(n, views, rays, radius, fan_angle,
+                                                      samples, seed,
+                                                      out.view(np.float64).ravel(),
+                                                      C.byref(dead)), "empirical_mask")
+        return out, dead.value
 
     def fanbeam_apply(self, n, views, rays, radius, fan_angle, v, adjoint=False):
         v = np.ascontiguousarray(v, np.float64).ravel()

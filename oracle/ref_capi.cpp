@@ -153,6 +153,22 @@ int ref_fanbeam_triplets(int n, int views, int rays, double source_radius, doubl
   });
 }
 
+// measurement_mask for a non-parallel geometry = empirical_mask(NormalMap(A),
+// n, samples, seed).mask (pipeline.cpp:100-110, circulant.cpp:98-140) on the
+// fan-beam SparseMap; *n_dead = number of dead bins.
+int ref_fanbeam_empirical_mask(int n, int views, int rays, double source_radius,
+                               double fan_angle, int samples, uint64_t seed, double* mask_out,
+                               int* n_dead) {
+  return guard([&] {
+    FanBeamGeometry g{views, rays, source_radius, fan_angle};
+    auto A = std::make_shared<SparseMap>(build_fanbeam(n, g));
+    NormalMap normal(A);
+    EmpiricalMask e = empirical_mask(normal, n, samples, seed);
+    mask_to(e.mask, mask_out);
+    *n_dead = static_cast<int>(e.dead_bins.size());
+  });
+}
+
 // SparseMap::forward / adjoint (sparse.cpp:55-71) of the fan-beam matrix.
 int ref_fanbeam_apply(int n, int views, int rays, double source_radius, double fan_angle,
                       int adjoint, const double* in, double* out) {

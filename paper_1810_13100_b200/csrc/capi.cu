@@ -1394,6 +1394,99 @@ ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t se
   });
 }
 
+ncsg_status ncsg_sparse_empirical_mask(const ncsg_sparse* a, int n_samples, uint64_t seed,
+                                       double* mask, int* n_dead) {
+  return guard([&] {
+    // measurement_mask for non-parallel geometry: empirical_mask(NormalMap(A),
+    // n, samples, seed) (pipeline.cpp:100-110, circulant.cpp:98-140).  Per bin
+    // the mean over probes of F(A^T A v) / F(v), skipping bins with
+    // |F v| < 1e-12 ||F v||; computed on half spectra (F v of a real v is
+    // conjugate-symmetric) and expanded to the full N x N mask on the host.
+    if (!a || !mask) throw Error{NCSG_INVALID, "bad empirical_mask arguments"};
+    if (n_samples < 1) throw Error{NCSG_INVALID, "n_samples must be positive"};
+    const SparseDev& A = a->dev;
+    const int n = A.n;
+    if (n & (n - 1)) throw Error{NCSG_INVALID, "GPU FFT sizes are powers of two"};
+    NCSG_CUDA_CHECK(cudaSetDevice(a->device));
+    cudaStream_t s = a->stream.s;
+    const size_t nn = A.cols, nk = static_cast<size_t>(n / 2 + 1), half = nk * n;
+    FftPlan f;
+    f.init(n, s);
+    const int B = std::min(n_samples, 8);
+    DevBuf<float> v, mid, av;
+    DevBuf<float2> fv, fav;
+    DevBuf<double2> sum;
+    DevBuf<int> hits;
+    DevBuf<double> red, cut;
+    v.alloc(nn * B);
+    av.alloc(nn * B);
+    mid.alloc(A.rows * B);
+    fv.alloc(half * B);
+    fav.alloc(half * B);
+    sum.alloc(half);
+    hits.alloc(half);
+    red.alloc(static_cast<size_t>(dot_pair_blocks()) * B);
+    cut.alloc(B);
+    NCSG_CUDA_CHECK(cudaMemsetAsync(sum.p, 0, half * sizeof(double2), s));
+    NCSG_CUDA_CHECK(cudaMemsetAsync(hits.p, 0, half * sizeof(int), s));
+    std::vector<float> hv(nn * B);
+    for (int s0 = 0; s0 < n_samples; s0 += B) {
+      const int nb = std::min(B, n_samples - s0);
+      for (int b = 0; b < nb; ++b) {  // probe_image (circulant.cpp:89-94)
+        HostRng rng(seed, static_cast<uint64_t>(s0 + b));
+        for (size_t i = 0; i < nn; ++i) hv[b * nn + i] = static_cast<float>(rng.next_normal());
+      }
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(v.p, hv.data(), nb * nn * 4, cudaMemcpyHostToDevice, s));
+      launch_sparse_forward(A, v.p, nn, mid.p, A.rows, nb, s);
+      launch_sparse_adjoint(A, mid.p, A.rows, av.p, nn, nb, s);
+      AtuTerms T;
+      T.n = n;
+      T.plain = v.p;
+      launch_fft_rows_r2c(f, T, fv.p, nb, s);
+      launch_fft_cols_forward(f, fv.p, nb, s);
+      T.plain = av.p;
+      launch_fft_rows_r2c(f, T, fav.p, nb, s);
+      launch_fft_cols_forward(f, fav.p, nb, s);
+      launch_spec_norm(fv.p, n, nb, red.p, s);
+      std::vector<double> h(static_cast<size_t>(dot_pair_blocks()) * nb), cutoff(nb, 0.0);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(h.data(), red.p, h.size() * sizeof(double),
+                                      cudaMemcpyDeviceToHost, s));
+      NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+      for (int b = 0; b < nb; ++b) {
+        double acc = 0.0;
+        for (int k = 0; k < dot_pair_blocks(); ++k) acc += h[static_cast<size_t>(b) * dot_pair_blocks() + k];
+        cutoff[b] = 1e-12 * std::sqrt(acc);
+      }
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(cut.p, cutoff.data(), nb * sizeof(double),
+                                      cudaMemcpyHostToDevice, s));
+      launch_mask_accumulate(fv.p, fav.p, cut.p, nb, half, sum.p, hits.p, s);
+    }
+    std::vector<double2> hs(half);
+    std::vector<int> hh(half);
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(hs.data(), sum.p, half * sizeof(double2),
+                                    cudaMemcpyDeviceToHost, s));
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(hh.data(), hits.p, half * sizeof(int), cudaMemcpyDeviceToHost, s));
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+    int dead = 0;
+    for (int j = 0; j < n; ++j)
+      for (int k = 0; k < n; ++k) {
+        // bin (j, k) = row frequency j, column frequency k; half spectrum holds k <= n/2
+        const bool direct = k <= n / 2;
+        const size_t src = direct ? static_cast<size_t>(k) * n + j
+                                  : static_cast<size_t>(n - k) * n + (n - j) % n;
+        double* o = mask + 2 * (static_cast<size_t>(j) * n + k);
+        if (hh[src] == 0) {
+          o[0] = o[1] = 0.0;
+          ++dead;
+          continue;
+        }
+        o[0] = hs[src].x / hh[src];
+        o[1] = (direct ? 1.0 : -1.0) * hs[src].y / hh[src];
+      }
+    if (n_dead) *n_dead = dead;
+  });
+}
+
 ncsg_status ncsg_radon_dc_response(const ncsg_radon* r, double* dc) {
   return guard([&] {
     // <1, R^T R 1> / N^2 = ||R 1||^2 / N^2: the DC bin of radon_mask.

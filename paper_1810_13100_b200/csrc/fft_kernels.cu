@@ -228,6 +228,23 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
+// Forward column FFTs only (in place): with the row pass this is the
+// unnormalised forward 2-D FFT of a real image as a half spectrum
+// (empirical_mask's F v, circulant.cpp:111-117).
+__global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
+                                        const float2* __restrict__ tw, int n, int logn) {
+  extern __shared__ float2 zs[];
+  const int k0 = blockIdx.x * kColsPerBlock;
+  const int b = blockIdx.y;
+  const int nk = n / 2 + 1;
+  const int nc = min(kColsPerBlock, nk - k0);
+  float2* col = specT + (static_cast<size_t>(b) * nk + k0) * n;
+  float2* zb = zs + kColsPerBlock * n;
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) zs[j] = col[j];
+  const float2* z = fft_stockham<-1>(zs, zb, nc, n, logn, tw);
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
+}
+
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
                                     const float2* __restrict__ tw, int n, int logn) {
   extern __shared__ float2 zs[];
@@ -363,6 +380,19 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
   fft_cols_filter_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, maskT, f.tw.p, n,
                                                                 log2i(n));
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStream_t s) {
+  const int n = f.n;
+  size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
+  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_cols_forward_kernel,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(smem)));
+  dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
+  fft_cols_forward_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, f.tw.p, n,
+                                                                               log2i(n));
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

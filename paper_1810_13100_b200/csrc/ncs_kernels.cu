@@ -528,6 +528,47 @@ __global__ void x_update_kernel(float* x, float* x_old, const double* d, double 
     atomicMin(flag, *(volatile int*)(flag + 1));
 }
 
+// empirical_mask (circulant.cpp:119-127) on the half spectrum specT[k][j]:
+// per-block partial sums of sum |F v|^2 over the FULL spectrum (columns
+// 0 < k < n/2 stand for two bins each).
+__global__ void spec_norm_kernel(const float2* spec, int n, double* out) {
+  __shared__ double sh[32];
+  const int nk = n / 2 + 1;
+  const size_t total = static_cast<size_t>(nk) * n;
+  const float2* sb = spec + blockIdx.y * total;
+  double acc = 0.0;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int k = static_cast<int>(i / n);
+    const double w = (k == 0 || k == n / 2) ? 1.0 : 2.0;
+    const double a = sb[i].x, b = sb[i].y;
+    acc += w * (a * a + b * b);
+  }
+  const double t = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+// sum += F(Av) / F(v), hits += 1 where |F v| >= cutoff[b] (fp64 division).
+__global__ void mask_accumulate_kernel(const float2* fv, const float2* fav, const double* cutoff,
+                                       int batch, size_t total, double2* sum, int* hits) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    double2 s = sum[i];
+    int h = hits[i];
+    for (int b = 0; b < batch; ++b) {
+      const double a = fv[b * total + i].x, c0 = fv[b * total + i].y;
+      if (hypot(a, c0) < cutoff[b]) continue;
+      const double c = fav[b * total + i].x, d = fav[b * total + i].y;
+      const double den = a * a + c0 * c0;
+      s.x += (c * a + d * c0) / den;
+      s.y += (d * a - c * c0) / den;
+      ++h;
+    }
+    sum[i] = s;
+    hits[i] = h;
+  }
+}
+
 __global__ void scale_kernel(const float* in, float s, float* out, size_t count) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < count;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
@@ -610,6 +651,20 @@ void launch_cg_dot(const double* p, const float* ap, size_t count, double* out, 
 void launch_x_update(float* x, float* x_old, const double* d, double inv_alpha, size_t count,
                      int* flag, cudaStream_t s) {
   x_update_kernel<<<grid_for(count, 256), 256, 0, s>>>(x, x_old, d, inv_alpha, count, flag);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_spec_norm(const float2* spec, int n, int batch, double* out, cudaStream_t s) {
+  spec_norm_kernel<<<dim3(dot_pair_blocks(), batch), 256, 0, s>>>(spec, n, out);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_mask_accumulate(const float2* fv, const float2* fav, const double* cutoff, int batch,
+                            size_t total, double2* sum, int* hits, cudaStream_t s) {
+  mask_accumulate_kernel<<<grid_for(total, 256), 256, 0, s>>>(fv, fav, cutoff, batch, total, sum,
+                                                              hits);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

@@ -89,4 +89,11 @@ void launch_cg_direction(double* p, const double* r, double beta, float* p32, si
 void launch_cg_dot(const double* p, const float* ap, size_t count, double* out, cudaStream_t s);
 void launch_x_update(float* x, float* x_old, const double* d, double inv_alpha, size_t count,
                      int* flag, cudaStream_t s);
+
+// empirical_mask (circulant.cpp:98-140) on half spectra [batch][n/2+1][n]:
+// out[batch][dot_pair_blocks()] partial sums of the full-spectrum |F v|^2;
+// sum / hits accumulate F(Av)/F(v) where |F v| >= cutoff[b].
+void launch_spec_norm(const float2* spec, int n, int batch, double* out, cudaStream_t s);
+void launch_mask_accumulate(const float2* fv, const float2* fav, const double* cutoff, int batch,
+                            size_t total, double2* sum, int* hits, cudaStream_t s);
 }  // namespace ncsg

@@ -234,6 +234,8 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
 // Column pass: forward FFT along j, multiply by maskT[k][j], inverse FFT.
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
                             cudaStream_t s);
+// Column pass without the filter: forward FFT only (half spectrum of F x).
+void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStream_t s);
 // Inverse rows (C2R) fused with the x update: out = x_in - w (or w when
 // x_in == nullptr); optional x_old copy, transposed copy, finiteness flag.
 struct XUpdate {

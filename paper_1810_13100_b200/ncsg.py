@@ -69,7 +69,7 @@ SYMBOLS = [
     "ncsg_calibrate_scale", "ncsg_radon_dc_response", "ncsg_screen_step_condition",
     "ncsg_set_cg", "ncsg_fanbeam_create", "ncsg_fan_defaults", "ncsg_sparse_create",
     "ncsg_sparse_destroy", "ncsg_sparse_nnz", "ncsg_sparse_forward", "ncsg_sparse_adjoint",
-    "ncsg_sparse_forward_host", "ncsg_sparse_adjoint_host",
+    "ncsg_sparse_forward_host", "ncsg_sparse_adjoint_host", "ncsg_sparse_empirical_mask",
 ]
 PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
 
@@ -128,6 +128,8 @@ def lib():
     L.ncsg_sparse_create.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_void_p, C.c_void_p,
                                      C.c_void_p, C.c_int, C.POINTER(C.c_void_p)]
     L.ncsg_sparse_destroy.argtypes = [C.c_void_p]
+    L.ncsg_sparse_empirical_mask.argtypes = [C.c_void_p, C.c_int, C.c_uint64, _dp,
+                                             C.POINTER(C.c_int)]
     L.ncsg_sparse_nnz.restype = C.c_int64
     L.ncsg_sparse_nnz.argtypes = [C.c_void_p]
     for name in ("ncsg_sparse_forward", "ncsg_sparse_adjoint"):
@@ -342,6 +344,19 @@ class SparseMap:
         out = np.zeros((batch, self.n, self.n))
         _check(lib().ncsg_sparse_adjoint_host(self._h, u.ravel(), out.ravel(), batch), "adjoint")
         return out.reshape(u.shape[:-2] + (self.n, self.n))
+
+
+def _sparse_empirical_mask(self, samples: int = 8, seed: int = 0):
+    """measurement_mask for this (non-parallel) geometry: empirical_mask(NormalMap(A),
+    n, samples, seed) (circulant.cpp:98-140) -> ((n, n) complex mask, dead bins)."""
+    out = np.zeros((self.n, self.n), np.complex128)
+    dead = C.c_int()
+    _check(lib().ncsg_sparse_empirical_mask(self._h, samples, seed, out.view(np.float64).ravel(),
+                                            C.byref(dead)), "empirical_mask")
+    return out, dead.value
+
+
+SparseMap.empirical_mask = _sparse_empirical_mask
 
 
 class FanBeam(SparseMap):

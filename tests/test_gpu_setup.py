@@ -149,3 +149,18 @@ def test_pinned_setup_values_full_size(ncsg, name):
                      n_angles=cfg.angles, n_det=cfg.det)
     est, shift = p.screen(0, 40)
     _check_screen(est, shift, cfg.pinned["screen_lmax"])
+
+
+@pytest.mark.parametrize("n,views,rays,samples", [(16, 12, 23, 4), (32, 24, 45, 8)])
+def test_fanbeam_empirical_mask(ncsg, port, ref, n, views, rays, samples):
+    # measurement_mask for fan beam = empirical_mask (circulant.cpp:98-140):
+    # fp32 spectra on the GPU against the fp64 oracle (itself pinned to the
+    # reference at 1e-12); per-bin ratios of F(A^T A v)/F(v), so bins where
+    # a probe's |F v| is small carry larger relative error.
+    R, fan = port.fan_defaults(n)
+    want, dead_o = port.fanbeam_empirical_mask(n, views, rays, R, fan, samples, 3)
+    got, dead_g = ncsg.FanBeam(n, views, rays).empirical_mask(samples, 3)
+    assert dead_g == dead_o
+    scale = np.max(np.abs(want))
+    assert np.max(np.abs(got - want)) <= 1e-4 * scale
+    assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)

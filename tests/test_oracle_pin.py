@@ -393,3 +393,14 @@ def test_fanbeam_ct_solve_matches_reference_bitwise(port, ref):
     np.testing.assert_array_equal(r1.x, r2.x)
     np.testing.assert_array_equal(r1.u, r2.u)
     np.testing.assert_array_equal(r1.rows[:, :4], r2.rows[:, :4])
+
+
+def test_fanbeam_empirical_mask_matches_reference(port, ref):
+    # measurement_mask for a non-parallel geometry (pipeline.cpp:100-110):
+    # empirical_mask(NormalMap(SparseMap), n, samples, seed) (circulant.cpp:98-140)
+    n, views, rays = 16, 12, 23
+    R, fan = ref.fan_defaults(n)
+    m1, d1 = ref.fanbeam_empirical_mask(n, views, rays, R, fan, 4, 7)
+    m2, d2 = port.fanbeam_empirical_mask(n, views, rays, R, fan, 4, 7, threads=1)
+    assert d1 == d2
+    np.testing.assert_allclose(m2, m1, rtol=1e-12, atol=1e-12 * np.max(np.abs(m1)))
