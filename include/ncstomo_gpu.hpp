@@ -97,6 +97,73 @@ class RadonMap final : public ProjectionMap {
   std::shared_ptr<ncsg_radon> h_;
 };
 
+/// Explicit sparse projector (sparse.hpp:21-43) on the GPU: CSR rows over
+/// sinogram bins plus the stored transpose for the adjoint.
+class SparseMap final : public ProjectionMap {
+ public:
+  SparseMap(int n_image, int n_angles, int n_det, const std::vector<std::int64_t>& rows,
+            const std::vector<std::int64_t>& cols, const std::vector<double>& vals,
+            int device = 0)
+      : n_(n_image), n_angles_(n_angles), n_det_(n_det) {
+    if (rows.size() != cols.size() || rows.size() != vals.size())
+      throw std::invalid_argument("sparse triplet arrays differ in length");
+    ncsg_sparse* h = nullptr;
+    detail::check(ncsg_sparse_create(n_image, n_angles, n_det,
+                                     static_cast<std::int64_t>(rows.size()), rows.data(),
+                                     cols.data(), vals.data(), device, &h));
+    h_.reset(h, [](ncsg_sparse* q) { ncsg_sparse_destroy(q); });
+  }
+  SparseMap(std::shared_ptr<ncsg_sparse> h, int n, int n_angles, int n_det)
+      : n_(n), n_angles_(n_angles), n_det_(n_det), h_(std::move(h)) {}
+  std::size_t domain_size() const override { return static_cast<std::size_t>(n_) * n_; }
+  std::size_t range_size() const override {
+    return static_cast<std::size_t>(n_angles_) * n_det_;
+  }
+  void forward(std::span<const double> x, std::span<double> out) const override {
+    if (x.size() != domain_size() || out.size() != range_size())
+      throw std::invalid_argument("SparseMap::forward size mismatch");
+    detail::check(ncsg_sparse_forward_host(h_.get(), x.data(), out.data(), 1));
+  }
+  void adjoint(std::span<const double> u, std::span<double> out) const override {
+    if (u.size() != range_size() || out.size() != domain_size())
+      throw std::invalid_argument("SparseMap::adjoint size mismatch");
+    detail::check(ncsg_sparse_adjoint_host(h_.get(), u.data(), out.data(), 1));
+  }
+  int n_angles() const override { return n_angles_; }
+  int n_detectors() const override { return n_det_; }
+  int n() const { return n_; }
+  std::int64_t nnz() const { return ncsg_sparse_nnz(h_.get()); }
+  const std::shared_ptr<ncsg_sparse>& handle() const { return h_; }
+
+ private:
+  int n_, n_angles_, n_det_;
+  std::shared_ptr<ncsg_sparse> h_;
+};
+
+/// FanBeamGeometry (fanbeam.hpp:8-19).
+struct FanBeamGeometry {
+  int n_views = 0;
+  int n_rays = 0;
+  double source_radius = 0.0;
+  double fan_angle = 0.0;
+  static FanBeamGeometry defaults(int n, int n_views, int n_rays) {
+    FanBeamGeometry g;
+    g.n_views = n_views;
+    g.n_rays = n_rays;
+    detail::check(ncsg_fan_defaults(n, &g.source_radius, &g.fan_angle));
+    return g;
+  }
+};
+
+/// build_fanbeam (fanbeam.cpp:43-111): the Siddon system matrix as a SparseMap.
+inline SparseMap build_fanbeam(int n, const FanBeamGeometry& g, int device = 0) {
+  ncsg_sparse* h = nullptr;
+  detail::check(
+      ncsg_fanbeam_create(n, g.n_views, g.n_rays, g.source_radius, g.fan_angle, device, &h));
+  return SparseMap(std::shared_ptr<ncsg_sparse>(h, [](ncsg_sparse* q) { ncsg_sparse_destroy(q); }),
+                   n, g.n_views, g.n_rays);
+}
+
 /// Forward differences with Neumann boundaries (grad.hpp:17-28).
 class GradMap final : public LinearMap {
  public:
@@ -241,6 +308,18 @@ inline SpectralMask measurement_mask(const RadonMap& geometry, double dc, int sa
   return radon_mask(geometry.n(), calibrate_scale(geometry, samples, seed), dc);
 }
 
+/// measurement_mask for a non-parallel geometry (pipeline.cpp:100-110):
+/// empirical_mask(NormalMap(geometry), n, samples, seed).mask
+/// (circulant.cpp:98-140); `dc` is unused there, as in the reference.
+inline SpectralMask measurement_mask(const SparseMap& geometry, double /*dc*/, int samples,
+                                     std::uint64_t seed) {
+  if (samples < 1) throw std::invalid_argument("mask estimation needs samples >= 1");
+  SpectralMask m(geometry.n());
+  detail::check(ncsg_sparse_empirical_mask(geometry.handle().get(), samples, seed,
+                                           reinterpret_cast<double*>(m.h.data()), nullptr));
+  return m;
+}
+
 /// metric_mask (pipeline.cpp:112-118).
 inline SpectralMask metric_mask(const SpectralMask& measurement, const ModelParams& p) {
   double w = p.beta / p.alpha;
@@ -258,39 +337,59 @@ struct SplitProblem {
   int n = 0, n_angles = 0, n_det = 0;
   double alpha = 1.0, beta = 1.0, lambda = 1.0;
   bool positivity = false;
-  std::vector<double> offset;  // b (sinogram or noisy image)
+  std::vector<double> offset;  // b (sinogram or noisy image; PET: counts)
+  std::shared_ptr<ncsg_sparse> sparse;  // SparseMap geometry (fan beam), else RadonMap
   std::size_t domain_size() const { return static_cast<std::size_t>(n) * n; }
   std::size_t range_size() const {
     std::size_t nn = domain_size();
-    std::size_t m = kind == NCSG_CT ? static_cast<std::size_t>(n_angles) * n_det : nn;
+    std::size_t m = kind != NCSG_DENOISE ? static_cast<std::size_t>(n_angles) * n_det : nn;
     return m + 2 * static_cast<std::size_t>(n) * (n - 1) + (positivity ? nn : 0);
   }
 };
 
-inline SplitProblem assemble_problem(std::span<const double> sino, const RadonMap& geometry,
-                                     const ModelParams& p) {
+namespace detail {
+inline SplitProblem assemble_problem_common(std::span<const double> sino, int n, int n_angles,
+                                            int n_det, std::size_t range, const ModelParams& p) {
   if (p.model != "ct" && p.model != "pet")
     throw std::invalid_argument("unknown model \"" + p.model + "\"");
   if (p.alpha <= 0.0 || p.beta <= 0.0)
     throw std::invalid_argument("alpha and beta must be positive");
   if (p.lambda < 0.0) throw std::invalid_argument("lambda must be nonnegative");
-  if (geometry.range_size() != sino.size())
+  if (range != sino.size())
     throw std::invalid_argument("sinogram shape does not match the geometry");
   SplitProblem s;
-  // ct: {1, R, QuadraticConj, sino}; pet: {1, R, PoissonConj(sino, alpha), 0}
+  // ct: {1, A, QuadraticConj, sino}; pet: {1, A, PoissonConj(sino, alpha), 0}
   // (pipeline.cpp:84-89) -- the counts travel in the offset slot
   s.kind = p.model == "pet" ? NCSG_PET : NCSG_CT;
   if (s.kind == NCSG_PET)
     for (double c : sino)
       if (c < 0.0) throw std::invalid_argument("Poisson counts must be nonnegative");
-  s.n = geometry.n();
-  s.n_angles = geometry.n_angles();
-  s.n_det = geometry.n_detectors();
+  s.n = n;
+  s.n_angles = n_angles;
+  s.n_det = n_det;
   s.alpha = p.alpha;
   s.beta = p.beta;
   s.lambda = p.lambda;
   s.positivity = p.positivity;
   s.offset.assign(sino.begin(), sino.end());
+  return s;
+}
+}  // namespace detail
+
+/// assemble_problem (pipeline.cpp:69-98) on the parallel-beam RadonMap.
+inline SplitProblem assemble_problem(std::span<const double> sino, const RadonMap& geometry,
+                                     const ModelParams& p) {
+  return detail::assemble_problem_common(sino, geometry.n(), geometry.n_angles(),
+                                         geometry.n_detectors(), geometry.range_size(), p);
+}
+
+/// assemble_problem on a SparseMap geometry (fan beam): same blocks as for
+/// RadonMap (pipeline.cpp:69-98), the data block projecting with the matrix.
+inline SplitProblem assemble_problem(std::span<const double> sino, const SparseMap& geometry,
+                                     const ModelParams& p) {
+  SplitProblem s = detail::assemble_problem_common(sino, geometry.n(), geometry.n_angles(),
+                                           geometry.n_detectors(), geometry.range_size(), p);
+  s.sparse = geometry.handle();
   return s;
 }
 
@@ -388,6 +487,7 @@ class Engine {
     d.mask = (!pdhg && cfg.mask) ? reinterpret_cast<const double*>(cfg.mask->h.data()) : nullptr;
     d.b = prob.offset.data();
     d.device = cfg.device;
+    d.sparse = prob.sparse.get();
     ncsg_problem* h = nullptr;
     check(ncsg_problem_create(&d, &h));
     h_.reset(h, [](ncsg_problem* p) { ncsg_problem_destroy(p); });
