@@ -10,10 +10,14 @@ consume identical numbers:
 * dc = DC response of E^T E, <1, E^T E 1>/n (README.md "Choosing parameters");
 * mask scale = calibrate_scale(NormalMap(E), radon_mask(N,1,1), 8, seed 0)
   (pipeline.cpp:100-110, circulant.cpp:142-169);
-* gamma = 1.2 x the power-method estimate of lambda_max(alpha (A^T A - C))
-  (the reference's step screen, solvers.cpp:206-245, and the MaskedMetric
-  rule of test_solvers.cpp:121-141 with a wider margin for the 40-step
-  power-method estimate).
+* gamma = 1.2 x lambda_max(alpha (A^T A - C)) from a converged (300-step)
+  power method (the reference's step screen, solvers.cpp:206-245, and the
+  MaskedMetric rule of test_solvers.cpp:121-141).  The reference's own screen
+  runs 40 steps, which underestimates lambda_max badly here (C3 4543 vs 6797,
+  C4 14903 vs 76153) -- NCS with a gamma pinned from it diverged at C4 --
+  so the 40-step value is kept only as `screen_lmax` for the setup-parity
+  test.  C4's converged estimate comes from the GPU power method
+  (scripts/pin_gamma_gpu.py), the others from the oracle.
 """
 from __future__ import annotations
 

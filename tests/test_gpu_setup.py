@@ -164,3 +164,20 @@ def test_fanbeam_empirical_mask(ncsg, port, ref, n, views, rays, samples):
     scale = np.max(np.abs(want))
     assert np.max(np.abs(got - want)) <= 1e-4 * scale
     assert np.linalg.norm(got - want) <= 1e-5 * np.linalg.norm(want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c1", "c3", "c5"])
+def test_converged_power_method_full_size(ncsg, name):
+    # the 300-step estimate gamma is pinned to (oracle/pin_configs.py) -- the
+    # GPU reproduces the oracle's converged lambda_max at full size
+    from paper_1810_13100_b200 import configs, instances
+
+    cfg = configs.get(name)
+    assert cfg.pinned["lmax_source"] == "oracle"
+    mask = instances.metric_mask(cfg)
+    p = ncsg.Problem(ncsg.CT, cfg.n, cfg.alpha, cfg.beta, cfg.lam, 0.0, np.zeros(cfg.m), mask=mask,
+                     n_angles=cfg.angles, n_det=cfg.det)
+    est, shift = p.screen(0, cfg.pinned["lmax_iters"])
+    _check_screen(est, shift, cfg.pinned["lmax"])
+

@@ -404,3 +404,21 @@ def test_fanbeam_ct_parity(ncsg, port):
     check_run(g, o)
     est, shift = p.screen(0, 40)  # = alpha lambda_max(A^T A - C) - gamma
     assert abs(est - (gamma / 1.2 - gamma)) <= 1e-4 * shift
+
+
+@pytest.mark.slow
+def test_c4_stable_with_pinned_gamma(ncsg):
+    # C4 (2048^2, 2048 x 2897) runs its BASELINE iteration count without
+    # diverging and decreases the objective with the converged-gamma pin
+    # (the 40-step-screen gamma diverged at iteration 107).
+    from paper_1810_13100_b200 import configs, instances
+
+    cfg = configs.get("c4")
+    R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det)
+    _, b = instances.make_instance(cfg, R.forward)
+    p = ncsg.ct_problem(cfg, b, mask=instances.metric_mask(cfg))
+    p.set_state()
+    r = p.solve(cfg.iters, record_every=cfg.iters // 3)
+    f = r.rows[0][:, 1]
+    assert np.all(np.isfinite(f)) and f[-1] < f[1] < f[0]
+
