@@ -144,47 +144,69 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
   const double c = 0.5 * (n - 1);
   const double s_mid = 0.5 * (n_det - 1);
   const double edge = n - 1;
+  // Ray table replay, angle-parallel on the host cores (each angle writes its
+  // own rows of g.rays and its own sample count).
+  std::vector<int64_t> samples_t(n_angles, 0);
+  auto replay = [&](int t0, int t1) {
+    for (int t = t0; t < t1; ++t) {
+      double theta = std::numbers::pi * t / n_angles;
+      double ct = std::cos(theta);
+      double st = std::sin(theta);
+      for (int d = 0; d < n_det; ++d) {
+        RayRange rr{1, 0};
+        double s = d - s_mid;
+        Interval ix = axis_interval(s * ct + c, -st, 0.0, n - 1);
+        Interval iy = axis_interval(c - s * st, -ct, 0.0, n - 1);
+        double lo = std::max(ix.lo, iy.lo);
+        double hi = std::min(ix.hi, iy.hi);
+        if (lo <= hi) {
+          double k0 = std::ceil(lo);
+          double k1 = std::floor(hi);
+          if (k0 <= k1) {
+            double px0 = s * ct - k0 * st + c;
+            double py0 = c - s * st - k0 * ct;
+            double dpx = -st, dpy = -ct;
+            int count = static_cast<int>(k1 - k0) + 1;
+            // per-sample box check (radon.cpp:88-90); valid samples of a ray
+            // form one interval because px, py are monotone in k.
+            auto valid = [&](int k) {
+              double px = px0 + k * dpx;
+              double py = py0 + k * dpy;
+              return !(px < 0.0 || px > edge || py < 0.0 || py > edge);
+            };
+            int kf = 0;
+            while (kf < count && !valid(kf)) ++kf;
+            if (kf < count) {
+              int kl = count - 1;
+              while (kl > kf && !valid(kl)) --kl;
+              int base = static_cast<int>(k0);
+              rr.first = base + kf;
+              rr.last = base + kl;
+              samples_t[t] += kl - kf + 1;
+            }
+          }
+        }
+        g.rays[static_cast<size_t>(t) * n_det + d] = rr;
+      }
+    }
+  };
+  {
+    const int nt = static_cast<int>(
+        std::max<size_t>(1, std::min<size_t>(16, std::thread::hardware_concurrency())));
+    std::vector<std::thread> th;
+    const int per = (n_angles + nt - 1) / nt;
+    for (int k = 0; k < nt; ++k) {
+      const int t0 = k * per, t1 = std::min(n_angles, t0 + per);
+      if (t0 < t1) th.emplace_back(replay, t0, t1);
+    }
+    for (auto& x : th) x.join();
+  }
   for (int t = 0; t < n_angles; ++t) {
     double theta = std::numbers::pi * t / n_angles;
     double ct = std::cos(theta);
     double st = std::sin(theta);
     bool own = t >= angle_begin && t < angle_end;
-    for (int d = 0; d < n_det; ++d) {
-      RayRange rr{1, 0};
-      double s = d - s_mid;
-      Interval ix = axis_interval(s * ct + c, -st, 0.0, n - 1);
-      Interval iy = axis_interval(c - s * st, -ct, 0.0, n - 1);
-      double lo = std::max(ix.lo, iy.lo);
-      double hi = std::min(ix.hi, iy.hi);
-      if (lo <= hi) {
-        double k0 = std::ceil(lo);
-        double k1 = std::floor(hi);
-        if (k0 <= k1) {
-          double px0 = s * ct - k0 * st + c;
-          double py0 = c - s * st - k0 * ct;
-          double dpx = -st, dpy = -ct;
-          int count = static_cast<int>(k1 - k0) + 1;
-          // per-sample box check (radon.cpp:88-90); valid samples of a ray
-          // form one interval because px, py are monotone in k.
-          auto valid = [&](int k) {
-            double px = px0 + k * dpx;
-            double py = py0 + k * dpy;
-            return !(px < 0.0 || px > edge || py < 0.0 || py > edge);
-          };
-          int kf = 0;
-          while (kf < count && !valid(kf)) ++kf;
-          if (kf < count) {
-            int kl = count - 1;
-            while (kl > kf && !valid(kl)) --kl;
-            int base = static_cast<int>(k0);
-            rr.first = base + kf;
-            rr.last = base + kl;
-            if (own) g.samples += kl - kf + 1;
-          }
-        }
-      }
-      g.rays[static_cast<size_t>(t) * n_det + d] = rr;
-    }
+    if (own) g.samples += samples_t[t];
     if (!own) continue;
 
     AngleGeom a{};
