@@ -327,9 +327,12 @@ __global__ void stacked_rest_kernel(StackArgs a) {
 
 }  // namespace
 
+#ifndef NCSG_DUAL_WAVES
+#define NCSG_DUAL_WAVES 8
+#endif
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
   size_t big = std::max<size_t>(a.m_end - a.m_begin, 2 * static_cast<size_t>(a.n) * a.n);
-  dim3 grid(grid_for(big, 256, 148 * 4), a.positivity ? 3 : 2, batch);
+  dim3 grid(grid_for(big, 256, 148 * NCSG_DUAL_WAVES), a.positivity ? 3 : 2, batch);
   dual_update_kernel<<<grid, 256, 0, s>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();

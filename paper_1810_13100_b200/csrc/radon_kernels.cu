@@ -427,8 +427,11 @@ size_t orbit_smem(int rmax) {
   return sizeof(float) * (4 * kOrbTile + kOrbWarps * 5 * rmax) + 128;
 }
 
+#ifndef NCSG_ORB_MINB
+#define NCSG_ORB_MINB 1
+#endif
 template <bool USE_TMA>
-__global__ void __launch_bounds__(kOrbWarps * 32)
+__global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
     fp_orbit_kernel(OrbArgs a, const __grid_constant__ CUtensorMap map) {
   constexpr int W = kOrbW, T = kOrbT, P = kOrbP, NW = kOrbWarps;
   constexpr int ROWS = T + 4;
