@@ -305,7 +305,11 @@ def bench_multi(args, cfg):
     e2e_s = float(dt.item())
     if rank == 0:
         clocks = clk.summary()
-        m_own = (s.range[1] - s.range[0]) * cfg.det
+        if s.range == (0, 0):  # orbit sharding
+            own = sum(multigpu.orbit_owner(t, cfg.angles, world) == rank for t in range(cfg.angles))
+            m_own = own * cfg.det
+        else:
+            m_own = (s.range[1] - s.range[0]) * cfg.det
         line = {"metric": METRIC, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

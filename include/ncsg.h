@@ -160,6 +160,12 @@ typedef struct {
    * parallel-beam RadonMap (nullable; n_angles / n_det then come from it).
    * The handle must outlive the problem (the reference's shared_ptr). */
   const struct ncsg_sparse* sparse;
+  /* Orbit sharding (shard_count > 1, n_angles % 4 == 0, angle_end == 0):
+   * this rank owns the dihedral angle orbits whose representative index is
+   * == shard_rank mod shard_count, so every shard keeps the orbit forward.
+   * 0, 0 = off (contiguous angle_begin/angle_end sharding or none). */
+  int shard_rank;
+  int shard_count;
 } ncsg_problem_desc;
 
 typedef struct ncsg_problem ncsg_problem;

@@ -133,6 +133,8 @@ struct ncsg_problem {
   DevBuf<float> x_prev, u_prev, dx, du, adx, mdx, dxT;
   int64_t iter = 0;
   size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
+  bool sharded = false;            // angle- or orbit-sharded (multi-GPU phases)
+  DevBuf<uint8_t> own_angle;       // orbit sharding: own[t] (nullptr otherwise)
   bool rank0 = true;              // adds the replicated blocks to A^T u
   float* atu_ext = nullptr;       // caller-owned A^T u buffer (sharded phases)
   DevBuf<float> atu_own;
@@ -305,6 +307,8 @@ void forward_and_dual(ncsg_problem* p) {
   a.m = p->m0;
   a.m_begin = p->m_begin;
   a.m_end = p->m_end;
+  a.own = p->own_angle.p;
+  a.det = p->d.n_det;
   a.u0 = p->u.p;
   a.axs = p->axs.p;
   a.b = p->b.p;
@@ -369,6 +373,8 @@ std::vector<double> objective_values(ncsg_problem* p) {
   a.m = p->m0;
   a.m_begin = p->m_begin;
   a.m_end = p->m_end;
+  a.own = p->own_angle.p;
+  a.det = p->d.n_det;
   const int nb = objective_blocks();
   a.out = p->red.p;
   launch_objective(a, p->batch, s);
@@ -990,7 +996,8 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       p->m_end = p->m0;
       p->rank0 = true;
     } else if (d.kind != NCSG_DENOISE) {
-      Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end);
+      Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end,
+                                    d.shard_rank, d.shard_count);
       p->m0 = static_cast<size_t>(d.n_angles) * d.n_det;
       int ab = d.angle_end > 0 ? d.angle_begin : 0;
       int ae = d.angle_end > 0 ? d.angle_end : d.n_angles;
@@ -998,6 +1005,15 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       p->m_end = static_cast<size_t>(ae) * d.n_det;
       p->rank0 = ab == 0;
       require_device(d.device);
+      if (geo.orbit_sharded) {  // own rays = members of own orbits, scattered over [0, m0)
+        p->rank0 = d.shard_rank == 0;
+        p->sharded = true;
+        std::vector<uint8_t> own(geo.own.begin(), geo.own.end());
+        p->own_angle.alloc(own.size());
+        NCSG_CUDA_CHECK(cudaMemcpy(p->own_angle.p, own.data(), own.size(), cudaMemcpyHostToDevice));
+      } else if (d.angle_end > 0) {
+        p->sharded = ab != 0 || ae != d.n_angles;
+      }
       p->radon = std::make_unique<RadonDev>();
       p->radon->geo = std::move(geo);
       p->radon->device = d.device;
@@ -1236,7 +1252,7 @@ ncsg_status ncsg_solve(ncsg_problem* p, int max_iters, int record_every,
     reset_flag(p);
     if (screen_est) *screen_est = NAN;
     if (check_step_condition && p->n_cg == 0) {  // solvers.cpp:207, 278 (warning only)
-      if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
+      if (p->sharded)
         throw Error{NCSG_INVALID, "the step-condition screen needs the unsharded problem"};
       double e = screen_estimate(p, seed, 40, nullptr);
       if (screen_est) *screen_est = e;
@@ -1297,8 +1313,7 @@ ncsg_status ncsg_set_cg(ncsg_problem* p, int n_cg) {
       if (p->has_mask)
         throw Error{NCSG_INVALID, "admm_cg uses M = alpha A^T A; drop the mask/overrides"};
       if (p->batch != 1) throw Error{NCSG_INVALID, "the CG x-update runs one problem (batch 1)"};
-      if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
-        throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};
+      if (p->sharded) throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};
       NCSG_CUDA_CHECK(cudaSetDevice(p->device));
       if (!p->cg_x.n) {
         p->cg_x.alloc(p->nn);
@@ -1519,7 +1534,7 @@ ncsg_status ncsg_screen_step_condition(ncsg_problem* p, uint64_t seed, int iters
   return guard([&] {
     if (!p || !est) throw Error{NCSG_INVALID, "bad screen arguments"};
     if (iters < 1) throw Error{NCSG_INVALID, "iters must be positive"};
-    if (!p->rank0 || p->m_begin != 0 || p->m_end != p->m0)
+    if (p->sharded)
       throw Error{NCSG_INVALID, "the step-condition screen needs the unsharded problem"};
     NCSG_CUDA_CHECK(cudaSetDevice(p->device));
     *est = screen_estimate(p, seed, iters, shift_out);

@@ -118,7 +118,8 @@ void choose_strides(Geometry& g) {
 
 }  // namespace
 
-Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end) {
+Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end,
+                        int shard_rank, int shard_count) {
   // RadonMap::RadonMap validation (radon.cpp:37-42), same messages.
   if (n < 2) throw Error{NCSG_INVALID, "image size must be >= 2"};
   if (n_angles < 1) throw Error{NCSG_INVALID, "need at least one angle"};
@@ -132,6 +133,14 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
   }
   if (angle_begin < 0 || angle_end > n_angles || angle_begin >= angle_end)
     throw Error{NCSG_INVALID, "angle shard out of range"};
+  const bool orbit_sharded = shard_count > 1;
+  if (orbit_sharded) {
+    if (n_angles % 4 != 0) throw Error{NCSG_INVALID, "orbit sharding needs a multiple of 4 angles"};
+    if (shard_rank < 0 || shard_rank >= shard_count)
+      throw Error{NCSG_INVALID, "shard rank out of range"};
+    if (angle_begin != 0 || angle_end != n_angles)
+      throw Error{NCSG_INVALID, "orbit sharding and angle ranges are exclusive"};
+  }
 
   Geometry g;
   g.n = n;
@@ -140,6 +149,11 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
   g.s_mid = (n_det - 1) / 2;
   g.P0 = static_cast<long long>(n - 1) << 31;  // c = (n-1)/2 in Q32
   g.rays.resize(static_cast<size_t>(n_angles) * n_det);
+  g.orbit_sharded = orbit_sharded;
+  g.own.assign(n_angles, 0);
+  for (int t = 0; t < n_angles; ++t)
+    g.own[t] = orbit_sharded ? (orbit_rep(t, n_angles) % shard_count == shard_rank)
+                             : (t >= angle_begin && t < angle_end);
 
   const double c = 0.5 * (n - 1);
   const double s_mid = 0.5 * (n_det - 1);
@@ -205,7 +219,7 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     double theta = std::numbers::pi * t / n_angles;
     double ct = std::cos(theta);
     double st = std::sin(theta);
-    bool own = t >= angle_begin && t < angle_end;
+    bool own = g.own[t] != 0;
     if (own) g.samples += samples_t[t];
     if (!own) continue;
 
@@ -232,7 +246,7 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
   }
   choose_strides(g);
   // Dihedral orbits (only for a full, unsharded angle set divisible by 4).
-  if (n_angles % 4 == 0 && angle_begin == 0 && angle_end == n_angles) {
+  if (n_angles % 4 == 0 && angle_begin == 0 && angle_end == n_angles) {  // full set or orbit shard
     const int q = n_angles / 4;
     for (const AngleGeom& a : g.cls[0]) {
       if (a.t > q) continue;  // reps: theta in [0, 45 deg]

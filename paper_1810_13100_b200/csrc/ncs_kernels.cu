@@ -54,6 +54,7 @@ __global__ void dual_update_kernel(DualArgs a) {
       float* ax = a.axs + b * a.m;
       const float* bb = a.b + b * a.m;
       for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+        if (a.own && !a.own[i / a.det]) continue;  // another shard's orbit
         float rx = 0.f;
         for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
         const float r = us[i] + alpha * (2.f * rx - ax[i] - bb[i]);
@@ -71,6 +72,7 @@ __global__ void dual_update_kernel(DualArgs a) {
       float* ax = a.axs + b * a.m;
       const float* cnt = a.b + b * a.m;
       for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+        if (a.own && !a.own[i / a.det]) continue;  // another shard's orbit
         float rx = 0.f;
         for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
         const double r = static_cast<double>(us[i]) + alpha * (2.f * rx - ax[i]);
@@ -155,6 +157,7 @@ __global__ void objective_kernel(ObjArgs a) {
     const float* ax = a.axs + b * a.m;
     const float* bb = a.b + b * a.m;
     for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+      if (a.own && !a.own[i / a.det]) continue;
       const double z = static_cast<double>(ax[i]) - static_cast<double>(bb[i]);
       q += z * z;
     }
@@ -163,6 +166,7 @@ __global__ void objective_kernel(ObjArgs a) {
     const float* ax = a.axs + b * a.m;
     const float* cnt = a.b + b * a.m;
     for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+      if (a.own && !a.own[i / a.det]) continue;
       const double y = ax[i], c = cnt[i];
       if (c > 0.0)
         q += y <= 0.0 ? INFINITY : y - c * log(y);

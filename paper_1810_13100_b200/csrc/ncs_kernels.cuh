@@ -21,6 +21,8 @@ struct DualArgs {
   const float* x = nullptr;
   const float* x_old = nullptr;
   int* flag = nullptr;
+  const uint8_t* own = nullptr;  // orbit sharding: own[t] of ray t*det + d (nullable)
+  int det = 0;
 };
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
 
@@ -31,6 +33,8 @@ struct ObjArgs {
   const float* b = nullptr;
   const float* x = nullptr;
   size_t m = 0, m_begin = 0, m_end = 0;
+  const uint8_t* own = nullptr;  // orbit sharding (nullable)
+  int det = 0;
   double* out = nullptr;  // [batch][objective_blocks()][4]
 };
 int objective_blocks();

@@ -75,13 +75,24 @@ struct Geometry {
   std::vector<AngleGeom> cls[2];   // class 0 = V, class 1 = H
   std::vector<RayRange> rays;      // [t][d]
   std::vector<OrbitGeom> orbits;   // filled when every angle belongs to an orbit
+  std::vector<uint8_t> own;        // own[t]: angle t belongs to this shard
+  bool orbit_sharded = false;
   int64_t samples = 0;
 };
+// Orbit representative of angle t (n_angles % 4 == 0): the member in [0, A/4].
+inline int orbit_rep(int t, int n_angles) {
+  const int q = n_angles / 4;
+  if (t <= q) return t;
+  if (t < 2 * q) return 2 * q - t;
+  if (t <= 3 * q) return t - 2 * q;
+  return n_angles - t;
+}
 
 // Replays the reference's fp64 ray table and per-sample box check
 // (radon.cpp:35-72, 85-90) and builds the fixed-point angle table.
 // Throws Error{NCSG_INVALID} with the reference's messages.
-Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end);
+Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end,
+                        int shard_rank = 0, int shard_count = 0);
 
 // Explicit sparse projector (SparseMap, sparse.cpp): CSR over sinogram rows
 // (view-major) and its stored transpose over image pixels, fp64 on the host.

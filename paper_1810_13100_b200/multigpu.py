@@ -22,6 +22,24 @@ import os
 import time
 
 
+def orbit_rep(t: int, n_angles: int) -> int:
+    """Representative (in [0, A/4]) of angle t's dihedral orbit {t, t+A/2,
+    A-t, A/2-t} (ncsg_internal.cuh orbit_rep)."""
+    q = n_angles // 4
+    if t <= q:
+        return t
+    if t < 2 * q:
+        return 2 * q - t
+    if t <= 3 * q:
+        return t - 2 * q
+    return n_angles - t
+
+
+def orbit_owner(t: int, n_angles: int, world: int) -> int:
+    """Rank owning angle t under orbit sharding (orbits round-robin by rep)."""
+    return orbit_rep(t, n_angles) % world
+
+
 def shard_angles(n_angles: int, world: int, rank: int) -> tuple[int, int]:
     """Contiguous balanced angle block [begin, end) of `rank`."""
     base, rem = divmod(n_angles, world)
@@ -38,8 +56,14 @@ class ShardedSolver:
         from . import ncsg
 
         self.rank, self.world = rank, world
-        self.range = shard_angles(cfg.angles, world, rank)
-        self.prob = ncsg.ct_problem(cfg, b, mask=mask, angle_range=self.range, device=device)
+        if cfg.angles % 4 == 0 and world > 1:
+            # orbit sharding: every rank keeps the dihedral orbit forward
+            self.range = (0, 0)
+            self.prob = ncsg.ct_problem(cfg, b, mask=mask, orbit_shard=(rank, world),
+                                        device=device)
+        else:
+            self.range = shard_angles(cfg.angles, world, rank)
+            self.prob = ncsg.ct_problem(cfg, b, mask=mask, angle_range=self.range, device=device)
         self.prob.set_state()
         self.atu = torch.zeros(cfg.batch * cfg.n * cfg.n, dtype=torch.float32,
                                device=f"cuda:{device}")

@@ -45,7 +45,7 @@ class ProblemDesc(C.Structure):
         ("beta", C.c_double), ("lambda_", C.c_double), ("gamma", C.c_double),
         ("pinv_rel_tol", C.c_double), ("mask", C.c_void_p), ("b", C.c_void_p),
         ("angle_begin", C.c_int), ("angle_end", C.c_int), ("device", C.c_int),
-        ("sparse", C.c_void_p),
+        ("sparse", C.c_void_p), ("shard_rank", C.c_int), ("shard_count", C.c_int),
     ]
 
 
@@ -385,7 +385,7 @@ class Problem:
                  b, mask=None, n_angles: int = 0, n_det: int = 0, batch: int = 1,
                  positivity: bool = False, pinv_rel_tol: float = 1e-12,
                  angle_range: tuple[int, int] = (0, 0), device: int = 0,
-                 sparse: SparseMap | None = None):
+                 sparse: SparseMap | None = None, orbit_shard: tuple[int, int] = (0, 0)):
         self.kind, self.n, self.batch = kind, n, batch
         self._sparse = sparse  # keep the projector alive for the problem's lifetime
         if sparse is not None:
@@ -415,6 +415,7 @@ class Problem:
         d.angle_begin, d.angle_end = angle_range
         d.device = device
         d.sparse = sparse._h if sparse is not None else None
+        d.shard_rank, d.shard_count = orbit_shard
         h = C.c_void_p()
         _check(lib().ncsg_problem_create(C.byref(d), C.byref(h)), "problem_create")
         self._h = h

@@ -268,6 +268,46 @@ def test_sharded_phases_on_one_gpu(ncsg, port):
     assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 1e-5
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_orbit_sharded_phases_on_one_gpu(ncsg, port, world):
+    """Orbit sharding (each rank owns whole dihedral orbits and keeps the orbit
+    forward): the phases emulated on one device match the unsharded engine."""
+    import torch
+
+    prob, mask, gamma = small_ct(port, n=64, A=40)
+    full = gpu_problem(ncsg, prob, gamma, mask)
+    full.step(30)
+    xf, uf, _ = full.get_state()
+    shards = [gpu_problem(ncsg, prob, gamma, mask, orbit_shard=(r, world)) for r in range(world)]
+    bufs = [torch.zeros(prob.n * prob.n, device="cuda") for _ in shards]
+    for s, bf in zip(shards, bufs):
+        s.bind_atu(bf)
+    for _ in range(30):
+        for s in shards:
+            s.phase_a()
+        torch.cuda.synchronize()
+        tot = sum(bufs)
+        for bf in bufs:
+            bf.copy_(tot)
+        torch.cuda.synchronize()
+        for s in shards:
+            s.phase_b()
+        torch.cuda.synchronize()
+    xs = [s.get_state() for s in shards]
+    for x, u, _ in xs[1:]:
+        np.testing.assert_array_equal(x, xs[0][0])
+    assert rel(xs[0][0], xf) <= 1e-5
+    from paper_1810_13100_b200.multigpu import orbit_owner
+
+    us = np.zeros(prob.m0)
+    for t in range(prob.angles):
+        r = orbit_owner(t, prob.angles, world)
+        sl = slice(t * prob.det, (t + 1) * prob.det)
+        us[sl] = xs[r][1][0, sl]
+    assert rel(us, uf[0, : prob.m0]) <= 1e-5
+    assert rel(xs[0][1][0, prob.m0:], uf[0, prob.m0:]) <= 1e-5
+
+
 @pytest.mark.parametrize("name", ["ct16", "ct32", "ct32_pos", "tv32"])
 def test_gpu_matches_reference_golden(ncsg, name):
     # Fixtures computed by the reference's own build (oracle/gen_golden.py):

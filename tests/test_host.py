@@ -150,14 +150,31 @@ def test_angle_shards_cover_and_balance():
             assert max(sizes) - min(sizes) <= 1
 
 
-def _sharded_atu_worker(rank, world, port_so, out_q):
+def test_orbit_shards_partition_orbits():
+    from paper_1810_13100_b200.multigpu import orbit_owner, orbit_rep
+
+    for A in (12, 180, 720, 2048):
+        q = A // 4
+        for t in range(A):  # the four members share one representative in [0, q]
+            r = orbit_rep(t, A)
+            assert 0 <= r <= q
+            members = {r, (r + 2 * q) % A, (A - r) % A, (2 * q - r) % A}
+            assert t in members
+        for world in (2, 3, 8):
+            owners = [orbit_owner(t, A, world) for t in range(A)]
+            counts = [owners.count(w) for w in range(world)]
+            assert sum(counts) == A
+            assert max(counts) - min(counts) <= 8  # at most ~one orbit (4 angles, x2 at 0/45 deg) apart
+
+
+def _sharded_atu_worker(rank, world, port_so, out_q, mode="contiguous"):
     import torch.distributed as dist
 
     from oracle.oracle import Port
-    from paper_1810_13100_b200.multigpu import shard_angles
+    from paper_1810_13100_b200.multigpu import orbit_owner, shard_angles
 
-    dist.init_process_group("gloo", init_method="tcp://127.0.0.1:29533", rank=rank,
-                            world_size=world)
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{29533 + (mode == 'orbit')}",
+                            rank=rank, world_size=world)
     P = Port(port_so)
     rng = np.random.default_rng(1)
     n, A = 24, 16
@@ -165,9 +182,14 @@ def _sharded_atu_worker(rank, world, port_so, out_q):
     us = rng.standard_normal((A, D))
     ug = rng.standard_normal(2 * n * (n - 1))
     w = 0.7
-    a0, a1 = shard_angles(A, world, rank)
     own = np.zeros_like(us)
-    own[a0:a1] = us[a0:a1]
+    if mode == "orbit":
+        for t in range(A):
+            if orbit_owner(t, A, world) == rank:
+                own[t] = us[t]
+    else:
+        a0, a1 = shard_angles(A, world, rank)
+        own[a0:a1] = us[a0:a1]
     part = P.radon_adjoint(own, n, threads=1)
     if rank == 0:  # the replicated blocks are contributed once
         part = part + w * P.grad_adjoint(ug, n)
@@ -180,16 +202,19 @@ def _sharded_atu_worker(rank, world, port_so, out_q):
     dist.destroy_process_group()
 
 
-def test_sharded_adjoint_allreduce_gloo():
-    """The N>1 decomposition: per-rank partial A^T u over own angles (+ the
-    replicated D^T u_g on rank 0) all-reduced equals the full A^T u."""
+@pytest.mark.parametrize("mode", ["contiguous", "orbit"])
+def test_sharded_adjoint_allreduce_gloo(mode):
+    """The N>1 decomposition: per-rank partial A^T u over own angles (a
+    contiguous block, or whole dihedral orbits) plus the replicated D^T u_g on
+    rank 0, all-reduced, equals the full A^T u."""
     import multiprocessing as mp
 
     from oracle.oracle import PORT_SO
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    procs = [ctx.Process(target=_sharded_atu_worker, args=(r, 2, PORT_SO, q)) for r in range(2)]
+    procs = [ctx.Process(target=_sharded_atu_worker, args=(r, 2, PORT_SO, q, mode))
+             for r in range(2)]
     for p in procs:
         p.start()
     res = [q.get(timeout=120) for _ in procs]
