@@ -1,27 +1,29 @@
 // Parallel-beam projector R and its exact transpose R^T on sm_100a.
 //
-// Both kernels walk the reference's sample lattice (radon.cpp:43-71, 82-127)
+// All kernels walk the reference's sample lattice (radon.cpp:43-71, 82-127)
 // in exact Q32 fixed point (see AngleGeom in ncsg_internal.cuh), so every
 // kernel assigns each sample to the same cell and the per-ray valid interval
 // replayed on the host reproduces the reference's box check.  Lanes of a warp
 // own rays; all lanes of a warp start a tile at the same row phase ("y-aligned
 // stepping"), so at any step the active lanes sit within one pixel row of each
-// other.  That keeps the forward gathers' shared-memory bank spread wide and
-// makes the adjoint's scatter provably conflict-free between lanes whose rays
-// are >= 3 apart ("R^T without atomics").
+// other.
 //
-// R  (fp_strip_kernel):  CTA = (image strip of kFpW columns, kFpWarps angles).
-//     The strip is swept top to bottom in kFpT-row tiles staged in shared
-//     memory; every warp integrates its angle's rays over the tile (bilinear,
-//     radon.cpp:91-98) and accumulates per-ray sums in shared memory; the
-//     strip's partial ray sums go to part[strip][ray] and are summed in strip
-//     order by the consumer (deterministic, no atomics).
+// R  (fp_orbit_kernel, default when the angle set is closed under the
+//     dihedral maps): CTA = (128-column strip, 64-row segment, 8 orbits); the
+//     four member images are interleaved per pixel (make_quad_kernel) and
+//     arrive per 32-row tile by one 4-D TMA box; one lattice walk serves the
+//     four member angles with four 128-bit shared loads per sample.
+// R  (fp_strip_kernel, sharded / other angle sets): CTA = (strip of kFpW
+//     columns, kFpWarps angles), one angle per warp, class-H angles on x^T.
+//     Both write per-(ray, strip[, segment]) partial sums that the consumer
+//     adds in a fixed order (deterministic, no atomics).
 // R^T (bp_tile_kernel):  CTA = (W x T output tile, chunk of angles).
 //     Each warp owns a private shared-memory accumulator of the tile plus a
-//     one-pixel halo and scatters w * bilinear weights (radon.cpp:116-125)
-//     with plain read-modify-write; lanes take rays 5 apart in 5 phases, so
-//     two lanes of one instruction never touch the same pixel.  Warps are
-//     reduced once per CTA into a partial image per angle chunk.
+//     halo and scatters w * bilinear weights (radon.cpp:116-125) with plain
+//     read-modify-write; lanes of one phase take rays `bp_stride` >= 3 apart
+//     (chosen per angle by a host bank-conflict model), so two lanes of one
+//     instruction never touch the same pixel (race-free without atomics).
+//     Warps are reduced once per CTA into a partial image per angle chunk.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
