@@ -162,7 +162,6 @@ int* step_counter(ncsg_problem* p) { return p->flag.p; }
 // explicit SparseMap (fan beam).  Both write R x as partial slots summed by
 // the dual update / strip_sum, and R^T u as partial images (class-V frame,
 // then class-H transposed) summed into A^T u by the FFT loader.
-bool has_projector(const ncsg_problem* p) { return p->radon || p->sparse; }
 int proj_slots(const ncsg_problem* p) {
   return p->sparse ? 1 : (p->radon ? p->radon->fp_slots() : 0);
 }
@@ -1344,7 +1343,6 @@ ncsg_status ncsg_calibrate_scale(const ncsg_radon* r, int n_samples, uint64_t se
     RadonDev& dev = const_cast<RadonDev&>(r->dev);
     const Geometry& g = dev.geo;
     const int n = g.n;
-    if (n & (n - 1)) throw Error{NCSG_INVALID, "GPU FFT sizes are powers of two"};
     cudaStream_t s = r->stream.s;
     const size_t nn = static_cast<size_t>(n) * n, m = static_cast<size_t>(g.n_angles) * g.n_det;
     std::vector<std::complex<double>> t(nn);
@@ -1421,7 +1419,6 @@ ncsg_status ncsg_sparse_empirical_mask(const ncsg_sparse* a, int n_samples, uint
     if (n_samples < 1) throw Error{NCSG_INVALID, "n_samples must be positive"};
     const SparseDev& A = a->dev;
     const int n = A.n;
-    if (n & (n - 1)) throw Error{NCSG_INVALID, "GPU FFT sizes are powers of two"};
     NCSG_CUDA_CHECK(cudaSetDevice(a->device));
     cudaStream_t s = a->stream.s;
     const size_t nn = A.cols, nk = static_cast<size_t>(n / 2 + 1), half = nk * n;

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <string>
 #include <vector>
 
 #include "ncs_device.cuh"
@@ -145,8 +146,90 @@ __device__ float2* fft_stockham(float2* a, float2* b, int nfft, int n, int logn,
   return a;
 }
 
+// ---- mixed-radix Stockham (sizes 2^a 3^b 5^c 7^d that are not powers of 2)
+template <int R, int SIGN>
+__device__ __forceinline__ void dft_small(float2* v) {
+  if constexpr (R == 2 || R == 4 || R == 8) {
+    dftR<R, SIGN>(v);
+  } else {
+  float2 out[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    float re = 0.f, im = 0.f;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      float sn, cs;
+      sincospif(2.0f * static_cast<float>((r * k) % R) / R, &sn, &cs);
+      sn *= static_cast<float>(SIGN);
+      re += v[r].x * cs - v[r].y * sn;
+      im += v[r].x * sn + v[r].y * cs;
+    }
+    out[k] = make_float2(re, im);
+  }
+#pragma unroll
+  for (int k = 0; k < R; ++k) v[k] = out[k];
+  }
+}
+
+template <int R, int SIGN>
+__device__ void stockham_stage_mixed(const float2* in, float2* out, int nfft, int n, int Ns,
+                                     const float2* __restrict__ tw) {
+  const int m = n / R;
+  const int step = n / (Ns * R);
+  for (int bi = threadIdx.x; bi < nfft * m; bi += blockDim.x) {
+    const int q = bi / m, j = bi - q * m;
+    const float2* src = in + q * n;
+    float2* dst = out + q * n;
+    const int k = j % Ns;
+    float2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = src[j + r * m];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      float2 w = __ldg(tw + r * k * step);
+      if (SIGN > 0) w.y = -w.y;
+      v[r] = cmul(v[r], w);
+    }
+    dft_small<R, SIGN>(v);
+    const int idx = (j - k) * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) dst[idx + r * Ns] = v[r];
+  }
+}
+
+template <int SIGN>
+__device__ float2* fft_mixed(float2* a, float2* b, int nfft, const FftShape& sh,
+                             const float2* __restrict__ tw) {
+  int Ns = 1;
+  for (int st = 0; st < sh.nst; ++st) {
+    __syncthreads();
+    const int R = sh.rad[st];
+    switch (R) {
+      case 2: stockham_stage_mixed<2, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      case 3: stockham_stage_mixed<3, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      case 4: stockham_stage_mixed<4, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      case 5: stockham_stage_mixed<5, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      case 7: stockham_stage_mixed<7, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      default: stockham_stage_mixed<8, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+    }
+    Ns *= R;
+    float2* t = a;
+    a = b;
+    b = t;
+  }
+  __syncthreads();
+  return a;
+}
+
+template <int SIGN>
+__device__ __forceinline__ float2* fft_run(float2* a, float2* b, int nfft, const FftShape& sh,
+                                           const float2* __restrict__ tw) {
+  return sh.logn >= 0 ? fft_stockham<SIGN>(a, b, nfft, sh.n, sh.logn, tw)
+                      : fft_mixed<SIGN>(a, b, nfft, sh, tw);
+}
+
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
-                                    const float2* __restrict__ tw, int logn) {
+                                    const float2* __restrict__ tw, FftShape sh) {
   extern __shared__ float2 zs[];
   const int n = T.n;
   const int y0 = blockIdx.x * kRowsPerBlock;
@@ -185,7 +268,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
         slot->x += v;
     }
   }
-  const float2* z = fft_stockham<-1>(zs, zb, npair, n, logn, tw);
+  const float2* z = fft_run<-1>(zs, zb, npair, sh, tw);
   // Unpack the two real rows of each pair: A = (Z_k + conj Z_-k)/2,
   // B = (Z_k - conj Z_-k)/(2i); write specT[k][y] (k = 0..n/2).
   const int nk = n / 2 + 1;
@@ -196,7 +279,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     if (y >= n) continue;
     const float2* zq = z + (r >> 1) * n;
     const float2 zk = zq[k];
-    const float2 zm = zq[(n - k) & (n - 1)];
+    const float2 zm = zq[(n - k) % n];
     float2 v;
     if (r & 1)
       v = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
@@ -212,7 +295,8 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
 constexpr int kColsPerBlock = NCSG_FFT_COLS;  // columns per column-pass CTA
 
 __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2* __restrict__ maskT,
-                                       const float2* __restrict__ tw, int n, int logn) {
+                                       const float2* __restrict__ tw, FftShape sh) {
+  const int n = sh.n;
   extern __shared__ float2 zs[];
   const int k0 = blockIdx.x * kColsPerBlock;
   const int b = blockIdx.y;
@@ -222,9 +306,9 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   const float2* mk = maskT + static_cast<size_t>(k0) * n;
   float2* zb = zs + kColsPerBlock * n;
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) zs[j] = col[j];
-  float2* z = fft_stockham<-1>(zs, zb, nc, n, logn, tw);
+  float2* z = fft_run<-1>(zs, zb, nc, sh, tw);
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
-  z = fft_stockham<+1>(z, z == zs ? zb : zs, nc, n, logn, tw);
+  z = fft_run<+1>(z, z == zs ? zb : zs, nc, sh, tw);
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
@@ -232,7 +316,8 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
 // unnormalised forward 2-D FFT of a real image as a half spectrum
 // (empirical_mask's F v, circulant.cpp:111-117).
 __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
-                                        const float2* __restrict__ tw, int n, int logn) {
+                                        const float2* __restrict__ tw, FftShape sh) {
+  const int n = sh.n;
   extern __shared__ float2 zs[];
   const int k0 = blockIdx.x * kColsPerBlock;
   const int b = blockIdx.y;
@@ -241,12 +326,13 @@ __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
   float2* col = specT + (static_cast<size_t>(b) * nk + k0) * n;
   float2* zb = zs + kColsPerBlock * n;
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) zs[j] = col[j];
-  const float2* z = fft_stockham<-1>(zs, zb, nc, n, logn, tw);
+  const float2* z = fft_run<-1>(zs, zb, nc, sh, tw);
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
-                                    const float2* __restrict__ tw, int n, int logn) {
+                                    const float2* __restrict__ tw, FftShape sh) {
+  const int n = sh.n;
   extern __shared__ float2 zs[];
   const int y0 = blockIdx.x * kRowsPerBlock;
   const int b = blockIdx.y;
@@ -261,12 +347,12 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
     float2* zq = zs + (r >> 1) * n;
     const unsigned ik = k;
-    const unsigned im = (n - k) & (n - 1);
+    const unsigned im = (n - k) % n;
     if ((r & 1) == 0) {
       // a part: Z[k] += G_a[k], Z[n-k] += conj(G_a[k])
       zq[ik].x = g.x;
       zq[ik].y = g.y;
-      if (k > 0 && k < n / 2) {
+      if (k > 0 && 2 * k != n) {
         zq[im].x = g.x;
         zq[im].y = -g.y;
       }
@@ -280,16 +366,16 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
     float2* zq = zs + (r >> 1) * n;
     const unsigned ik = k;
-    const unsigned im = (n - k) & (n - 1);
+    const unsigned im = (n - k) % n;
     // b part: Z[k] += i G_b[k], Z[n-k] += i conj(G_b[k])
     zq[ik].x -= g.y;
     zq[ik].y += g.x;
-    if (k > 0 && k < n / 2) {
+    if (k > 0 && 2 * k != n) {
       zq[im].x += g.y;
       zq[im].y += g.x;
     }
   }
-  float2* z = fft_stockham<+1>(zs, zb, kRowsPerBlock / 2, n, logn, tw);
+  float2* z = fft_run<+1>(zs, zb, kRowsPerBlock / 2, sh, tw);
   // x update, row-major.
   int bad = 0;
   for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
@@ -341,9 +427,29 @@ int fft_threads(int work) { return std::max(64, std::min(512, work)); }
 }  // namespace
 
 void FftPlan::init(int n_, cudaStream_t s) {
-  if (n_ < 8 || (n_ & (n_ - 1)))
-    throw Error{NCSG_INVALID, "GPU circulant solve needs a power-of-two image size >= 8"};
+  if (n_ < 2) throw Error{NCSG_INVALID, "GPU circulant solve needs an image size >= 2"};
   n = n_;
+  shape = FftShape{};
+  shape.n = n;
+  if (n >= 8 && (n & (n - 1)) == 0) {
+    shape.logn = log2i(n);  // radix-8 fast path
+  } else {
+    // 2^a 3^b 5^c 7^d: radix 8 / 4 / 2 for the power of two, then 3, 5, 7
+    int r = n;
+    auto push = [&](int f) {
+      if (shape.nst >= 24) throw Error{NCSG_INVALID, "FFT size has too many factors"};
+      shape.rad[shape.nst++] = f;
+    };
+    while (r % 8 == 0) push(8), r /= 8;
+    while (r % 4 == 0) push(4), r /= 4;
+    while (r % 2 == 0) push(2), r /= 2;
+    for (int f : {3, 5, 7})
+      while (r % f == 0) push(f), r /= f;
+    if (r != 1)
+      throw Error{NCSG_INVALID,
+                  "GPU FFT sizes need prime factors 2, 3, 5 and 7 (got a factor " +
+                      std::to_string(r) + ")"};
+  }
   std::vector<float2> h(n);
   for (int k = 0; k < n; ++k) {
     double ang = -2.0 * 3.14159265358979323846 * k / n;
@@ -365,7 +471,7 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   // the loader (sums of adjoint partial images) wants more threads than the FFT
   fft_rows_r2c_kernel<<<grid, fft_threads(kRowsPerBlock * n / 4), smem, s>>>(
-      terms, specT, f.tw.p, log2i(n));
+      terms, specT, f.tw.p, f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -378,8 +484,8 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
-  fft_cols_filter_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, maskT, f.tw.p, n,
-                                                                log2i(n));
+  fft_cols_filter_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, maskT, f.tw.p,
+                                                                               f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -391,8 +497,8 @@ void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStr
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
-  fft_cols_forward_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, f.tw.p, n,
-                                                                               log2i(n));
+  fft_cols_forward_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, f.tw.p,
+                                                                               f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -406,7 +512,7 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
                                        static_cast<int>(smem)));
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   fft_rows_c2r_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 4), smem, s>>>(
-      specT, xu, f.tw.p, n, log2i(n));
+      specT, xu, f.tw.p, f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

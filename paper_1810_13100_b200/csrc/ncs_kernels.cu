@@ -547,7 +547,7 @@ __global__ void spec_norm_kernel(const float2* spec, int n, double* out) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const int k = static_cast<int>(i / n);
-    const double w = (k == 0 || k == n / 2) ? 1.0 : 2.0;
+    const double w = (k == 0 || 2 * k == n) ? 1.0 : 2.0;  // self-conjugate columns count once
     const double a = sb[i].x, b = sb[i].y;
     acc += w * (a * a + b * b);
   }

@@ -231,8 +231,16 @@ void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, i
                          cudaStream_t s);
 
 // ------------------------------------------------------------------ FFT
+// Radix schedule of a length-n Stockham FFT: powers of two use the radix-8
+// fast path (logn >= 0); other sizes n = 2^a 3^b 5^c 7^d run mixed-radix
+// stages (logn = -1).
+struct FftShape {
+  int n = 0, logn = -1, nst = 0;
+  int rad[24] = {};
+};
 struct FftPlan {
   int n = 0;
+  FftShape shape;
   DevBuf<float2> tw;  // exp(-2 pi i k / n), k < n
   void init(int n_, cudaStream_t s);
 };

@@ -429,12 +429,8 @@ size_t orbit_smem(int rmax) {
   return sizeof(float) * (4 * kOrbTile + kOrbWarps * 5 * rmax) + 128;
 }
 
-#ifndef NCSG_ORB_UNROLL
-#define NCSG_ORB_UNROLL 2
-#endif
-constexpr int kOrbUnroll = NCSG_ORB_UNROLL;  // inner lattice-step unroll
 #ifndef NCSG_ORB_MINB
-#define NCSG_ORB_MINB 1
+#define NCSG_ORB_MINB 2  // two CTAs per SM: caps ptxas at 128 registers (146 without)
 #endif
 template <bool USE_TMA>
 __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
@@ -576,7 +572,7 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
 #pragma unroll
         for (int k = 0; k < 4; ++k) sp[k] = static_cast<unsigned>(jh[k] - jl[k]);
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll kOrbUnroll
+#pragma unroll 2
         for (int j = J0; j < J1; ++j) {
           const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
           const int idx = on ? base + (Y >> 23) * P + (X >> 23) : 0;

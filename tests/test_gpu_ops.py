@@ -143,9 +143,22 @@ def test_mask_apply_identity_and_constants(ncsg):
     assert np.abs(ncsg.mask_apply(laplacian_mask(n), np.full((n, n), 3.0))).max() < 1e-5
 
 
-def test_fft_needs_power_of_two(ncsg):
-    with pytest.raises(ValueError, match="power-of-two"):
-        ncsg.mask_apply(np.ones((12, 12)), np.ones((12, 12)))
+@pytest.mark.parametrize("n", [9, 12, 15, 30, 100, 105, 126, 96])
+def test_mask_apply_mixed_radix_sizes(ncsg, port, n):
+    # MaskApplier::apply for sizes the reference's FFTW handles and the
+    # radix-8 fast path does not: mixed-radix (2, 3, 4, 5, 7, 8) Stockham
+    # stages, odd sizes included (the half spectrum then has no Nyquist column)
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n))
+    h = (port.laplacian_mask(n) + port.radon_mask(n, 3.0, 5.0)
+         + 0.3j * rng.standard_normal((n, n)))
+    want = port.mask_apply(h, x)
+    assert rel(ncsg.mask_apply(h, x), want) <= 1e-5
+
+
+def test_fft_rejects_other_primes(ncsg):
+    with pytest.raises(ValueError, match="prime factors"):
+        ncsg.mask_apply(np.ones((22, 22)), np.ones((22, 22)))
 
 
 @pytest.mark.parametrize("n,views,rays", [(16, 12, 21), (32, 24, 45), (64, 40, 91)])

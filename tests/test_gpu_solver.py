@@ -462,3 +462,12 @@ def test_c4_stable_with_pinned_gamma(ncsg):
     f = r.rows[0][:, 1]
     assert np.all(np.isfinite(f)) and f[-1] < f[1] < f[0]
 
+
+@pytest.mark.parametrize("n,A", [(30, 24), (36, 40)])
+def test_mixed_radix_size_solve(ncsg, port, n, A):
+    # NCS at image sizes that are not powers of two (mixed-radix FFT solve)
+    prob, mask, gamma = small_ct(port, n=n, A=A)
+    o = port.solve(prob, gamma, mask, 40, record_every=20)
+    g = gpu_problem(ncsg, prob, gamma, mask).solve(40, record_every=20)
+    check_run(g, o)
+
