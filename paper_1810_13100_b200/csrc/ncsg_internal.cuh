@@ -169,6 +169,35 @@ inline void bp_tile_shape(int n, int& W, int& T, int& P) {
 constexpr int kBpWarps = NCSG_BP_WARPS;  // adjoint: warps per CTA (private accumulators)
 constexpr int kBpWaves = NCSG_BP_WAVES;  // adjoint: target CTAs = 148 * 3 * waves
 
+// Orbit-mode adjoint (bp_gather_kernel): pixel-driven, TW x TH pixel tiles
+// of the representative's frame, kGaPx pixels per thread, orbits staged in
+// batches of kGaBatch.
+#ifndef NCSG_GA_TH
+#define NCSG_GA_TH 16
+#endif
+#ifndef NCSG_GA_BATCH
+#define NCSG_GA_BATCH 16
+#endif
+#ifndef NCSG_GA_WAVES
+#define NCSG_GA_WAVES 2
+#endif
+constexpr int kGaTW = 32, kGaTH = NCSG_GA_TH, kGaThreads = 256;
+constexpr int kGaPx = kGaTW * kGaTH / kGaThreads;  // pixels per thread
+constexpr int kGaBatch = NCSG_GA_BATCH, kGaWaves = NCSG_GA_WAVES;
+constexpr int kGaSW = kGaTW + kGaTH + 8;            // staged rays per orbit and tile
+constexpr int kGaMaxChunk = 1024;                   // orbits per chunk (lowest-ray table)
+// Per-orbit constants of the gather (host fp64 from the Q32 lattice): the
+// lattice is p(s, k) = c + s a + k d; (sigma, kappa) = M^-1 (q - c) are the
+// continuous lattice coordinates of pixel q.
+struct GatherGeom {
+  double ia_x, ia_y, id_x, id_y;  // rows of M^-1, M = [a d]
+  float ax, ay, dx, dy;           // lattice vectors (pixels)
+  float rho, inv_dy;              // sigma half-extent of the |e| < 1 window, 1 / dy
+  int t[4];                       // member angles (-1: absent)
+  int dir;                        // tau = dir * k
+  int pad;
+};
+
 // SparseMap on the device (sparse_kernels.cu): fp32 values, int32 indices.
 struct SparseDev {
   int n = 0, views = 0, rays = 0;
@@ -194,6 +223,12 @@ struct RadonDev {
   int bp_chunks[2] = {0, 0};
   int bp_chunk_len[2] = {0, 0};
   int bp_batch_planned = 0;
+  // Orbit-mode adjoint (bp_gather_kernel): bp_orbit_chunks chunks of
+  // bp_orbit_len orbits, four image-frame partials per chunk
+  // (bp_chunks[0] = 4 * chunks, bp_chunks[1] = 0).
+  bool bp_orbit = false;
+  int bp_orbit_chunks = 0, bp_orbit_len = 0;
+  DevBuf<GatherGeom> gather;
   DevBuf<int2> strip_range[2];                // [angle][strip] s-range (forward)
   std::vector<int2> strip_range_host[2];
   // Orbit-mode forward (fp_orbit_kernel): strips x segments of rows; each

@@ -764,6 +764,248 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
   }
 }
 
+// R^T for the four members of an orbit, pixel-driven (the transpose of
+// fp_orbit_kernel as a gather).  Pixel q of the representative's frame
+// receives w * tent(px - X) * tent(py - Y) from every lattice sample p(s, k)
+// within one pixel of it on both axes (radon.cpp:116-125 with the n-2 clamp,
+// which is the tent written per cell).  In lattice coordinates (sigma, kappa)
+// = M^-1 (q - c) that window holds at most 3 rays s and, per ray, at most 3
+// steps k (|a|, |d| = 1, |dy| >= 1/sqrt2), about 4 samples on average.  The
+// window geometry and weights are shared by the four member angles (acc_m
+// belongs to image pixel T_m(q), OrbitGeom), so each (pixel, orbit) costs
+// three 128-bit reads of the staged member weights (u_t0..3 interleaved per
+// ray) and registers for the sums -- no shared-memory read-modify-write.
+// Sample validity: every lattice point strictly inside the image square is a
+// reference sample, and a point outside can only reach a border pixel, so
+// border pixels check the replayed per-member ray ranges exactly and the
+// others need no test.
+// CTA = (TW x TH tile, chunk of orbits), orbits staged kGaBatch at a time;
+// the epilogue writes member m to partial image 4 * chunk + m at T_m(q),
+// transposing members 1 and 3 through shared memory.
+struct GaArgs {
+  const GatherGeom* geo;
+  int n_orb, chunk_len, n_chunks;  // orbits, orbits per chunk, chunks per problem
+  const RayRange* rays;
+  const float* u;  // [batch][u_stride], sinogram dual first
+  float* out;      // [batch][4 * n_chunks][nn]
+  int n, det, s_mid;
+  size_t nn, u_stride;
+};
+
+__device__ __forceinline__ float tent(float e) { return __saturatef(1.0f - fabsf(e)); }
+
+__device__ __forceinline__ void cp_async4(unsigned dst, const float* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
+               "r"(ok ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+
+template <int TW, int TH, int NB>
+__global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
+  constexpr int PX = TW * TH / kGaThreads;
+  constexpr int SW = TW + TH + 8;
+  static_assert(kGaThreads % TW == 0 && kGaThreads % TH == 0, "tile rows / columns per pass");
+  __shared__ __align__(16) float4 U4[2][NB][SW];
+  __shared__ __align__(16) GatherGeom G[2][NB];
+  __shared__ int slo[kGaMaxChunk];
+  const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
+  const int b = blockIdx.z / a.n_chunks;
+  const int chunk = blockIdx.z - b * a.n_chunks;
+  const int n = a.n;
+  const double c = 0.5 * (n - 1);
+  const int o_begin = chunk * a.chunk_len;
+  const int o_end = min(a.n_orb, o_begin + a.chunk_len);
+  const float* ub = a.u + static_cast<size_t>(b) * a.u_stride + a.s_mid;
+  // Pixel i = thread + p * kGaThreads of the tile, row-major (a warp = a
+  // row segment); tiles on the left / right image edge go column-major so
+  // that the border column falls in one warp.
+  const bool colmajor = X0 == 0 || X0 + TW >= n;
+  int xl[PX], yl[PX];
+  float4 acc[PX];
+  bool any_border = false;
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    const int i = threadIdx.x + p * kGaThreads;
+    xl[p] = colmajor ? i / TH : i % TW;
+    yl[p] = colmajor ? i % TH : i / TW;
+    acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+    const int X = X0 + xl[p], Y = Y0 + yl[p];
+    any_border |= X == 0 || X == n - 1 || Y == 0 || Y == n - 1;
+  }
+  any_border = __any_sync(0xffffffffu, any_border);
+  // pixel p = pixel 0 + (DXP, DYP)
+  const int DXP = colmajor ? kGaThreads / TH : 0, DYP = colmajor ? 0 : kGaThreads / TW;
+  const double qx0 = X0 + xl[0] - c, qy0 = Y0 + yl[0] - c;
+  const float lim = static_cast<float>(n - 1);
+  constexpr float kEps = 4e-3f;  // > fp32 rounding of X + e for X < 4096
+
+  // Lowest staged ray of every orbit of the chunk for this tile: sigma over
+  // the tile corners minus the window half-extent.
+  for (int o = threadIdx.x; o < o_end - o_begin; o += kGaThreads) {
+    const GatherGeom& g = a.geo[o_begin + o];
+    const double x0 = X0 - c, x1 = X0 + TW - 1 - c, y0 = Y0 - c, y1 = Y0 + TH - 1 - c;
+    const double s0 = fmin(g.ia_x * x0, g.ia_x * x1) + fmin(g.ia_y * y0, g.ia_y * y1);
+    slo[o] = static_cast<int>(floor(s0 - g.rho)) - 1;
+  }
+  __syncthreads();
+
+  // Stage orbits [ob, ob + nb) into buffer `buf` with cp.async: the member
+  // weights u_t0..3 of the tile's rays interleaved per ray (zero outside the
+  // detector and for absent members) and the orbit constants.
+  auto stage = [&](int ob, int buf) {
+    const int nb = min(NB, o_end - ob);
+    constexpr int kQ = sizeof(GatherGeom) / 16;
+    static_assert(sizeof(GatherGeom) % 16 == 0, "GatherGeom is copied in 16-byte pieces");
+    for (int i = threadIdx.x; i < nb * kQ; i += kGaThreads) {
+      const int o = i / kQ, q = i - o * kQ;
+      cp_async16(static_cast<unsigned>(__cvta_generic_to_shared(&G[buf][o])) + 16u * q,
+                 reinterpret_cast<const float4*>(a.geo + ob + o) + q);
+    }
+    for (int i = threadIdx.x; i < nb * SW * 4; i += kGaThreads) {
+      const int m = i & 3, e = i >> 2;
+      const int o = e / SW, r = e - o * SW;
+      const int s = slo[ob - o_begin + o] + r;
+      const int t = __ldg(&a.geo[ob + o].t[m]);
+      const bool ok = s >= -a.s_mid && s <= a.s_mid && t >= 0;
+      cp_async4(static_cast<unsigned>(__cvta_generic_to_shared(&U4[buf][o][r])) + 4u * m,
+                ok ? ub + static_cast<size_t>(t) * a.det + s : ub, ok);
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+
+  int buf = 0;
+  if (o_begin < o_end) stage(o_begin, 0);
+  for (int ob = o_begin; ob < o_end; ob += NB, buf ^= 1) {
+    const int nb = min(NB, o_end - ob);
+    if (ob + NB < o_end) {
+      stage(ob + NB, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
+    __syncthreads();
+    for (int o = 0; o < nb; ++o) {
+      const GatherGeom& g = G[buf][o];
+      const float ax = g.ax, ay = g.ay, dx = g.dx, dy = g.dy;
+      const float4* Uo = U4[buf][o];
+      const int sl = slo[ob - o_begin + o];
+      double sg = fma(g.ia_x, qx0, g.ia_y * qy0);
+      double kp = fma(g.id_x, qx0, g.id_y * qy0);
+      const double dsg = g.ia_x * DXP + g.ia_y * DYP, dkp = g.id_x * DXP + g.id_y * DYP;
+#pragma unroll
+      for (int p = 0; p < PX; ++p) {
+        if (p > 0) sg += dsg, kp += dkp;
+        const double sf = floor(sg), kf = floor(kp);
+        const float fs = static_cast<float>(sg - sf), fk = static_cast<float>(kp - kf);
+        const int u0 = static_cast<int>(ceilf(fs - g.rho));
+        const int r0 = static_cast<int>(sf) + u0 - sl;
+        const float du0 = static_cast<float>(u0) - fs;
+        const float fk1 = fk - 1.0f;
+        if (!any_border) {
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const float du = du0 + u;
+            const float dv = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
+            float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
+            float w = tent(ex) * tent(ey);
+            ex += dx, ey += dy;
+            w = fmaf(tent(ex), tent(ey), w);
+            ex += dx, ey += dy;
+            w = fmaf(tent(ex), tent(ey), w);
+            const float4 uv = Uo[r0 + u];
+            acc[p].x = fmaf(w, uv.x, acc[p].x);
+            acc[p].y = fmaf(w, uv.y, acc[p].y);
+            acc[p].z = fmaf(w, uv.z, acc[p].z);
+            acc[p].w = fmaf(w, uv.w, acc[p].w);
+          }
+        } else {
+          // Warps holding a border pixel: a sample farther than kEps inside
+          // the image square is valid for every member, one farther than kEps
+          // outside for none; the few in between check the replayed ranges.
+          const float Xf = static_cast<float>(X0 + xl[p]), Yf = static_cast<float>(Y0 + yl[p]);
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const float du = du0 + u;
+            const float vf = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
+            float ex = fmaf(du, ax, (vf - fk) * dx), ey = fmaf(du, ay, (vf - fk) * dy);
+            const float4 uv = Uo[r0 + u];
+            float w = 0.f;
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+              const float wj = tent(ex) * tent(ey);
+              const float px = Xf + ex, py = Yf + ey;
+              const float lo = fminf(px, py), hi = fmaxf(px, py);
+              const bool in = lo > kEps && hi < lim - kEps;
+              const bool out = lo < -kEps || hi > lim + kEps;
+              if (in) w += wj;
+              if (!in && !out && wj != 0.f) {
+                const int s = static_cast<int>(sf) + u0 + u;
+                const int tau = g.dir * (static_cast<int>(kf) + static_cast<int>(vf) + j);
+                float add[4] = {0.f, 0.f, 0.f, 0.f};
+                const float um[4] = {uv.x, uv.y, uv.z, uv.w};
+                if (s >= -a.s_mid && s <= a.s_mid) {
+#pragma unroll
+                  for (int m = 0; m < 4; ++m) {
+                    const int t = g.t[m];
+                    if (t < 0) continue;
+                    const RayRange rr = a.rays[static_cast<size_t>(t) * a.det + a.s_mid + s];
+                    const int tm = m >= 2 ? -tau : tau;
+                    if (tm >= rr.first && tm <= rr.last) add[m] = wj * um[m];
+                  }
+                }
+                acc[p].x += add[0];
+                acc[p].y += add[1];
+                acc[p].z += add[2];
+                acc[p].w += add[3];
+              }
+              ex += dx, ey += dy;
+            }
+            acc[p].x = fmaf(w, uv.x, acc[p].x);
+            acc[p].y = fmaf(w, uv.y, acc[p].y);
+            acc[p].z = fmaf(w, uv.z, acc[p].z);
+            acc[p].w = fmaf(w, uv.w, acc[p].w);
+          }
+        }
+      }
+    }
+    __syncthreads();  // buffer `buf` is restaged two batches later
+  }
+  // Epilogue through shared memory (the staging buffers are free): member m
+  // goes to partial image 4 * chunk + m at T_m(q), every store coalesced.
+  static_assert(sizeof(U4) >= sizeof(float) * 4 * TH * (TW + 1), "epilogue tile fits");
+  float(*ot)[TH][TW + 1] = reinterpret_cast<float(*)[TH][TW + 1]>(&U4[0][0][0]);
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    ot[0][yl[p]][xl[p]] = acc[p].x;
+    ot[1][yl[p]][xl[p]] = acc[p].y;
+    ot[2][yl[p]][xl[p]] = acc[p].z;
+    ot[3][yl[p]][xl[p]] = acc[p].w;
+  }
+  __syncthreads();
+  const size_t nn = a.nn;
+  float* o0 = a.out + (static_cast<size_t>(b) * 4 * a.n_chunks + 4 * chunk) * nn;
+  float* o1 = o0 + nn;
+  float* o2 = o1 + nn;
+  float* o3 = o2 + nn;
+  for (int i = threadIdx.x; i < TW * TH; i += kGaThreads) {
+    int x = i % TW, y = i / TW;  // members 0, 2: along rows
+    int X = X0 + x, Y = Y0 + y;
+    if (X < n && Y < n) {
+      o0[static_cast<size_t>(Y) * n + X] = ot[0][y][x];
+      o2[static_cast<size_t>(Y) * n + (n - 1 - X)] = ot[2][y][x];
+    }
+    x = i / TH, y = i % TH;  // members 1, 3: pixel (N-1-X, Y), (N-1-X, N-1-Y)
+    X = X0 + x, Y = Y0 + y;
+    if (X < n && Y < n) {
+      o1[static_cast<size_t>(n - 1 - X) * n + Y] = ot[1][y][x];
+      o3[static_cast<size_t>(n - 1 - X) * n + (n - 1 - Y)] = ot[3][y][x];
+    }
+  }
+}
+
 __global__ void strip_sum_kernel(const float* part, float* out, int n_strips, size_t m,
                                  int batch) {
   size_t total = m * batch;
@@ -856,12 +1098,59 @@ void RadonDev::upload() {
       orb_range.alloc(orr.size());
       NCSG_CUDA_CHECK(cudaMemcpy(orb_range.p, orr.data(), orr.size() * sizeof(int2),
                                  cudaMemcpyHostToDevice));
+      // Gather constants of every orbit (bp_gather_kernel), fp64 from the
+      // Q32 lattice vectors.
+      std::vector<GatherGeom> gg(geo.orbits.size());
+      for (size_t oi = 0; oi < geo.orbits.size(); ++oi) {
+        const OrbitGeom& o = geo.orbits[oi];
+        const double ax = std::ldexp(static_cast<double>(o.rep.aX), -32);
+        const double ay = std::ldexp(static_cast<double>(o.rep.aY), -32);
+        const double dx = std::ldexp(static_cast<double>(o.rep.dX), -32);
+        const double dy = std::ldexp(static_cast<double>(o.rep.dY), -32);
+        const double det = ax * dy - dx * ay;
+        GatherGeom& q = gg[oi];
+        q.ia_x = dy / det;
+        q.ia_y = -dx / det;
+        q.id_x = -ay / det;
+        q.id_y = ax / det;
+        q.ax = static_cast<float>(ax);
+        q.ay = static_cast<float>(ay);
+        q.dx = static_cast<float>(dx);
+        q.dy = static_cast<float>(dy);
+        q.rho = static_cast<float>(std::fabs(q.ia_x) + std::fabs(q.ia_y) + 1e-6);
+        q.inv_dy = static_cast<float>(1.0 / dy);
+        for (int m = 0; m < 4; ++m) q.t[m] = o.t[m];
+        q.dir = o.rep.dir;
+        q.pad = 0;
+      }
+      gather.alloc(gg.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(gather.p, gg.data(), gg.size() * sizeof(GatherGeom),
+                                 cudaMemcpyHostToDevice));
     }
   }
 }
 
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
+  bp_orbit = orbit_mode && !getenv("NCSG_NO_GATHER");
+  if (bp_orbit) {
+    // bp_gather_kernel: chunks of orbits for about kGaWaves waves of 4
+    // resident CTAs per SM; each chunk adds four partial images.
+    const int tiles = ((n + kGaTW - 1) / kGaTW) * ((n + kGaTH - 1) / kGaTH);
+    const long target = 148L * 4 * kGaWaves;
+    const int no = static_cast<int>(geo.orbits.size());
+    const long per = static_cast<long>(tiles) * batch;
+    int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
+    chunks = std::min(chunks, std::max(1, no / kGaBatch));
+    chunks = std::max(chunks, (no + kGaMaxChunk - 1) / kGaMaxChunk);
+    bp_orbit_len = (no + chunks - 1) / chunks;
+    bp_orbit_chunks = (no + bp_orbit_len - 1) / bp_orbit_len;
+    bp_chunks[0] = 4 * bp_orbit_chunks;
+    bp_chunks[1] = 0;
+    bp_chunk_len[0] = bp_chunk_len[1] = 1;
+    bp_batch_planned = batch;
+    return;
+  }
   int bw, bt, bpitch;
   bp_tile_shape(n, bw, bt, bpitch);
   const int tiles = ((n + bw - 1) / bw) * ((n + bt - 1) / bt);
@@ -1049,6 +1338,26 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
   const Geometry& g = r.geo;
   const int n = g.n;
   if (r.n_partials() == 0) return;
+  if (r.bp_orbit) {
+    GaArgs a;
+    a.geo = r.gather.p;
+    a.n_orb = static_cast<int>(g.orbits.size());
+    a.chunk_len = r.bp_orbit_len;
+    a.n_chunks = r.bp_orbit_chunks;
+    a.rays = r.rays.p;
+    a.u = u;
+    a.out = bp_part;
+    a.n = n;
+    a.det = g.n_det;
+    a.s_mid = g.s_mid;
+    a.nn = static_cast<size_t>(n) * n;
+    a.u_stride = u_stride ? u_stride : static_cast<size_t>(g.n_angles) * g.n_det;
+    dim3 grid((n + kGaTW - 1) / kGaTW, (n + kGaTH - 1) / kGaTH, a.n_chunks * batch);
+    bp_gather_kernel<kGaTW, kGaTH, kGaBatch><<<grid, kGaThreads, 0, s>>>(a);
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   BpArgs a;
   for (int k = 0; k < 2; ++k) {
     a.ang[k] = r.angles[k].p;

