@@ -777,11 +777,12 @@ __global__ void __launch_bounds__(NW * 32) bp_tile_kernel(BpArgs a) {
 // ray) and registers for the sums -- no shared-memory read-modify-write.
 // Sample validity: every lattice point strictly inside the image square is a
 // reference sample, and a point outside can only reach a border pixel, so
-// border pixels check the replayed per-member ray ranges exactly and the
-// others need no test.
-// CTA = (TW x TH tile, chunk of orbits), orbits staged kGaBatch at a time;
-// the epilogue writes member m to partial image 4 * chunk + m at T_m(q),
-// transposing members 1 and 3 through shared memory.
+// the main loop takes every window sample as valid and the epilogue takes
+// the invalid ones back out of the border pixels (per-member replayed ray
+// ranges for samples on the edge up to rounding), spread over all warps.
+// CTA = (TW x TH tile, chunk of orbits), orbits staged kGaBatch at a time
+// (cp.async, double-buffered); the epilogue writes member m to partial image
+// 4 * chunk + m at T_m(q) through shared memory so every store is coalesced.
 struct GaArgs {
   const GatherGeom* geo;
   int n_orb, chunk_len, n_chunks;  // orbits, orbits per chunk, chunks per problem
@@ -808,9 +809,14 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   constexpr int PX = TW * TH / kGaThreads;
   constexpr int SW = TW + TH + 8;
   static_assert(kGaThreads % TW == 0 && kGaThreads % TH == 0, "tile rows / columns per pass");
+  static_assert(NB <= 32 && (NB & (NB - 1)) == 0, "border items reduce within a warp");
   __shared__ __align__(16) float4 U4[2][NB][SW];
   __shared__ __align__(16) GatherGeom G[2][NB];
   __shared__ int slo[kGaMaxChunk];
+  constexpr int MAXB = 2 * (TW + TH);  // border pixels of a tile
+  __shared__ int2 bpix[MAXB];         // border pixels of this tile (tile-local)
+  __shared__ float4 bacc[MAXB];       // their corrections
+  __shared__ int nbp;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   const int b = blockIdx.z / a.n_chunks;
   const int chunk = blockIdx.z - b * a.n_chunks;
@@ -819,26 +825,25 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   const int o_begin = chunk * a.chunk_len;
   const int o_end = min(a.n_orb, o_begin + a.chunk_len);
   const float* ub = a.u + static_cast<size_t>(b) * a.u_stride + a.s_mid;
-  // Pixel i = thread + p * kGaThreads of the tile, row-major (a warp = a
-  // row segment); tiles on the left / right image edge go column-major so
-  // that the border column falls in one warp.
-  const bool colmajor = X0 == 0 || X0 + TW >= n;
-  int xl[PX], yl[PX];
+  // Pixel p of a thread: column tx, row ty + p * RS (a warp = a row segment).
+  constexpr int RS = kGaThreads / TW;
+  const int tx = threadIdx.x % TW, ty = threadIdx.x / TW;
   float4 acc[PX];
-  bool any_border = false;
+#pragma unroll
+  for (int p = 0; p < PX; ++p) acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const double qx0 = X0 + tx - c, qy0 = Y0 + ty - c;
+  // Border pixels (image row / column 0 or n-1) of this tile.
+  if (threadIdx.x == 0) nbp = 0;
+  __syncthreads();
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
-    const int i = threadIdx.x + p * kGaThreads;
-    xl[p] = colmajor ? i / TH : i % TW;
-    yl[p] = colmajor ? i % TH : i / TW;
-    acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
-    const int X = X0 + xl[p], Y = Y0 + yl[p];
-    any_border |= X == 0 || X == n - 1 || Y == 0 || Y == n - 1;
+    const int X = X0 + tx, Y = Y0 + ty + p * RS;
+    if (X < n && Y < n && (X == 0 || Y == 0 || X == n - 1 || Y == n - 1)) {
+      const int k = atomicAdd(&nbp, 1);
+      bpix[k] = make_int2(tx, ty + p * RS);
+      bacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
-  any_border = __any_sync(0xffffffffu, any_border);
-  // pixel p = pixel 0 + (DXP, DYP)
-  const int DXP = colmajor ? kGaThreads / TH : 0, DYP = colmajor ? 0 : kGaThreads / TW;
-  const double qx0 = X0 + xl[0] - c, qy0 = Y0 + yl[0] - c;
   const float lim = static_cast<float>(n - 1);
   constexpr float kEps = 4e-3f;  // > fp32 rounding of X + e for X < 4096
 
@@ -894,7 +899,7 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
       const int sl = slo[ob - o_begin + o];
       double sg = fma(g.ia_x, qx0, g.ia_y * qy0);
       double kp = fma(g.id_x, qx0, g.id_y * qy0);
-      const double dsg = g.ia_x * DXP + g.ia_y * DYP, dkp = g.id_x * DXP + g.id_y * DYP;
+      const double dsg = g.ia_y * RS, dkp = g.id_y * RS;
 #pragma unroll
       for (int p = 0; p < PX; ++p) {
         if (p > 0) sg += dsg, kp += dkp;
@@ -904,71 +909,84 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
         const int r0 = static_cast<int>(sf) + u0 - sl;
         const float du0 = static_cast<float>(u0) - fs;
         const float fk1 = fk - 1.0f;
-        if (!any_border) {
 #pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            const float du = du0 + u;
-            const float dv = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
-            float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
-            float w = tent(ex) * tent(ey);
-            ex += dx, ey += dy;
-            w = fmaf(tent(ex), tent(ey), w);
-            ex += dx, ey += dy;
-            w = fmaf(tent(ex), tent(ey), w);
-            const float4 uv = Uo[r0 + u];
-            acc[p].x = fmaf(w, uv.x, acc[p].x);
-            acc[p].y = fmaf(w, uv.y, acc[p].y);
-            acc[p].z = fmaf(w, uv.z, acc[p].z);
-            acc[p].w = fmaf(w, uv.w, acc[p].w);
-          }
-        } else {
-          // Warps holding a border pixel: a sample farther than kEps inside
-          // the image square is valid for every member, one farther than kEps
-          // outside for none; the few in between check the replayed ranges.
-          const float Xf = static_cast<float>(X0 + xl[p]), Yf = static_cast<float>(Y0 + yl[p]);
+        for (int u = 0; u < 3; ++u) {
+          const float du = du0 + u;
+          const float dv = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
+          float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
+          float w = tent(ex) * tent(ey);
+          ex += dx, ey += dy;
+          w = fmaf(tent(ex), tent(ey), w);
+          ex += dx, ey += dy;
+          w = fmaf(tent(ex), tent(ey), w);
+          const float4 uv = Uo[r0 + u];
+          acc[p].x = fmaf(w, uv.x, acc[p].x);
+          acc[p].y = fmaf(w, uv.y, acc[p].y);
+          acc[p].z = fmaf(w, uv.z, acc[p].z);
+          acc[p].w = fmaf(w, uv.w, acc[p].w);
+        }
+      }
+    }
+    // Border pixels: the loop above took every window sample as valid. A
+    // sample farther than kEps inside the image square is (for every
+    // member); the others -- outside, or on the edge up to rounding -- are
+    // checked against each member's replayed ray range and the invalid ones
+    // taken back out. Items (border pixel, orbit): NB lanes per pixel,
+    // reduced in a fixed order.
+    const int nbt = (nbp * NB + 31) / 32 * 32;
+    for (int it = threadIdx.x; it < nbt; it += kGaThreads) {
+      const int bq = it / NB, o = it % NB;
+      float cr[4] = {0.f, 0.f, 0.f, 0.f};
+      if (bq < nbp && o < nb) {
+        const GatherGeom& g = G[buf][o];
+        const float ax = g.ax, ay = g.ay, dx = g.dx, dy = g.dy;
+        const int2 bl = bpix[bq];
+        const int X = X0 + bl.x, Y = Y0 + bl.y;
+        const float Xf = static_cast<float>(X), Yf = static_cast<float>(Y);
+        const double sg = fma(g.ia_x, X - c, g.ia_y * (Y - c));
+        const double kp = fma(g.id_x, X - c, g.id_y * (Y - c));
+        const double sf = floor(sg), kf = floor(kp);
+        const float fs = static_cast<float>(sg - sf), fk = static_cast<float>(kp - kf);
+        const int u0 = static_cast<int>(ceilf(fs - g.rho));
+        const int r0 = static_cast<int>(sf) + u0 - slo[ob - o_begin + o];
+        for (int u = 0; u < 3; ++u) {
+          const float du = static_cast<float>(u0 + u) - fs;
+          const float vf = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
+          const float4 uv = U4[buf][o][r0 + u];
+          const float um[4] = {uv.x, uv.y, uv.z, uv.w};
+          for (int j = 0; j < 3; ++j) {
+            const float dv = vf + j - fk;
+            const float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
+            const float w = tent(ex) * tent(ey);
+            const float px = Xf + ex, py = Yf + ey;
+            const float lo = fminf(px, py), hi = fmaxf(px, py);
+            if (w == 0.f || (lo > kEps && hi < lim - kEps)) continue;
+            const bool out = lo < -kEps || hi > lim + kEps;
+            const int sr = static_cast<int>(sf) + u0 + u;
+            const int tau = g.dir * (static_cast<int>(kf) + static_cast<int>(vf) + j);
 #pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            const float du = du0 + u;
-            const float vf = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
-            float ex = fmaf(du, ax, (vf - fk) * dx), ey = fmaf(du, ay, (vf - fk) * dy);
-            const float4 uv = Uo[r0 + u];
-            float w = 0.f;
-#pragma unroll
-            for (int j = 0; j < 3; ++j) {
-              const float wj = tent(ex) * tent(ey);
-              const float px = Xf + ex, py = Yf + ey;
-              const float lo = fminf(px, py), hi = fmaxf(px, py);
-              const bool in = lo > kEps && hi < lim - kEps;
-              const bool out = lo < -kEps || hi > lim + kEps;
-              if (in) w += wj;
-              if (!in && !out && wj != 0.f) {
-                const int s = static_cast<int>(sf) + u0 + u;
-                const int tau = g.dir * (static_cast<int>(kf) + static_cast<int>(vf) + j);
-                float add[4] = {0.f, 0.f, 0.f, 0.f};
-                const float um[4] = {uv.x, uv.y, uv.z, uv.w};
-                if (s >= -a.s_mid && s <= a.s_mid) {
-#pragma unroll
-                  for (int m = 0; m < 4; ++m) {
-                    const int t = g.t[m];
-                    if (t < 0) continue;
-                    const RayRange rr = a.rays[static_cast<size_t>(t) * a.det + a.s_mid + s];
-                    const int tm = m >= 2 ? -tau : tau;
-                    if (tm >= rr.first && tm <= rr.last) add[m] = wj * um[m];
-                  }
-                }
-                acc[p].x += add[0];
-                acc[p].y += add[1];
-                acc[p].z += add[2];
-                acc[p].w += add[3];
+            for (int m = 0; m < 4; ++m) {
+              bool valid = false;
+              const int t = g.t[m];
+              if (!out && t >= 0 && sr >= -a.s_mid && sr <= a.s_mid) {
+                const RayRange rr = a.rays[static_cast<size_t>(t) * a.det + a.s_mid + sr];
+                const int tm = m >= 2 ? -tau : tau;
+                valid = tm >= rr.first && tm <= rr.last;
               }
-              ex += dx, ey += dy;
+              if (!valid) cr[m] -= w * um[m];
             }
-            acc[p].x = fmaf(w, uv.x, acc[p].x);
-            acc[p].y = fmaf(w, uv.y, acc[p].y);
-            acc[p].z = fmaf(w, uv.z, acc[p].z);
-            acc[p].w = fmaf(w, uv.w, acc[p].w);
           }
         }
+      }
+#pragma unroll
+      for (int m = 0; m < 4; ++m)
+#pragma unroll
+        for (int off = NB / 2; off > 0; off >>= 1)
+          cr[m] += __shfl_xor_sync(0xffffffffu, cr[m], off);
+      if (o == 0 && bq < nbp) {
+        float4 v = bacc[bq];
+        v.x += cr[0], v.y += cr[1], v.z += cr[2], v.w += cr[3];
+        bacc[bq] = v;
       }
     }
     __syncthreads();  // buffer `buf` is restaged two batches later
@@ -979,10 +997,20 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   float(*ot)[TH][TW + 1] = reinterpret_cast<float(*)[TH][TW + 1]>(&U4[0][0][0]);
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
-    ot[0][yl[p]][xl[p]] = acc[p].x;
-    ot[1][yl[p]][xl[p]] = acc[p].y;
-    ot[2][yl[p]][xl[p]] = acc[p].z;
-    ot[3][yl[p]][xl[p]] = acc[p].w;
+    const int y = ty + p * RS;
+    ot[0][y][tx] = acc[p].x;
+    ot[1][y][tx] = acc[p].y;
+    ot[2][y][tx] = acc[p].z;
+    ot[3][y][tx] = acc[p].w;
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < nbp; k += kGaThreads) {
+    const int2 bl = bpix[k];
+    const float4 v = bacc[k];
+    ot[0][bl.y][bl.x] += v.x;
+    ot[1][bl.y][bl.x] += v.y;
+    ot[2][bl.y][bl.x] += v.z;
+    ot[3][bl.y][bl.x] += v.w;
   }
   __syncthreads();
   const size_t nn = a.nn;
