@@ -184,7 +184,10 @@ void* ncsg_problem_stream(const ncsg_problem* p);
  * solvers.cpp:118-122). */
 ncsg_status ncsg_set_state(ncsg_problem* p, const double* x, const double* u, int64_t iter);
 ncsg_status ncsg_get_state(ncsg_problem* p, double* x, double* u, int64_t* iter);
-/* Device views of the state (fp32, batch-major) for zero-copy callers. */
+/* Device views of the state (fp32, batch-major) for zero-copy callers.
+ * Writing u through the view: fetch it again (or ncsg_set_state) after the
+ * write and before the next step -- the call marks the engine's derived copy
+ * of u stale. */
 float* ncsg_state_x(ncsg_problem* p);
 float* ncsg_state_u(ncsg_problem* p);
 

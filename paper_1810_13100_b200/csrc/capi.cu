@@ -134,6 +134,10 @@ struct ncsg_problem {
   int64_t iter = 0;
   size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
   bool sharded = false;            // angle- or orbit-sharded (multi-GPU phases)
+  // Orbit-interleaved copy of the sinogram dual (gather-mode adjoint input),
+  // written by the dual update; fresh while u has not been written otherwise.
+  DevBuf<float> u4;
+  bool u4_fresh = false;
   DevBuf<uint8_t> own_angle;       // orbit sharding: own[t] (nullptr otherwise)
   bool rank0 = true;              // adds the replicated blocks to A^T u
   float* atu_ext = nullptr;       // caller-owned A^T u buffer (sharded phases)
@@ -175,11 +179,12 @@ void proj_forward(ncsg_problem* p, const float* img, const float* aux, float* pa
   else
     launch_radon_forward_partial(*p->radon, img, aux, part, batch, p->stream.s);
 }
-void proj_adjoint(ncsg_problem* p, const float* u, size_t u_stride, float* part, int batch) {
+void proj_adjoint(ncsg_problem* p, const float* u, size_t u_stride, float* part, int batch,
+                  const float* u4 = nullptr) {
   if (p->sparse)
     launch_sparse_adjoint(*p->sparse, u, u_stride, part, p->nn, batch, p->stream.s);
   else
-    launch_radon_adjoint_partial(*p->radon, u, u_stride, part, batch, p->stream.s);
+    launch_radon_adjoint_partial(*p->radon, u, u_stride, part, batch, p->stream.s, u4);
 }
 
 // Second input of the forward: x^T for class-H angles, or the symmetry
@@ -240,7 +245,7 @@ void phase_a(ncsg_problem* p) {
   mark(p);
   if (p->d.kind != NCSG_DENOISE) {
     // u_s is the first m0 entries of each problem's dual (stride range).
-    proj_adjoint(p, p->u.p, p->range, p->bp_part.p, p->batch);
+    proj_adjoint(p, p->u.p, p->range, p->bp_part.p, p->batch, p->u4_fresh ? p->u4.p : nullptr);
   }
 }
 
@@ -317,7 +322,15 @@ void forward_and_dual(ncsg_problem* p) {
   a.x = p->x.p;
   a.x_old = p->x_old.p;
   a.flag = p->flag.p;
+  if (p->u4.n) {
+    a.u4 = p->u4.p;
+    a.slot = p->radon->angle_slot.p;
+    a.u4_row = p->radon->u4_row();
+    a.u4_pad = kGaSW;
+    a.u4_stride = p->radon->u4_size();
+  }
   launch_dual_update(a, p->batch, s);
+  p->u4_fresh = p->u4.n > 0;
   mark(p);
 }
 
@@ -1072,6 +1085,10 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     p->x_old.zero(s);
     p->xT.zero(s);
     p->u.zero(s);
+    if (p->radon && p->radon->bp_orbit) {  // zero padding and absent members stay zero
+      p->u4.alloc(p->radon->u4_size() * p->batch);
+      p->u4.zero(s);
+    }
     reset_flag(p.get());
     NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
     *out = p.release();
@@ -1086,7 +1103,10 @@ size_t ncsg_problem_domain_size(const ncsg_problem* p) { return p->nn; }
 size_t ncsg_problem_range_size(const ncsg_problem* p) { return p->range; }
 void* ncsg_problem_stream(const ncsg_problem* p) { return p->stream.s; }
 float* ncsg_state_x(ncsg_problem* p) { return p->x.p; }
-float* ncsg_state_u(ncsg_problem* p) { return p->u.p; }
+float* ncsg_state_u(ncsg_problem* p) {
+  p->u4_fresh = false;  // the caller may write u through this view
+  return p->u.p;
+}
 float* ncsg_atu_buffer(ncsg_problem* p) {
   if (p->atu_ext) return p->atu_ext;
   if (!p->atu_own.n) p->atu_own.alloc(p->nn * p->batch);
@@ -1109,6 +1129,7 @@ ncsg_status ncsg_set_state(ncsg_problem* p, const double* x, const double* u, in
       upload_f64(p, u, p->u.p, p->range * p->batch);
     else
       p->u.zero(s);
+    p->u4_fresh = false;
     p->iter = iter;
     engine_init(p);
     reset_flag(p);

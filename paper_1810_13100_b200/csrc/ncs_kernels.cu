@@ -37,6 +37,15 @@ __device__ __forceinline__ float grad_at(const float* x, int n, size_t e) {
 // with QuadraticConj (prox.cpp:21-24), ScaledL1Conj (prox.cpp:36-38, bound
 // lambda*alpha/beta) and NonnegConj (prox.cpp:103-105); CT data rays also
 // sum the projector's strip partials into ax_new and store it as the new ax.
+// Orbit-interleaved copy of the sinogram dual for bp_gather_kernel.
+__device__ __forceinline__ void put_u4(const DualArgs& a, int b, size_t i, float v) {
+  const int t = static_cast<int>(i / a.det);
+  const int sl = a.slot[t];
+  if (sl < 0) return;
+  const size_t d = i - static_cast<size_t>(t) * a.det;
+  a.u4[b * a.u4_stride + ((static_cast<size_t>(sl >> 2) * a.u4_row + a.u4_pad + d) << 2) + (sl & 3)] = v;
+}
+
 __global__ void dual_update_kernel(DualArgs a) {
   const int b = blockIdx.z;
   const int section = blockIdx.y;
@@ -62,6 +71,7 @@ __global__ void dual_update_kernel(DualArgs a) {
         us[i] = un;
         ax[i] = rx;
         bad |= isnan(un);
+        if (a.u4) put_u4(a, b, i, un);
       }
     } else if (a.kind == NCSG_PET) {
       // PoissonConj block (pipeline.cpp:86-88): offset 0, counts in b,
@@ -83,6 +93,7 @@ __global__ void dual_update_kernel(DualArgs a) {
         us[i] = static_cast<float>(un);
         ax[i] = rx;
         bad |= isnan(un);
+        if (a.u4) put_u4(a, b, i, static_cast<float>(un));
       }
     } else {
       float* ud = a.u0 + b * a.u_stride;

@@ -23,6 +23,12 @@ struct DualArgs {
   int* flag = nullptr;
   const uint8_t* own = nullptr;  // orbit sharding: own[t] of ray t*det + d (nullable)
   int det = 0;
+  // Orbit gather input (nullable): the new data-block dual also goes to
+  // u4[b][orbit][pad + d].member (slot[t] = 4 * orbit + member, -1: none).
+  float* u4 = nullptr;
+  const int* slot = nullptr;
+  int u4_row = 0, u4_pad = 0;
+  size_t u4_stride = 0;  // floats per problem
 };
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
 

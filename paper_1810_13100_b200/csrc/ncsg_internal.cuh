@@ -229,6 +229,11 @@ struct RadonDev {
   bool bp_orbit = false;
   int bp_orbit_chunks = 0, bp_orbit_len = 0;
   DevBuf<GatherGeom> gather;
+  // Orbit-interleaved dual (optional gather input): angle t's member slot
+  // 4 * orbit + member (-1: none) and the padded row of rays per orbit.
+  DevBuf<int> angle_slot;
+  int u4_row() const { return geo.n_det + 2 * kGaSW; }
+  size_t u4_size() const { return geo.orbits.size() * static_cast<size_t>(u4_row()) * 4; }
   DevBuf<int2> strip_range[2];                // [angle][strip] s-range (forward)
   std::vector<int2> strip_range_host[2];
   // Orbit-mode forward (fp_orbit_kernel): strips x segments of rows; each
@@ -259,8 +264,11 @@ void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, in
                       cudaStream_t s);
 // Adjoint partial images: bp_part[batch][n_partials][n*n]; class-H partials
 // are stored transposed.
+// u4 (nullable, gather mode): the orbit-interleaved copy of u written by the
+// dual update (RadonDev::u4_size() floats per problem), staged instead of u.
 void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_stride,
-                                  float* bp_part, int batch, cudaStream_t s);
+                                  float* bp_part, int batch, cudaStream_t s,
+                                  const float* u4 = nullptr);
 // out[b] = sum of the class-V partials + transposed class-H partials.
 void launch_sum_partials(const float* part, int nV, int nH, float* out, int n, int batch,
                          cudaStream_t s);

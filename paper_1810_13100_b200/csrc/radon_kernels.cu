@@ -791,9 +791,40 @@ struct GaArgs {
   float* out;      // [batch][4 * n_chunks][nn]
   int n, det, s_mid;
   size_t nn, u_stride;
+  const float4* u4;  // orbit-interleaved u ([batch][orbit][u4_row], nullable)
+  int u4_row, u4_pad;
 };
 
 __device__ __forceinline__ float tent(float e) { return __saturatef(1.0f - fabsf(e)); }
+
+// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a; a pk(w, w) operand
+// becomes the scalar-broadcast form): one instruction for an (x, y) pair.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f32x2 r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
 
 __device__ __forceinline__ void cp_async4(unsigned dst, const float* src, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
@@ -825,12 +856,14 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   const int o_begin = chunk * a.chunk_len;
   const int o_end = min(a.n_orb, o_begin + a.chunk_len);
   const float* ub = a.u + static_cast<size_t>(b) * a.u_stride + a.s_mid;
+  const float4* u4b =
+      a.u4 ? a.u4 + static_cast<size_t>(b) * a.n_orb * a.u4_row : nullptr;
   // Pixel p of a thread: column tx, row ty + p * RS (a warp = a row segment).
   constexpr int RS = kGaThreads / TW;
   const int tx = threadIdx.x % TW, ty = threadIdx.x / TW;
-  float4 acc[PX];
+  f32x2 acc_xy[PX], acc_zw[PX];  // members (0, 1), (2, 3)
 #pragma unroll
-  for (int p = 0; p < PX; ++p) acc[p] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int p = 0; p < PX; ++p) acc_xy[p] = acc_zw[p] = pk(0.f, 0.f);
   const double qx0 = X0 + tx - c, qy0 = Y0 + ty - c;
   // Border pixels (image row / column 0 or n-1) of this tile.
   if (threadIdx.x == 0) nbp = 0;
@@ -869,14 +902,23 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
       cp_async16(static_cast<unsigned>(__cvta_generic_to_shared(&G[buf][o])) + 16u * q,
                  reinterpret_cast<const float4*>(a.geo + ob + o) + q);
     }
-    for (int i = threadIdx.x; i < nb * SW * 4; i += kGaThreads) {
-      const int m = i & 3, e = i >> 2;
-      const int o = e / SW, r = e - o * SW;
-      const int s = slo[ob - o_begin + o] + r;
-      const int t = __ldg(&a.geo[ob + o].t[m]);
-      const bool ok = s >= -a.s_mid && s <= a.s_mid && t >= 0;
-      cp_async4(static_cast<unsigned>(__cvta_generic_to_shared(&U4[buf][o][r])) + 4u * m,
-                ok ? ub + static_cast<size_t>(t) * a.det + s : ub, ok);
+    if (u4b) {  // rows of the interleaved copy: zero-padded, 16-byte pieces
+      for (int i = threadIdx.x; i < nb * SW; i += kGaThreads) {
+        const int o = i / SW, r = i - o * SW;
+        const int d = slo[ob - o_begin + o] + r + a.s_mid + a.u4_pad;
+        cp_async16(static_cast<unsigned>(__cvta_generic_to_shared(&U4[buf][o][r])),
+                   u4b + static_cast<size_t>(ob + o) * a.u4_row + d);
+      }
+    } else {
+      for (int i = threadIdx.x; i < nb * SW * 4; i += kGaThreads) {
+        const int m = i & 3, e = i >> 2;
+        const int o = e / SW, r = e - o * SW;
+        const int s = slo[ob - o_begin + o] + r;
+        const int t = __ldg(&a.geo[ob + o].t[m]);
+        const bool ok = s >= -a.s_mid && s <= a.s_mid && t >= 0;
+        cp_async4(static_cast<unsigned>(__cvta_generic_to_shared(&U4[buf][o][r])) + 4u * m,
+                  ok ? ub + static_cast<size_t>(t) * a.det + s : ub, ok);
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
@@ -894,7 +936,8 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
     __syncthreads();
     for (int o = 0; o < nb; ++o) {
       const GatherGeom& g = G[buf][o];
-      const float ax = g.ax, ay = g.ay, dx = g.dx, dy = g.dy;
+      const float ay = g.ay;
+      const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
       const float4* Uo = U4[buf][o];
       const int sl = slo[ob - o_begin + o];
       double sg = fma(g.ia_x, qx0, g.ia_y * qy0);
@@ -913,17 +956,18 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
         for (int u = 0; u < 3; ++u) {
           const float du = du0 + u;
           const float dv = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
-          float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
-          float w = tent(ex) * tent(ey);
-          ex += dx, ey += dy;
-          w = fmaf(tent(ex), tent(ey), w);
-          ex += dx, ey += dy;
-          w = fmaf(tent(ex), tent(ey), w);
+          f32x2 e = ffma2(pk(du, du), A, fmul2(pk(dv, dv), D));  // (ex, ey)
+          float2 v = upk(e);
+          float w = tent(v.x) * tent(v.y);
+          e = fadd2(e, D);
+          v = upk(e);
+          w = fmaf(tent(v.x), tent(v.y), w);
+          e = fadd2(e, D);
+          v = upk(e);
+          w = fmaf(tent(v.x), tent(v.y), w);
           const float4 uv = Uo[r0 + u];
-          acc[p].x = fmaf(w, uv.x, acc[p].x);
-          acc[p].y = fmaf(w, uv.y, acc[p].y);
-          acc[p].z = fmaf(w, uv.z, acc[p].z);
-          acc[p].w = fmaf(w, uv.w, acc[p].w);
+          acc_xy[p] = ffma2(pk(w, w), pk(uv.x, uv.y), acc_xy[p]);
+          acc_zw[p] = ffma2(pk(w, w), pk(uv.z, uv.w), acc_zw[p]);
         }
       }
     }
@@ -998,10 +1042,11 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     const int y = ty + p * RS;
-    ot[0][y][tx] = acc[p].x;
-    ot[1][y][tx] = acc[p].y;
-    ot[2][y][tx] = acc[p].z;
-    ot[3][y][tx] = acc[p].w;
+    const float2 v01 = upk(acc_xy[p]), v23 = upk(acc_zw[p]);
+    ot[0][y][tx] = v01.x;
+    ot[1][y][tx] = v01.y;
+    ot[2][y][tx] = v23.x;
+    ot[3][y][tx] = v23.y;
   }
   __syncthreads();
   for (int k = threadIdx.x; k < nbp; k += kGaThreads) {
@@ -1153,6 +1198,13 @@ void RadonDev::upload() {
       }
       gather.alloc(gg.size());
       NCSG_CUDA_CHECK(cudaMemcpy(gather.p, gg.data(), gg.size() * sizeof(GatherGeom),
+                                 cudaMemcpyHostToDevice));
+      std::vector<int> slot(geo.n_angles, -1);
+      for (size_t oi = 0; oi < geo.orbits.size(); ++oi)
+        for (int m = 0; m < 4; ++m)
+          if (geo.orbits[oi].t[m] >= 0) slot[geo.orbits[oi].t[m]] = static_cast<int>(4 * oi + m);
+      angle_slot.alloc(slot.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(angle_slot.p, slot.data(), slot.size() * sizeof(int),
                                  cudaMemcpyHostToDevice));
     }
   }
@@ -1362,7 +1414,7 @@ void launch_strip_sum(const RadonDev& r, const float* fp_partial, float* out, in
 }
 
 void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_stride,
-                                  float* bp_part, int batch, cudaStream_t s) {
+                                  float* bp_part, int batch, cudaStream_t s, const float* u4) {
   const Geometry& g = r.geo;
   const int n = g.n;
   if (r.n_partials() == 0) return;
@@ -1380,6 +1432,9 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     a.s_mid = g.s_mid;
     a.nn = static_cast<size_t>(n) * n;
     a.u_stride = u_stride ? u_stride : static_cast<size_t>(g.n_angles) * g.n_det;
+    a.u4 = reinterpret_cast<const float4*>(u4);
+    a.u4_row = r.u4_row();
+    a.u4_pad = kGaSW;
     dim3 grid((n + kGaTW - 1) / kGaTW, (n + kGaTH - 1) / kGaTH, a.n_chunks * batch);
     bp_gather_kernel<kGaTW, kGaTH, kGaBatch><<<grid, kGaThreads, 0, s>>>(a);
     NCSG_CUDA_CHECK(cudaGetLastError());
