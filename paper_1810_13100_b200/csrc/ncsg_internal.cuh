@@ -187,14 +187,16 @@ constexpr int kGaBatch = NCSG_GA_BATCH, kGaWaves = NCSG_GA_WAVES;
 constexpr int kGaSW = kGaTW + kGaTH + 8;            // staged rays per orbit and tile
 constexpr int kGaMaxChunk = 1024;                   // orbits per chunk (lowest-ray table)
 // Per-orbit constants of the gather (host fp64 from the Q32 lattice): the
-// lattice is p(s, k) = c + s a + k d; (sigma, kappa) = M^-1 (q - c) are the
-// continuous lattice coordinates of pixel q.
+// lattice is p(s, k) = c + s a + k d, and pixel (X, Y) has the continuous
+// lattice coordinates (sigma, kappa) = M^-1 (q - c), M = [a d], kept in Q32
+// fixed point as affine functions of (X, Y).
 struct GatherGeom {
-  double ia_x, ia_y, id_x, id_y;  // rows of M^-1, M = [a d]
-  float ax, ay, dx, dy;           // lattice vectors (pixels)
-  float rho, inv_dy;              // sigma half-extent of the |e| < 1 window, 1 / dy
-  int t[4];                       // member angles (-1: absent)
-  int dir;                        // tau = dir * k
+  long long s0, sx, sy;  // sigma(X, Y) = s0 + X sx + Y sy   (Q32)
+  long long k0, kx, ky;  // kappa(X, Y) = k0 + X kx + Y ky   (Q32)
+  float ax, ay, dx, dy;  // lattice vectors (pixels)
+  float rho, inv_dy;     // sigma half-extent of the |e| < 1 window, 1 / dy
+  int t[4];              // member angles (-1: absent)
+  int dir;               // tau = dir * k
   int pad;
 };
 

@@ -797,6 +797,18 @@ struct GaArgs {
 
 __device__ __forceinline__ float tent(float e) { return __saturatef(1.0f - fabsf(e)); }
 
+// Q32 lattice coordinate -> integer part (hi word) and fraction (top 23 bits
+// of the lo word as a float in [0, 1)), ALU only.
+__device__ __forceinline__ int q32_floor(long long v) { return static_cast<int>(v >> 32); }
+__device__ __forceinline__ float q32_frac(long long v) {
+  return __uint_as_float(0x3f800000u | (static_cast<unsigned>(v) >> 9)) - 1.0f;
+}
+// floor(z) for |z| < 2^21 by round-to-nearest of z - 1/2 (floor(z) - 1 when
+// z is an integer -- the gather's candidate windows tolerate either).
+__device__ __forceinline__ float floor_rn(float z) {
+  return __fsub_rn(__fadd_rn(__fsub_rn(z, 0.5f), 12582912.0f), 12582912.0f);
+}
+
 // Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a; a pk(w, w) operand
 // becomes the scalar-broadcast form): one instruction for an (x, y) pair.
 typedef unsigned long long f32x2;
@@ -852,7 +864,6 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   const int b = blockIdx.z / a.n_chunks;
   const int chunk = blockIdx.z - b * a.n_chunks;
   const int n = a.n;
-  const double c = 0.5 * (n - 1);
   const int o_begin = chunk * a.chunk_len;
   const int o_end = min(a.n_orb, o_begin + a.chunk_len);
   const float* ub = a.u + static_cast<size_t>(b) * a.u_stride + a.s_mid;
@@ -864,7 +875,7 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   f32x2 acc_xy[PX], acc_zw[PX];  // members (0, 1), (2, 3)
 #pragma unroll
   for (int p = 0; p < PX; ++p) acc_xy[p] = acc_zw[p] = pk(0.f, 0.f);
-  const double qx0 = X0 + tx - c, qy0 = Y0 + ty - c;
+  const long long Xt = X0 + tx, Yt = Y0 + ty;
   // Border pixels (image row / column 0 or n-1) of this tile.
   if (threadIdx.x == 0) nbp = 0;
   __syncthreads();
@@ -884,9 +895,9 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
   // the tile corners minus the window half-extent.
   for (int o = threadIdx.x; o < o_end - o_begin; o += kGaThreads) {
     const GatherGeom& g = a.geo[o_begin + o];
-    const double x0 = X0 - c, x1 = X0 + TW - 1 - c, y0 = Y0 - c, y1 = Y0 + TH - 1 - c;
-    const double s0 = fmin(g.ia_x * x0, g.ia_x * x1) + fmin(g.ia_y * y0, g.ia_y * y1);
-    slo[o] = static_cast<int>(floor(s0 - g.rho)) - 1;
+    const long long smin = g.s0 + min(X0 * g.sx, (X0 + TW - 1LL) * g.sx) +
+                           min(Y0 * g.sy, (Y0 + TH - 1LL) * g.sy);
+    slo[o] = q32_floor(smin - static_cast<long long>(ldexpf(g.rho, 32))) - 1;
   }
   __syncthreads();
 
@@ -940,22 +951,20 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
       const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
       const float4* Uo = U4[buf][o];
       const int sl = slo[ob - o_begin + o];
-      double sg = fma(g.ia_x, qx0, g.ia_y * qy0);
-      double kp = fma(g.id_x, qx0, g.id_y * qy0);
-      const double dsg = g.ia_y * RS, dkp = g.id_y * RS;
+      long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
+      long long kq = g.k0 + Xt * g.kx + Yt * g.ky;
 #pragma unroll
       for (int p = 0; p < PX; ++p) {
-        if (p > 0) sg += dsg, kp += dkp;
-        const double sf = floor(sg), kf = floor(kp);
-        const float fs = static_cast<float>(sg - sf), fk = static_cast<float>(kp - kf);
-        const int u0 = static_cast<int>(ceilf(fs - g.rho));
-        const int r0 = static_cast<int>(sf) + u0 - sl;
-        const float du0 = static_cast<float>(u0) - fs;
+        if (p > 0) sq += RS * g.sy, kq += RS * g.ky;
+        const float fs = q32_frac(sq), fk = q32_frac(kq);
+        const bool first = fs - g.rho > -1.0f;  // u0 = ceil(fs - rho) is 0 or -1
+        const int r0 = q32_floor(sq) - (first ? 0 : 1) - sl;
+        const float du0 = (first ? 0.0f : -1.0f) - fs;
         const float fk1 = fk - 1.0f;
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           const float du = du0 + u;
-          const float dv = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
+          const float dv = floor_rn(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
           f32x2 e = ffma2(pk(du, du), A, fmul2(pk(dv, dv), D));  // (ex, ey)
           float2 v = upk(e);
           float w = tent(v.x) * tent(v.y);
@@ -987,15 +996,15 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
         const int2 bl = bpix[bq];
         const int X = X0 + bl.x, Y = Y0 + bl.y;
         const float Xf = static_cast<float>(X), Yf = static_cast<float>(Y);
-        const double sg = fma(g.ia_x, X - c, g.ia_y * (Y - c));
-        const double kp = fma(g.id_x, X - c, g.id_y * (Y - c));
-        const double sf = floor(sg), kf = floor(kp);
-        const float fs = static_cast<float>(sg - sf), fk = static_cast<float>(kp - kf);
-        const int u0 = static_cast<int>(ceilf(fs - g.rho));
-        const int r0 = static_cast<int>(sf) + u0 - slo[ob - o_begin + o];
+        const long long sq = g.s0 + X * g.sx + Y * g.sy;
+        const long long kq = g.k0 + X * g.kx + Y * g.ky;
+        const int sf = q32_floor(sq), kf = q32_floor(kq);
+        const float fs = q32_frac(sq), fk = q32_frac(kq);
+        const int u0 = fs - g.rho > -1.0f ? 0 : -1;
+        const int r0 = sf + u0 - slo[ob - o_begin + o];
         for (int u = 0; u < 3; ++u) {
           const float du = static_cast<float>(u0 + u) - fs;
-          const float vf = floorf(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
+          const float vf = floor_rn(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
           const float4 uv = U4[buf][o][r0 + u];
           const float um[4] = {uv.x, uv.y, uv.z, uv.w};
           for (int j = 0; j < 3; ++j) {
@@ -1006,8 +1015,8 @@ __global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
             const float lo = fminf(px, py), hi = fmaxf(px, py);
             if (w == 0.f || (lo > kEps && hi < lim - kEps)) continue;
             const bool out = lo < -kEps || hi > lim + kEps;
-            const int sr = static_cast<int>(sf) + u0 + u;
-            const int tau = g.dir * (static_cast<int>(kf) + static_cast<int>(vf) + j);
+            const int sr = sf + u0 + u;
+            const int tau = g.dir * (kf + static_cast<int>(vf) + j);
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
               bool valid = false;
@@ -1181,16 +1190,20 @@ void RadonDev::upload() {
         const double dx = std::ldexp(static_cast<double>(o.rep.dX), -32);
         const double dy = std::ldexp(static_cast<double>(o.rep.dY), -32);
         const double det = ax * dy - dx * ay;
+        const double ia_x = dy / det, ia_y = -dx / det, id_x = -ay / det, id_y = ax / det;
+        const double cc = 0.5 * (n - 1);
         GatherGeom& q = gg[oi];
-        q.ia_x = dy / det;
-        q.ia_y = -dx / det;
-        q.id_x = -ay / det;
-        q.id_y = ax / det;
+        q.sx = std::llround(std::ldexp(ia_x, 32));
+        q.sy = std::llround(std::ldexp(ia_y, 32));
+        q.s0 = std::llround(std::ldexp(-cc * (ia_x + ia_y), 32));
+        q.kx = std::llround(std::ldexp(id_x, 32));
+        q.ky = std::llround(std::ldexp(id_y, 32));
+        q.k0 = std::llround(std::ldexp(-cc * (id_x + id_y), 32));
         q.ax = static_cast<float>(ax);
         q.ay = static_cast<float>(ay);
         q.dx = static_cast<float>(dx);
         q.dy = static_cast<float>(dy);
-        q.rho = static_cast<float>(std::fabs(q.ia_x) + std::fabs(q.ia_y) + 1e-6);
+        q.rho = static_cast<float>(std::fabs(ia_x) + std::fabs(ia_y) + 1e-6);
         q.inv_dy = static_cast<float>(1.0 / dy);
         for (int m = 0; m < 4; ++m) q.t[m] = o.t[m];
         q.dir = o.rep.dir;
