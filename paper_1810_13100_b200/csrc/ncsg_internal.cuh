@@ -173,13 +173,13 @@ constexpr int kBpWaves = NCSG_BP_WAVES;  // adjoint: target CTAs = 148 * 3 * wav
 // of the representative's frame, kGaPx pixels per thread, orbits staged in
 // batches of kGaBatch.
 #ifndef NCSG_GA_TH
-#define NCSG_GA_TH 16
+#define NCSG_GA_TH 32
 #endif
 #ifndef NCSG_GA_BATCH
 #define NCSG_GA_BATCH 16
 #endif
 #ifndef NCSG_GA_WAVES
-#define NCSG_GA_WAVES 2
+#define NCSG_GA_WAVES 4
 #endif
 constexpr int kGaTW = 32, kGaTH = NCSG_GA_TH, kGaThreads = 256;
 constexpr int kGaPx = kGaTW * kGaTH / kGaThreads;  // pixels per thread
