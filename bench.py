@@ -210,10 +210,13 @@ def main():
 
 def roofline_of(cfg, phase_avg, S, clocks):
     """Roofline object for the dominant phase: algorithmic HBM bytes per launch
-    / its CUDA-event time against the measured HBM peak, plus the gather
-    roofline that actually bounds the projectors (16 B of texel reads per
-    sample against 148 SM x 128 B/clk of shared memory at the sampled clock)
-    and the ncu DRAM traffic of the same kernel (profiles/ncu_traffic.json)."""
+    / its CUDA-event time against the measured HBM peak, the ncu DRAM traffic
+    of the same kernel (profiles/ncu_traffic.json), and the on-chip roofline
+    that actually bounds each projector: R (fp_orbit_kernel) reads 16 B of
+    texels per sample from shared memory (148 SM x 128 B/clk at the sampled
+    clock); R^T (bp_gather_kernel) is a register gather bound by instruction
+    issue (148 SM x 4 warp-instructions/clk), measured instructions per launch
+    from the same ncu capture."""
     pk, pk_kind = peaks()
     n_strips = (cfg.n + 127) // 128
     nb = algorithmic_bytes(cfg, n_strips, 8)
@@ -222,29 +225,41 @@ def roofline_of(cfg, phase_avg, S, clocks):
     achieved = nb[dom] / (dom_ms * 1e-3) / 1e9
     sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
     smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # TB/s at the measured clock
-    traffic, wf_frac = None, None
-    try:  # DRAM bytes / smem wavefront use of the same kernel from the committed ncu capture
+    issue_peak = 148 * 4 * sm_mhz * 1e6           # warp-instructions / s
+    prof = {}
+    try:  # DRAM bytes / smem wavefronts / instructions of the committed ncu capture
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
             prof = json.load(fh)
-        traffic = prof["dram_bytes_per_launch"].get(dom)
-        wf_frac = prof.get("smem_wavefront_frac", {}).get(dom)
-    except (OSError, ValueError, KeyError):
+    except (OSError, ValueError):
         pass
-    gather = {}
-    if dom in ("adjoint", "forward"):
-        # R reads 4 texels per sample (16 B); R^T read-modify-writes them (32 B)
-        per = 32 if dom == "adjoint" else 16
-        gather = {"bytes_per_launch": per * S, "achieved_tbs": per * S / (dom_ms * 1e-3) / 1e12,
-                  "peak_tbs": smem_peak, "frac": per * S / (dom_ms * 1e-3) / 1e12 / smem_peak,
-                  "ncu_smem_wavefront_frac": wf_frac,
-                  "note": f"{per} B of shared-memory texel traffic per bilinear sample against "
-                          "148 SM x 128 B/clk at the sampled SM clock; ncu_smem_wavefront_frac "
-                          "= measured share of the wavefront peak (bank conflicts included)"}
+    traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
+    proj = {}
+    if "forward" in phase_avg:
+        ms = phase_avg["forward"]
+        proj["forward"] = {
+            "model": "shared-memory gather", "bytes_per_launch": 16 * S,
+            "achieved_tbs": 16 * S / (ms * 1e-3) / 1e12, "peak_tbs": smem_peak,
+            "frac": 16 * S / (ms * 1e-3) / 1e12 / smem_peak, "launch_ms": ms,
+            "ncu_smem_wavefront_frac": prof.get("smem_wavefront_frac", {}).get("forward"),
+            "note": "16 B of texel reads per bilinear sample (four 128-bit loads per sample of "
+                    "an orbit) against 148 SM x 128 B/clk at the sampled SM clock"}
+    if "adjoint" in phase_avg:
+        ms = phase_avg["adjoint"]
+        inst = prof.get("inst_per_launch", {}).get("adjoint")
+        proj["adjoint"] = {
+            "model": "instruction issue", "launch_ms": ms,
+            "pixel_angle_pairs": cfg.n * cfg.n * cfg.angles,
+            "inst_per_launch": inst, "peak_inst_per_s": issue_peak,
+            "frac": (inst / (ms * 1e-3) / issue_peak) if inst else None,
+            "ncu_issue_active_frac": prof.get("issue_active_frac", {}).get("adjoint"),
+            "note": "pixel-driven orbit gather in registers (no shared-memory read-modify-"
+                    "write): warp-instructions per launch (ncu) / event time against "
+                    "148 SM x 4 issue/clk at the sampled SM clock"}
     return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
             "peak_kind": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
             "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
             "algorithmic_bytes_per_launch": nb[dom], "launch_ms": dom_ms,
-            "gather_roofline": gather}
+            "on_chip": proj}
 
 
 def bench_multi(args, cfg):
