@@ -135,6 +135,35 @@ __device__ __forceinline__ void sts(unsigned a, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v));
 }
 
+// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a; a pk(w, w) operand
+// becomes the scalar-broadcast form): one instruction for an (x, y) pair.
+typedef unsigned long long f32x2;
+__device__ __forceinline__ f32x2 pk(float a, float b) {
+  f32x2 r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ float2 upk(f32x2 r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
+  f32x2 d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
+  f32x2 d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+
 // ---- TMA (cp.async.bulk.tensor) + mbarrier helpers ----
 __device__ __forceinline__ void mbar_init(unsigned bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
@@ -580,17 +609,20 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
           const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
           const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
           const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
-          const float v00[4] = {q00.x, q00.y, q00.z, q00.w};
-          const float v01[4] = {q01.x, q01.y, q01.z, q01.w};
-          const float v10[4] = {q10.x, q10.y, q10.z, q10.w};
-          const float v11[4] = {q11.x, q11.y, q11.z, q11.w};
+          // bilinear weights once, then members (0, 1) and (2, 3) as f32x2
+          const float w11 = fx * fy, w01 = fx - w11, w10 = fy - w11, w00 = 1.0f - fx - w10;
+          f32x2 v01 = fmul2(pk(w00, w00), pk(q00.x, q00.y));
+          f32x2 v23 = fmul2(pk(w00, w00), pk(q00.z, q00.w));
+          v01 = ffma2(pk(w01, w01), pk(q01.x, q01.y), v01);
+          v23 = ffma2(pk(w01, w01), pk(q01.z, q01.w), v23);
+          v01 = ffma2(pk(w10, w10), pk(q10.x, q10.y), v01);
+          v23 = ffma2(pk(w10, w10), pk(q10.z, q10.w), v23);
+          v01 = ffma2(pk(w11, w11), pk(q11.x, q11.y), v01);
+          v23 = ffma2(pk(w11, w11), pk(q11.z, q11.w), v23);
+          const float2 a01 = upk(v01), a23 = upk(v23);
+          const float v[4] = {a01.x, a01.y, a23.x, a23.y};
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            const float v0 = fmaf(fx, v01[k] - v00[k], v00[k]);
-            const float v1 = fmaf(fx, v11[k] - v10[k], v10[k]);
-            const float v = fmaf(fy, v1 - v0, v0);
-            acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v : 0.f;
-          }
+          for (int k = 0; k < 4; ++k) acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v[k] : 0.f;
           X += g.dXq;
           Y += g.dYq;
         }
@@ -809,34 +841,6 @@ __device__ __forceinline__ float floor_rn(float z) {
   return __fsub_rn(__fadd_rn(__fsub_rn(z, 0.5f), 12582912.0f), 12582912.0f);
 }
 
-// Packed f32x2 arithmetic (FFMA2 / FADD2 on sm_100a; a pk(w, w) operand
-// becomes the scalar-broadcast form): one instruction for an (x, y) pair.
-typedef unsigned long long f32x2;
-__device__ __forceinline__ f32x2 pk(float a, float b) {
-  f32x2 r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-  return r;
-}
-__device__ __forceinline__ float2 upk(f32x2 r) {
-  float2 v;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
-  return v;
-}
-__device__ __forceinline__ f32x2 ffma2(f32x2 a, f32x2 b, f32x2 c) {
-  f32x2 d;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
-  return d;
-}
-__device__ __forceinline__ f32x2 fmul2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
-__device__ __forceinline__ f32x2 fadd2(f32x2 a, f32x2 b) {
-  f32x2 d;
-  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
-  return d;
-}
 
 __device__ __forceinline__ void cp_async4(unsigned dst, const float* src, bool ok) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(dst), "l"(src),
