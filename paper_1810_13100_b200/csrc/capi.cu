@@ -80,11 +80,16 @@ std::vector<std::complex<double>> read_mask(int n, const double* m) {
 // pinv_mask (circulant.cpp:47-55)
 std::vector<std::complex<double>> pinv(const std::vector<std::complex<double>>& h,
                                        double rel_tol) {
-  double hmax = 0.0;
-  for (const auto& z : h) hmax = std::max(hmax, std::abs(z));
+  // |h| compared squared and 1/h = conj(h) / |h|^2: the same filter to fp32
+  // without hypot and the libgcc complex division per bin.
+  double hmax2 = 0.0;
+  for (const auto& z : h) hmax2 = std::max(hmax2, std::norm(z));
   std::vector<std::complex<double>> out(h.size());
-  double cutoff = rel_tol * hmax;
-  for (size_t i = 0; i < h.size(); ++i) out[i] = std::abs(h[i]) > cutoff ? 1.0 / h[i] : 0.0;
+  const double cutoff2 = rel_tol * rel_tol * hmax2;
+  for (size_t i = 0; i < h.size(); ++i) {
+    const double a = h[i].real(), b = h[i].imag(), d = a * a + b * b;
+    out[i] = d > cutoff2 ? std::complex<double>(a / d, -b / d) : 0.0;
+  }
   return out;
 }
 
@@ -967,7 +972,21 @@ ncsg_status ncsg_mask_apply_host(int n, const double* mask, const double* x, dou
   });
 }
 
+// NCSG_SETUP_TIMES=1: host wall time of the problem-creation stages on stderr.
+struct SetupClock {
+  bool on = std::getenv("NCSG_SETUP_TIMES") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "ncsg setup %-18s %8.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
+
 ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** out) {
+  SetupClock clk;
   return guard([&] {
     if (!desc || !out) throw Error{NCSG_INVALID, "null problem descriptor"};
     const ncsg_problem_desc& d = *desc;
@@ -1010,6 +1029,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     } else if (d.kind != NCSG_DENOISE) {
       Geometry geo = build_geometry(d.n, d.n_angles, d.n_det, d.angle_begin, d.angle_end,
                                     d.shard_rank, d.shard_count);
+      clk.mark("geometry");
       p->m0 = static_cast<size_t>(d.n_angles) * d.n_det;
       int ab = d.angle_end > 0 ? d.angle_begin : 0;
       int ae = d.angle_end > 0 ? d.angle_end : d.n_angles;
@@ -1030,6 +1050,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       p->radon->geo = std::move(geo);
       p->radon->device = d.device;
       p->radon->upload();
+      clk.mark("upload");
       p->radon->plan_adjoint(d.batch);
     } else {
       p->m0 = p->nn;
@@ -1040,7 +1061,9 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     p->range = p->m0 + p->g + (d.positivity ? p->nn : 0);
     NCSG_CUDA_CHECK(cudaStreamCreateWithFlags(&p->stream.s, cudaStreamNonBlocking));
     cudaStream_t s = p->stream.s;
+    clk.mark("stream");
     p->fft.init(d.n, s);
+    clk.mark("fft plan");
     // Engine::Engine (solvers.cpp:93-99): m = gamma + alpha C, m_pinv = pinv(m).
     std::vector<std::complex<double>> minv;
     const double scale = 1.0 / (static_cast<double>(d.n) * d.n);
@@ -1060,10 +1083,12 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       // through the same filter path with a constant spectrum.
       minv.assign(p->nn, std::complex<double>(1.0 / d.gamma, 0.0));
     }
+    clk.mark("mask pinv");
     auto hm = half_mask(d.n, minv, scale);
     p->maskT.alloc(hm.size());
     NCSG_CUDA_CHECK(cudaMemcpy(p->maskT.p, hm.data(), hm.size() * sizeof(float2),
                                cudaMemcpyHostToDevice));
+    clk.mark("filter upload");
     size_t xs = p->nn * p->batch;
     p->x.alloc(xs);
     p->x_old.alloc(xs);
@@ -1091,6 +1116,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     }
     reset_flag(p.get());
     NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+    clk.mark("buffers");
     *out = p.release();
   });
 }

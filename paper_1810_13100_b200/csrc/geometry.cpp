@@ -83,9 +83,15 @@ double scatter_cost(double aX, double aY, double bX, double bY, int stride, int 
   return (tot / std::max(1, cnt)) / util;
 }
 
+}  // namespace
+
 // Adjoint lane stride of every angle: the stride in 3..7 with the lowest
 // scatter_cost, evaluated on all host cores (the model is ~1 ms per angle).
-void choose_strides(Geometry& g) {
+// Only the per-angle scatter (bp_tile_kernel) uses it, so RadonDev computes
+// it on first use.
+void choose_adjoint_strides(Geometry& g) {
+  if (g.strides_ready) return;
+  g.strides_ready = true;
   int bpW, bpT, bpP;
   bp_tile_shape(g.n, bpW, bpT, bpP);
   std::vector<AngleGeom*> all;
@@ -115,8 +121,6 @@ void choose_strides(Geometry& g) {
   }
   for (auto& t : th) t.join();
 }
-
-}  // namespace
 
 Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end,
                         int shard_rank, int shard_count) {
@@ -240,11 +244,10 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
     a.inv_adX16 =
         a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
     a.dXq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dX), -9)));
-    a.bp_stride = 5;  // chosen below (choose_strides)
+    a.bp_stride = 5;  // chosen on first use (choose_adjoint_strides)
     a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }
-  choose_strides(g);
   // Dihedral orbits (only for a full, unsharded angle set divisible by 4).
   if (n_angles % 4 == 0 && angle_begin == 0 && angle_end == n_angles) {  // full set or orbit shard
     const int q = n_angles / 4;

@@ -77,6 +77,7 @@ struct Geometry {
   std::vector<OrbitGeom> orbits;   // filled when every angle belongs to an orbit
   std::vector<uint8_t> own;        // own[t]: angle t belongs to this shard
   bool orbit_sharded = false;
+  bool strides_ready = false;      // AngleGeom::bp_stride chosen (choose_adjoint_strides)
   int64_t samples = 0;
 };
 // Orbit representative of angle t (n_angles % 4 == 0): the member in [0, A/4].
@@ -93,6 +94,8 @@ inline int orbit_rep(int t, int n_angles) {
 // Throws Error{NCSG_INVALID} with the reference's messages.
 Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int angle_end,
                         int shard_rank = 0, int shard_count = 0);
+// Lane strides of the per-angle scatter adjoint (once per geometry).
+void choose_adjoint_strides(Geometry& g);
 
 // Explicit sparse projector (SparseMap, sparse.cpp): CSR over sinogram rows
 // (view-major) and its stored transpose over image pixels, fp64 on the host.

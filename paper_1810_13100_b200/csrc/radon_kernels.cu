@@ -1251,6 +1251,13 @@ void RadonDev::plan_adjoint(int batch) {
   int bw, bt, bpitch;
   bp_tile_shape(n, bw, bt, bpitch);
   const int tiles = ((n + bw - 1) / bw) * ((n + bt - 1) / bt);
+  if (!geo.strides_ready) {  // per-angle scatter: lane strides, then the angle tables again
+    choose_adjoint_strides(geo);
+    for (int k = 0; k < 2; ++k)
+      if (!geo.cls[k].empty())
+        NCSG_CUDA_CHECK(cudaMemcpy(angles[k].p, geo.cls[k].data(),
+                                   geo.cls[k].size() * sizeof(AngleGeom), cudaMemcpyHostToDevice));
+  }
   // Aim for about four waves of 3 resident CTAs per SM over 148 SMs.
   const long target = 148L * 3 * kBpWaves;
   const int na0 = static_cast<int>(geo.cls[0].size()), na1 = static_cast<int>(geo.cls[1].size());
