@@ -339,6 +339,24 @@ void forward_and_dual(ncsg_problem* p) {
   mark(p);
 }
 
+// The orbit-interleaved dual copy, rebuilt from u when u was written
+// outside the dual update (set_state, the raw state view).
+void refresh_u4(ncsg_problem* p) {
+  if (!p->u4.n || p->u4_fresh) return;
+  DualArgs a;
+  a.u0 = p->u.p;
+  a.u_stride = p->range;
+  a.m = p->m0;
+  a.det = p->d.n_det;
+  a.u4 = p->u4.p;
+  a.slot = p->radon->angle_slot.p;
+  a.u4_row = p->radon->u4_row();
+  a.u4_pad = kGaSW;
+  a.u4_stride = p->radon->u4_size();
+  launch_u4_pack(a, p->batch, p->stream.s);
+  p->u4_fresh = true;
+}
+
 void do_step(ncsg_problem* p) {
   phase_a(p);
   phase_b(p);
@@ -1189,6 +1207,7 @@ ncsg_status ncsg_step_graph(ncsg_problem* p, int iters) {
       p->iter += iters;
       return;
     }
+    refresh_u4(p);  // the captured steps read u4 from their first adjoint on
     auto it = p->graphs.find(iters);
     if (it == p->graphs.end()) {
       cudaGraph_t graph;

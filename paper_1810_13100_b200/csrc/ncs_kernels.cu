@@ -353,6 +353,23 @@ void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
   count_launch();
 }
 
+// u4 from u for every owned sinogram ray (after the state was set from
+// outside the dual update).
+__global__ void u4_pack_kernel(DualArgs a) {
+  const int b = blockIdx.y;
+  const float* us = a.u0 + b * a.u_stride;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < a.m;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    put_u4(a, b, i, us[i]);
+}
+
+void launch_u4_pack(const DualArgs& a, int batch, cudaStream_t s) {
+  dim3 grid(grid_for(a.m, 256, 148 * 4), batch);
+  u4_pack_kernel<<<grid, 256, 0, s>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
 int objective_blocks() { return 148; }
 
 void launch_objective(const ObjArgs& a, int batch, cudaStream_t s) {

@@ -31,6 +31,8 @@ struct DualArgs {
   size_t u4_stride = 0;  // floats per problem
 };
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
+// Rebuilds u4 from u0 (fields u0, u_stride, m, det, u4, slot, u4_row, u4_pad, u4_stride).
+void launch_u4_pack(const DualArgs& a, int batch, cudaStream_t s);
 
 struct ObjArgs {
   int kind = 0, n = 0, positivity = 0, with_grad = 1;

@@ -93,6 +93,33 @@ def test_graph_replay_equals_eager(ncsg, port):
     np.testing.assert_array_equal(p.get_state()[0], q.get_state()[0])
 
 
+def test_state_roundtrip_and_graph_after_set_state(ncsg, port):
+    """The gather adjoint reads an orbit-interleaved copy of u written by the
+    dual update; a state set from outside (set_state) must invalidate it, in
+    eager steps and in replays of an already captured graph."""
+    prob, mask, gamma = small_ct(port)
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    p.step(10)
+    x10, u10, _ = p.get_state()
+    p.step(10)
+    x20, u20, _ = p.get_state()
+    q = gpu_problem(ncsg, prob, gamma, mask)
+    q.set_state(x10, u10, 10)
+    q.step(10)
+    xq, uq, _ = q.get_state()
+    np.testing.assert_array_equal(xq, x20)
+    np.testing.assert_array_equal(uq, u20)
+    g = gpu_problem(ncsg, prob, gamma, mask)
+    g.step(3)
+    g.step(5, graph=True)  # captured with the interleaved copy fresh
+    g.set_state(x10, u10, 10)
+    g.step(5, graph=True)  # replay after an outside write
+    g.step(5, graph=True)
+    xg, ug, _ = g.get_state()
+    np.testing.assert_array_equal(xg, x20)
+    np.testing.assert_array_equal(ug, u20)
+
+
 def test_small_ct_parity_with_records(ncsg, port):
     prob, mask, gamma = small_ct(port)
     o = port.solve(prob, gamma, mask, 200, record_every=20)
