@@ -11,6 +11,7 @@
 #include <complex>
 #include <cstring>
 #include <map>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -57,17 +58,42 @@ void require_device(int device) {
 
 // Hermitian part of a full N x N complex mask, half spectrum stored [k][j]
 // (k = 0..N/2) and scaled by `scale` (the 1/N^2 of fft.cpp:46-47).
+// Rows [r0, r1) of a setup loop on all host cores (setup only).
+template <class F>
+void parallel_rows(int rows, F f) {
+  const int nt = std::max(1, std::min<int>(16, static_cast<int>(std::thread::hardware_concurrency())));
+  if (rows < 64 || nt == 1) {
+    f(0, rows);
+    return;
+  }
+  std::vector<std::thread> th;
+  const int per = (rows + nt - 1) / nt;
+  for (int t = 0; t < nt; ++t) {
+    const int r0 = t * per, r1 = std::min(rows, r0 + per);
+    if (r0 < r1) th.emplace_back(f, r0, r1);
+  }
+  for (auto& t : th) t.join();
+}
+
+// Hermitian part of h on the half spectrum, transposed to [k][j] (the
+// device's column-major half spectrum), 32 x 32 blocks so both the reads
+// (rows j and N-j of h) and the writes stay in cache.
 std::vector<float2> half_mask(int n, const std::vector<std::complex<double>>& h, double scale) {
   const int nk = n / 2 + 1;
   std::vector<float2> out(static_cast<size_t>(nk) * n);
-  for (int k = 0; k < nk; ++k)
-    for (int j = 0; j < n; ++j) {
-      std::complex<double> a = h[static_cast<size_t>(j) * n + k];
-      std::complex<double> b = h[static_cast<size_t>((n - j) % n) * n + (n - k) % n];
-      std::complex<double> v = 0.5 * (a + std::conj(b)) * scale;
-      out[static_cast<size_t>(k) * n + j] =
-          make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
-    }
+  parallel_rows((n + 31) / 32, [&](int b0, int b1) {
+    for (int jb = b0 * 32; jb < std::min(n, b1 * 32); jb += 32)
+      for (int kb = 0; kb < nk; kb += 32)
+        for (int j = jb; j < std::min(n, jb + 32); ++j) {
+          const std::complex<double>* hr = h.data() + static_cast<size_t>(j) * n;
+          const std::complex<double>* hc = h.data() + static_cast<size_t>((n - j) % n) * n;
+          for (int k = kb; k < std::min(nk, kb + 32); ++k) {
+            const std::complex<double> v = 0.5 * (hr[k] + std::conj(hc[(n - k) % n])) * scale;
+            out[static_cast<size_t>(k) * n + j] =
+                make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
+          }
+        }
+  });
   return out;
 }
 

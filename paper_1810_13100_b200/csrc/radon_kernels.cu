@@ -852,7 +852,10 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
 }
 
 template <int TW, int TH, int NB>
-__global__ void __launch_bounds__(kGaThreads) bp_gather_kernel(GaArgs a) {
+#ifndef NCSG_GA_MINB
+#define NCSG_GA_MINB 4  // 64 registers, 4 CTAs per SM (without a minimum ptxas takes 70 -> 3 CTAs; with 1, 134)
+#endif
+__global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaArgs a) {
   constexpr int PX = TW * TH / kGaThreads;
   constexpr int SW = TW + TH + 8;
   static_assert(kGaThreads % TW == 0 && kGaThreads % TH == 0, "tile rows / columns per pass");
