@@ -290,7 +290,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
 }
 
 #ifndef NCSG_FFT_COLS
-#define NCSG_FFT_COLS 4
+#define NCSG_FFT_COLS 2
 #endif
 constexpr int kColsPerBlock = NCSG_FFT_COLS;  // columns per column-pass CTA
 
