@@ -32,6 +32,10 @@ std::atomic<int64_t> g_launches{0};
 }
 int64_t launch_count() { return g_launches.load(); }
 void count_launch(int k) { g_launches += k; }
+bool pdl_enabled() {
+  static const bool on = std::getenv("NCSG_NO_PDL") == nullptr;
+  return on;
+}
 
 template <class F>
 ncsg_status guard(F&& f) {

@@ -230,6 +230,7 @@ __device__ __forceinline__ float2* fft_run(float2* a, float2* b, int nfft, const
 
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
                                     const float2* __restrict__ tw, FftShape sh) {
+  pdl_wait();
   extern __shared__ float2 zs[];
   const int n = T.n;
   const int y0 = blockIdx.x * kRowsPerBlock;
@@ -296,6 +297,7 @@ constexpr int kColsPerBlock = NCSG_FFT_COLS;  // columns per column-pass CTA
 
 __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2* __restrict__ maskT,
                                        const float2* __restrict__ tw, FftShape sh) {
+  pdl_wait();
   const int n = sh.n;
   extern __shared__ float2 zs[];
   const int k0 = blockIdx.x * kColsPerBlock;
@@ -332,6 +334,7 @@ __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
 
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
                                     const float2* __restrict__ tw, FftShape sh) {
+  pdl_wait();
   const int n = sh.n;
   extern __shared__ float2 zs[];
   const int y0 = blockIdx.x * kRowsPerBlock;
@@ -470,8 +473,8 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
                                        static_cast<int>(smem)));
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   // the loader (sums of adjoint partial images) wants more threads than the FFT
-  fft_rows_r2c_kernel<<<grid, fft_threads(kRowsPerBlock * n / 4), smem, s>>>(
-      terms, specT, f.tw.p, f.shape);
+  launch_pdl(fft_rows_r2c_kernel, grid, dim3(fft_threads(kRowsPerBlock * n / 4)), smem, s, terms,
+             specT, f.tw.p, f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -484,8 +487,8 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
-  fft_cols_filter_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, maskT, f.tw.p,
-                                                                               f.shape);
+  launch_pdl(fft_cols_filter_kernel, grid, dim3(fft_threads(kColsPerBlock * n / 8)), smem, s,
+             specT, maskT, f.tw.p, f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -511,8 +514,8 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
-  fft_rows_c2r_kernel<<<grid, fft_threads((kRowsPerBlock / 2) * n / 4), smem, s>>>(
-      specT, xu, f.tw.p, f.shape);
+  launch_pdl(fft_rows_c2r_kernel, grid, dim3(fft_threads((kRowsPerBlock / 2) * n / 4)), smem, s,
+             specT, xu, f.tw.p, f.shape);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

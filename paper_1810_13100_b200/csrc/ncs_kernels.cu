@@ -47,6 +47,7 @@ __device__ __forceinline__ void put_u4(const DualArgs& a, int b, size_t i, float
 }
 
 __global__ void dual_update_kernel(DualArgs a) {
+  pdl_wait();
   const int b = blockIdx.z;
   const int section = blockIdx.y;
   const float alpha = a.alpha;
@@ -348,7 +349,7 @@ __global__ void stacked_rest_kernel(StackArgs a) {
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
   size_t big = std::max<size_t>(a.m_end - a.m_begin, 2 * static_cast<size_t>(a.n) * a.n);
   dim3 grid(grid_for(big, 256, 148 * NCSG_DUAL_WAVES), a.positivity ? 3 : 2, batch);
-  dual_update_kernel<<<grid, 256, 0, s>>>(a);
+  launch_pdl(dual_update_kernel, grid, dim3(256), 0, s, a);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

@@ -28,6 +28,30 @@ struct Error {
       throw ::ncsg::Error{NCSG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)}; \
   } while (0)
 
+// ------------------------------------------------- programmatic launches
+// The NCS step's kernels are launched with programmatic stream serialization
+// (PDL): each may be scheduled while its predecessor drains and waits in
+// pdl_wait() -- its first statement, before any global access -- until the
+// predecessor has completed and its writes are visible. NCSG_NO_PDL=1 turns
+// it off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
+
 // ------------------------------------------------------------- geometry
 // Fixed-point sample positions: value * 2^-32 pixels, int64.  The lattice
 // point (s, tau) of angle t sits at

@@ -464,6 +464,7 @@ size_t orbit_smem(int rmax) {
 template <bool USE_TMA>
 __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
     fp_orbit_kernel(OrbArgs a, const __grid_constant__ CUtensorMap map) {
+  pdl_wait();
   constexpr int W = kOrbW, T = kOrbT, P = kOrbP, NW = kOrbWarps;
   constexpr int ROWS = T + 4;
   // D cells of zeroed slack, then the (T+4) x P tile of cells. TMA box starts
@@ -657,6 +658,7 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
 // 32 x 32 output blocks; the three transposed/flipped sources are staged
 // through shared memory so every global read and write is coalesced.
 __global__ void make_quad_kernel(const float* x, float4* quad, int n) {
+  pdl_wait();
   __shared__ float t1[32][33], t3[32][33];
   const size_t nn = static_cast<size_t>(n) * n;
   const int b = blockIdx.z;
@@ -856,6 +858,7 @@ template <int TW, int TH, int NB>
 #define NCSG_GA_MINB 4  // 64 registers, 4 CTAs per SM (without a minimum ptxas takes 70 -> 3 CTAs; with 1, 134)
 #endif
 __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaArgs a) {
+  pdl_wait();
   constexpr int PX = TW * TH / kGaThreads;
   constexpr int SW = TW + TH + 8;
   static_assert(kGaThreads % TW == 0 && kGaThreads % TH == 0, "tile rows / columns per pass");
@@ -1380,10 +1383,10 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     if (tma) {
       set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<true>), smem);
-      fp_orbit_kernel<true><<<grid, kOrbWarps * 32, smem, s>>>(a, map);
+      launch_pdl(fp_orbit_kernel<true>, grid, dim3(kOrbWarps * 32), smem, s, a, map);
     } else {
       set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<false>), smem);
-      fp_orbit_kernel<false><<<grid, kOrbWarps * 32, smem, s>>>(a, map);
+      launch_pdl(fp_orbit_kernel<false>, grid, dim3(kOrbWarps * 32), smem, s, a, map);
     }
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
@@ -1463,7 +1466,7 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     a.u4_row = r.u4_row();
     a.u4_pad = kGaSW;
     dim3 grid((n + kGaTW - 1) / kGaTW, (n + kGaTH - 1) / kGaTH, a.n_chunks * batch);
-    bp_gather_kernel<kGaTW, kGaTH, kGaBatch><<<grid, kGaThreads, 0, s>>>(a);
+    launch_pdl(bp_gather_kernel<kGaTW, kGaTH, kGaBatch>, grid, dim3(kGaThreads), 0, s, a);
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
     return;
@@ -1500,7 +1503,7 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
 
 void launch_make_planes(const float* x, float* planes, int n, int batch, cudaStream_t s) {
   dim3 grid((n + 31) / 32, (n + 31) / 32, batch);
-  make_quad_kernel<<<grid, dim3(32, 8), 0, s>>>(x, reinterpret_cast<float4*>(planes), n);
+  launch_pdl(make_quad_kernel, grid, dim3(32, 8), 0, s, x, reinterpret_cast<float4*>(planes), n);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
