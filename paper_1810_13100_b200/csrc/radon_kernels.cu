@@ -17,7 +17,12 @@
 //     columns, kFpWarps angles), one angle per warp, class-H angles on x^T.
 //     Both write per-(ray, strip[, segment]) partial sums that the consumer
 //     adds in a fixed order (deterministic, no atomics).
-// R^T (bp_tile_kernel):  CTA = (W x T output tile, chunk of angles).
+// R^T (bp_gather_kernel, orbit mode): pixel-driven gather -- each thread
+//     owns pixels of a 32 x 32 tile and sums, per orbit, the <= 9 lattice
+//     samples within one pixel of them (tent weights shared by the four
+//     member angles, member weights staged per tile with cp.async); border
+//     pixels are corrected against the replayed ray ranges.  See the kernel.
+// R^T (bp_tile_kernel, per-angle mode): CTA = (W x T output tile, chunk of angles).
 //     Each warp owns a private shared-memory accumulator of the tile plus a
 //     halo and scatters w * bilinear weights (radon.cpp:116-125) with plain
 //     read-modify-write; lanes of one phase take rays `bp_stride` >= 3 apart
