@@ -1097,6 +1097,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       p->radon = std::make_unique<RadonDev>();
       p->radon->geo = std::move(geo);
       p->radon->device = d.device;
+      p->radon->batch_hint = d.batch;
       p->radon->upload();
       clk.mark("upload");
       p->radon->plan_adjoint(d.batch);

@@ -269,6 +269,8 @@ struct RadonDev {
   // ray's partial sums land in the slot of its monotone staircase path.
   bool orbit_mode = false;
   int n_segs = 1;
+  int orb_seg = 64;      // rows per forward segment (upload chooses 32 or 64)
+  int batch_hint = 1;    // problems per launch the plan is sized for (set before upload)
   int orb_rmax = 0;
   DevBuf<OrbitGeom> orbits;
   DevBuf<int2> orb_range;                     // [orbit][strip][seg] s-range

@@ -367,14 +367,10 @@ constexpr int kOrbW = 128;   // strip width
 #ifndef NCSG_ORB_T
 #define NCSG_ORB_T 32
 #endif
-#ifndef NCSG_ORB_SEG
-#define NCSG_ORB_SEG 64
-#endif
 #ifndef NCSG_ORB_WARPS
 #define NCSG_ORB_WARPS 8
 #endif
 constexpr int kOrbT = NCSG_ORB_T;          // tile-row height
-constexpr int kOrbSeg = NCSG_ORB_SEG;      // rows per segment (one CTA sweeps one segment)
 constexpr int kOrbWarps = NCSG_ORB_WARPS;  // orbits per CTA (one per warp)
 #ifndef NCSG_ORB_P
 #define NCSG_ORB_P (kOrbW + 8)
@@ -390,6 +386,7 @@ struct OrbArgs {
   const float4* quad;         // [batch][n][n] (x, x1, x2, x3) per pixel (make_quad_kernel)
   float* part;                // [batch][slots][m]
   int n, det, s_mid, s_lo, n_strips, n_segs, slots, rmax;
+  int seg_tiles;              // tile rows per segment (one CTA sweeps one segment)
   long long P0;
   size_t nn, m;
 };
@@ -497,8 +494,8 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
   const int n = a.n;
   const float c = 0.5f * (n - 1);
   const int n_rows = (n + T - 1) / T;
-  const int r_begin = seg * (kOrbSeg / T);
-  const int r_end = min(n_rows, r_begin + kOrbSeg / T);
+  const int r_begin = seg * a.seg_tiles;
+  const int r_end = min(n_rows, r_begin + a.seg_tiles);
   const float4* quad = a.quad + static_cast<size_t>(b) * a.nn;
   const unsigned barA = static_cast<unsigned>(__cvta_generic_to_shared(&bar));
   const unsigned tile0 = sm_addr + pad;
@@ -1167,7 +1164,18 @@ void RadonDev::upload() {
   orbit_mode = false;
   if (!geo.orbits.empty() && !getenv("NCSG_NO_ORBIT")) {
     const int ns = (n + kOrbW - 1) / kOrbW;
-    n_segs = (n + kOrbSeg - 1) / kOrbSeg;
+    // Segment height: 32-row segments (one tile row per CTA) when 64-row
+    // segments give fewer than ~8 waves of the 2 resident CTAs per SM -- the
+    // wave quantisation of a 2.5-wave grid costs more than the extra partial
+    // slots (C3: forward 0.222 -> 0.201 ms, C1 0.061 -> 0.036 ms); 64 rows
+    // otherwise (C4, C5: fewer slots for the dual update to sum).
+    const long ctas64 = static_cast<long>(ns) * ((n + 63) / 64) *
+                        ((static_cast<long>(geo.orbits.size()) + kOrbWarps - 1) / kOrbWarps) *
+                        batch_hint;
+    orb_seg = ctas64 < 8L * 148 * 2 ? kOrbT : 2 * kOrbT;
+    if (const char* e = getenv("NCSG_ORB_SEG_ROWS")) orb_seg = std::max(kOrbT, atoi(e) / kOrbT * kOrbT);
+    const int seg_rows = orb_seg;
+    n_segs = (n + seg_rows - 1) / seg_rows;
     std::vector<int2> orr(geo.orbits.size() * ns * n_segs);
     int rmax = 1;
     for (size_t oi = 0; oi < geo.orbits.size(); ++oi) {
@@ -1177,7 +1185,7 @@ void RadonDev::upload() {
       for (int st = 0; st < ns; ++st)
         for (int sg = 0; sg < n_segs; ++sg) {
           double x0 = st * kOrbW - 3.0, x1 = st * kOrbW + kOrbW + 3.0;
-          double y0 = sg * kOrbSeg - 3.0, y1 = sg * kOrbSeg + kOrbSeg + 3.0;
+          double y0 = sg * seg_rows - 3.0, y1 = sg * seg_rows + seg_rows + 3.0;
           double p = (x0 - c) * ax, q = (x1 - c) * ax, e = (y0 - c) * ay, f = (y1 - c) * ay;
           int lo = std::max(-geo.s_mid, static_cast<int>(std::floor(std::min(p, q) + std::min(e, f))) - 2);
           int hi = std::min(geo.s_mid, static_cast<int>(std::ceil(std::max(p, q) + std::max(e, f))) + 2);
@@ -1377,6 +1385,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     a.s_lo = -g.s_mid;
     a.n_strips = r.n_strips;
     a.n_segs = r.n_segs;
+    a.seg_tiles = r.orb_seg / kOrbT;
     a.slots = r.fp_slots();
     a.rmax = r.orb_rmax;
     a.P0 = g.P0;
