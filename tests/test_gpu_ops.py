@@ -63,6 +63,28 @@ def test_gather_adjoint_border_pixels(ncsg, port, n, A, D):
     assert rel(got, scat) <= TOL
 
 
+@pytest.mark.parametrize("knob,values", [("NCSG_ORB_SEG_ROWS", ["32", "64", "96"]),
+                                         ("NCSG_GA_CHUNKS", ["1", "3", "7", "12"])])
+def test_projector_sizing_knobs(ncsg, port, knob, values):
+    """The launch-shape choices (forward segment height, adjoint orbit
+    chunks) only change the partial-sum grouping: every setting matches the
+    oracle."""
+    import os
+    n, A, D = 160, 48, 229
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((n, n))
+    u = rng.standard_normal((A, D))
+    ref_f, ref_a = port.radon_forward(x, A, D), port.radon_adjoint(u, n)
+    for v in values:
+        os.environ[knob] = v
+        try:
+            R = ncsg.RadonMap(n, A, D)
+            assert rel(R.forward(x), ref_f) <= TOL, (knob, v)
+            assert rel(R.adjoint(u), ref_a) <= TOL, (knob, v)
+        finally:
+            del os.environ[knob]
+
+
 @pytest.mark.parametrize("name", ["c1", "c3", "c5"])
 def test_radon_config_sizes(ncsg, port, name):
     from paper_1810_13100_b200 import configs
