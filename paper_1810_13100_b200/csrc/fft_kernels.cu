@@ -307,9 +307,34 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   float2* col = specT + (static_cast<size_t>(b) * nk + k0) * n;  // nc contiguous columns
   const float2* mk = maskT + static_cast<size_t>(k0) * n;
   float2* zb = zs + kColsPerBlock * n;
-  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) zs[j] = col[j];
+  // the filter goes to the scratch half now, so its load overlaps the
+  // column load instead of stalling between the two transforms
+  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) {
+    zs[j] = col[j];
+    zb[j] = __ldg(mk + j);
+  }
+  __syncthreads();
+  // the forward transform reuses zb as scratch: each thread keeps its
+  // filter values in registers meanwhile (<= 8 per thread for every size the
+  // launch configures; larger sizes read the filter again)
+  constexpr int kMaxPer = 8;
+  float2 fr[kMaxPer];
+  const bool in_regs = nc * n <= kMaxPer * static_cast<int>(blockDim.x);
+#pragma unroll
+  for (int t = 0; t < kMaxPer; ++t) {
+    const int j = threadIdx.x + t * blockDim.x;
+    if (in_regs && j < nc * n) fr[t] = zb[j];
+  }
   float2* z = fft_run<-1>(zs, zb, nc, sh, tw);
-  for (int j = threadIdx.x; j < nc * n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
+  if (in_regs) {
+#pragma unroll
+    for (int t = 0; t < kMaxPer; ++t) {
+      const int j = threadIdx.x + t * blockDim.x;
+      if (j < nc * n) z[j] = cmul(z[j], fr[t]);
+    }
+  } else {
+    for (int j = threadIdx.x; j < nc * n; j += blockDim.x) z[j] = cmul(z[j], __ldg(mk + j));
+  }
   z = fft_run<+1>(z, z == zs ? zb : zs, nc, sh, tw);
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
@@ -343,6 +368,20 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   const size_t nn = static_cast<size_t>(n) * n;
   const float2* in = specT + static_cast<size_t>(b) * nk * n;
   float2* zb = zs + (kRowsPerBlock / 2) * n;  // Stockham scratch
+  // x (to be updated) streams into shared memory with cp.async now, so its
+  // latency overlaps the spectrum load and the transform
+  float* xs = reinterpret_cast<float*>(zs + kRowsPerBlock * n);
+  const bool x_pre = xu.subtract && (n & 3) == 0;
+  if (x_pre) {
+    for (int i = threadIdx.x; i < kRowsPerBlock * n / 4; i += blockDim.x) {
+      const int r = (4 * i) / n, x = 4 * i - r * n;
+      if (y0 + r >= n) continue;
+      const float* src = xu.x + b * nn + static_cast<size_t>(y0 + r) * n + x;
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(xs + 4 * i));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
   // Build Z = G_a + i G_b with Hermitian extension (G_r[n-k] = conj G_r[k]).
   for (int i = threadIdx.x; i < nk * kRowsPerBlock; i += blockDim.x) {
     const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
@@ -381,7 +420,30 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   float2* z = fft_run<+1>(zs, zb, kRowsPerBlock / 2, sh, tw);
   // x update, row-major.
   int bad = 0;
-  for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
+  if (x_pre) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < kRowsPerBlock * n && x_pre; i += blockDim.x) {
+    const int r = i / n, x = i - r * n;
+    const int y = y0 + r;
+    if (y >= n) continue;
+    const float2 zz = z[(r >> 1) * n + x];
+    const float w = (r & 1) ? zz.y : zz.x;
+    const size_t gi = b * nn + static_cast<size_t>(y) * n + x;
+    const float xo = xs[i];
+    if (xu.x_old) xu.x_old[gi] = xo;
+    const float xn = xo - w;
+    xu.x[gi] = xn;
+    bad |= !isfinite(xn);
+    if (xu.xT) {
+      if (r & 1)
+        z[(r >> 1) * n + x].y = xn;
+      else
+        z[(r >> 1) * n + x].x = xn;
+    }
+  }
+  for (int i = threadIdx.x; i < kRowsPerBlock * n && !x_pre; i += blockDim.x) {
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
     if (y >= n) continue;
@@ -509,7 +571,7 @@ void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStr
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s) {
   const int n = f.n;
-  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
+  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n + sizeof(float) * kRowsPerBlock * n;
   NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_rows_c2r_kernel,
                                        cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        static_cast<int>(smem)));
