@@ -85,6 +85,20 @@ def test_projector_sizing_knobs(ncsg, port, knob, values):
             del os.environ[knob]
 
 
+def test_radon_batched_multi_chunk(ncsg, port):
+    """Batched operators with several orbit chunks per problem (the gather's
+    partial images and tile bookkeeping are per batch element)."""
+    n, A, D = 96, 40, 137
+    rng = np.random.default_rng(9)
+    x = rng.standard_normal((3, n, n))
+    u = rng.standard_normal((3, A, D))
+    R = ncsg.RadonMap(n, A, D)
+    fx, au = R.forward(x), R.adjoint(u)
+    for q in range(3):
+        assert rel(fx[q], port.radon_forward(x[q], A, D)) <= TOL
+        assert rel(au[q], port.radon_adjoint(u[q], n)) <= TOL
+
+
 @pytest.mark.parametrize("name", ["c1", "c3", "c5"])
 def test_radon_config_sizes(ncsg, port, name):
     from paper_1810_13100_b200 import configs
