@@ -82,17 +82,19 @@ void parallel_rows(int rows, F f) {
 // Hermitian part of h on the half spectrum, transposed to [k][j] (the
 // device's column-major half spectrum), 32 x 32 blocks so both the reads
 // (rows j and N-j of h) and the writes stay in cache.
-std::vector<float2> half_mask(int n, const std::vector<std::complex<double>>& h, double scale) {
+// h given as a function of the flat bin index (no n^2 temporary).
+template <class F>
+std::vector<float2> half_mask_f(int n, F h, double scale) {
   const int nk = n / 2 + 1;
   std::vector<float2> out(static_cast<size_t>(nk) * n);
   parallel_rows((n + 31) / 32, [&](int b0, int b1) {
     for (int jb = b0 * 32; jb < std::min(n, b1 * 32); jb += 32)
       for (int kb = 0; kb < nk; kb += 32)
         for (int j = jb; j < std::min(n, jb + 32); ++j) {
-          const std::complex<double>* hr = h.data() + static_cast<size_t>(j) * n;
-          const std::complex<double>* hc = h.data() + static_cast<size_t>((n - j) % n) * n;
+          const size_t hr = static_cast<size_t>(j) * n;
+          const size_t hc = static_cast<size_t>((n - j) % n) * n;
           for (int k = kb; k < std::min(nk, kb + 32); ++k) {
-            const std::complex<double> v = 0.5 * (hr[k] + std::conj(hc[(n - k) % n])) * scale;
+            const std::complex<double> v = 0.5 * (h(hr + k) + std::conj(h(hc + (n - k) % n))) * scale;
             out[static_cast<size_t>(k) * n + j] =
                 make_float2(static_cast<float>(v.real()), static_cast<float>(v.imag()));
           }
@@ -100,27 +102,14 @@ std::vector<float2> half_mask(int n, const std::vector<std::complex<double>>& h,
   });
   return out;
 }
+std::vector<float2> half_mask(int n, const std::vector<std::complex<double>>& h, double scale) {
+  return half_mask_f(n, [&](size_t i) { return h[i]; }, scale);
+}
 
 std::vector<std::complex<double>> read_mask(int n, const double* m) {
   std::vector<std::complex<double>> h(static_cast<size_t>(n) * n);
   for (size_t i = 0; i < h.size(); ++i) h[i] = {m[2 * i], m[2 * i + 1]};
   return h;
-}
-
-// pinv_mask (circulant.cpp:47-55)
-std::vector<std::complex<double>> pinv(const std::vector<std::complex<double>>& h,
-                                       double rel_tol) {
-  // |h| compared squared and 1/h = conj(h) / |h|^2: the same filter to fp32
-  // without hypot and the libgcc complex division per bin.
-  double hmax2 = 0.0;
-  for (const auto& z : h) hmax2 = std::max(hmax2, std::norm(z));
-  std::vector<std::complex<double>> out(h.size());
-  const double cutoff2 = rel_tol * rel_tol * hmax2;
-  for (size_t i = 0; i < h.size(); ++i) {
-    const double a = h[i].real(), b = h[i].imag(), d = a * a + b * b;
-    out[i] = d > cutoff2 ? std::complex<double>(a / d, -b / d) : 0.0;
-  }
-  return out;
 }
 
 struct Stream {
@@ -1113,27 +1102,48 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     clk.mark("stream");
     p->fft.init(d.n, s);
     clk.mark("fft plan");
-    // Engine::Engine (solvers.cpp:93-99): m = gamma + alpha C, m_pinv = pinv(m).
-    std::vector<std::complex<double>> minv;
+    // Engine::Engine (solvers.cpp:93-99): m = gamma + alpha C, m_pinv = pinv(m)
+    // (pinv_mask, circulant.cpp:47-55: 1/m where |m| > tol max|m|, else 0;
+    // |m| compared squared and 1/m = conj(m)/|m|^2, the same filter to fp32).
+    std::vector<float2> hm;  // herm(pinv(gamma + alpha C)) / N^2 on the half spectrum
     const double scale = 1.0 / (static_cast<double>(d.n) * d.n);
     if (desc->mask) {
       p->has_mask = true;
       p->mask_full = read_mask(d.n, desc->mask);
-      std::vector<std::complex<double>> m(p->mask_full.size());
-      for (size_t i = 0; i < m.size(); ++i) m[i] = d.gamma + d.alpha * p->mask_full[i];
-      double tol = d.pinv_rel_tol > 0 ? d.pinv_rel_tol : 1e-12;
-      minv = pinv(m, tol);
+      clk.mark("  read mask");
+      // m = gamma + alpha C and its pinv, bin by bin (no n^2 temporaries):
+      // max |m|^2 first, then the filter's half spectrum straight from it
+      const double tol = d.pinv_rel_tol > 0 ? d.pinv_rel_tol : 1e-12;
+      const std::vector<std::complex<double>>& C = p->mask_full;
+      const double ga = d.gamma, al = d.alpha;
+      std::vector<double> part_max(64, 0.0);
+      std::atomic<int> slot{0};
+      parallel_rows(d.n, [&](int r0, int r1) {
+        double mx = 0.0;
+        for (size_t i = static_cast<size_t>(r0) * d.n; i < static_cast<size_t>(r1) * d.n; ++i)
+          mx = std::max(mx, std::norm(ga + al * C[i]));
+        part_max[slot++ % 64] = mx;
+      });
+      double hmax2 = 0.0;
+      for (double v : part_max) hmax2 = std::max(hmax2, v);
+      const double cutoff2 = tol * tol * hmax2;
+      hm = half_mask_f(d.n, [&](size_t i) {
+        const std::complex<double> z = ga + al * C[i];
+        const double a = z.real(), bq = z.imag(), q = a * a + bq * bq;
+        return q > cutoff2 ? std::complex<double>(a / q, -bq / q) : std::complex<double>(0.0);
+      }, scale);
+      clk.mark("  pinv");
       auto ho = half_mask(d.n, p->mask_full, scale);
+      clk.mark("  half spectrum");
       p->maskT_orig.alloc(ho.size());
       NCSG_CUDA_CHECK(cudaMemcpy(p->maskT_orig.p, ho.data(), ho.size() * sizeof(float2),
                                  cudaMemcpyHostToDevice));
     } else {
       // pdhg: M = gamma I -> w = atu / gamma (solvers.cpp:133-137), applied
       // through the same filter path with a constant spectrum.
-      minv.assign(p->nn, std::complex<double>(1.0 / d.gamma, 0.0));
+      hm = half_mask_f(d.n, [&](size_t) { return std::complex<double>(1.0 / d.gamma, 0.0); }, scale);
     }
     clk.mark("mask pinv");
-    auto hm = half_mask(d.n, minv, scale);
     p->maskT.alloc(hm.size());
     NCSG_CUDA_CHECK(cudaMemcpy(p->maskT.p, hm.data(), hm.size() * sizeof(float2),
                                cudaMemcpyHostToDevice));
