@@ -160,8 +160,9 @@ def cpu_reference_rate(cfg, b, mask, iters_hi=3, iters_lo=1):
         import multiprocessing as mp
 
         P = max(1, min(cfg.batch, len(os.sched_getaffinity(0))))
-        bb = np.asarray(b).reshape(cfg.batch, -1)
-        jobs = [(cfg.name, q, bb[q], mask, iters_hi, iters_lo) for q in range(P)]
+        m = cfg.angles * cfg.det if cfg.kind == "ct" else cfg.n * cfg.n
+        bb = np.asarray(b).reshape(-1, m)  # the batch, or one instance (reference arm)
+        jobs = [(cfg.name, q, bb[q % len(bb)], mask, iters_hi, iters_lo) for q in range(P)]
         with mp.get_context("spawn").Pool(P) as pool:
             res = pool.map(_ref_problem_rate, jobs)
         rate = sum(1.0 / r[0] for r in res)
