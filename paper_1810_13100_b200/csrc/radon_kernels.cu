@@ -501,7 +501,10 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
   const unsigned tile0 = sm_addr + pad;
   constexpr unsigned kBytes = ROWS * P * 16;
   if (USE_TMA) {
-    for (int i = threadIdx.x; i < 4 * kOrbTile; i += NW * 32) tiles[i] = 0.f;
+    // only the slack before the box and the padding after it: every box load
+    // writes all of its ROWS x P cells (zeros outside the image)
+    for (int i = threadIdx.x; i < 4 * kOrbTile; i += NW * 32)
+      if (i < 4 * D || i >= 4 * (D + ROWS * P)) tiles[i] = 0.f;
     if (threadIdx.x == 0) {
       mbar_init(barA, 1);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
