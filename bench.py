@@ -454,12 +454,13 @@ def e2e_rate(cfg, b, mask, steps):
     iters = cfg.iters
     make = ncsg.ct_problem if cfg.kind == "ct" else ncsg.denoise_problem
     runs = []
-    for _ in range(3):  # median of three full calls (host-side setup varies run to run)
+    for k in range(6):  # one untimed warm-up call, then the median of five
         t = time.perf_counter()
         prob = make(cfg, b, mask=mask)
         prob.set_state()
         res = prob.solve(iters, record_every=iters)
-        runs.append(time.perf_counter() - t)
+        if k:
+            runs.append(time.perf_counter() - t)
         del prob
     dt = statistics.median(runs)
     nk = cfg.n // 2 + 1
@@ -471,7 +472,7 @@ def e2e_rate(cfg, b, mask, steps):
             "d2h_bytes_per_step": d2h / iters, "iters": iters, "seconds": dt,
             "seconds_runs": runs,
             "note": f"ncsg.Problem create + set_state + solve({iters}) + state/records download, "
-                    "wall clock, median of 3 calls"}
+                    "wall clock, median of 5 calls after one untimed warm-up call"}
 
 
 if __name__ == "__main__":
