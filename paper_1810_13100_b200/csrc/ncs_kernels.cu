@@ -63,16 +63,44 @@ __global__ void dual_update_kernel(DualArgs a) {
       float* us = a.u0 + b * a.u_stride;
       float* ax = a.axs + b * a.m;
       const float* bb = a.b + b * a.m;
-      for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
-        if (a.own && !a.own[i / a.det]) continue;  // another shard's orbit
-        float rx = 0.f;
-        for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
-        const float r = us[i] + alpha * (2.f * rx - ax[i] - bb[i]);
-        const float un = r * a.s_quad;
-        us[i] = un;
-        ax[i] = rx;
-        bad |= isnan(un);
-        if (a.u4) put_u4(a, b, i, un);
+      if (!a.own && ((a.m | a.m_begin | a.m_end | a.u_stride) & 3) == 0) {
+        // four rays per thread, float4 loads of every partial slot
+        for (size_t i = a.m_begin + 4 * i0; i < a.m_end; i += 4 * stride) {
+          float4 rx = make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int k = 0; k < a.n_strips; ++k) {
+            const float4 q = *reinterpret_cast<const float4*>(part + k * a.m + i);
+            rx.x += q.x, rx.y += q.y, rx.z += q.z, rx.w += q.w;
+          }
+          const float4 uo = *reinterpret_cast<const float4*>(us + i);
+          const float4 ao = *reinterpret_cast<const float4*>(ax + i);
+          const float4 bo = *reinterpret_cast<const float4*>(bb + i);
+          float4 un;
+          un.x = (uo.x + alpha * (2.f * rx.x - ao.x - bo.x)) * a.s_quad;
+          un.y = (uo.y + alpha * (2.f * rx.y - ao.y - bo.y)) * a.s_quad;
+          un.z = (uo.z + alpha * (2.f * rx.z - ao.z - bo.z)) * a.s_quad;
+          un.w = (uo.w + alpha * (2.f * rx.w - ao.w - bo.w)) * a.s_quad;
+          *reinterpret_cast<float4*>(us + i) = un;
+          *reinterpret_cast<float4*>(ax + i) = rx;
+          bad |= isnan(un.x) || isnan(un.y) || isnan(un.z) || isnan(un.w);
+          if (a.u4) {
+            put_u4(a, b, i, un.x);
+            put_u4(a, b, i + 1, un.y);
+            put_u4(a, b, i + 2, un.z);
+            put_u4(a, b, i + 3, un.w);
+          }
+        }
+      } else {
+        for (size_t i = a.m_begin + i0; i < a.m_end; i += stride) {
+          if (a.own && !a.own[i / a.det]) continue;  // another shard's orbit
+          float rx = 0.f;
+          for (int k = 0; k < a.n_strips; ++k) rx += part[k * a.m + i];
+          const float r = us[i] + alpha * (2.f * rx - ax[i] - bb[i]);
+          const float un = r * a.s_quad;
+          us[i] = un;
+          ax[i] = rx;
+          bad |= isnan(un);
+          if (a.u4) put_u4(a, b, i, un);
+        }
       }
     } else if (a.kind == NCSG_PET) {
       // PoissonConj block (pipeline.cpp:86-88): offset 0, counts in b,
