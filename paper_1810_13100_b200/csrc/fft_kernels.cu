@@ -397,40 +397,27 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   }
-  // Build Z = G_a + i G_b with Hermitian extension (G_r[n-k] = conj G_r[k]).
-  for (int i = threadIdx.x; i < nk * kRowsPerBlock; i += blockDim.x) {
-    const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
-    const int y = y0 + r;
-    const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
-    float2* zq = zs + (r >> 1) * n;
-    const unsigned ik = k;
-    const unsigned im = (n - k) % n;
-    if ((r & 1) == 0) {
-      // a part: Z[k] += G_a[k], Z[n-k] += conj(G_a[k])
-      zq[ik].x = g.x;
-      zq[ik].y = g.y;
-      if (k > 0 && 2 * k != n) {
-        zq[im].x = g.x;
-        zq[im].y = -g.y;
+  // Build Z = G_a + i G_b with Hermitian extension (G_r[n-k] = conj G_r[k]):
+  // one thread per (row pair, k) reads both rows' bins as one float4 and
+  // writes Z[k] and Z[n-k] (no other thread touches them).
+  for (int i = threadIdx.x; i < nk * (kRowsPerBlock / 2); i += blockDim.x) {
+    const int k = i / (kRowsPerBlock / 2), q = i - k * (kRowsPerBlock / 2);
+    const int y = y0 + 2 * q;
+    float4 g = make_float4(0.f, 0.f, 0.f, 0.f);  // (G_a, G_b) of rows y, y + 1
+    const float2* src = in + static_cast<size_t>(k) * n + y;
+    if (y + 1 < n && (n & 1) == 0) {  // 16-byte aligned pair
+      g = *reinterpret_cast<const float4*>(src);
+    } else if (y < n) {
+      const float2 ga = src[0];
+      g.x = ga.x, g.y = ga.y;
+      if (y + 1 < n) {
+        const float2 gb = src[1];
+        g.z = gb.x, g.w = gb.y;
       }
     }
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nk * kRowsPerBlock; i += blockDim.x) {
-    const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
-    const int y = y0 + r;
-    if ((r & 1) == 0) continue;
-    const float2 g = y < n ? in[static_cast<size_t>(k) * n + y] : make_float2(0.f, 0.f);
-    float2* zq = zs + (r >> 1) * n;
-    const unsigned ik = k;
-    const unsigned im = (n - k) % n;
-    // b part: Z[k] += i G_b[k], Z[n-k] += i conj(G_b[k])
-    zq[ik].x -= g.y;
-    zq[ik].y += g.x;
-    if (k > 0 && 2 * k != n) {
-      zq[im].x += g.y;
-      zq[im].y += g.x;
-    }
+    float2* zq = zs + q * n;
+    zq[k] = make_float2(g.x - g.w, g.y + g.z);
+    if (k > 0 && 2 * k != n) zq[n - k] = make_float2(g.x + g.w, g.z - g.y);
   }
   float2* z = fft_run<+1>(zs, zb, kRowsPerBlock / 2, sh, tw);
   // x update, row-major.
