@@ -289,19 +289,23 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
   // B = (Z_k - conj Z_-k)/(2i); write specT[k][y] (k = 0..n/2).
   const int nk = n / 2 + 1;
   float2* out = specT + static_cast<size_t>(b) * nk * n;
-  for (int i = threadIdx.x; i < nk * kRowsPerBlock; i += blockDim.x) {
-    const int k = i / kRowsPerBlock, r = i - k * kRowsPerBlock;
-    const int y = y0 + r;
+  // one thread per (row pair, k): both rows' bins leave as one float4 (even n)
+  for (int i = threadIdx.x; i < nk * (kRowsPerBlock / 2); i += blockDim.x) {
+    const int k = i / (kRowsPerBlock / 2), q = i - k * (kRowsPerBlock / 2);
+    const int y = y0 + 2 * q;
     if (y >= n) continue;
-    const float2* zq = z + (r >> 1) * n;
+    const float2* zq = z + q * n;
     const float2 zk = zq[k];
     const float2 zm = zq[(n - k) % n];
-    float2 v;
-    if (r & 1)
-      v = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-    else
-      v = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
-    out[static_cast<size_t>(k) * n + y] = v;
+    const float2 va = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    const float2 vb = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    float2* dst = out + static_cast<size_t>(k) * n + y;
+    if (y + 1 < n && (n & 1) == 0) {
+      *reinterpret_cast<float4*>(dst) = make_float4(va.x, va.y, vb.x, vb.y);
+    } else {
+      dst[0] = va;
+      if (y + 1 < n) dst[1] = vb;
+    }
   }
 }
 
