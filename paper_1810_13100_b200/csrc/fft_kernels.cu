@@ -444,23 +444,29 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     asm volatile("cp.async.wait_group 0;" ::: "memory");
     __syncthreads();
   }
-  for (int i = threadIdx.x; i < kRowsPerBlock * n && x_pre; i += blockDim.x) {
+  // four pixels per thread (x_pre implies n % 4 == 0): float4 in and out
+  for (int i4 = threadIdx.x; i4 < kRowsPerBlock * n / 4 && x_pre; i4 += blockDim.x) {
+    const int i = 4 * i4;
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
     if (y >= n) continue;
-    const float2 zz = z[(r >> 1) * n + x];
-    const float w = (r & 1) ? zz.y : zz.x;
+    float2* zr = z + (r >> 1) * n + x;
+    const float4 xo = *reinterpret_cast<const float4*>(xs + i);
     const size_t gi = b * nn + static_cast<size_t>(y) * n + x;
-    const float xo = xs[i];
-    if (xu.x_old) xu.x_old[gi] = xo;
-    const float xn = xo - w;
-    xu.x[gi] = xn;
-    bad |= !isfinite(xn);
+    float4 xn;
+    if (r & 1)
+      xn = make_float4(xo.x - zr[0].y, xo.y - zr[1].y, xo.z - zr[2].y, xo.w - zr[3].y);
+    else
+      xn = make_float4(xo.x - zr[0].x, xo.y - zr[1].x, xo.z - zr[2].x, xo.w - zr[3].x);
+    if (xu.x_old) *reinterpret_cast<float4*>(xu.x_old + gi) = xo;
+    *reinterpret_cast<float4*>(xu.x + gi) = xn;
+    bad |= !isfinite(xn.x) || !isfinite(xn.y) || !isfinite(xn.z) || !isfinite(xn.w);
     if (xu.xT) {
-      if (r & 1)
-        z[(r >> 1) * n + x].y = xn;
-      else
-        z[(r >> 1) * n + x].x = xn;
+      if (r & 1) {
+        zr[0].y = xn.x, zr[1].y = xn.y, zr[2].y = xn.z, zr[3].y = xn.w;
+      } else {
+        zr[0].x = xn.x, zr[1].x = xn.y, zr[2].x = xn.z, zr[3].x = xn.w;
+      }
     }
   }
   for (int i = threadIdx.x; i < kRowsPerBlock * n && !x_pre; i += blockDim.x) {
