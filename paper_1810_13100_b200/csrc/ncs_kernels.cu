@@ -127,24 +127,58 @@ __global__ void dual_update_kernel(DualArgs a) {
     } else {
       float* ud = a.u0 + b * a.u_stride;
       const float* bb = a.b + b * nn;
-      for (size_t i = i0; i < nn; i += stride) {
-        const float r = ud[i] + alpha * (2.f * x[i] - xo[i] - bb[i]);
-        const float un = r * a.s_quad;
-        ud[i] = un;
-        bad |= isnan(un);
+      if (((nn | a.u_stride) & 3) == 0) {  // four pixels per thread, float4
+        for (size_t i = 4 * i0; i < nn; i += 4 * stride) {
+          const float4 u0 = *reinterpret_cast<const float4*>(ud + i);
+          const float4 x4 = *reinterpret_cast<const float4*>(x + i);
+          const float4 o4 = *reinterpret_cast<const float4*>(xo + i);
+          const float4 b4 = *reinterpret_cast<const float4*>(bb + i);
+          float4 un;
+          un.x = (u0.x + alpha * (2.f * x4.x - o4.x - b4.x)) * a.s_quad;
+          un.y = (u0.y + alpha * (2.f * x4.y - o4.y - b4.y)) * a.s_quad;
+          un.z = (u0.z + alpha * (2.f * x4.z - o4.z - b4.z)) * a.s_quad;
+          un.w = (u0.w + alpha * (2.f * x4.w - o4.w - b4.w)) * a.s_quad;
+          *reinterpret_cast<float4*>(ud + i) = un;
+          bad |= isnan(un.x) || isnan(un.y) || isnan(un.z) || isnan(un.w);
+        }
+      } else {
+        for (size_t i = i0; i < nn; i += stride) {
+          const float r = ud[i] + alpha * (2.f * x[i] - xo[i] - bb[i]);
+          const float un = r * a.s_quad;
+          ud[i] = un;
+          bad |= isnan(un);
+        }
       }
     }
   } else if (section == 1) {
     float* ug = a.ug + b * a.u_stride;
     const size_t g = 2 * static_cast<size_t>(a.n) * (a.n - 1);
     const float wd = a.wd, bd = a.bound;
-    for (size_t e = i0; e < g; e += stride) {
-      const float an = wd * grad_at(x, a.n, e);
-      const float ao = wd * grad_at(xo, a.n, e);
-      const float z = ug[e] + alpha * (2.f * an - ao - 0.f);
-      const float un = z < -bd ? -bd : (z > bd ? bd : z);
-      ug[e] = un;
-      bad |= isnan(z);
+    if (((a.ug - a.u0) & 3) == 0 && (a.u_stride & 3) == 0 && (g & 3) == 0) {
+      // four edges per thread: the dual as float4, the differences per edge
+      for (size_t e = 4 * i0; e < g; e += 4 * stride) {
+        const float4 u4v = *reinterpret_cast<const float4*>(ug + e);
+        const float uo[4] = {u4v.x, u4v.y, u4v.z, u4v.w};
+        float un[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float an = wd * grad_at(x, a.n, e + q);
+          const float ao = wd * grad_at(xo, a.n, e + q);
+          const float z = uo[q] + alpha * (2.f * an - ao - 0.f);
+          un[q] = z < -bd ? -bd : (z > bd ? bd : z);
+          bad |= isnan(z);
+        }
+        *reinterpret_cast<float4*>(ug + e) = make_float4(un[0], un[1], un[2], un[3]);
+      }
+    } else {
+      for (size_t e = i0; e < g; e += stride) {
+        const float an = wd * grad_at(x, a.n, e);
+        const float ao = wd * grad_at(xo, a.n, e);
+        const float z = ug[e] + alpha * (2.f * an - ao - 0.f);
+        const float un = z < -bd ? -bd : (z > bd ? bd : z);
+        ug[e] = un;
+        bad |= isnan(z);
+      }
     }
   } else {
     float* up = a.up + b * a.u_stride;
