@@ -1261,8 +1261,8 @@ void RadonDev::plan_adjoint(int batch) {
     const long per = static_cast<long>(tiles) * batch;
     int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
     chunks = std::min(chunks, std::max(1, no / kGaBatch));
-    chunks = std::max(chunks, (no + kGaMaxChunk - 1) / kGaMaxChunk);
     if (const char* e = getenv("NCSG_GA_CHUNKS")) chunks = std::max(1, std::min(no, atoi(e)));
+    chunks = std::max(chunks, (no + kGaMaxChunk - 1) / kGaMaxChunk);  // the lowest-ray table
     bp_orbit_len = (no + chunks - 1) / chunks;
     // A chunk is staged kGaBatch orbits at a time: a nearly empty last batch
     // (C3: 18 = 16 + 2 orbits per chunk) costs a whole staging round, so such
