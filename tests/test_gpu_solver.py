@@ -297,7 +297,7 @@ def test_sharded_phases_on_one_gpu(ncsg, port):
     assert rel(u0[0, prob.m0:], uf[0, prob.m0:]) <= 5e-5
 
 
-@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("world", [2, 3, 8])
 def test_orbit_sharded_phases_on_one_gpu(ncsg, port, world):
     """Orbit sharding (each rank owns whole dihedral orbits and keeps the orbit
     forward): the phases emulated on one device match the unsharded engine."""
