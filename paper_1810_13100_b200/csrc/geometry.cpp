@@ -245,6 +245,7 @@ Geometry build_geometry(int n, int n_angles, int n_det, int angle_begin, int ang
         a.dX == 0 ? 0.f : static_cast<float>(65536.0 / static_cast<double>(std::llabs(a.dX)));
     a.dXq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dX), -9)));
     a.bp_stride = 5;  // chosen on first use (choose_adjoint_strides)
+    a.fp_rq = 8;      // orbit reps: chosen by RadonDev::upload (orbit_lane_rays)
     a.dYq = static_cast<int>(std::llround(std::ldexp(static_cast<double>(a.dY), -9)));
     g.cls[cls].push_back(a);
   }

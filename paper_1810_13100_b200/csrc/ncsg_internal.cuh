@@ -73,6 +73,7 @@ struct AngleGeom {
   float inv_adX16;   // 65536 / |dX| (0 when dX == 0)
   int dXq, dYq;      // dX, dY rounded to Q9.23 (tile-local stepping)
   int bp_stride;     // adjoint lane ray stride (>= 3), chosen per angle on the host
+  int fp_rq;         // orbit forward: rays per quarter-warp (4..8, host bank-cost model)
 };
 
 struct RayRange {  // valid tau interval [first, last] of one ray (empty: first > last)

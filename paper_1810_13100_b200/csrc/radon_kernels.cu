@@ -566,28 +566,38 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
                 tlo, thi);
       tlo = max(tlo, slo);
       thi = min(thi, shi);
+      // Lane -> ray map: quarter-warp q takes rays q*R .. q*R+R-1 of the group
+      // (R = g.fp_rq, chosen per orbit by the host bank-cost model so that
+      // the 8 cells one 128-bit load touches per quarter-warp fall in distinct
+      // 16-byte bank groups); its lanes past R, and lanes past the last ray,
+      // duplicate a ray (same address: a broadcast, no extra wavefront) and
+      // never store.
+      const int R = g.fp_rq, G = 4 * R;
+      const int loff = (lane >> 3) * R + min(lane & 7, R - 1);
+      const bool dup = (lane & 7) >= R;
       RayRange nxt[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], tlo + lane, tlo + lane <= thi);
-      for (int sb = tlo; sb <= thi; sb += 32) {
-        const int s = sb + lane;
-        const bool act = s <= thi;
+        nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(tlo + loff, thi), true);
+      for (int sb = tlo; sb <= thi; sb += G) {
+        const int s_raw = sb + loff;
+        const int s = min(s_raw, thi);
+        const bool act = !dup && s_raw <= thi;
         RayRange cur[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // prefetch the next group's ray ranges
           cur[k] = nxt[k];
-          nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], s + 32, s + 32 <= thi);
+          nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(s_raw + G, thi),
+                               sb + G <= thi);
         }
         // shared run: ownership of the rep's lattice (x strip, y tile row)
         const RayRange all{-0x3fffffff, 0x3fffffff};
-        LaneRun run{OX, OY, 0, 0, 0};
-        if (act) run = setup_run(g, a.P0, s, all, Xlo, Xhi, Ylo, Yhi);
+        const LaneRun run = setup_run(g, a.P0, s, all, Xlo, Xhi, Ylo, Yhi);
         const int k0 = run.k0;
         int jl[4], jh[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          if (act && run.jhi > run.jlo)
+          if (run.jhi > run.jlo)
             member_range(cur[k], o.t[k], k >= 2, g.dir, k0, run.jlo, run.jhi, jl[k], jh[k]);
           else
             jl[k] = jh[k] = 0;
@@ -610,7 +620,11 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
 #pragma unroll 2
         for (int j = J0; j < J1; ++j) {
           const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
-          const int idx = on ? base + (Y >> 23) * P + (X >> 23) : 0;
+          // lanes outside their run read a cell of the slack with the same
+          // bank group as their lattice point (P % 8 == 0), so they add no
+          // conflict the lane map has not already priced in
+          const int idx_l = base + (Y >> 23) * P + (X >> 23);
+          const int idx = on ? idx_l : (idx_l & 7);
           const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
           const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
           const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
@@ -1121,6 +1135,67 @@ int grid_for(size_t total, int block) {
   return static_cast<int>(std::min<size_t>(g, 148 * 16));
 }
 
+// Bank-cost model of the orbit forward's lane map (fp_orbit_kernel): the
+// rep's lattice walked as the kernel walks it (y-aligned starts, kOrbP-cell
+// tile pitch) from a fixed set of sub-pixel tile offsets; each of the four
+// 128-bit loads of a step costs, per quarter-warp, the largest number of
+// distinct cells that share a 16-byte bank group. Returns the R in [4, 8]
+// (rays per quarter-warp) with the fewest wavefronts per useful ray-step.
+// Adjacent rays are 1/cos(theta) columns apart and up to one row apart, so
+// 8 consecutive rays span 8-11 columns (pairs 8 apart collide); fewer rays
+// per quarter-warp trade idle lanes for conflict-free loads.
+int orbit_lane_rays(const AngleGeom& g) {
+  if (const char* e = getenv("NCSG_ORB_RQ")) return std::min(8, std::max(4, atoi(e)));
+  const double ax = std::ldexp(static_cast<double>(g.aX), -32);
+  const double ay = std::ldexp(static_cast<double>(g.aY), -32);
+  const double dx = std::ldexp(static_cast<double>(g.dX), -32);
+  const double dy = std::ldexp(static_cast<double>(g.dY), -32);
+  double best = 1e30;
+  int best_r = 8;
+  for (int R = 8; R >= 4; --R) {
+    long long wave = 0;
+    unsigned seed = 12345u;
+    for (int trial = 0; trial < 24; ++trial) {
+      seed = seed * 1664525u + 1013904223u;
+      const double ox = 40.0 + (seed >> 8) * (1.0 / 16777216.0);
+      seed = seed * 1664525u + 1013904223u;
+      const double oy = (seed >> 8) * (1.0 / 16777216.0);
+      double px[32], py[32];
+      for (int lane = 0; lane < 32; ++lane) {
+        const int r = (lane >> 3) * R + std::min(lane & 7, R - 1);
+        const double x0 = ox + r * ax, y0 = oy + r * ay;
+        const double k0 = std::ceil((4.0 - y0) / dy);  // y-aligned start
+        px[lane] = x0 + k0 * dx;
+        py[lane] = y0 + k0 * dy;
+      }
+      for (int j = 0; j < 32; ++j)
+        for (int ld = 0; ld < 4; ++ld)
+          for (int q = 0; q < 4; ++q) {
+            long long cell[8];
+            int nc = 0;
+            for (int i = 0; i < 8; ++i) {
+              const int L = q * 8 + i;
+              const long long row = static_cast<long long>(std::floor(py[L] + j * dy)) + (ld >> 1);
+              const long long col = static_cast<long long>(std::floor(px[L] + j * dx)) + (ld & 1);
+              const long long c = row * kOrbP + col;
+              bool seen = false;
+              for (int k = 0; k < nc; ++k) seen |= cell[k] == c;
+              if (!seen) cell[nc++] = c;
+            }
+            int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0}, mx = 0;
+            for (int k = 0; k < nc; ++k) mx = std::max(mx, ++cnt[((cell[k] % 8) + 8) % 8]);
+            wave += mx;
+          }
+    }
+    const double cost = static_cast<double>(wave) / R;
+    if (cost < best * 0.999) {
+      best = cost;
+      best_r = R;
+    }
+  }
+  return best_r;
+}
+
 }  // namespace
 
 // --------------------------------------------------------------- host side
@@ -1199,6 +1274,7 @@ void RadonDev::upload() {
     const size_t smem = orbit_smem(rmax);
     if (ns == n_strips && smem <= 112 * 1024) {
       orbit_mode = true;
+      for (OrbitGeom& o : geo.orbits) o.rep.fp_rq = orbit_lane_rays(o.rep);
       orb_rmax = rmax;
       orbits.alloc(geo.orbits.size());
       NCSG_CUDA_CHECK(cudaMemcpy(orbits.p, geo.orbits.data(),
