@@ -856,6 +856,9 @@ __device__ __forceinline__ int q32_floor(long long v) { return static_cast<int>(
 __device__ __forceinline__ float q32_frac(long long v) {
   return __uint_as_float(0x3f800000u | (static_cast<unsigned>(v) >> 9)) - 1.0f;
 }
+__device__ __forceinline__ float q32_frac1(long long v) {  // 1 + fraction
+  return __uint_as_float(0x3f800000u | (static_cast<unsigned>(v) >> 9));
+}
 // floor(z) for |z| < 2^21 by round-to-nearest of z - 1/2 (floor(z) - 1 when
 // z is an integer -- the gather's candidate windows tolerate either).
 __device__ __forceinline__ float floor_rn(float z) {
@@ -976,8 +979,11 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
     __syncthreads();
     for (int o = 0; o < nb; ++o) {
       const GatherGeom& g = G[buf][o];
-      const float ay = g.ay;
       const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
+      // first step of ray u with ey > -1: floor(z_u) + 1 - fk, where
+      // z_u - 1/2 = (du0 + u) * cu + fk + K is affine in u (cu, K per orbit)
+      const float cu = -g.ay * g.inv_dy, K1 = -g.inv_dy - 1.5f;
+      const f32x2 negD = pk(-g.dx, -g.dy), D2 = pk(2.0f * g.dx, 2.0f * g.dy);
       const float4* Uo = U4[buf][o];
       const int sl = slo[ob - o_begin + o];
       long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
@@ -985,16 +991,21 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
 #pragma unroll
       for (int p = 0; p < PX; ++p) {
         if (p > 0) sq += RS * g.sy, kq += RS * g.ky;
-        const float fs = q32_frac(sq), fk = q32_frac(kq);
-        const bool first = fs - g.rho > -1.0f;  // u0 = ceil(fs - rho) is 0 or -1
+        // fractions as 1 + frac in [1, 2) (one LEA.HI each)
+        const float fs1 = q32_frac1(sq), fk1p = q32_frac1(kq);
+        const bool first = fs1 > g.rho;  // fs - rho > -1: u0 = ceil(fs - rho) is 0, else -1
         const int r0 = q32_floor(sq) - (first ? 0 : 1) - sl;
-        const float du0 = (first ? 0.0f : -1.0f) - fs;
-        const float fk1 = fk - 1.0f;
+        const float du0 = (first ? 1.0f : 0.0f) - fs1;
+        // e_u = (du0 + u) A + (floor(z_u) - fk + 1) D = Bu + floor(z_u) D with
+        // B0 = du0 A - (fk - 1) D = du0 A - fk1p D + 2 D, B_{u+1} = B_u + A
+        const float z0 = fmaf(du0, cu, fk1p + K1);
+        f32x2 Bu = ffma2(pk(du0, du0), A, ffma2(pk(fk1p, fk1p), negD, D2));
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
-          const float du = du0 + u;
-          const float dv = floor_rn(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) - fk1;
-          f32x2 e = ffma2(pk(du, du), A, fmul2(pk(dv, dv), D));  // (ex, ey)
+          if (u > 0) Bu = fadd2(Bu, A);
+          const float zl = __fsub_rn(__fadd_rn(u == 0 ? z0 : __fadd_rn(z0, u * cu), 12582912.0f),
+                                     12582912.0f);  // floor (round-to-nearest of z - 1/2)
+          f32x2 e = ffma2(pk(zl, zl), D, Bu);  // (ex, ey)
           float2 v = upk(e);
           float w = tent(v.x) * tent(v.y);
           e = fadd2(e, D);
