@@ -574,7 +574,7 @@ inline void ncs_step(SolverState& state, const SplitProblem& prob, const SolverC
   detail::check(ncsg_step(eng.get(), 1));
   std::int64_t div = -1;
   ncsg_status st = ncsg_sync(eng.get(), &div);
-  if (st == NCSG_DIVERGED) throw DivergenceError(state.iter + 1, ncsg_last_error());
+  if (st == NCSG_DIVERGED) throw DivergenceError(div, ncsg_last_error());  // absolute
   detail::check(st);
   detail::check(ncsg_get_state(eng.get(), state.x.data(), state.u.data(), nullptr));
   ++state.iter;

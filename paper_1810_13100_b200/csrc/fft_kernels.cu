@@ -556,9 +556,7 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
                          cudaStream_t s) {
   const int n = f.n;
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
-  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_rows_r2c_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+  ensure_smem(reinterpret_cast<const void*>(fft_rows_r2c_kernel), smem);
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   // the loader (sums of adjoint partial images) wants more threads than the FFT
   launch_pdl(fft_rows_r2c_kernel, grid, dim3(fft_threads(kRowsPerBlock * n / 4)), smem, s, terms,
@@ -571,9 +569,7 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
                             cudaStream_t s) {
   const int n = f.n;
   size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
-  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_cols_filter_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+  ensure_smem(reinterpret_cast<const void*>(fft_cols_filter_kernel), smem);
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
   launch_pdl(fft_cols_filter_kernel, grid, dim3(fft_threads(kColsPerBlock * n / 8)), smem, s,
              specT, maskT, f.tw.p, f.shape);
@@ -584,9 +580,7 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
 void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStream_t s) {
   const int n = f.n;
   size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
-  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_cols_forward_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+  ensure_smem(reinterpret_cast<const void*>(fft_cols_forward_kernel), smem);
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
   fft_cols_forward_kernel<<<grid, fft_threads(kColsPerBlock * n / 8), smem, s>>>(specT, f.tw.p,
                                                                                f.shape);
@@ -598,9 +592,7 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
                          cudaStream_t s) {
   const int n = f.n;
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n + sizeof(float) * kRowsPerBlock * n;
-  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fft_rows_c2r_kernel,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(smem)));
+  ensure_smem(reinterpret_cast<const void*>(fft_rows_c2r_kernel), smem);
   dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   launch_pdl(fft_rows_c2r_kernel, grid, dim3(fft_threads((kRowsPerBlock / 2) * n / 4)), smem, s,
              specT, xu, f.tw.p, f.shape);

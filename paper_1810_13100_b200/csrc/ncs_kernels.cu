@@ -63,7 +63,37 @@ __global__ void dual_update_kernel(DualArgs a) {
       float* us = a.u0 + b * a.u_stride;
       float* ax = a.axs + b * a.m;
       const float* bb = a.b + b * a.m;
-      if (!a.own && ((a.m | a.m_begin | a.m_end | a.u_stride) & 3) == 0) {
+      if (a.orb_t) {
+        // orbit-major: a block item is (orbit o, 64 detectors); thread
+        // (member k, detector d) updates ray t_k*det + d (coalesced along d),
+        // then the four members of each detector leave as one 16-byte u4 cell
+        __shared__ float sh[4][64];
+        const int nch = (a.det + 63) / 64;
+        const size_t items = static_cast<size_t>(a.n_orb) * nch;
+        float4* u4b = reinterpret_cast<float4*>(a.u4 + b * a.u4_stride);
+        const int k = threadIdx.x >> 6, dl = threadIdx.x & 63;
+        for (size_t it = blockIdx.x; it < items; it += gridDim.x) {
+          const int o = static_cast<int>(it / nch);
+          const int d = static_cast<int>(it - static_cast<size_t>(o) * nch) * 64 + dl;
+          const int t = __ldg(reinterpret_cast<const int*>(a.orb_t + o) + k);
+          float un = 0.f;
+          if (t >= 0 && d < a.det) {
+            const size_t i = static_cast<size_t>(t) * a.det + d;
+            float rx = 0.f;
+            for (int q = 0; q < a.n_strips; ++q) rx += part[q * a.m + i];
+            un = (us[i] + alpha * (2.f * rx - ax[i] - bb[i])) * a.s_quad;
+            us[i] = un;
+            ax[i] = rx;
+            bad |= isnan(un);
+          }
+          sh[k][dl] = un;
+          __syncthreads();
+          if (threadIdx.x < 64 && d < a.det)
+            u4b[static_cast<size_t>(o) * a.u4_row + a.u4_pad + d] =
+                make_float4(sh[0][dl], sh[1][dl], sh[2][dl], sh[3][dl]);
+          __syncthreads();
+        }
+      } else if (!a.own && ((a.m | a.m_begin | a.m_end | a.u_stride) & 3) == 0) {
         // four rays per thread, float4 loads of every partial slot
         for (size_t i = a.m_begin + 4 * i0; i < a.m_end; i += 4 * stride) {
           float4 rx = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -188,8 +218,9 @@ __global__ void dual_update_kernel(DualArgs a) {
       bad |= isnan(z);
     }
   }
+  // dual NaN (check_finite's second test, solvers.cpp:252-254): flag word 2
   if (a.flag && __syncthreads_or(bad) && threadIdx.x == 0)
-    atomicMin(a.flag, *(volatile int*)(a.flag + 1));
+    atomicMin(a.flag + 2, *(volatile int*)(a.flag + 1));
 }
 
 __device__ double block_sum(double v, double* sh) {

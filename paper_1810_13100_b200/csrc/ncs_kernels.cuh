@@ -29,6 +29,12 @@ struct DualArgs {
   const int* slot = nullptr;
   int u4_row = 0, u4_pad = 0;
   size_t u4_stride = 0;  // floats per problem
+  // Orbit-major data block (nullable; CT with u4): item (orbit o, detector d)
+  // updates the rays d of the member angles orb_t[o] (-1: absent) and stores
+  // their four duals as one coalesced 16-byte u4 cell.  Covers exactly the
+  // rays of the listed (own) orbits.
+  const int4* orb_t = nullptr;
+  int n_orb = 0;
 };
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
 // Rebuilds u4 from u0 (fields u0, u_stride, m, det, u4, slot, u4_row, u4_pad, u4_stride).

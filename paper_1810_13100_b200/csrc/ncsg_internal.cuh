@@ -36,6 +36,9 @@ struct Error {
 // it off.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 bool pdl_enabled();
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device,
+// size): the attribute only ever grows, so repeated launches skip the call.
+void ensure_smem(const void* kernel, size_t bytes);
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                 Args... args) {
@@ -262,6 +265,7 @@ struct RadonDev {
   // Orbit-interleaved dual (optional gather input): angle t's member slot
   // 4 * orbit + member (-1: none) and the padded row of rays per orbit.
   DevBuf<int> angle_slot;
+  DevBuf<int4> orbit_t;  // member angles of each orbit (-1: absent)
   int u4_row() const { return geo.n_det + 2 * kGaSW; }
   size_t u4_size() const { return geo.orbits.size() * static_cast<size_t>(u4_row()) * 4; }
   DevBuf<int2> strip_range[2];                // [angle][strip] s-range (forward)
@@ -275,6 +279,15 @@ struct RadonDev {
   int orb_rmax = 0;
   DevBuf<OrbitGeom> orbits;
   DevBuf<int2> orb_range;                     // [orbit][strip][seg] s-range
+  // Cached TMA descriptor of the orbit forward's member-image buffer (encoded
+  // once per (buffer, batch), not per launch).
+  struct QuadMap {
+    alignas(64) unsigned char bytes[128];
+    const float* ptr = nullptr;
+    int batch = 0;
+    bool ok = false;
+  };
+  mutable QuadMap quad_map;
   void upload();
   void plan_adjoint(int batch);
   int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }

@@ -35,6 +35,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <cstring>
+#include <map>
+#include <mutex>
 
 #include "ncsg_internal.cuh"
 
@@ -1332,6 +1335,14 @@ void RadonDev::upload() {
       angle_slot.alloc(slot.size());
       NCSG_CUDA_CHECK(cudaMemcpy(angle_slot.p, slot.data(), slot.size() * sizeof(int),
                                  cudaMemcpyHostToDevice));
+      std::vector<int4> ot(geo.orbits.size());
+      for (size_t oi = 0; oi < geo.orbits.size(); ++oi) {
+        const int* t = geo.orbits[oi].t;
+        ot[oi] = make_int4(t[0], t[1], t[2], t[3]);
+      }
+      orbit_t.alloc(ot.size());
+      NCSG_CUDA_CHECK(cudaMemcpy(orbit_t.p, ot.data(), ot.size() * sizeof(int4),
+                                 cudaMemcpyHostToDevice));
     }
   }
 }
@@ -1459,11 +1470,21 @@ bool make_quad_map(CUtensorMap* m, const float* quad, int n, int batch, int box_
 size_t bp_smem(int T, int P) {
   return sizeof(float) * kBpWarps * ((((T + 5) * P + 2) + 31) / 32 * 32);
 }
-void set_smem(const void* fn, size_t bytes) {
-  NCSG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       static_cast<int>(bytes)));
-}
+void set_smem(const void* fn, size_t bytes) { ensure_smem(fn, bytes); }
 }  // namespace
+
+void ensure_smem(const void* kernel, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  NCSG_CUDA_CHECK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& have = done[{kernel, dev}];
+  if (bytes <= have) return;
+  NCSG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       static_cast<int>(bytes)));
+  have = bytes;
+}
 
 void launch_radon_forward_partial(const RadonDev& r, const float* img, const float* imgT,
                                   float* fp_partial, int batch, cudaStream_t s) {
@@ -1489,8 +1510,17 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     a.P0 = g.P0;
     a.nn = static_cast<size_t>(g.n) * g.n;
     a.m = static_cast<size_t>(g.n_angles) * g.n_det;
-    CUtensorMap map{};
-    const bool tma = make_quad_map(&map, imgT, g.n, batch, kOrbP, kOrbT + 4);
+    static_assert(sizeof(CUtensorMap) == sizeof(RadonDev::QuadMap::bytes), "descriptor size");
+    RadonDev::QuadMap& qm = r.quad_map;
+    if (qm.ptr != imgT || qm.batch != batch) {
+      qm.ok = make_quad_map(reinterpret_cast<CUtensorMap*>(qm.bytes), imgT, g.n, batch, kOrbP,
+                            kOrbT + 4);
+      qm.ptr = imgT;
+      qm.batch = batch;
+    }
+    CUtensorMap map;
+    std::memcpy(&map, qm.bytes, sizeof(map));
+    const bool tma = qm.ok;
     const size_t smem = orbit_smem(a.rmax);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     if (tma) {

@@ -502,3 +502,51 @@ def test_mixed_radix_size_solve(ncsg, port, n, A):
     g = gpu_problem(ncsg, prob, gamma, mask).solve(40, record_every=20)
     check_run(g, o)
 
+
+
+def test_dual_nan_divergence_message_and_iteration(ncsg, port):
+    # check_finite (solvers.cpp:248-255): x is tested before u. With a NaN in b
+    # the first step leaves x = 0 (A^T u0 = 0) and makes u NaN, so the
+    # reference throws DivergenceError(iter = base + 1, "dual iterate became
+    # NaN"); the iteration is absolute (counted from set_state's iter).
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    b = np.array(prob.b, dtype=np.float64, copy=True)
+    b.ravel()[7] = np.nan
+    bad = Prob(prob.kind, prob.n, prob.angles, prob.det, prob.alpha, prob.beta, prob.lam, b)
+    p = gpu_problem(ncsg, bad, gamma, mask)
+    p.set_state(iter_=5)
+    p.step(1)
+    with pytest.raises(ncsg.DivergenceError, match="dual iterate became NaN") as ei:
+        p.sync()
+    assert ei.value.iter == 6
+    assert "iteration 6" in str(ei.value)
+
+
+def test_sharded_problem_refuses_whole_steps(ncsg, port):
+    # a shard holds only its rank's part of A^T u: ncsg_step / solve must refuse
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    p = gpu_problem(ncsg, prob, gamma, mask, angle_range=(0, 8))
+    with pytest.raises(ValueError, match="unsharded"):
+        p.step(1)
+    with pytest.raises(ValueError, match="unsharded"):
+        p.solve(2)
+
+
+def test_atu_buffer_alignment_checked(ncsg, port):
+    import torch
+
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    p = gpu_problem(ncsg, prob, gamma, mask, angle_range=(0, 8))
+    t = torch.zeros(16 * 16 + 1, device="cuda:0")
+    with pytest.raises(ValueError, match="16-byte aligned"):
+        p.bind_atu(t[1:])
+    p.bind_atu(t[:256])
+
+
+def test_pinv_rel_tol_zero_passes_through(ncsg, port):
+    # pinv_mask with rel_tol = 0 inverts every nonzero bin (circulant.cpp:47-55):
+    # the GPU filter must not substitute its own default
+    prob, mask, gamma = small_ct(port, n=16, A=16)
+    o = port.solve(prob, gamma, mask, 20, record_every=20)
+    g = gpu_problem(ncsg, prob, gamma, mask, pinv_rel_tol=0.0).solve(20, record_every=20)
+    check_run(g, o)
