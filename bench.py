@@ -99,20 +99,54 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
-def algorithmic_bytes(cfg, n_strips, n_parts):
-    """Per-step HBM bytes of the minimal fused design and of
-    each phase as implemented (fp32)."""
-    n, m, g = cfg.n * cfg.n, cfg.m, cfg.g
-    f = 4
-    return {
-        "adjoint": f * (m + n_parts * n),                 # read u_s, write partial images
-        "fft_rows_r2c": f * (n_parts * n + g + (n + 2 * n)),  # partials + u_g in, half spectrum out
-        "fft_cols": f * (4 * n + 2 * n),                  # spectrum r+w, filter
-        "fft_rows_c2r": f * (2 * n + 4 * n),              # spectrum in, x r/w, x_old, x^T
-        "forward": f * (2 * n + n_strips * m),            # x, x^T in, strip partials out
-        "dual_update": f * (n_strips * m + 5 * m + 2 * n + 2 * g),
-        "survey_minimal": f * (4 * m + 3 * g + 12.5 * n),
-    }
+def kernel_bytes(cfg, plan):
+    """Per-launch algorithmic bytes of every phase of the step AS PLANNED
+    (partial-slot and partial-image counts from the live plan,
+    ncsg_problem_plan), whole batch, fp32, and the bound each is measured
+    against:
+
+      * projectors (forward R, adjoint R^T): on-chip gather, 16 B of texel
+        traffic per bilinear sample (4 texels x 4 B), S samples
+        per application -> shared-memory roofline;
+      * streaming passes: HBM bytes their inputs and outputs must cross once.
+    """
+    N = cfg.n
+    n = N * N
+    spec = 8 * N * (N // 2 + 1)  # half spectrum, complex64
+    B = max(1, int(plan["batch"]))
+    m, g, P, F = plan["m0"], plan["g"], plan["bp_partials"], plan["fp_slots"]
+    S = plan["samples"]
+    ct = cfg.kind == "ct"
+    out = {}
+    if ct:
+        out["adjoint"] = ("smem", 16 * S)
+        out["forward"] = ("smem", 16 * S)
+        if plan["orbit_forward"]:
+            out["make_quad"] = ("hbm", 4 * n + 16 * n)  # x in, member cells out
+    # r2c: A^T u assembly (partial images or the identity dual, D^T u_g) in,
+    # half spectrum out
+    r2c_in = 4 * (P * n if ct else n) + 4 * g
+    out["fft_rows_r2c"] = ("hbm", r2c_in + spec)
+    out["fft_cols"] = ("hbm", 3 * spec)  # spectrum r/w + filter
+    out["fft_rows_c2r"] = ("hbm", spec + 4 * n * (3 + plan["transposed_copy"]))
+    # dual: data block (CT: F partial slots + u r/w + ax r/w + b; denoise:
+    # u r/w + b), gradient block u_g r/w, x and x_old
+    data = 4 * (F * m + 5 * m) if ct else 4 * 3 * n
+    out["dual_update"] = ("hbm", data + 4 * 2 * g + 4 * 2 * n)
+    return {k: (bound, B * v) for k, (bound, v) in out.items()}
+
+
+def load_ncu(cfg_name):
+    """Per-kernel ncu figures of this config's committed capture
+    (profiles/ncu_<cfg>.json, written by scripts/ncu_summary.py), or {}."""
+    path = os.path.join(ROOT, "profiles", f"ncu_{cfg_name}.json")
+    try:
+        with open(path) as fh:
+            d = json.load(fh)
+        d["_path"] = os.path.relpath(path, ROOT)
+        return d
+    except (OSError, ValueError):
+        return {}
 
 
 def setup_problem(cfg, nc, dev=0, angle_range=(0, 0)):
@@ -246,58 +280,45 @@ def main():
     bench_single(args, cfg)
 
 
-def roofline_of(cfg, phase_avg, S, clocks):
-    """Roofline object for the dominant phase: algorithmic HBM bytes per launch
-    / its CUDA-event time against the measured HBM peak, the ncu DRAM traffic
-    of the same kernel (profiles/ncu_traffic.json), and the on-chip roofline
-    that actually bounds each projector: R (fp_orbit_kernel) reads 16 B of
-    texels per sample from shared memory (148 SM x 128 B/clk at the sampled
-    clock); R^T (bp_gather_kernel) is a register gather bound by instruction
-    issue (148 SM x 4 warp-instructions/clk), measured instructions per launch
-    from the same ncu capture."""
+def roofline_of(cfg, plan, phase_avg, clocks):
+    """Per-kernel roofline table and the headline entry (the dominant phase).
+
+    achieved = algorithmic bytes per launch (kernel_bytes) / the phase's mean
+    CUDA-event time on the solver stream; peak = measured HBM copy bandwidth
+    (MEASURED_PEAKS.json) for streaming passes, 148 SM x 128 B/clk at the
+    clock sampled during the timed region for the shared-memory gathers of
+    the projectors; traffic / L2 hit rate = this config's ncu
+    capture (dram__bytes_read + write, lts__t_sector_hit_rate) when committed."""
     pk, pk_kind = peaks()
-    n_strips = (cfg.n + 127) // 128
-    nb = algorithmic_bytes(cfg, n_strips, 8)
-    dom = max(phase_avg, key=phase_avg.get)
-    dom_ms = phase_avg[dom]
-    achieved = nb[dom] / (dom_ms * 1e-3) / 1e9
     sm_mhz = clocks.get("sm_mhz") or pk.get("sm_max_mhz", 1965.0)
-    smem_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # TB/s at the measured clock
-    issue_peak = 148 * 4 * sm_mhz * 1e6           # warp-instructions / s
-    prof = {}
-    try:  # DRAM bytes / smem wavefronts / instructions of the committed ncu capture
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            prof = json.load(fh)
-    except (OSError, ValueError):
-        pass
-    traffic = prof.get("dram_bytes_per_launch", {}).get(dom)
-    proj = {}
-    if "forward" in phase_avg:
-        ms = phase_avg["forward"]
-        proj["forward"] = {
-            "model": "shared-memory gather", "bytes_per_launch": 16 * S,
-            "achieved_tbs": 16 * S / (ms * 1e-3) / 1e12, "peak_tbs": smem_peak,
-            "frac": 16 * S / (ms * 1e-3) / 1e12 / smem_peak, "launch_ms": ms,
-            "ncu_smem_wavefront_frac": prof.get("smem_wavefront_frac", {}).get("forward"),
-            "note": "16 B of texel reads per bilinear sample (four 128-bit loads per sample of "
-                    "an orbit) against 148 SM x 128 B/clk at the sampled SM clock"}
-    if "adjoint" in phase_avg:
-        ms = phase_avg["adjoint"]
-        inst = prof.get("inst_per_launch", {}).get("adjoint")
-        proj["adjoint"] = {
-            "model": "instruction issue", "launch_ms": ms,
-            "pixel_angle_pairs": cfg.n * cfg.n * cfg.angles,
-            "inst_per_launch": inst, "peak_inst_per_s": issue_peak,
-            "frac": (inst / (ms * 1e-3) / issue_peak) if inst else None,
-            "ncu_issue_active_frac": prof.get("issue_active_frac", {}).get("adjoint"),
-            "note": "pixel-driven orbit gather in registers (no shared-memory read-modify-"
-                    "write): warp-instructions per launch (ncu) / event time against "
-                    "148 SM x 4 issue/clk at the sampled SM clock"}
-    return {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": pk["hbm_gbs"],
-            "peak_kind": pk_kind, "unit": "GB/s", "frac": achieved / pk["hbm_gbs"],
-            "traffic": traffic, "traffic_source": "profiles/ncu_traffic.json",
-            "algorithmic_bytes_per_launch": nb[dom], "launch_ms": dom_ms,
-            "on_chip": proj}
+    peaks_gbs = {"hbm": pk["hbm_gbs"], "smem": 148 * 128 * sm_mhz * 1e6 / 1e9}
+    kinds = {"hbm": f"{pk_kind} (MEASURED_PEAKS.json hbm_gbs)",
+             "smem": f"148 SM x 128 B/clk x {sm_mhz:.0f} MHz (sampled SM clock under load)"}
+    prof = load_ncu(cfg.name)
+    table = {}
+    for k, (bound, nbytes) in kernel_bytes(cfg, plan).items():
+        ms = phase_avg.get(k)
+        if not ms:
+            continue
+        ach = nbytes / (ms * 1e-3) / 1e9
+        row = {"bound": bound, "launch_ms": ms, "bytes_per_launch": nbytes, "achieved": ach,
+               "peak": peaks_gbs[bound], "unit": "GB/s", "frac": ach / peaks_gbs[bound]}
+        kp = prof.get("kernels", {}).get(k)
+        if kp:
+            row["traffic"] = kp.get("dram_bytes")
+            row["l2_hit_rate"] = kp.get("l2_hit_rate")
+            row["ncu_us"] = kp.get("duration_us")
+        table[k] = row
+    dom = max(table, key=lambda k: table[k]["launch_ms"])
+    h = table[dom]
+    return {"bound": h["bound"], "kernel": dom, "achieved": h["achieved"], "peak": h["peak"],
+            "peak_kind": kinds[h["bound"]], "unit": "GB/s", "frac": h["frac"],
+            "traffic": h.get("traffic"), "l2_hit_rate": h.get("l2_hit_rate"),
+            "traffic_source": prof.get("_path"), "bytes_per_launch": h["bytes_per_launch"],
+            "launch_ms": h["launch_ms"], "kernels": table,
+            "note": "projectors: on-chip gather bound (16 B per bilinear sample, SURVEY §8d) "
+                    "against shared-memory bandwidth; streaming passes: algorithmic HBM bytes "
+                    "against the measured HBM copy peak"}
 
 
 def bench_multi(args, cfg):
@@ -367,7 +388,7 @@ def bench_multi(args, cfg):
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
                 "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": workload(cfg),
-                "roofline": roofline_of(cfg, phase_avg, R.sample_count() // world, clocks),
+                "roofline": roofline_of(cfg, s.prob.plan(), phase_avg, clocks),
                 "phases_ms_rank0": phase_avg, "gpu_launches": launches, "clocks": clocks,
                 "objective_after": float(np.sum(f)),
                 "collective": "NCCL all_reduce of the partial A^T u (N^2 fp32) per step",
@@ -424,8 +445,9 @@ def bench_single(args, cfg):
     phase_avg = {k: v / max(1, nprof) for k, v in phase_ms.items()}
 
     clocks = clk.summary()
-    S = R.sample_count() if R is not None else 0
-    roofline = roofline_of(cfg, phase_avg, S, clocks)
+    plan = prob.plan()
+    S = plan["samples"]
+    roofline = roofline_of(cfg, plan, phase_avg, clocks)
 
     line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": 1,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,

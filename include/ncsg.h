@@ -289,11 +289,25 @@ ncsg_status ncsg_step_phase_b(ncsg_problem* p);
 /* ------------------------------------------------------------ measurement
  * Phase timing for bench.py: while profiling, every step records CUDA events
  * on the handle's stream between its phases (adjoint, FFT rows r2c + combine,
- * FFT columns, FFT rows c2r + x update, forward, dual update);
+ * FFT columns, FFT rows c2r + x update, member images for the orbit forward,
+ * forward, dual update);
  * ncsg_profile_end synchronises and returns the summed milliseconds per phase
  * and the number of profiled steps. */
 ncsg_status ncsg_profile_begin(ncsg_problem* p);
 ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int* steps);
+/* The live plan of a problem (bench.py's roofline: the partial-sum counts
+ * and sample count the per-kernel byte models use). */
+typedef struct ncsg_plan_info {
+  int orbit_forward;  /* 1: dihedral-orbit forward (fp_orbit_kernel) */
+  int gather_adjoint; /* 1: pixel-driven orbit gather adjoint (bp_gather_kernel) */
+  int fp_slots;       /* forward partial slots per ray summed by the dual update */
+  int bp_partials;    /* adjoint partial images summed by the FFT row pass */
+  int n_orbits;       /* dihedral orbits of the (own) angle set */
+  int transposed_copy;/* 1: the x update also writes x^T (per-angle class-H forward) */
+  int64_t samples;    /* bilinear samples per R application (own angles) */
+  int64_t m0, g, range, batch;
+} ncsg_plan_info;
+ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out);
 /* Kernel launches issued by this library since load. */
 int64_t ncsg_launch_count(void);
 

@@ -254,7 +254,7 @@ AtuTerms atu_terms_for(ncsg_problem* p, float* u) {
   return T;
 }
 
-constexpr int kPhases = 6;  // adjoint, fft rows r2c, fft cols, fft rows c2r, forward, dual
+constexpr int kPhases = 7;  // adjoint, fft rows r2c, fft cols, fft rows c2r, make_quad, forward, dual
 
 void mark(ncsg_problem* p) {
   if (!p->profiling) return;
@@ -318,10 +318,10 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
 void forward_and_dual(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   mark(p);
-  if (p->d.kind != NCSG_DENOISE) {
-    if (p->radon && p->radon->orbit_mode) launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
-    proj_forward(p, p->x.p, p->xT.p, p->fp_part.p, p->batch);
-  }
+  if (p->d.kind != NCSG_DENOISE && p->radon && p->radon->orbit_mode)
+    launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
+  mark(p);
+  if (p->d.kind != NCSG_DENOISE) proj_forward(p, p->x.p, p->xT.p, p->fp_part.p, p->batch);
   mark(p);
   DualArgs a;
   a.kind = p->d.kind;
@@ -1358,6 +1358,29 @@ ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int
 }
 
 int64_t ncsg_launch_count(void) { return ncsg::launch_count(); }
+
+ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out) {
+  return guard([&] {
+    if (!p || !out) throw Error{NCSG_INVALID, "null argument"};
+    ncsg_plan_info r{};
+    if (p->radon) {
+      r.orbit_forward = p->radon->orbit_mode ? 1 : 0;
+      r.gather_adjoint = p->radon->bp_orbit ? 1 : 0;
+      r.n_orbits = static_cast<int>(p->radon->geo.orbits.size());
+      r.samples = p->radon->geo.samples;
+      r.transposed_copy = (!p->radon->orbit_mode && !p->radon->geo.cls[1].empty()) ? 1 : 0;
+    }
+    if (p->d.kind != NCSG_DENOISE) {
+      r.fp_slots = proj_slots(p);
+      r.bp_partials = proj_parts(p);
+    }
+    r.m0 = static_cast<int64_t>(p->m0);
+    r.g = static_cast<int64_t>(p->g);
+    r.range = static_cast<int64_t>(p->range);
+    r.batch = p->batch;
+    *out = r;
+  });
+}
 
 ncsg_status ncsg_step_phase_a(ncsg_problem* p) {
   return guard([&] {

@@ -38,6 +38,14 @@ class DivergenceError(NcsgError):
         self.iter = iter_
 
 
+class PlanInfo(C.Structure):
+    """ncsg_plan_info: the live plan of a problem (include/ncsg.h)."""
+    _fields_ = [("orbit_forward", C.c_int), ("gather_adjoint", C.c_int), ("fp_slots", C.c_int),
+                ("bp_partials", C.c_int), ("n_orbits", C.c_int), ("transposed_copy", C.c_int),
+                ("samples", C.c_int64), ("m0", C.c_int64), ("g", C.c_int64),
+                ("range", C.c_int64), ("batch", C.c_int64)]
+
+
 class ProblemDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("n", C.c_int), ("n_angles", C.c_int), ("n_det", C.c_int),
@@ -71,7 +79,8 @@ SYMBOLS = [
     "ncsg_sparse_destroy", "ncsg_sparse_nnz", "ncsg_sparse_forward", "ncsg_sparse_adjoint",
     "ncsg_sparse_forward_host", "ncsg_sparse_adjoint_host", "ncsg_sparse_empirical_mask",
 ]
-PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "forward", "dual_update"]
+PHASES = ["adjoint", "fft_rows_r2c", "fft_cols", "fft_rows_c2r", "make_quad", "forward",
+          "dual_update"]
 
 
 def lib():
@@ -145,6 +154,7 @@ def lib():
     L.ncsg_set_atu_buffer.argtypes = [C.c_void_p, C.c_void_p]
     L.ncsg_profile_end.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(C.c_int)]
     L.ncsg_launch_count.restype = C.c_int64
+    L.ncsg_problem_plan.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
     _lib = L
     return L
 
@@ -479,6 +489,13 @@ class Problem:
         steps = C.c_int()
         _check(lib().ncsg_profile_end(self._h, out, len(PHASES), C.byref(steps)), "profile_end")
         return dict(zip(PHASES, out.tolist())), steps.value
+
+    def plan(self) -> dict:
+        """The live plan (partial-slot / partial-image counts, orbit mode,
+        sample count) -- ncsg_problem_plan."""
+        info = PlanInfo()
+        _check(lib().ncsg_problem_plan(self._h, C.byref(info)), "plan")
+        return {k: getattr(info, k) for k, _ in PlanInfo._fields_}
 
     def objective(self) -> np.ndarray:
         out = np.zeros(self.batch)
