@@ -166,6 +166,15 @@ typedef struct {
    * 0, 0 = off (contiguous angle_begin/angle_end sharding or none). */
   int shard_rank;
   int shard_count;
+  /* SolverConfig::m_pinv_override / m_override (solvers.hpp:70-71) as
+   * circulant operators: interleaved complex N*N symbols, nullable.  m_pinv
+   * set selects the reference's Override mode (mode_from, solvers.cpp:75-79;
+   * it wins over `mask`): the x-update applies Re(F^-1 (m_pinv . F A^T u))
+   * as given (no gamma, no pseudoinverse), and M in the step seminorm and the
+   * step-condition screen is the m_symbol circulant (required there, as
+   * Engine::apply_m requires m_override, solvers.cpp:193-197). */
+  const double* m_pinv;
+  const double* m_symbol;
 } ncsg_problem_desc;
 
 typedef struct ncsg_problem ncsg_problem;

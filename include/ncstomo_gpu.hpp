@@ -9,9 +9,15 @@
 //   laplacian_mask_2d, radon_mask ......... circulant.hpp:16-66
 //   ModelParams, assemble_problem,
 //   metric_mask ........................... pipeline.hpp:38-71
-//   SolverConfig, SolverState, RecordRow,
+//   ImageGrid, Sinogram ................... image.hpp:9-36
+//   StackedMap, ProxConj, QuadraticConj,
+//   ScaledL1Conj, PoissonConj, NonnegConj . linear_map.hpp:37-61, prox.hpp:9-95
+//   SplitBlock, SplitProblem(n, blocks) ... solvers.hpp:17-52 (block lists the
+//                                           device engine has kernels for)
+//   SolverConfig (incl. m_pinv_override /
+//   m_override as CirculantMap), SolverState, RecordRow,
 //   SolveResult, DivergenceError,
-//   ncs_step, ncs_solve, pdhg_solve, admm_cg_solve ... solvers.hpp:59-121
+//   ncs_step, ncs_solve, pdhg_solve, admm_cg_solve ... solvers.hpp:54-121
 // Exceptions: std::invalid_argument for validation failures, DivergenceError
 // (a std::runtime_error with .iter) for divergence, std::runtime_error for
 // device failures (there is no CPU fallback).
@@ -23,6 +29,7 @@
 #include <cstdint>
 #include <cstdio>
 #include <fstream>
+#include <limits>
 #include <memory>
 #include <optional>
 #include <span>
@@ -329,85 +336,444 @@ inline SpectralMask metric_mask(const SpectralMask& measurement, const ModelPara
   return mask;
 }
 
-/// The two SplitProblem shapes of the hot path: CT-TV as assemble_problem
-/// builds it (pipeline.cpp:84-97) and TV denoising {I, D} (the SplitProblem of
-/// test_solvers.cpp:646-664).
-struct SplitProblem {
-  ncsg_kind kind = NCSG_CT;
-  int n = 0, n_angles = 0, n_det = 0;
-  double alpha = 1.0, beta = 1.0, lambda = 1.0;
-  bool positivity = false;
-  std::vector<double> offset;  // b (sinogram or noisy image; PET: counts)
-  std::shared_ptr<ncsg_sparse> sparse;  // SparseMap geometry (fan beam), else RadonMap
-  std::size_t domain_size() const { return static_cast<std::size_t>(n) * n; }
-  std::size_t range_size() const {
-    std::size_t nn = domain_size();
-    std::size_t m = kind != NCSG_DENOISE ? static_cast<std::size_t>(n_angles) * n_det : nn;
-    return m + 2 * static_cast<std::size_t>(n) * (n - 1) + (positivity ? nn : 0);
+/// Square N x N image, row-major doubles (image.hpp:9-20).
+struct ImageGrid {
+  int n = 0;
+  std::vector<double> v;
+  ImageGrid() = default;
+  explicit ImageGrid(int n_) : n(n_), v(static_cast<std::size_t>(n_) * n_, 0.0) {}
+  double& at(int row, int col) { return v[static_cast<std::size_t>(row) * n + col]; }
+  double at(int row, int col) const { return v[static_cast<std::size_t>(row) * n + col]; }
+  std::size_t size() const { return v.size(); }
+};
+
+/// Projection data, angle-major (image.hpp:22-36).
+struct Sinogram {
+  int n_angles = 0, n_det = 0;
+  std::vector<double> v;
+  Sinogram() = default;
+  Sinogram(int a, int d) : n_angles(a), n_det(d), v(static_cast<std::size_t>(a) * d, 0.0) {}
+  double& at(int angle, int det) { return v[static_cast<std::size_t>(angle) * n_det + det]; }
+  double at(int angle, int det) const { return v[static_cast<std::size_t>(angle) * n_det + det]; }
+  std::size_t size() const { return v.size(); }
+};
+
+/// IdentityMap (linear_map.hpp:25-35).  On the device it is the identity
+/// block of TV denoising or of the positivity constraint.
+class IdentityMap final : public LinearMap {
+ public:
+  explicit IdentityMap(std::size_t n) : n_(n) {}
+  std::size_t domain_size() const override { return n_; }
+  std::size_t range_size() const override { return n_; }
+  void forward(std::span<const double> x, std::span<double> out) const override {
+    std::copy(x.begin(), x.end(), out.begin());
   }
+  void adjoint(std::span<const double> u, std::span<double> out) const override {
+    std::copy(u.begin(), u.end(), out.begin());
+  }
+
+ private:
+  std::size_t n_;
+};
+
+/// StackedMap (linear_map.hpp:37-61): x -> (w_1 A_1 x, ..., w_m A_m x).
+class StackedMap final : public LinearMap {
+ public:
+  struct Block {
+    double weight = 1.0;
+    std::shared_ptr<const LinearMap> map;
+  };
+  explicit StackedMap(std::vector<Block> blocks) : blocks_(std::move(blocks)) {
+    if (blocks_.empty()) throw std::invalid_argument("StackedMap needs at least one block");
+    domain_ = blocks_.front().map->domain_size();
+    for (const auto& b : blocks_) {
+      if (b.map->domain_size() != domain_)
+        throw std::invalid_argument("StackedMap blocks must share a domain");
+      offsets_.push_back(range_);
+      range_ += b.map->range_size();
+    }
+  }
+  std::size_t domain_size() const override { return domain_; }
+  std::size_t range_size() const override { return range_; }
+  std::size_t block_offset(std::size_t i) const { return offsets_.at(i); }
+  const std::vector<Block>& blocks() const { return blocks_; }
+  void forward(std::span<const double> x, std::span<double> out) const override {
+    for (std::size_t i = 0; i < blocks_.size(); ++i) {
+      auto seg = out.subspan(offsets_[i], blocks_[i].map->range_size());
+      blocks_[i].map->forward(x, seg);
+      for (double& s : seg) s *= blocks_[i].weight;
+    }
+  }
+  void adjoint(std::span<const double> u, std::span<double> out) const override {
+    std::fill(out.begin(), out.end(), 0.0);
+    std::vector<double> tmp(domain_);
+    for (std::size_t i = 0; i < blocks_.size(); ++i) {
+      blocks_[i].map->adjoint(u.subspan(offsets_[i], blocks_[i].map->range_size()), tmp);
+      for (std::size_t j = 0; j < domain_; ++j) out[j] += blocks_[i].weight * tmp[j];
+    }
+  }
+
+ private:
+  std::vector<Block> blocks_;
+  std::vector<std::size_t> offsets_;
+  std::size_t domain_ = 0, range_ = 0;
+};
+
+/// A circulant operator given by its eigenvalue grid: x -> Re(F^-1 (h .* F x))
+/// (MaskApplier, circulant.hpp:31-42).  The GPU engine accepts
+/// SolverConfig::m_pinv_override / m_override in this form.
+class CirculantMap final : public LinearMap {
+ public:
+  explicit CirculantMap(SpectralMask mask, int device = 0)
+      : mask_(std::move(mask)), device_(device) {}
+  std::size_t domain_size() const override { return static_cast<std::size_t>(mask_.n) * mask_.n; }
+  std::size_t range_size() const override { return domain_size(); }
+  void forward(std::span<const double> x, std::span<double> out) const override {
+    MaskApplier(mask_.n, device_).apply(mask_, x, out);
+  }
+  void adjoint(std::span<const double> u, std::span<double> out) const override {
+    SpectralMask c(mask_.n);
+    for (std::size_t i = 0; i < c.h.size(); ++i) c.h[i] = std::conj(mask_.h[i]);
+    MaskApplier(mask_.n, device_).apply(c, u, out);
+  }
+  const SpectralMask& mask() const { return mask_; }
+
+ private:
+  SpectralMask mask_;
+  int device_;
+};
+
+inline constexpr double kInf = std::numeric_limits<double>::infinity();
+
+/// prox_{alpha g*} for g = 1/2 ||.||^2 and friends (prox.hpp:9-25).
+inline double prox_conj_quadratic(double z, double alpha) { return z / (1.0 + alpha); }
+inline double project_box(double z, double bound) {
+  return z < -bound ? -bound : (z > bound ? bound : z);
+}
+inline double prox_conj_poisson(double u, double c) {
+  if (c < 0.0) throw std::invalid_argument("prox_conj_poisson needs c >= 0");
+  double d = u - 1.0;
+  return 1.0 + 0.5 * (d - std::sqrt(d * d + 4.0 * c));
+}
+inline double prox_conj_nonneg(double u) { return u < 0.0 ? u : 0.0; }
+
+/// Dual-block prox plus the matching primal objective term (prox.hpp:30-43).
+/// The host evaluate/objective follow prox.cpp; the GPU engine recognises the
+/// four concrete types below and runs their device kernels.
+class ProxConj {
+ public:
+  virtual ~ProxConj() = default;
+  virtual void evaluate(std::span<double> u, double alpha) const = 0;
+  virtual double objective(std::span<const double> y) const = 0;
+  virtual std::uint64_t param_hash() const = 0;
 };
 
 namespace detail {
-inline SplitProblem assemble_problem_common(std::span<const double> sino, int n, int n_angles,
-                                            int n_det, std::size_t range, const ModelParams& p) {
+inline std::uint64_t fnv1a(const void* data, std::size_t len, std::uint64_t h) {
+  const auto* p = static_cast<const unsigned char*>(data);
+  for (std::size_t i = 0; i < len; ++i) h = (h ^ p[i]) * 0x100000001b3ULL;
+  return h;
+}
+}  // namespace detail
+
+/// g = 1/2 ||.||^2 (prox.cpp:21-30).
+class QuadraticConj final : public ProxConj {
+ public:
+  void evaluate(std::span<double> u, double alpha) const override {
+    double s = 1.0 / (1.0 + alpha);
+    for (double& z : u) z *= s;
+  }
+  double objective(std::span<const double> y) const override {
+    double acc = 0.0;
+    for (double z : y) acc += z * z;
+    return 0.5 * acc;
+  }
+  std::uint64_t param_hash() const override { return 0x9a0d; }
+};
+
+/// g = bound * ||.||_1 (prox.cpp:32-45).
+class ScaledL1Conj final : public ProxConj {
+ public:
+  explicit ScaledL1Conj(double bound) : bound_(bound) {
+    if (bound < 0.0) throw std::invalid_argument("l1 weight must be nonnegative");
+  }
+  void evaluate(std::span<double> u, double) const override {
+    for (double& z : u) z = project_box(z, bound_);
+  }
+  double objective(std::span<const double> y) const override {
+    double acc = 0.0;
+    for (double z : y) acc += std::abs(z);
+    return bound_ * acc;
+  }
+  std::uint64_t param_hash() const override {
+    return detail::fnv1a(&bound_, sizeof bound_, 0x11);
+  }
+  double bound() const { return bound_; }
+
+ private:
+  double bound_;
+};
+
+/// Poisson log-likelihood, c = alpha * counts folded in (prox.cpp:47-74).
+class PoissonConj final : public ProxConj {
+ public:
+  PoissonConj(std::vector<double> counts, double alpha) : counts_(std::move(counts)), alpha_(alpha) {
+    if (alpha <= 0.0) throw std::invalid_argument("PoissonConj needs alpha > 0");
+    for (double c : counts_)
+      if (c < 0.0) throw std::invalid_argument("Poisson counts must be nonnegative");
+  }
+  void evaluate(std::span<double> u, double alpha) const override {
+    if (u.size() != counts_.size()) throw std::invalid_argument("PoissonConj size mismatch");
+    if (alpha != alpha_) throw std::invalid_argument("PoissonConj built for a different alpha");
+    for (std::size_t i = 0; i < u.size(); ++i) u[i] = prox_conj_poisson(u[i], alpha_ * counts_[i]);
+  }
+  double objective(std::span<const double> y) const override {
+    if (y.size() != counts_.size()) throw std::invalid_argument("PoissonConj size mismatch");
+    double acc = 0.0;
+    for (std::size_t i = 0; i < y.size(); ++i) {
+      if (counts_[i] > 0.0) {
+        if (y[i] <= 0.0) return kInf;
+        acc += y[i] - counts_[i] * std::log(y[i]);
+      } else {
+        if (y[i] < 0.0) return kInf;
+        acc += y[i];
+      }
+    }
+    return acc;
+  }
+  std::uint64_t param_hash() const override {
+    std::uint64_t h = detail::fnv1a(&alpha_, sizeof alpha_, 0x90155);
+    return detail::fnv1a(counts_.data(), counts_.size() * sizeof(double), h);
+  }
+  const std::vector<double>& counts() const { return counts_; }
+  double alpha() const { return alpha_; }
+
+ private:
+  std::vector<double> counts_;
+  double alpha_;
+};
+
+/// g = indicator of the nonnegative orthant (prox.cpp:98-113).
+class NonnegConj final : public ProxConj {
+ public:
+  void evaluate(std::span<double> u, double) const override {
+    for (double& z : u) z = prox_conj_nonneg(z);
+  }
+  double objective(std::span<const double> y) const override {
+    double hi = 0.0;
+    for (double z : y) hi = std::max(hi, std::abs(z));
+    double tol = 1e-9 * std::max(1.0, hi);
+    for (double z : y)
+      if (z < -tol) return kInf;
+    return 0.0;
+  }
+  std::uint64_t param_hash() const override { return 0x20e6; }
+};
+
+/// One term of min_x sum_i g_i(w_i A_i x - o_i) (solvers.hpp:17-22).
+struct SplitBlock {
+  double weight = 1.0;
+  std::shared_ptr<const LinearMap> map;
+  std::shared_ptr<const ProxConj> prox;
+  std::vector<double> offset;
+};
+
+/// SplitProblem(n, blocks) (solvers.hpp:24-52, solvers.cpp:341-360): same
+/// validation and stacked layout.  The constructor also maps the block list
+/// onto the device engine's problem kinds (ncsg.h):
+///   {1, RadonMap|SparseMap, QuadraticConj, b}  + {w, GradMap, ScaledL1Conj(B)}  -> CT
+///   {1, RadonMap|SparseMap, PoissonConj(c, a)} + {w, GradMap, ScaledL1Conj(B)}  -> PET
+///   {1, IdentityMap(N^2), QuadraticConj, b}    + {w, GradMap, ScaledL1Conj(B)}  -> denoise
+/// each optionally followed by {1, IdentityMap(N^2), NonnegConj} (positivity)
+/// -- the shapes assemble_problem builds (pipeline.cpp:84-97) and the
+/// denoising problem of test_solvers.cpp:646-664.  Any other list is valid
+/// for the reference but has no device kernel: std::invalid_argument.
+class SplitProblem {
+ public:
+  SplitProblem(int n, std::vector<SplitBlock> blocks) : n(n), blocks_(std::move(blocks)) {
+    if (n < 1) throw std::invalid_argument("image size must be positive");
+    std::vector<StackedMap::Block> stack;
+    for (const auto& b : blocks_) {
+      if (!b.map || !b.prox) throw std::invalid_argument("block needs a map and a prox");
+      if (b.map->domain_size() != static_cast<std::size_t>(n) * n)
+        throw std::invalid_argument("block domain does not match the image size");
+      if (!b.offset.empty() && b.offset.size() != b.map->range_size())
+        throw std::invalid_argument("block offset size mismatch");
+      stack.push_back({b.weight, b.map});
+    }
+    stacked_ = std::make_shared<StackedMap>(std::move(stack));
+    offsets_.assign(stacked_->range_size(), 0.0);
+    for (std::size_t i = 0; i < blocks_.size(); ++i)
+      if (!blocks_[i].offset.empty())
+        std::copy(blocks_[i].offset.begin(), blocks_[i].offset.end(),
+                  offsets_.begin() + stacked_->block_offset(i));
+    classify();
+  }
+
+  std::size_t domain_size() const { return stacked_->domain_size(); }
+  std::size_t range_size() const { return stacked_->range_size(); }
+  const std::vector<SplitBlock>& blocks() const { return blocks_; }
+  std::size_t block_offset(std::size_t i) const { return stacked_->block_offset(i); }
+  const StackedMap& stacked() const { return *stacked_; }
+  const std::vector<double>& offsets() const { return offsets_; }
+
+  /// objective_from_ax / objective (solvers.cpp:362-388), on the host.
+  double objective_from_ax(std::span<const double> ax) const {
+    double total = 0.0;
+    std::vector<double> tmp;
+    for (std::size_t i = 0; i < blocks_.size(); ++i) {
+      std::size_t off = block_offset(i), len = blocks_[i].map->range_size();
+      std::span<const double> seg = ax.subspan(off, len);
+      if (!blocks_[i].offset.empty()) {
+        tmp.resize(len);
+        for (std::size_t j = 0; j < len; ++j) tmp[j] = seg[j] - blocks_[i].offset[j];
+        seg = tmp;
+      }
+      total += blocks_[i].prox->objective(seg);
+      if (std::isinf(total)) return kInf;
+    }
+    return total;
+  }
+  double objective(std::span<const double> x) const {
+    std::vector<double> ax(range_size());
+    stacked_->forward(x, ax);
+    return objective_from_ax(ax);
+  }
+
+  // ---- the device engine's view of the block list (set by classify) ----
+  int n = 0;
+  ncsg_kind kind = NCSG_CT;
+  int n_angles = 0, n_det = 0;
+  // engine parameters with the same block weights: D weight beta/alpha = w,
+  // ScaledL1 bound lambda*alpha/beta = B (alpha = 1, beta = w, lambda = B w)
+  double alpha = 1.0, beta = 1.0, lambda = 1.0;
+  bool positivity = false;
+  std::vector<double> offset;           // data-block offset b (PET: the counts)
+  std::shared_ptr<ncsg_sparse> sparse;  // SparseMap data block (fan beam), else RadonMap
+  double poisson_alpha = 0.0;           // PoissonConj's alpha (PET)
+
+ private:
+  void classify() {
+    auto no_kernel = [](const std::string& why) {
+      throw std::invalid_argument(
+          "SplitProblem has no GPU kernel for this block list (" + why +
+          "); the device engine runs {1, RadonMap|SparseMap|IdentityMap, Quadratic|Poisson} + "
+          "{w, GradMap, ScaledL1Conj} [+ {1, IdentityMap, NonnegConj}] (pipeline.cpp:84-97)");
+    };
+    const std::size_t nn = static_cast<std::size_t>(n) * n;
+    if (blocks_.size() < 2 || blocks_.size() > 3) no_kernel("2 or 3 blocks expected");
+    const SplitBlock& d0 = blocks_[0];
+    const SplitBlock& d1 = blocks_[1];
+    if (d0.weight != 1.0) no_kernel("the data block weight must be 1");
+    const auto* radon = dynamic_cast<const RadonMap*>(d0.map.get());
+    const auto* sp = dynamic_cast<const SparseMap*>(d0.map.get());
+    const auto* id0 = dynamic_cast<const IdentityMap*>(d0.map.get());
+    const auto* quad = dynamic_cast<const QuadraticConj*>(d0.prox.get());
+    const auto* pois = dynamic_cast<const PoissonConj*>(d0.prox.get());
+    if (radon || sp) {
+      n_angles = radon ? radon->n_angles() : sp->n_angles();
+      n_det = radon ? radon->n_detectors() : sp->n_detectors();
+      if (sp) sparse = sp->handle();
+      if (quad) {
+        kind = NCSG_CT;
+        offset = d0.offset.empty() ? std::vector<double>(d0.map->range_size(), 0.0) : d0.offset;
+      } else if (pois) {
+        kind = NCSG_PET;
+        for (double o : d0.offset)
+          if (o != 0.0) no_kernel("a Poisson data block takes no offset");
+        offset = pois->counts();
+        poisson_alpha = pois->alpha();
+      } else {
+        no_kernel("the data block prox must be QuadraticConj or PoissonConj");
+      }
+    } else if (id0 && id0->domain_size() == nn && quad) {
+      kind = NCSG_DENOISE;
+      offset = d0.offset.empty() ? std::vector<double>(nn, 0.0) : d0.offset;
+    } else {
+      no_kernel("unsupported data-block map / prox");
+    }
+    const auto* grad = dynamic_cast<const GradMap*>(d1.map.get());
+    const auto* l1 = dynamic_cast<const ScaledL1Conj*>(d1.prox.get());
+    if (!grad || !l1 || grad->n() != n) no_kernel("the second block must be {w, GradMap(n), ScaledL1Conj}");
+    if (!(d1.weight > 0.0)) no_kernel("the GradMap block weight must be positive");
+    for (double o : d1.offset)
+      if (o != 0.0) no_kernel("the GradMap block takes no offset");
+    alpha = 1.0;
+    beta = d1.weight;
+    lambda = l1->bound() * d1.weight;
+    positivity = false;
+    if (blocks_.size() == 3) {
+      const SplitBlock& d2 = blocks_[2];
+      const auto* id2 = dynamic_cast<const IdentityMap*>(d2.map.get());
+      if (!id2 || !dynamic_cast<const NonnegConj*>(d2.prox.get()) || d2.weight != 1.0)
+        no_kernel("the third block must be {1, IdentityMap, NonnegConj}");
+      for (double o : d2.offset)
+        if (o != 0.0) no_kernel("the positivity block takes no offset");
+      positivity = true;
+    }
+  }
+
+  std::vector<SplitBlock> blocks_;
+  std::shared_ptr<const StackedMap> stacked_;
+  std::vector<double> offsets_;
+};
+
+/// assemble_problem (pipeline.cpp:69-98): the reference's block list on a
+/// RadonMap or SparseMap geometry.
+template <class Geometry>
+inline SplitProblem assemble_problem(std::span<const double> sino,
+                                     const std::shared_ptr<const Geometry>& geometry,
+                                     const ModelParams& p) {
   if (p.model != "ct" && p.model != "pet")
     throw std::invalid_argument("unknown model \"" + p.model + "\"");
   if (p.alpha <= 0.0 || p.beta <= 0.0)
     throw std::invalid_argument("alpha and beta must be positive");
   if (p.lambda < 0.0) throw std::invalid_argument("lambda must be nonnegative");
-  if (range != sino.size())
+  if (geometry->range_size() != sino.size())
     throw std::invalid_argument("sinogram shape does not match the geometry");
-  SplitProblem s;
-  // ct: {1, A, QuadraticConj, sino}; pet: {1, A, PoissonConj(sino, alpha), 0}
-  // (pipeline.cpp:84-89) -- the counts travel in the offset slot
-  s.kind = p.model == "pet" ? NCSG_PET : NCSG_CT;
-  if (s.kind == NCSG_PET)
-    for (double c : sino)
-      if (c < 0.0) throw std::invalid_argument("Poisson counts must be nonnegative");
-  s.n = n;
-  s.n_angles = n_angles;
-  s.n_det = n_det;
-  s.alpha = p.alpha;
-  s.beta = p.beta;
-  s.lambda = p.lambda;
-  s.positivity = p.positivity;
-  s.offset.assign(sino.begin(), sino.end());
-  return s;
+  const int n = geometry->n();
+  std::vector<double> s(sino.begin(), sino.end());
+  std::vector<SplitBlock> blocks;
+  if (p.model == "ct")
+    blocks.push_back({1.0, geometry, std::make_shared<QuadraticConj>(), s});
+  else
+    blocks.push_back({1.0, geometry, std::make_shared<PoissonConj>(s, p.alpha), {}});
+  blocks.push_back({p.beta / p.alpha, std::make_shared<GradMap>(n),
+                    std::make_shared<ScaledL1Conj>(p.lambda * p.alpha / p.beta), {}});
+  if (p.positivity)
+    blocks.push_back({1.0, std::make_shared<IdentityMap>(geometry->domain_size()),
+                      std::make_shared<NonnegConj>(), {}});
+  return SplitProblem(n, std::move(blocks));
 }
-}  // namespace detail
-
-/// assemble_problem (pipeline.cpp:69-98) on the parallel-beam RadonMap.
 inline SplitProblem assemble_problem(std::span<const double> sino, const RadonMap& geometry,
                                      const ModelParams& p) {
-  return detail::assemble_problem_common(sino, geometry.n(), geometry.n_angles(),
-                                         geometry.n_detectors(), geometry.range_size(), p);
+  return assemble_problem(sino, std::make_shared<const RadonMap>(geometry), p);
 }
-
-/// assemble_problem on a SparseMap geometry (fan beam): same blocks as for
-/// RadonMap (pipeline.cpp:69-98), the data block projecting with the matrix.
 inline SplitProblem assemble_problem(std::span<const double> sino, const SparseMap& geometry,
                                      const ModelParams& p) {
-  SplitProblem s = detail::assemble_problem_common(sino, geometry.n(), geometry.n_angles(),
-                                           geometry.n_detectors(), geometry.range_size(), p);
-  s.sparse = geometry.handle();
-  return s;
+  return assemble_problem(sino, std::make_shared<const SparseMap>(geometry), p);
 }
 
+/// TV denoising {1, I, QuadraticConj, noisy} + {beta/alpha, D, ScaledL1Conj}
+/// (test_solvers.cpp:646-664).
 inline SplitProblem denoise_problem(std::span<const double> noisy, int n, const ModelParams& p) {
   if (noisy.size() != static_cast<std::size_t>(n) * n)
     throw std::invalid_argument("image size mismatch");
-  SplitProblem s;
-  s.kind = NCSG_DENOISE;
-  s.n = n;
-  s.alpha = p.alpha;
-  s.beta = p.beta;
-  s.lambda = p.lambda;
-  s.positivity = p.positivity;
-  s.offset.assign(noisy.begin(), noisy.end());
-  return s;
+  std::vector<SplitBlock> blocks;
+  blocks.push_back({1.0, std::make_shared<IdentityMap>(noisy.size()),
+                    std::make_shared<QuadraticConj>(),
+                    std::vector<double>(noisy.begin(), noisy.end())});
+  blocks.push_back({p.beta / p.alpha, std::make_shared<GradMap>(n),
+                    std::make_shared<ScaledL1Conj>(p.lambda * p.alpha / p.beta), {}});
+  if (p.positivity)
+    blocks.push_back({1.0, std::make_shared<IdentityMap>(noisy.size()),
+                      std::make_shared<NonnegConj>(), {}});
+  return SplitProblem(n, std::move(blocks));
 }
 
-/// SolverConfig (solvers.hpp:59-72).
+/// SolverConfig (solvers.hpp:54-72).  m_pinv_override / m_override are the
+/// reference's explicit metric hooks; the device engine takes them as
+/// CirculantMap (anything else: std::invalid_argument).
 struct SolverConfig {
   double alpha = 1.0;
   double gamma = 0.0;
@@ -419,20 +785,22 @@ struct SolverConfig {
   /// Power-method screen of M >= alpha A^T A at solve start (solvers.hpp:67-69);
   /// a violation becomes a warning in the record, as in the reference.
   bool check_step_condition = true;
+  std::shared_ptr<const LinearMap> m_pinv_override;
+  std::shared_ptr<const LinearMap> m_override;
   int device = 0;
 };
 
+/// SolverState (solvers.hpp:74-78).
 struct SolverState {
-  int n = 0;
-  std::vector<double> x;  // row-major N*N
-  std::vector<double> u;  // stacked dual
+  ImageGrid x;
+  std::vector<double> u;
   std::int64_t iter = 0;
 };
 
+/// make_state (solvers.cpp:406-411): zeros.
 inline SolverState make_state(const SplitProblem& prob) {
   SolverState s;
-  s.n = prob.n;
-  s.x.assign(prob.domain_size(), 0.0);
+  s.x = ImageGrid(prob.n);
   s.u.assign(prob.range_size(), 0.0);
   return s;
 }
@@ -464,12 +832,27 @@ namespace detail {
 class Engine {
  public:
   Engine(const SplitProblem& prob, const SolverConfig& cfg, bool pdhg, int n_cg = 0) {
-    if (pdhg && cfg.mask) throw std::invalid_argument("pdhg uses M = gamma I; drop the mask");
-    if (n_cg > 0 && cfg.mask)
+    // pdhg_solve / admm_cg_solve preconditions (solvers.cpp:428-440)
+    if (pdhg && (cfg.mask || cfg.m_pinv_override))
+      throw std::invalid_argument("pdhg uses M = gamma I; drop the mask/overrides");
+    if (n_cg > 0 && (cfg.mask || cfg.m_pinv_override))
       throw std::invalid_argument("admm_cg uses M = alpha A^T A; drop the mask/overrides");
     if (!(cfg.alpha > 0.0)) throw std::invalid_argument("alpha must be positive");
-    if (cfg.mask && cfg.mask->n != prob.n)
+    // mode_from (solvers.cpp:75-79): Override > Mask > Scaled
+    const bool override_mode = !pdhg && n_cg == 0 && cfg.m_pinv_override != nullptr;
+    if (!override_mode && cfg.mask && cfg.mask->n != prob.n)
       throw std::invalid_argument("mask/problem size mismatch");
+    if (prob.kind == NCSG_PET && prob.poisson_alpha != cfg.alpha)  // PoissonConj::evaluate
+      throw std::invalid_argument("PoissonConj built for a different alpha");
+    auto circulant = [&](const std::shared_ptr<const LinearMap>& m, const char* what) {
+      const auto* c = dynamic_cast<const CirculantMap*>(m.get());
+      if (!c)
+        throw std::invalid_argument(std::string(what) +
+                                    ": the GPU engine applies explicit metrics as circulants; "
+                                    "pass a CirculantMap");
+      if (c->mask().n != prob.n) throw std::invalid_argument("mask/problem size mismatch");
+      return reinterpret_cast<const double*>(c->mask().h.data());
+    };
     ncsg_problem_desc d{};
     d.kind = prob.kind;
     d.n = prob.n;
@@ -484,7 +867,13 @@ class Engine {
     d.lambda = prob.lambda;
     d.gamma = (n_cg > 0 && !(cfg.gamma > 0.0)) ? 1.0 : cfg.gamma;  // unused by the CG update
     d.pinv_rel_tol = cfg.pinv_rel_tol;
-    d.mask = (!pdhg && cfg.mask) ? reinterpret_cast<const double*>(cfg.mask->h.data()) : nullptr;
+    d.mask = (!pdhg && !override_mode && cfg.mask)
+                 ? reinterpret_cast<const double*>(cfg.mask->h.data())
+                 : nullptr;
+    if (override_mode) {
+      d.m_pinv = circulant(cfg.m_pinv_override, "m_pinv_override");
+      if (cfg.m_override) d.m_symbol = circulant(cfg.m_override, "m_override");
+    }
     d.b = prob.offset.data();
     d.device = cfg.device;
     d.sparse = prob.sparse.get();
@@ -514,7 +903,10 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
   if (n_cg < 0) throw std::invalid_argument("n_cg must be >= 1");
   Engine eng(prob, cfg, pdhg, n_cg);
   SolverState s = init ? *init : make_state(prob);
-  check(ncsg_set_state(eng.get(), s.x.data(), s.u.data(), 0));
+  s.iter = 0;  // solve_template (solvers.cpp:272)
+  if (s.x.n != prob.n || s.u.size() != prob.range_size())  // Engine::init (solvers.cpp:118-121)
+    throw std::invalid_argument("state does not match problem");
+  check(ncsg_set_state(eng.get(), s.x.v.data(), s.u.data(), 0));
   int max_rows = cfg.max_iters / cfg.record_every + 3;
   std::vector<ncsg_record_row> rows(max_rows);
   int nr = 0;
@@ -527,10 +919,16 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
   SolveResult res;
   if (cfg.check_step_condition && n_cg == 0) {  // screen_step_condition (solvers.cpp:207-244)
     double shift = cfg.gamma;
-    if (!pdhg && cfg.mask) {
+    auto hmax_of = [](const SpectralMask& m) {
       double hmax = 0.0;
-      for (const auto& z : cfg.mask->h) hmax = std::max(hmax, std::abs(z));
-      shift = cfg.gamma + cfg.alpha * hmax;
+      for (const auto& z : m.h) hmax = std::max(hmax, std::abs(z));
+      return hmax;
+    };
+    if (!pdhg && cfg.m_pinv_override) {  // Override: 1.3 |lambda_max(M)| + 1 (solvers.cpp:219-226)
+      const auto* c = dynamic_cast<const CirculantMap*>(cfg.m_override.get());
+      shift = 1.3 * (c ? hmax_of(c->mask()) : 0.0) + 1.0;
+    } else if (!pdhg && cfg.mask) {
+      shift = cfg.gamma + cfg.alpha * hmax_of(*cfg.mask);
     }
     if (est > 1e-8 * std::max(1.0, shift)) {
       std::ostringstream os;
@@ -540,8 +938,7 @@ inline SolveResult solve(const SplitProblem& prob, const SolverConfig& cfg, bool
     }
   }
   res.state = std::move(s);
-  check(ncsg_get_state(eng.get(), res.state.x.data(), res.state.u.data(), nullptr));
-  res.state.iter = 0;
+  check(ncsg_get_state(eng.get(), res.state.x.v.data(), res.state.u.data(), &res.state.iter));
   for (int i = 0; i < nr; ++i)
     res.record.rows.push_back({rows[i].iter, rows[i].objective, rows[i].rel_subopt,
                                rows[i].seminorm_step, rows[i].wall_ms});
@@ -570,20 +967,24 @@ inline void write_record_csv(const std::string& path, const ConvergenceRecord& r
 /// ncs_step (solvers.cpp:417-421): one splitting iteration in place.
 inline void ncs_step(SolverState& state, const SplitProblem& prob, const SolverConfig& cfg) {
   detail::Engine eng(prob, cfg, false);
-  detail::check(ncsg_set_state(eng.get(), state.x.data(), state.u.data(), state.iter));
+  if (state.x.n != prob.n || state.u.size() != prob.range_size())
+    throw std::invalid_argument("state does not match problem");
+  detail::check(ncsg_set_state(eng.get(), state.x.v.data(), state.u.data(), state.iter));
   detail::check(ncsg_step(eng.get(), 1));
   std::int64_t div = -1;
   ncsg_status st = ncsg_sync(eng.get(), &div);
   if (st == NCSG_DIVERGED) throw DivergenceError(div, ncsg_last_error());  // absolute
   detail::check(st);
-  detail::check(ncsg_get_state(eng.get(), state.x.data(), state.u.data(), nullptr));
+  detail::check(ncsg_get_state(eng.get(), state.x.v.data(), state.u.data(), nullptr));
   ++state.iter;
 }
 
-/// ncs_solve (solvers.cpp:423-426).
+/// ncs_solve (solvers.cpp:423-426): the x-update mode follows mode_from
+/// (solvers.cpp:75-79) -- m_pinv_override (a CirculantMap), else the mask's
+/// pinv(gamma + alpha C), else M = gamma I (Scaled: the same iteration as
+/// pdhg_solve).
 inline SolveResult ncs_solve(const SplitProblem& prob, const SolverConfig& cfg,
                              const double* f_star = nullptr, const SolverState* init = nullptr) {
-  if (!cfg.mask) throw std::invalid_argument("ncs_solve needs cfg.mask (use pdhg_solve)");
   return detail::solve(prob, cfg, false, f_star, init);
 }
 
@@ -599,7 +1000,8 @@ inline SolveResult pdhg_solve(const SplitProblem& prob, const SolverConfig& cfg,
 inline SolveResult admm_cg_solve(const SplitProblem& prob, const SolverConfig& cfg, int n_cg,
                                  const double* f_star = nullptr,
                                  const SolverState* init = nullptr) {
-  if (cfg.mask) throw std::invalid_argument("admm_cg uses M = alpha A^T A; drop the mask/overrides");
+  if (cfg.mask || cfg.m_pinv_override)
+    throw std::invalid_argument("admm_cg uses M = alpha A^T A; drop the mask/overrides");
   if (n_cg < 1) throw std::invalid_argument("n_cg must be >= 1");
   return detail::solve(prob, cfg, true, f_star, init, n_cg);
 }

@@ -141,7 +141,9 @@ struct ncsg_problem {
   std::unique_ptr<RadonDev> radon;
   const SparseDev* sparse = nullptr;  // SparseMap projector (caller keeps the handle alive)
   FftPlan fft;
-  bool has_mask = false;
+  bool has_mask = false;          // an M symbol for the seminorm / screen is on the device
+  bool override_mode = false;     // m_pinv given (XMode::Override)
+  double gamma_m = 0.0;           // gamma of M = gamma I + alpha C (0 in Override mode)
   std::vector<std::complex<double>> mask_full;  // cfg.mask (apply_m)
   DevBuf<float2> maskT;       // herm(pinv(gamma + alpha C)) / N^2
   DevBuf<float2> maskT_orig;  // herm(C) / N^2 for apply_m (seminorm, screen)
@@ -541,6 +543,8 @@ void apply_filter(ncsg_problem* p, const float* img, const float2* maskT, float*
 // Engine::step_seminorm (solvers.cpp:166-177) on the last step's (dx, du).
 std::vector<double> seminorm_values(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
+  if (p->override_mode && !p->has_mask)  // Engine::apply_m, solvers.cpp:193-197
+    throw Error{NCSG_INVALID, "m_override is required alongside m_pinv_override"};
   launch_sub(p->x.p, p->x_prev.p, p->dx.p, p->nn * p->batch, s);
   launch_sub(p->u.p, p->u_prev.p, p->du.p, p->range * p->batch, s);
   stacked_forward(p, p->dx.p, p->dxT.p, p->adx.p);
@@ -548,7 +552,7 @@ std::vector<double> seminorm_values(ncsg_problem* p) {
   SemArgs a;
   a.n = p->d.n;
   a.alpha = p->d.alpha;
-  a.gamma = p->d.gamma;
+  a.gamma = p->gamma_m;
   a.du = p->du.p;
   a.adx = p->adx.p;
   a.range = p->range;
@@ -604,7 +608,16 @@ double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_
   } guard_batch{p, p->batch};
   p->batch = 1;
   double shift = p->d.gamma;
-  if (p->has_mask) {
+  if (p->override_mode) {
+    // screen_step_condition's Override branch (solvers.cpp:219-226) shifts by
+    // 1.3 |power_method(M, 15)| + 1; for a circulant M the power method
+    // converges to max |symbol|, used here directly (the screen only warns)
+    if (!p->has_mask)
+      throw Error{NCSG_INVALID, "m_override is required alongside m_pinv_override"};
+    double hmax = 0.0;
+    for (const auto& z : p->mask_full) hmax = std::max(hmax, std::abs(z));
+    shift = 1.3 * hmax + 1.0;
+  } else if (p->has_mask) {
     double hmax = 0.0;
     for (const auto& z : p->mask_full) hmax = std::max(hmax, std::abs(z));
     shift = p->d.gamma + p->d.alpha * hmax;
@@ -636,7 +649,7 @@ double screen_estimate(ncsg_problem* p, uint64_t seed, int iters, double* shift_
     launch_atu_assemble(atu_terms_for(p, av), atav, 1, s);
     if (cv) apply_filter(p, v, p->maskT_orig.p, cv);
     launch_screen_combine(v, atav, cv, static_cast<float>(p->d.alpha),
-                          static_cast<float>(p->d.gamma), static_cast<float>(shift), w, nn, s);
+                          static_cast<float>(p->gamma_m), static_cast<float>(shift), w, nn, s);
     launch_dot_pair(v, w, w, w, nn, 1, red.p, s);
     auto d = read_dot_pairs(red.p, 1, s);
     lambda = d[0];
@@ -1054,13 +1067,14 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     if (!(d.alpha > 0.0) || !(d.beta > 0.0))
       throw Error{NCSG_INVALID, "alpha and beta must be positive"};
     if (d.lambda < 0.0) throw Error{NCSG_INVALID, "lambda must be nonnegative"};
-    if (!d.mask && !(d.gamma > 0.0))
+    if (!d.mask && !d.m_pinv && !(d.gamma > 0.0))
       throw Error{NCSG_INVALID, "gamma must be positive when no mask is set"};
     if (!d.b) throw Error{NCSG_INVALID, "missing offset b"};
     auto p = std::make_unique<ncsg_problem>();
     p->d = d;
     p->d.mask = nullptr;
     p->d.b = nullptr;
+    p->d.m_pinv = p->d.m_symbol = nullptr;  // host pointers: not kept
     p->device = d.device;
     p->batch = d.batch;
     p->nn = static_cast<size_t>(d.n) * d.n;
@@ -1126,7 +1140,25 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
     // |m| compared squared and 1/m = conj(m)/|m|^2, the same filter to fp32).
     std::vector<float2> hm;  // herm(pinv(gamma + alpha C)) / N^2 on the half spectrum
     const double scale = 1.0 / (static_cast<double>(d.n) * d.n);
-    if (desc->mask) {
+    p->gamma_m = d.gamma;
+    if (desc->m_pinv) {
+      // Override mode (mode_from, solvers.cpp:75-79; Engine::step :138-140):
+      // w = m_pinv_override(A^T u), here a circulant given by its symbol; M
+      // for the seminorm / screen is the m_override symbol, stored as
+      // herm(M) / (alpha N^2) so that the Mask-mode kernels' gamma v +
+      // alpha (C v) become M v with gamma_m = 0.
+      p->override_mode = true;
+      hm = half_mask(d.n, read_mask(d.n, desc->m_pinv), scale);
+      if (desc->m_symbol) {
+        p->has_mask = true;
+        p->mask_full = read_mask(d.n, desc->m_symbol);
+        auto ho = half_mask(d.n, p->mask_full, scale / d.alpha);
+        p->maskT_orig.alloc(ho.size());
+        NCSG_CUDA_CHECK(cudaMemcpy(p->maskT_orig.p, ho.data(), ho.size() * sizeof(float2),
+                                   cudaMemcpyHostToDevice));
+      }
+      p->gamma_m = 0.0;
+    } else if (desc->mask) {
       p->has_mask = true;
       p->mask_full = read_mask(d.n, desc->mask);
       clk.mark("  read mask");
@@ -1471,7 +1503,7 @@ ncsg_status ncsg_set_cg(ncsg_problem* p, int n_cg) {
     // admm_cg_solve (solvers.cpp:435-440) / Engine Cg mode (solvers.cpp:111-113)
     if (n_cg < 0) throw Error{NCSG_INVALID, "n_cg must be >= 1"};
     if (n_cg > 0) {
-      if (p->has_mask)
+      if (p->has_mask || p->override_mode)
         throw Error{NCSG_INVALID, "admm_cg uses M = alpha A^T A; drop the mask/overrides"};
       if (p->batch != 1) throw Error{NCSG_INVALID, "the CG x-update runs one problem (batch 1)"};
       if (p->sharded) throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};

@@ -54,6 +54,7 @@ class ProblemDesc(C.Structure):
         ("pinv_rel_tol", C.c_double), ("mask", C.c_void_p), ("b", C.c_void_p),
         ("angle_begin", C.c_int), ("angle_end", C.c_int), ("device", C.c_int),
         ("sparse", C.c_void_p), ("shard_rank", C.c_int), ("shard_count", C.c_int),
+        ("m_pinv", C.c_void_p), ("m_symbol", C.c_void_p),
     ]
 
 

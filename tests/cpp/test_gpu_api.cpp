@@ -106,7 +106,7 @@ int main() {
     SolverState s = make_state(prob);
     ncs_step(s, prob, cfg);
     bool ok = true;
-    for (double v : s.x) ok = ok && v == 0.0;
+    for (double v : s.x.v) ok = ok && v == 0.0;
     for (std::size_t i = 0; i < sino.size(); ++i)
       ok = ok && std::abs(s.u[i] + p.alpha * sino[i] / (1 + p.alpha)) <=
                      1e-6 * (1 + std::abs(sino[i]));
@@ -116,8 +116,9 @@ int main() {
     cfg.max_iters = 5;
     cfg.record_every = 5;
     SolveResult r = ncs_solve(prob, cfg);
-    CHECK(r.state.x == a.x && r.state.u == a.u, "ncs_solve(5) == 5 x ncs_step (bitwise)");
-    CHECK(r.record.rows.size() == 2 && r.record.rows.back().iter == 5, "record rows");
+    CHECK(r.state.x.v == a.x.v && r.state.u == a.u, "ncs_solve(5) == 5 x ncs_step (bitwise)");
+    CHECK(r.record.rows.size() == 2 && r.record.rows.back().iter == 5 && r.state.iter == 5,
+          "record rows, final state iter");
     // divergence (test_solvers.cpp:627-644)
     SolverConfig bad;
     bad.alpha = p.alpha;
@@ -238,6 +239,144 @@ int main() {
     CHECK(pet.kind == NCSG_PET && pr.state.u.size() == pet.range_size() &&
               std::isinf(pr.record.rows[0].objective) && pr.record.rows.size() == 3,
           "PET-TV problem (PoissonConj) solves");
+  }
+  // The reference's generic problem API (solvers.hpp:17-78): CT-TV built
+  // block by block exactly as assemble_problem does (pipeline.cpp:84-97),
+  // the denoising SplitProblem of test_solvers.cpp:646-664, Scaled mode of a
+  // mask-free ncs_solve, and the m_pinv_override / m_override hooks.
+  {
+    int n = 32, A = 24, D = default_detector_count(n);
+    auto geom = std::make_shared<const RadonMap>(n, A, D);
+    auto truth = randn(geom->domain_size(), 31);
+    for (auto& v : truth) v = std::max(0.0, v);
+    std::vector<double> sino(geom->range_size());
+    geom->forward(truth, sino);
+    ModelParams p;
+    p.alpha = p.beta = 0.1;
+    p.lambda = 0.01;
+    p.positivity = true;
+    std::vector<SplitBlock> blocks;
+    blocks.push_back({1.0, geom, std::make_shared<QuadraticConj>(), sino});
+    blocks.push_back({p.beta / p.alpha, std::make_shared<GradMap>(n),
+                      std::make_shared<ScaledL1Conj>(p.lambda * p.alpha / p.beta), {}});
+    blocks.push_back({1.0, std::make_shared<IdentityMap>(geom->domain_size()),
+                      std::make_shared<NonnegConj>(), {}});
+    SplitProblem by_blocks(n, blocks);
+    SplitProblem assembled = assemble_problem(sino, *geom, p);
+    CHECK(by_blocks.range_size() == assembled.range_size() &&
+              by_blocks.range_size() == geom->range_size() + 2u * n * (n - 1) + n * n &&
+              by_blocks.block_offset(2) == geom->range_size() + 2u * n * (n - 1),
+          "SplitProblem(n, blocks) stacked layout");
+    SolverConfig cfg;
+    cfg.alpha = p.alpha;
+    cfg.gamma = 400.0;
+    cfg.mask = metric_mask(radon_mask(n, 100.0, 400.0), p);
+    cfg.max_iters = 20;
+    cfg.record_every = 10;
+    cfg.check_step_condition = false;
+    SolveResult r1 = ncs_solve(by_blocks, cfg), r2 = ncs_solve(assembled, cfg);
+    CHECK(r1.state.x.v == r2.state.x.v && r1.state.u == r2.state.u &&
+              r1.objective == r2.objective,
+          "block-built CT-TV problem == assemble_problem (bitwise)");
+    // host objective of the block list against the device record
+    double f_host = by_blocks.objective(r1.state.x.v);
+    CHECK(std::abs(f_host - r1.objective) <= 1e-5 * std::abs(f_host), "SplitProblem::objective");
+    // Scaled mode: ncs_solve without a mask is pdhg_solve (mode_from, solvers.cpp:75-79)
+    SolverConfig sc = cfg;
+    sc.mask.reset();
+    sc.gamma = 50.0 * A * n;
+    SolveResult s1 = ncs_solve(by_blocks, sc), s2 = pdhg_solve(by_blocks, sc);
+    CHECK(s1.state.x.v == s2.state.x.v && s1.state.u == s2.state.u,
+          "mask-free ncs_solve == pdhg_solve (bitwise)");
+    // Override mode with circulant metrics equals Mask mode
+    SpectralMask m(n);
+    for (std::size_t i = 0; i < m.h.size(); ++i) m.h[i] = cfg.gamma + cfg.alpha * cfg.mask->h[i];
+    SolverConfig oc = cfg;
+    oc.mask.reset();
+    oc.m_pinv_override = std::make_shared<CirculantMap>(pinv_mask(m, cfg.pinv_rel_tol));
+    oc.m_override = std::make_shared<CirculantMap>(m);
+    SolveResult o1 = ncs_solve(by_blocks, oc);
+    double num = 0, den = 0;
+    for (std::size_t i = 0; i < o1.state.x.v.size(); ++i) {
+      num += std::pow(o1.state.x.v[i] - r1.state.x.v[i], 2);
+      den += std::pow(r1.state.x.v[i], 2);
+    }
+    bool rows_ok = o1.record.rows.size() == r1.record.rows.size();
+    for (std::size_t i = 0; rows_ok && i < o1.record.rows.size(); ++i)
+      rows_ok = std::abs(o1.record.rows[i].seminorm_step - r1.record.rows[i].seminorm_step) <=
+                1e-4 * std::max(1.0, std::abs(r1.record.rows[i].seminorm_step));
+    CHECK(std::sqrt(num / den) <= 1e-6 && rows_ok,
+          "m_pinv_override / m_override (CirculantMap) == mask mode");
+    SolverConfig oc2 = oc;
+    oc2.m_override.reset();
+    bool need = false;
+    try {
+      ncs_solve(by_blocks, oc2);
+    } catch (const std::invalid_argument& e) {
+      need = std::string(e.what()).find("m_override is required") != std::string::npos;
+    }
+    CHECK(need, "m_override required alongside m_pinv_override");
+    bool explicit_rejected = false;
+    SolverConfig oc3 = oc;
+    oc3.m_pinv_override = std::make_shared<GradMap>(n);  // not a circulant
+    try {
+      ncs_solve(by_blocks, oc3);
+    } catch (const std::invalid_argument&) {
+      explicit_rejected = true;
+    }
+    CHECK(explicit_rejected, "non-circulant metric override rejected");
+    bool unsupported = false;
+    try {
+      std::vector<SplitBlock> one;
+      one.push_back({10.0, std::make_shared<IdentityMap>(16), std::make_shared<QuadraticConj>(),
+                     randn(16, 98)});
+      SplitProblem bad(4, std::move(one));
+    } catch (const std::invalid_argument& e) {
+      unsupported = std::string(e.what()).find("no GPU kernel") != std::string::npos;
+    }
+    CHECK(unsupported, "block list without a device kernel rejected");
+    bool dom = false;
+    try {
+      std::vector<SplitBlock> wrong;
+      wrong.push_back({1.0, std::make_shared<GradMap>(8), std::make_shared<QuadraticConj>(), {}});
+      SplitProblem bad(4, std::move(wrong));
+    } catch (const std::invalid_argument& e) {
+      dom = std::string(e.what()) == "block domain does not match the image size";
+    }
+    CHECK(dom, "SplitProblem validation message (solvers.cpp:346-347)");
+    // TV denoising as the SplitProblem of test_solvers.cpp:646-664 / make_tv
+    int nd = 16;
+    auto noisy = randn(nd * nd, 41);
+    std::vector<SplitBlock> tv;
+    tv.push_back({1.0, std::make_shared<IdentityMap>(nd * nd), std::make_shared<QuadraticConj>(),
+                  noisy});
+    tv.push_back({0.05 / 0.05, std::make_shared<GradMap>(nd), std::make_shared<ScaledL1Conj>(0.3),
+                  {}});
+    SplitProblem tvp(nd, std::move(tv));
+    ModelParams dp;
+    dp.alpha = dp.beta = 0.05;
+    dp.lambda = 0.3;
+    SplitProblem tvd = denoise_problem(noisy, nd, dp);
+    SolverConfig tc;
+    tc.alpha = 0.05;
+    tc.gamma = 1.0;
+    tc.mask = laplacian_mask_2d(nd);
+    tc.max_iters = 30;
+    tc.record_every = 10;
+    SolveResult t1 = ncs_solve(tvp, tc), t2 = ncs_solve(tvd, tc);
+    CHECK(tvp.kind == NCSG_DENOISE && t1.state.x.v == t2.state.x.v && t1.objective == t2.objective,
+          "denoising SplitProblem by blocks == denoise_problem (bitwise)");
+    // an initial state is taken and replayed stepwise (test_solvers.cpp:607-625)
+    SolverState init = make_state(tvp);
+    init.x.v = randn(init.x.v.size(), 96);
+    init.u = randn(init.u.size(), 97);
+    tc.max_iters = 5;
+    SolveResult ri = ncs_solve(tvp, tc, nullptr, &init);
+    SolverState manual = init;
+    manual.iter = 0;
+    for (int k = 0; k < 5; ++k) ncs_step(manual, tvp, tc);
+    CHECK(ri.state.x.v == manual.x.v && ri.state.u == manual.u && ri.state.iter == 5,
+          "solve from an initial state replays the stepwise path");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
