@@ -304,6 +304,51 @@ ncsg_status ncsg_step_phase_b(ncsg_problem* p);
  * and the number of profiled steps. */
 ncsg_status ncsg_profile_begin(ncsg_problem* p);
 ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int* steps);
+/* ------------------------------------------------------------ multi-GPU
+ * Communicator of a sharded problem.  A problem created with
+ * an angle or orbit shard (angle_begin/angle_end, shard_rank/shard_count)
+ * holds only its rank's rows of R; with a communicator attached, ncsg_step /
+ * ncsg_step_graph* / ncsg_solve run the whole sharded iteration
+ * (Engine::step, solvers.cpp:124-161, with the StackedMap::adjoint sum of
+ * linear_map.cpp:47-55 across ranks):
+ *   NCSG_XCHG_SLAB       partial A^T u -> reduce-scatter into N/P-row slabs ->
+ *                        slab row FFT -> all-to-all -> column FFT . filter .
+ *                        inverse -> all-to-all -> slab inverse rows + x update
+ *                        -> all-gather of x (N % P == 0);
+ *   NCSG_XCHG_ALLREDUCE  one all-reduce of the partial A^T u, replicated
+ *                        circulant solve on every rank (latency-bound sizes).
+ * Objective / seminorm records and the divergence flags are reduced across
+ * ranks.  (* graph capture only with the NCCL transport.)
+ * Transports: NCCL (one communicator per rank, from a unique id shared by
+ * the caller -- MPI, torch.distributed, a file), caller callbacks, or an
+ * in-process group of ranks driven by host threads (tests, one GPU). */
+typedef struct ncsg_comm ncsg_comm;
+typedef enum { NCSG_F32 = 0, NCSG_F64 = 1, NCSG_I32 = 2 } ncsg_dtype;
+typedef enum { NCSG_SUM = 0, NCSG_MIN = 1, NCSG_MAX = 2 } ncsg_redop;
+typedef enum { NCSG_XCHG_ALLREDUCE = 0, NCSG_XCHG_SLAB = 1 } ncsg_exchange;
+/* Callback transport: device pointers; the library synchronises `stream`
+ * before each call and expects the result complete in device memory on
+ * return (a pageable H2D cudaMemcpy alone is not: synchronise after it, or
+ * copy on `stream` and synchronise that); 0 = success. */
+typedef struct ncsg_comm_ops {
+  void* ctx;
+  int rank, nranks;
+  int (*all_reduce)(void* ctx, void* buf, size_t count, int dtype, int op, void* stream);
+  int (*reduce_scatter)(void* ctx, const float* send, float* recv, size_t count, void* stream);
+  int (*all_gather)(void* ctx, const float* send, float* recv, size_t count, void* stream);
+  int (*all_to_all)(void* ctx, const float* send, float* recv, size_t count, void* stream);
+} ncsg_comm_ops;
+ncsg_status ncsg_nccl_unique_id(unsigned char id[128]);
+ncsg_status ncsg_comm_create_nccl(const unsigned char id[128], int rank, int nranks, int device,
+                                  ncsg_comm** out);
+ncsg_status ncsg_comm_create_callbacks(const ncsg_comm_ops* ops, ncsg_comm** out);
+/* nranks communicators of one in-process group (out[r] = rank r). */
+ncsg_status ncsg_comm_create_local(int nranks, ncsg_comm** out);
+ncsg_status ncsg_comm_destroy(ncsg_comm* c);
+/* Attach (or with NULL detach) the communicator; `exchange` = ncsg_exchange.
+ * The communicator must outlive the problem's use of it. */
+ncsg_status ncsg_problem_set_comm(ncsg_problem* p, ncsg_comm* c, int exchange);
+
 /* The live plan of a problem (bench.py's roofline: the partial-sum counts
  * and sample count the per-kernel byte models use). */
 typedef struct ncsg_plan_info {

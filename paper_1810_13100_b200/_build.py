@@ -16,8 +16,8 @@ CUDA = os.environ.get("CUDA_HOME", "/usr/local/cuda")
 NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CU_SRCS = ["radon_kernels.cu", "fft_kernels.cu", "ncs_kernels.cu", "sparse_kernels.cu", "capi.cu"]
-CPP_SRCS = ["geometry.cpp", "fanbeam.cpp"]
-HDRS = ["ncsg_internal.cuh", "ncs_kernels.cuh", "ncs_device.cuh"]
+CPP_SRCS = ["geometry.cpp", "fanbeam.cpp", "comm.cpp"]
+HDRS = ["ncsg_internal.cuh", "ncs_kernels.cuh", "ncs_device.cuh", "ncsg_comm.hpp"]
 
 
 def _newer(target: str, deps: list[str]) -> bool:

@@ -19,6 +19,7 @@
 
 #include "host_rng.hpp"
 #include "ncs_kernels.cuh"
+#include "ncsg_comm.hpp"
 #include "ncsg_internal.cuh"
 
 namespace ncsg {
@@ -175,6 +176,14 @@ struct ncsg_problem {
   DevBuf<double> cg_x, cg_r, cg_p;  // fp64 CG iterates
   DevBuf<float> cg_p32, cg_ap;       // operator input / output
   std::map<int, cudaGraphExec_t> graphs;
+  // multi-GPU (ncsg_problem_set_comm): the cross-rank exchange of a sharded
+  // step; slab mode: rows [rank R, rank R + R) of the image, wc spectrum
+  // columns per rank (P wc >= N/2+1, padded), the filter padded likewise
+  ncsg::Comm* comm = nullptr;
+  int xchg = NCSG_XCHG_ALLREDUCE;
+  int slab_R = 0, slab_logR = 0, slab_wc = 0;
+  DevBuf<float> atu_full, atu_slab;
+  DevBuf<float2> spec_slab, spec_recv, maskT_pad;
   // phase profiling (bench.py): events recorded between the phases of do_step
   bool profiling = false;
   std::vector<cudaEvent_t> events;  // kPhases + 1 per profiled step
@@ -387,7 +396,66 @@ void refresh_u4(ncsg_problem* p) {
   p->u4_fresh = true;
 }
 
+// One sharded step with the communicator (Engine::step,
+// solvers.cpp:124-161, with StackedMap::adjoint's sum, linear_map.cpp:47-55,
+// taken across ranks).  Every rank: its partial A^T u (own angles; rank 0
+// also the replicated D^T u_g / identity terms) as one image, then
+//   ALLREDUCE: all-reduce of the image, replicated circulant solve;
+//   SLAB:      reduce-scatter into N/P-row slabs, row FFT of the own slab,
+//              all-to-all transpose to wc-column slabs, column FFT . filter .
+//              inverse, all-to-all back, inverse rows + x update of the own
+//              rows, all-gather of x;
+// and the forward + dual update of the own rays and the replicated u_g.
+void sharded_step(ncsg_problem* p) {
+  cudaStream_t s = p->stream.s;
+  ncsg::Comm& C = *p->comm;
+  phase_a(p);
+  float* atu = p->atu_full.p;
+  AtuTerms T = atu_terms(p);
+  launch_atu_assemble(T, atu, p->batch, s);
+  if (p->xchg == NCSG_XCHG_ALLREDUCE) {
+    C.all_reduce(atu, p->nn * p->batch, NCSG_F32, NCSG_SUM, s);
+    phase_b(p, atu);
+    return;
+  }
+  const int n = p->d.n, P = C.nranks(), R = p->slab_R, wc = p->slab_wc;
+  const int r0 = C.rank() * R;
+  mark(p);
+  C.reduce_scatter(atu, p->atu_slab.p, static_cast<size_t>(R) * n, s);
+  AtuTerms S;
+  S.n = n;
+  S.plain = p->atu_slab.p - static_cast<size_t>(r0) * n;  // rows addressed globally
+  S.counter = step_counter(p);
+  const RowSlab rs{r0, R, R, static_cast<size_t>(P) * wc * R};
+  launch_fft_rows_r2c(p->fft, S, p->spec_slab.p, 1, s, rs);
+  mark(p);
+  const size_t chunk = 2 * static_cast<size_t>(wc) * R;  // floats per rank block
+  C.all_to_all(reinterpret_cast<const float*>(p->spec_slab.p),
+               reinterpret_cast<float*>(p->spec_recv.p), chunk, s);
+  const int nk = n / 2 + 1;
+  ColSlab cs{p->slab_logR, wc, C.rank() * wc, std::max(0, std::min(wc, nk - C.rank() * wc))};
+  launch_fft_cols_filter_slab(p->fft, p->spec_recv.p, p->maskT_pad.p, cs, s);
+  C.all_to_all(reinterpret_cast<const float*>(p->spec_recv.p),
+               reinterpret_cast<float*>(p->spec_slab.p), chunk, s);
+  mark(p);
+  NCSG_CUDA_CHECK(cudaMemcpyAsync(p->x_old.p, p->x.p, p->nn * 4, cudaMemcpyDeviceToDevice, s));
+  XUpdate xu;
+  xu.x = p->x.p;
+  xu.subtract = 1;
+  xu.flag = p->flag.p;
+  launch_fft_rows_c2r(p->fft, p->spec_slab.p, xu, 1, s, rs);
+  float* own_rows = p->x.p + static_cast<size_t>(r0) * n;
+  C.all_gather(own_rows, p->x.p, static_cast<size_t>(R) * n, s);
+  if (p->radon && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
+    launch_transpose(p->x.p, p->xT.p, n, 1, s);  // class-H forward input
+  forward_and_dual(p);
+}
+
 void do_step(ncsg_problem* p) {
+  if (p->comm) {
+    sharded_step(p);
+    return;
+  }
   phase_a(p);
   phase_b(p);
 }
@@ -422,6 +490,8 @@ void reset_flag(ncsg_problem* p) {
 // in the same step wins.
 void check_divergence(ncsg_problem* p, int64_t* diverged_iter = nullptr) {
   int h[3];
+  if (p->comm)  // a rank's own rays / rows: every rank sees the first bad step
+    p->comm->all_reduce(p->flag.p, 3, NCSG_I32, NCSG_MIN, p->stream.s);
   NCSG_CUDA_CHECK(cudaMemcpyAsync(h, p->flag.p, sizeof(h), cudaMemcpyDeviceToHost, p->stream.s));
   NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
   if (h[0] != INT_MAX || h[2] != INT_MAX) {
@@ -466,6 +536,17 @@ std::vector<double> objective_values(ncsg_problem* p) {
       l1 += r[1];
       mx = std::max(mx, r[2]);
       mn = std::min(mn, r[3]);
+    }
+    if (p->comm) {  // own rays' data term + rank 0's D term, summed over ranks
+      double qs[2] = {q, l1};
+      DevBuf<double> t;
+      t.alloc(2);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(t.p, qs, sizeof qs, cudaMemcpyHostToDevice, s));
+      p->comm->all_reduce(t.p, 2, NCSG_F64, NCSG_SUM, s);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(qs, t.p, sizeof qs, cudaMemcpyDeviceToHost, s));
+      NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+      q = qs[0];
+      l1 = qs[1];
     }
     // QuadraticConj / PoissonConj::objective + ScaledL1Conj::objective (prox.cpp:26-70)
     double total = (p->d.kind == NCSG_PET ? q : 0.5 * q) + static_cast<double>(p->bound) * l1;
@@ -561,6 +642,14 @@ std::vector<double> seminorm_values(ncsg_problem* p) {
   a.dx = p->dx.p;
   a.mdx = p->has_mask ? p->mdx.p : nullptr;
   a.out = p->red.p;
+  if (p->sharded) {
+    a.m0 = p->m0;
+    a.m_begin = p->m_begin;
+    a.m_end = p->m_end;
+    a.own = p->own_angle.p;
+    a.det = p->d.n_det;
+    a.rank0 = p->rank0 ? 1 : 0;
+  }
   launch_seminorm(a, p->batch, s);
   const int nb = objective_blocks();
   std::vector<double> h(static_cast<size_t>(p->batch) * nb * 3);
@@ -575,6 +664,18 @@ std::vector<double> seminorm_values(ncsg_problem* p) {
       t1 += r[0];
       aq += r[1];
       mq += r[2];
+    }
+    if (p->comm) {  // the ranks' shares of the three sums
+      double v3[3] = {t1, aq, mq};
+      DevBuf<double> t;
+      t.alloc(3);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(t.p, v3, sizeof v3, cudaMemcpyHostToDevice, s));
+      p->comm->all_reduce(t.p, 3, NCSG_F64, NCSG_SUM, s);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(v3, t.p, sizeof v3, cudaMemcpyDeviceToHost, s));
+      NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+      t1 = v3[0];
+      aq = v3[1];
+      mq = v3[2];
     }
     double a_quad = p->d.alpha * p->d.alpha * aq;
     double m_quad = p->n_cg > 0 ? a_quad : p->d.alpha * mq;  // Cg: M = alpha A^T A (solvers.cpp:174)
@@ -1291,12 +1392,14 @@ ncsg_status ncsg_get_state(ncsg_problem* p, double* x, double* u, int64_t* iter)
 
 // A sharded problem holds only its rank's part of A^T u: its steps need the
 // cross-rank sum between the phases (ncsg_step_phase_a / _b, or the
-// communicator path), so the whole-step entry points refuse it.
+// communicator path), so the whole-step entry points refuse it without a
+// communicator.
 void reject_sharded(const ncsg_problem* p, const char* what) {
-  if (p->sharded)
+  if (p->sharded && !p->comm)
     throw Error{NCSG_INVALID, std::string(what) +
                                   " needs the unsharded problem (a sharded one steps through "
-                                  "ncsg_step_phase_a/_b with the cross-rank sum in between)"};
+                                  "ncsg_step_phase_a/_b with the cross-rank sum in between, "
+                                  "or with a communicator: ncsg_problem_set_comm)"};
 }
 
 ncsg_status ncsg_step(ncsg_problem* p, int iters) {
@@ -1313,7 +1416,9 @@ ncsg_status ncsg_step_graph(ncsg_problem* p, int iters) {
     reject_sharded(p, "ncsg_step_graph");
     NCSG_CUDA_CHECK(cudaSetDevice(p->device));
     if (iters <= 0) return;
-    if (p->n_cg > 0) {  // CG reads its scalars back every step: not capturable
+    if (p->n_cg > 0 || (p->comm && !p->comm->capturable())) {
+      // CG reads its scalars back every step, host-driven transports
+      // synchronise inside the step: neither is capturable
       for (int k = 0; k < iters; ++k) do_step(p);
       p->iter += iters;
       return;
@@ -1390,6 +1495,95 @@ ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int
 }
 
 int64_t ncsg_launch_count(void) { return ncsg::launch_count(); }
+
+struct ncsg_comm {
+  std::unique_ptr<ncsg::Comm> c;
+};
+
+ncsg_status ncsg_nccl_unique_id(unsigned char id[128]) {
+  return guard([&] { ncsg::nccl_unique_id(id); });
+}
+
+ncsg_status ncsg_comm_create_nccl(const unsigned char id[128], int rank, int nranks, int device,
+                                  ncsg_comm** out) {
+  return guard([&] {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks)
+      throw Error{NCSG_INVALID, "invalid NCCL communicator arguments"};
+    auto c = std::make_unique<ncsg_comm>();
+    c->c.reset(ncsg::make_nccl_comm(id, rank, nranks, device));
+    *out = c.release();
+  });
+}
+
+ncsg_status ncsg_comm_create_callbacks(const ncsg_comm_ops* ops, ncsg_comm** out) {
+  return guard([&] {
+    if (!ops || !out || ops->nranks < 1 || ops->rank < 0 || ops->rank >= ops->nranks)
+      throw Error{NCSG_INVALID, "invalid communicator callbacks"};
+    auto c = std::make_unique<ncsg_comm>();
+    c->c.reset(ncsg::make_callback_comm(*ops));
+    *out = c.release();
+  });
+}
+
+ncsg_status ncsg_comm_create_local(int nranks, ncsg_comm** out) {
+  return guard([&] {
+    if (!out || nranks < 1) throw Error{NCSG_INVALID, "invalid local group size"};
+    auto g = ncsg::make_local_group(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      out[r] = new ncsg_comm;
+      out[r]->c.reset(g[r]);
+    }
+  });
+}
+
+ncsg_status ncsg_comm_destroy(ncsg_comm* c) {
+  return guard([&] { delete c; });
+}
+
+ncsg_status ncsg_problem_set_comm(ncsg_problem* p, ncsg_comm* c, int exchange) {
+  return guard([&] {
+    NCSG_CUDA_CHECK(cudaSetDevice(p->device));
+    for (auto& kv : p->graphs) cudaGraphExecDestroy(kv.second);  // captured without / with it
+    p->graphs.clear();
+    if (!c) {
+      p->comm = nullptr;
+      return;
+    }
+    ncsg::Comm& C = *c->c;
+    if (exchange != NCSG_XCHG_ALLREDUCE && exchange != NCSG_XCHG_SLAB)
+      throw Error{NCSG_INVALID, "unknown exchange mode"};
+    if (p->n_cg > 0) throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};
+    if (p->d.shard_count > 1 && (p->d.shard_count != C.nranks() || p->d.shard_rank != C.rank()))
+      throw Error{NCSG_INVALID, "orbit shard does not match the communicator's rank / size"};
+    const int n = p->d.n, P = C.nranks();
+    p->atu_full.alloc(p->nn * p->batch);
+    if (exchange == NCSG_XCHG_SLAB) {
+      const int R = n / P;
+      if (p->batch != 1) throw Error{NCSG_INVALID, "the slab FFT runs one problem (batch 1)"};
+      if (n % P != 0 || R % 2 != 0 || (R & (R - 1)) != 0)
+        throw Error{NCSG_INVALID, "the slab FFT needs N / ranks to be an even power of two"};
+      const int nk = n / 2 + 1, wc = (nk + P - 1) / P;
+      p->slab_R = R;
+      p->slab_logR = 0;
+      while ((1 << p->slab_logR) < R) ++p->slab_logR;
+      p->slab_wc = wc;
+      p->atu_slab.alloc(static_cast<size_t>(R) * n);
+      p->spec_slab.alloc(static_cast<size_t>(P) * wc * R);
+      p->spec_recv.alloc(static_cast<size_t>(P) * wc * R);
+      p->spec_slab.zero(p->stream.s);  // padded columns stay finite
+      p->spec_recv.zero(p->stream.s);
+      p->maskT_pad.alloc(static_cast<size_t>(P) * wc * n);
+      p->maskT_pad.zero(p->stream.s);
+      NCSG_CUDA_CHECK(cudaMemcpyAsync(p->maskT_pad.p, p->maskT.p,
+                                      static_cast<size_t>(nk) * n * sizeof(float2),
+                                      cudaMemcpyDeviceToDevice, p->stream.s));
+      ensure_scratch(p);
+    }
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+    p->comm = &C;
+    p->xchg = exchange;
+  });
+}
 
 ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out) {
   return guard([&] {

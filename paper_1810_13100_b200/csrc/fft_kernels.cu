@@ -229,11 +229,12 @@ __device__ __forceinline__ float2* fft_run(float2* a, float2* b, int nfft, const
 }
 
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
-                                    const float2* __restrict__ tw, FftShape sh) {
+                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
   pdl_wait();
   extern __shared__ float2 zs[];
   const int n = T.n;
-  const int y0 = blockIdx.x * kRowsPerBlock;
+  const int y0 = rs.r0 + blockIdx.x * kRowsPerBlock;
+  const int yend = rs.r0 + rs.rows;  // rows [r0, r0 + rows) of the image
   const int b = blockIdx.y;
   const int npair = kRowsPerBlock / 2;
   float2* zb = zs + npair * n;  // Stockham scratch
@@ -245,7 +246,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     for (int i = threadIdx.x; i < kRowsPerBlock * n / 4; i += blockDim.x) {
       const int r = (4 * i) / n, x = 4 * i - r * n;
       const int y = y0 + r;
-      const float4 v = y < n ? atu_rowmajor4(T, b, y, x) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 v = y < yend ? atu_rowmajor4(T, b, y, x) : make_float4(0.f, 0.f, 0.f, 0.f);
       float2* slot = zs + (r >> 1) * n + x;
       if (r & 1) {
         slot[0].y = v.x, slot[1].y = v.y, slot[2].y = v.z, slot[3].y = v.w;
@@ -257,7 +258,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
       const int r = i / n, x = i - r * n;
       const int y = y0 + r;
-      const float v = y < n ? atu_rowmajor(T, b, y, x) : 0.f;
+      const float v = y < yend ? atu_rowmajor(T, b, y, x) : 0.f;
       float2* slot = zs + (r >> 1) * n + x;
       if (r & 1)
         slot->y = v;
@@ -273,7 +274,7 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
     for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
       const int x = i / kRowsPerBlock, r = i - x * kRowsPerBlock;
       const int y = y0 + r;
-      if (y >= n) continue;
+      if (y >= yend) continue;
       float v = 0.f;
       const float* p = base + static_cast<size_t>(x) * n + y;
       for (int c = 0; c < T.nH; ++c) v += p[c * nn];
@@ -288,23 +289,23 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
   // Unpack the two real rows of each pair: A = (Z_k + conj Z_-k)/2,
   // B = (Z_k - conj Z_-k)/(2i); write specT[k][y] (k = 0..n/2).
   const int nk = n / 2 + 1;
-  float2* out = specT + static_cast<size_t>(b) * nk * n;
+  float2* out = specT + static_cast<size_t>(b) * rs.bstride;
   // one thread per (row pair, k): both rows' bins leave as one float4 (even n)
   for (int i = threadIdx.x; i < nk * (kRowsPerBlock / 2); i += blockDim.x) {
     const int k = i / (kRowsPerBlock / 2), q = i - k * (kRowsPerBlock / 2);
     const int y = y0 + 2 * q;
-    if (y >= n) continue;
+    if (y >= yend) continue;
     const float2* zq = z + q * n;
     const float2 zk = zq[k];
     const float2 zm = zq[(n - k) % n];
     const float2 va = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
     const float2 vb = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-    float2* dst = out + static_cast<size_t>(k) * n + y;
-    if (y + 1 < n && (n & 1) == 0) {
+    float2* dst = out + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    if (y + 1 < yend && ((n | rs.ld | rs.r0) & 1) == 0) {
       *reinterpret_cast<float4*>(dst) = make_float4(va.x, va.y, vb.x, vb.y);
     } else {
       dst[0] = va;
-      if (y + 1 < n) dst[1] = vb;
+      if (y + 1 < yend) dst[1] = vb;
     }
   }
 }
@@ -372,6 +373,38 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   }
 }
 
+// Sharded column pass: the same transform on a rank's column slab after the
+// all-to-all (ColSlab addressing: P row blocks of R bins per column).
+__global__ void fft_cols_filter_slab_kernel(float2* __restrict__ slab,
+                                            const float2* __restrict__ maskT,
+                                            const float2* __restrict__ tw, FftShape sh,
+                                            ColSlab cs) {
+  pdl_wait();
+  const int n = sh.n;
+  extern __shared__ float2 zs[];
+  const int c0 = blockIdx.x * kColsPerBlock;
+  const int nc = min(kColsPerBlock, cs.ncols - c0);
+  const int R = 1 << cs.logR;
+  float2* zb = zs + kColsPerBlock * n;
+  auto at = [&](int c, int j) -> size_t {
+    return (static_cast<size_t>((j >> cs.logR) * cs.wc + c0 + c) << cs.logR) + (j & (R - 1));
+  };
+  for (int i = threadIdx.x; i < nc * n; i += blockDim.x) {
+    const int c = i / n, j = i - c * n;
+    zs[i] = slab[at(c, j)];
+  }
+  float2* z = fft_run<-1>(zs, zb, nc, sh, tw);
+  for (int i = threadIdx.x; i < nc * n; i += blockDim.x) {
+    const int c = i / n, j = i - c * n;
+    z[i] = cmul(z[i], __ldg(maskT + static_cast<size_t>(cs.k0 + c0 + c) * n + j));
+  }
+  z = fft_run<+1>(z, z == zs ? zb : zs, nc, sh, tw);
+  for (int i = threadIdx.x; i < nc * n; i += blockDim.x) {
+    const int c = i / n, j = i - c * n;
+    slab[at(c, j)] = z[i];
+  }
+}
+
 // Forward column FFTs only (in place): with the row pass this is the
 // unnormalised forward 2-D FFT of a real image as a half spectrum
 // (empirical_mask's F v, circulant.cpp:111-117).
@@ -391,15 +424,16 @@ __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
 }
 
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
-                                    const float2* __restrict__ tw, FftShape sh) {
+                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
   pdl_wait();
   const int n = sh.n;
   extern __shared__ float2 zs[];
-  const int y0 = blockIdx.x * kRowsPerBlock;
+  const int y0 = rs.r0 + blockIdx.x * kRowsPerBlock;
+  const int yend = rs.r0 + rs.rows;
   const int b = blockIdx.y;
   const int nk = n / 2 + 1;
   const size_t nn = static_cast<size_t>(n) * n;
-  const float2* in = specT + static_cast<size_t>(b) * nk * n;
+  const float2* in = specT + static_cast<size_t>(b) * rs.bstride;
   float2* zb = zs + (kRowsPerBlock / 2) * n;  // Stockham scratch
   // x (to be updated) streams into shared memory with cp.async now, so its
   // latency overlaps the spectrum load and the transform
@@ -408,7 +442,7 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   if (x_pre) {
     for (int i = threadIdx.x; i < kRowsPerBlock * n / 4; i += blockDim.x) {
       const int r = (4 * i) / n, x = 4 * i - r * n;
-      if (y0 + r >= n) continue;
+      if (y0 + r >= yend) continue;
       const float* src = xu.x + b * nn + static_cast<size_t>(y0 + r) * n + x;
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(xs + 4 * i));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
@@ -422,13 +456,13 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     const int k = i / (kRowsPerBlock / 2), q = i - k * (kRowsPerBlock / 2);
     const int y = y0 + 2 * q;
     float4 g = make_float4(0.f, 0.f, 0.f, 0.f);  // (G_a, G_b) of rows y, y + 1
-    const float2* src = in + static_cast<size_t>(k) * n + y;
-    if (y + 1 < n && (n & 1) == 0) {  // 16-byte aligned pair
+    const float2* src = in + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    if (y + 1 < yend && ((n | rs.ld | rs.r0) & 1) == 0) {  // 16-byte aligned pair
       g = *reinterpret_cast<const float4*>(src);
-    } else if (y < n) {
+    } else if (y < yend) {
       const float2 ga = src[0];
       g.x = ga.x, g.y = ga.y;
-      if (y + 1 < n) {
+      if (y + 1 < yend) {
         const float2 gb = src[1];
         g.z = gb.x, g.w = gb.y;
       }
@@ -449,7 +483,7 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     const int i = 4 * i4;
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
-    if (y >= n) continue;
+    if (y >= yend) continue;
     float2* zr = z + (r >> 1) * n + x;
     const float4 xo = *reinterpret_cast<const float4*>(xs + i);
     const size_t gi = b * nn + static_cast<size_t>(y) * n + x;
@@ -472,7 +506,7 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   for (int i = threadIdx.x; i < kRowsPerBlock * n && !x_pre; i += blockDim.x) {
     const int r = i / n, x = i - r * n;
     const int y = y0 + r;
-    if (y >= n) continue;
+    if (y >= yend) continue;
     const float2 zz = z[(r >> 1) * n + x];
     const float w = (r & 1) ? zz.y : zz.x;
     const size_t gi = b * nn + static_cast<size_t>(y) * n + x;
@@ -500,7 +534,7 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
     for (int i = threadIdx.x; i < kRowsPerBlock * n; i += blockDim.x) {
       const int x = i / kRowsPerBlock, r = i - x * kRowsPerBlock;
       const int y = y0 + r;
-      if (y >= n) continue;
+      if (y >= yend) continue;
       const float2 zz = z[(r >> 1) * n + x];
       xu.xT[b * nn + static_cast<size_t>(x) * n + y] = (r & 1) ? zz.y : zz.x;
     }
@@ -553,14 +587,15 @@ void FftPlan::init(int n_, cudaStream_t s) {
 }
 
 void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT, int batch,
-                         cudaStream_t s) {
+                         cudaStream_t s, RowSlab rs) {
   const int n = f.n;
+  if (rs.rows == 0) rs = RowSlab::full(n);
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
   ensure_smem(reinterpret_cast<const void*>(fft_rows_r2c_kernel), smem);
-  dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
+  dim3 grid((rs.rows + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   // the loader (sums of adjoint partial images) wants more threads than the FFT
   launch_pdl(fft_rows_r2c_kernel, grid, dim3(fft_threads(kRowsPerBlock * n / 4)), smem, s, terms,
-             specT, f.tw.p, f.shape);
+             specT, f.tw.p, f.shape, rs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }
@@ -588,14 +623,28 @@ void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStr
   count_launch();
 }
 
-void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
-                         cudaStream_t s) {
+void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* maskT, ColSlab cs,
+                                 cudaStream_t s) {
   const int n = f.n;
+  if (cs.ncols <= 0) return;
+  size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
+  ensure_smem(reinterpret_cast<const void*>(fft_cols_filter_slab_kernel), smem);
+  dim3 grid((cs.ncols + kColsPerBlock - 1) / kColsPerBlock, 1);
+  launch_pdl(fft_cols_filter_slab_kernel, grid, dim3(fft_threads(kColsPerBlock * n / 8)), smem, s,
+             slab, maskT, f.tw.p, f.shape, cs);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
+
+void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
+                         cudaStream_t s, RowSlab rs) {
+  const int n = f.n;
+  if (rs.rows == 0) rs = RowSlab::full(n);
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n + sizeof(float) * kRowsPerBlock * n;
   ensure_smem(reinterpret_cast<const void*>(fft_rows_c2r_kernel), smem);
-  dim3 grid((n + kRowsPerBlock - 1) / kRowsPerBlock, batch);
+  dim3 grid((rs.rows + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   launch_pdl(fft_rows_c2r_kernel, grid, dim3(fft_threads((kRowsPerBlock / 2) * n / 4)), smem, s,
-             specT, xu, f.tw.p, f.shape);
+             specT, xu, f.tw.p, f.shape, rs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
 }

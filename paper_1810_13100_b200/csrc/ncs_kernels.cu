@@ -381,14 +381,16 @@ __global__ void seminorm_kernel(SemArgs a) {
   const float* adx = a.adx + b * a.range;
   double t1 = 0.0, aq = 0.0, mq = 0.0;
   for (size_t i = i0; i < a.range; i += stride) {
-    if (i >= a.r_begin && i < a.r_end) {
+    const bool mine = i < a.m0 ? (i >= a.m_begin && i < a.m_end && (!a.own || a.own[i / a.det]))
+                               : a.rank0 != 0;
+    if (mine && i >= a.r_begin && i < a.r_end) {
       const double d = static_cast<double>(du[i]) - a.alpha * static_cast<double>(adx[i]);
       t1 += d * d;
       aq += static_cast<double>(adx[i]) * adx[i];
     }
   }
   const size_t nn = static_cast<size_t>(a.n) * a.n;
-  {
+  if (a.rank0) {
     const float* dx = a.dx + b * nn;
     const float* w = a.mdx ? a.mdx + b * nn : nullptr;  // F^-1 (h F dx) (Engine::apply_m)
     for (size_t i = i0; i < nn; i += stride) {

@@ -63,6 +63,13 @@ struct SemArgs {
   const float* dx = nullptr;
   const float* mdx = nullptr;  // nullable (PDHG: M = gamma I handled by caller)
   double* out = nullptr;       // [batch][objective_blocks()][3]
+  // sharded problems: data rays i < m0 count when in [m_begin, m_end) and
+  // own[i / det] (own nullable); the replicated rest of the range and the
+  // x-space term only on rank 0 (summed across ranks by the caller)
+  size_t m0 = 0, m_begin = 0, m_end = ~size_t(0);
+  const uint8_t* own = nullptr;
+  int det = 1;
+  int rank0 = 1;
 };
 void launch_seminorm(const SemArgs& a, int batch, cudaStream_t s);
 

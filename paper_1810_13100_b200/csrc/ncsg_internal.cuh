@@ -333,14 +333,32 @@ struct FftPlan {
   void init(int n_, cudaStream_t s);
 };
 // Spectrum layout: specT[batch][n/2+1][n] complex (column-major half spectrum).
+// Row slabs (sharded slab FFT): the row passes cover image rows [r0, r0 +
+// rows) and address bin (k, y) at k * ld + (y - r0), batch stride bstride;
+// the unsharded layout is {0, n, n, (n/2+1) n}.
+struct RowSlab {
+  int r0 = 0, rows = 0, ld = 0;
+  size_t bstride = 0;
+  static RowSlab full(int n) { return RowSlab{0, n, n, static_cast<size_t>(n / 2 + 1) * n}; }
+};
+// Column slab of the sharded column pass: after the all-to-all a rank holds
+// P blocks [source rank i][wc columns][R rows]; bin (local column c, row j)
+// sits at ((j >> logR) * wc + c) * R + (j & (R-1)); its global column is
+// k0 + c (filter column).  ncols local columns are transformed.
+struct ColSlab {
+  int logR = 0, wc = 0, k0 = 0, ncols = 0;
+};
 // Real-to-half-spectrum row pass; `terms` (combine) describes how the real
 // input image is assembled (see ncs_kernels.cu).
 struct AtuTerms;
 void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT, int batch,
-                         cudaStream_t s);
+                         cudaStream_t s, RowSlab rs = RowSlab{});
 // Column pass: forward FFT along j, multiply by maskT[k][j], inverse FFT.
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
                             cudaStream_t s);
+// The sharded column pass (batch 1) on a rank's column slab (ColSlab layout).
+void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* maskT, ColSlab cs,
+                                 cudaStream_t s);
 // Column pass without the filter: forward FFT only (half spectrum of F x).
 void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStream_t s);
 // Inverse rows (C2R) fused with the x update: out = x_in - w (or w when
@@ -353,7 +371,7 @@ struct XUpdate {
   int* flag = nullptr;      // [0] = min(step counter [1]) over non-finite results (nullable)
 };
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
-                         cudaStream_t s);
+                         cudaStream_t s, RowSlab rs = RowSlab{});
 
 // ------------------------------------------------------------ NCS kernels
 // Terms summed into the image fed to the FFT: A^T u for the stacked problem.

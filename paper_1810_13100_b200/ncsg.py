@@ -46,6 +46,21 @@ class PlanInfo(C.Structure):
                 ("range", C.c_int64), ("batch", C.c_int64)]
 
 
+XCHG_ALLREDUCE, XCHG_SLAB = 0, 1
+F32, F64, I32 = 0, 1, 2
+SUM, MIN, MAX = 0, 1, 2
+_AllReduceFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int,
+                           C.c_void_p)
+_XferFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class CommOps(C.Structure):
+    """ncsg_comm_ops: the callback transport (include/ncsg.h)."""
+    _fields_ = [("ctx", C.c_void_p), ("rank", C.c_int), ("nranks", C.c_int),
+                ("all_reduce", _AllReduceFn), ("reduce_scatter", _XferFn),
+                ("all_gather", _XferFn), ("all_to_all", _XferFn)]
+
+
 class ProblemDesc(C.Structure):
     _fields_ = [
         ("kind", C.c_int), ("n", C.c_int), ("n_angles", C.c_int), ("n_det", C.c_int),
@@ -156,6 +171,13 @@ def lib():
     L.ncsg_profile_end.argtypes = [C.c_void_p, _dp, C.c_int, C.POINTER(C.c_int)]
     L.ncsg_launch_count.restype = C.c_int64
     L.ncsg_problem_plan.argtypes = [C.c_void_p, C.POINTER(PlanInfo)]
+    L.ncsg_nccl_unique_id.argtypes = [C.c_char_p]
+    L.ncsg_comm_create_nccl.argtypes = [C.c_char_p, C.c_int, C.c_int, C.c_int,
+                                        C.POINTER(C.c_void_p)]
+    L.ncsg_comm_create_callbacks.argtypes = [C.POINTER(CommOps), C.POINTER(C.c_void_p)]
+    L.ncsg_comm_create_local.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
+    L.ncsg_comm_destroy.argtypes = [C.c_void_p]
+    L.ncsg_problem_set_comm.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     _lib = L
     return L
 
@@ -491,6 +513,13 @@ class Problem:
         _check(lib().ncsg_profile_end(self._h, out, len(PHASES), C.byref(steps)), "profile_end")
         return dict(zip(PHASES, out.tolist())), steps.value
 
+    def set_comm(self, comm: "Comm | None", exchange: int = XCHG_SLAB) -> None:
+        """Attach a communicator: ncsg_step / solve then run the whole sharded
+        iteration (ncsg_problem_set_comm)."""
+        self._comm = comm
+        _check(lib().ncsg_problem_set_comm(self._h, comm._h if comm else None, exchange),
+               "set_comm")
+
     def plan(self) -> dict:
         """The live plan (partial-slot / partial-image counts, orbit mode,
         sample count) -- ncsg_problem_plan."""
@@ -535,6 +564,63 @@ class Problem:
                         for r in rows]).reshape(self.batch, max_rows, 5)[:, : nr.value]
         x, u, _ = self.get_state()
         return SolveResult(x, u, arr, arr[:, -1, 1].copy(), est.value)
+
+
+class Comm:
+    """A communicator of the sharded NCS step (ncsg_comm): NCCL, caller
+    callbacks, or one rank of an in-process group."""
+
+    def __init__(self, handle, keep=None):
+        self._h = handle
+        self._keep = keep  # callback objects the C side points to
+
+    @staticmethod
+    def nccl_unique_id() -> bytes:
+        buf = C.create_string_buffer(128)
+        _check(lib().ncsg_nccl_unique_id(buf), "nccl_unique_id")
+        return buf.raw
+
+    @classmethod
+    def nccl(cls, unique_id: bytes, rank: int, nranks: int, device: int = 0) -> "Comm":
+        h = C.c_void_p()
+        _check(lib().ncsg_comm_create_nccl(unique_id, rank, nranks, device, C.byref(h)),
+               "comm_create_nccl")
+        return cls(h)
+
+    @classmethod
+    def local_group(cls, nranks: int) -> list:
+        hs = (C.c_void_p * nranks)()
+        _check(lib().ncsg_comm_create_local(nranks, hs), "comm_create_local")
+        return [cls(C.c_void_p(hs[r])) for r in range(nranks)]
+
+    @classmethod
+    def callbacks(cls, rank: int, nranks: int, all_reduce, reduce_scatter, all_gather,
+                  all_to_all) -> "Comm":
+        """Python callbacks (device pointers as ints; the stream is already
+        synchronised; write results before returning)."""
+        def safe(f, *a):
+            try:
+                f(*a)
+                return 0
+            except Exception:  # reported as NCSG_CUDA by the library
+                import traceback
+
+                traceback.print_exc()
+                return -1
+
+        fns = (_AllReduceFn(lambda ctx, buf, cnt, dt, op, st: safe(all_reduce, buf, cnt, dt, op)),
+               _XferFn(lambda ctx, snd, rcv, cnt, st: safe(reduce_scatter, snd, rcv, cnt)),
+               _XferFn(lambda ctx, snd, rcv, cnt, st: safe(all_gather, snd, rcv, cnt)),
+               _XferFn(lambda ctx, snd, rcv, cnt, st: safe(all_to_all, snd, rcv, cnt)))
+        ops = CommOps(None, rank, nranks, *fns)
+        h = C.c_void_p()
+        _check(lib().ncsg_comm_create_callbacks(C.byref(ops), C.byref(h)), "comm_create_callbacks")
+        return cls(h, keep=(fns, ops))
+
+    def __del__(self):
+        if getattr(self, "_h", None) and _lib is not None:
+            _lib.ncsg_comm_destroy(self._h)
+            self._h = None
 
 
 def ct_problem(cfg, b, mask=None, batch=None, **kw) -> Problem:
