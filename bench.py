@@ -322,9 +322,12 @@ def roofline_of(cfg, plan, phase_avg, clocks):
 
 
 def bench_multi(args, cfg):
-    """N > 1 (torchrun, one rank per GPU, NCCL): angle-sharded steps, each
-    rank times its own steps with CUDA events on its solver stream between
-    barriers; the reported time is the max over ranks."""
+    """N > 1 (torchrun, one rank per GPU).  A single problem (C1-C4) is
+    sharded by angle and steps inside libncsg with an NCCL communicator
+    (slab FFT or all-reduce exchange, multigpu.default_exchange); a batched
+    config (C5) runs replicas -- rank r solves its share of the independent
+    problems.  Each rank times its own steps with CUDA events on its solver
+    stream between barriers; the reported time is the max over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -336,10 +339,37 @@ def bench_multi(args, cfg):
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=local)
-    x_true, b = instances.make_instance(cfg, R.forward)
     mask = instances.metric_mask(cfg)
-    s = multigpu.ShardedSolver(cfg, b, mask, rank, world, local)
-    s.step(args.warmup)
+    if cfg.batch > 1:  # replicas: this rank's problems of the batch
+        lo, hi = multigpu.replica_share(cfg.batch, world, rank)
+        bs = np.stack([instances.make_instance(cfg, R.forward, problem=q)[1]
+                       for q in range(lo, hi)])
+
+        def make():
+            p = ncsg.ct_problem(cfg, bs, mask=mask, batch=hi - lo, device=local)
+            p.set_state()
+            return p
+
+        prob = make()
+        units = hi - lo  # problems per step on this rank
+        mode = f"replicas: problems {lo}..{hi - 1} of {cfg.batch} on this rank, no collective"
+    else:
+        x_true, b = instances.make_instance(cfg, R.forward)
+        s = multigpu.ShardedSolver(cfg, b, mask, rank, world, local)
+        prob = s.prob
+        units = 1
+        mode = (f"{'orbit' if s.range == (0, 0) else 'angle'}-sharded, NCCL "
+                + ("reduce-scatter + slab FFT (2 all-to-all) + all-gather of x"
+                   if s.exchange == "slab" else "all-reduce of A^T u + replicated FFT solve"))
+
+        def make():
+            q = multigpu.ShardedSolver(cfg, b, mask, rank, world, local, comm=s.comm,
+                                       exchange=s.exchange)
+            return q.prob
+
+    stream = torch.cuda.ExternalStream(prob.stream, device=f"cuda:{local}")
+    prob.step(args.warmup)
+    prob.sync()
     torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -349,54 +379,61 @@ def bench_multi(args, cfg):
     launches0 = ncsg.launch_count()
     with ClockSampler(local) as clk:
         time.sleep(0.3)
-        with torch.cuda.stream(s.stream):
+        with torch.cuda.stream(stream):
             for k in range(args.steps):
                 flush.fill_(float(k))
-                starts[k].record(s.stream)
-                s.step(1)
-                ends[k].record(s.stream)
+                starts[k].record(stream)
+                prob.step(1)
+                ends[k].record(stream)
         torch.cuda.synchronize()
     dist.barrier()
     launches = ncsg.launch_count() - launches0
     ms_local = sum(a.elapsed_time(e) for a, e in zip(starts, ends)) / args.steps
-    t = torch.tensor([ms_local], device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    phase_ms, nprof = s.profile(min(args.steps, 10))
+    t = torch.tensor([ms_local, float(units)], device="cuda")
+    tm = t.clone()
+    dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+    ms = float(tm[0].item())
+    tu = t.clone()
+    dist.all_reduce(tu, op=dist.ReduceOp.SUM)
+    total_units = float(tu[1].item())  # problems per step over all ranks
+    prob.profile_begin()
+    with torch.cuda.stream(stream):
+        for k in range(min(args.steps, 10)):
+            flush.fill_(float(k))
+            prob.step(1)
+    phase_ms, nprof = prob.profile_end()
     phase_avg = {k: v / max(1, nprof) for k, v in phase_ms.items()}
     torch.cuda.synchronize()
-    # e2e: the public API, sharded: problem creation from host b and mask on
-    # every rank, solve of the config's iteration count, objective all-reduce,
-    # x back to host; wall clock, max over ranks.
+    # e2e: the public API on every rank -- problem creation from host arrays
+    # (its shard or its replicas), solve of the config's iteration count with
+    # the cross-rank records, state back to host; wall clock, max over ranks
     dist.barrier()
     t0 = time.perf_counter()
-    s2 = multigpu.ShardedSolver(cfg, b, mask, rank, world, local)
-    s2.step(cfg.iters)
-    f = s2.objective()
-    x, _, _ = s2.prob.get_state()
+    p2 = make()
+    res = p2.solve(cfg.iters, record_every=cfg.iters)
     dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     e2e_s = float(dt.item())
+    plan = prob.plan()
     if rank == 0:
         clocks = clk.summary()
-        if s.range == (0, 0):  # orbit sharding
-            own = sum(multigpu.orbit_owner(t, cfg.angles, world) == rank for t in range(cfg.angles))
-            m_own = own * cfg.det
-        else:
-            m_own = (s.range[1] - s.range[0]) * cfg.det
-        line = {"metric": METRIC, "value": 1000.0 / ms, "unit": "it/s", "n_gpus": world,
+        value = 1000.0 / ms * total_units
+        m_own = plan["m0"]  # rays of the offsets uploaded per problem (sinogram size)
+        line = {"metric": METRIC, "value": value, "unit": "it/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "higher_is_better": True,
+                "scaling": "weak" if cfg.batch > 1 else "strong", "vs_baseline": None,
                 "dtype": "f32", "data": "synthetic", "config": workload(cfg),
-                "roofline": roofline_of(cfg, s.prob.plan(), phase_avg, clocks),
+                "roofline": roofline_of(cfg, plan, phase_avg, clocks),
                 "phases_ms_rank0": phase_avg, "gpu_launches": launches, "clocks": clocks,
-                "objective_after": float(np.sum(f)),
-                "collective": "NCCL all_reduce of the partial A^T u (N^2 fp32) per step",
-                "e2e": {"value": cfg.iters / e2e_s, "unit": "it/s",
-                        "h2d_bytes_per_step": (4 * m_own + 2 * 8 * (cfg.n // 2 + 1) * cfg.n) / cfg.iters,
-                        "d2h_bytes_per_step": (4 * x.size + 8) / cfg.iters, "iters": cfg.iters,
-                        "seconds": e2e_s, "note": "per rank: sharded problem create + "
-                        f"{cfg.iters} steps + objective all-reduce + x download; max over ranks"}}
+                "exchange": mode,
+                "e2e": {"value": cfg.iters * total_units / e2e_s, "unit": "it/s",
+                        "h2d_bytes_per_step": (8 * m_own * units
+                                               + 2 * 8 * (cfg.n // 2 + 1) * cfg.n) / cfg.iters,
+                        "d2h_bytes_per_step": 8 * (res.x.size + res.u.size) / cfg.iters,
+                        "iters": cfg.iters, "seconds": e2e_s,
+                        "note": "per rank: problem create + solve(iters) with cross-rank "
+                                "records + state download; max over ranks"}}
         print(json.dumps(line), flush=True)
     dist.barrier()
     dist.destroy_process_group()

@@ -1,25 +1,25 @@
-"""Angle-sharded NCS over several GPUs of one node.
+"""Sharded NCS over the GPUs of one node.
 
-Each rank owns a contiguous block of projection angles: its rows of R, of the
-sinogram dual u_s, of b and of the cached R x.  One step is
+One process per GPU.  A single large problem is sharded by projection angle
+(whole dihedral orbits per rank when the angle count is a multiple of 4, so
+every shard keeps the orbit forward; contiguous angle blocks otherwise): each
+rank owns its rows of R, of the sinogram dual u_s, of b and of the cached
+R x.  The step runs inside libncsg with an NCCL communicator
+(ncsg_problem_set_comm), in one of two exchange modes:
 
-    phase A   partial A^T u = R_r^T u_s,r (+ w D^T u_g on rank 0)      [local]
-    exchange  all-reduce of the N x N partial over NVLink (NCCL)
-    phase B   replicated circulant solve + x update (identical on every rank),
-              R_r x for the own angles, dual update of the own rays and of the
-              replicated u_g                                            [local]
+  slab       partial A^T u -> NCCL reduce-scatter into N/P-row slabs -> row
+             FFT of the own slab -> all-to-all -> column FFT . filter .
+             inverse -> all-to-all -> inverse rows + x update of the own rows
+             -> all-gather of x (north_star's design; large N);
+  allreduce  one all-reduce of the N^2 partial, replicated circulant solve
+             (latency-bound sizes such as 512^2).
 
-The gradient dual u_g and x are replicated and updated identically on every
-rank, so they never need to move; the only collective per step is one
-all-reduce of N^2 floats (1 MiB at 512^2) -- the "one all-reduce + replicated
-FFT solve" variant of SURVEY.md §8f rank 3, which at 512^2 costs less than
-reduce-scatter + 2 all-to-all + all-gather latencies.
+Batched configs (C5) run as replicas: rank r solves its share of the
+independent problems, no collective in the step.
 """
 from __future__ import annotations
 
-import json
 import os
-import time
 
 
 def orbit_rep(t: int, n_angles: int) -> int:
@@ -47,10 +47,39 @@ def shard_angles(n_angles: int, world: int, rank: int) -> tuple[int, int]:
     return begin, begin + base + (1 if rank < rem else 0)
 
 
-class ShardedSolver:
-    """One rank's share of an angle-sharded CT problem."""
+def replica_share(batch: int, world: int, rank: int) -> tuple[int, int]:
+    """Problems [begin, end) of a batched config solved by `rank` (C5)."""
+    return shard_angles(batch, world, rank)
 
-    def __init__(self, cfg, b, mask, rank, world, device):
+
+def default_exchange(n: int, world: int) -> str:
+    """slab where the image splits into power-of-two slabs and is large
+    enough for the slab FFT to pay (N >= 1024), else the all-reduce."""
+    env = os.environ.get("NCSG_XCHG")
+    if env in ("slab", "allreduce"):
+        return env
+    r = n // world
+    ok = n % world == 0 and r % 2 == 0 and (r & (r - 1)) == 0
+    return "slab" if ok and n >= 1024 else "allreduce"
+
+
+def nccl_comm(rank: int, world: int, device: int):
+    """An ncsg NCCL communicator; the unique id travels over the already
+    initialised torch.distributed process group."""
+    import torch.distributed as dist
+
+    from . import ncsg
+
+    obj = [ncsg.Comm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return ncsg.Comm.nccl(obj[0], rank, world, device)
+
+
+class ShardedSolver:
+    """One rank's share of an angle-sharded CT problem, stepping inside
+    libncsg with a communicator (NCCL by default)."""
+
+    def __init__(self, cfg, b, mask, rank, world, device, comm=None, exchange=None):
         import torch
 
         from . import ncsg
@@ -62,39 +91,30 @@ class ShardedSolver:
             self.prob = ncsg.ct_problem(cfg, b, mask=mask, orbit_shard=(rank, world),
                                         device=device)
         else:
-            self.range = shard_angles(cfg.angles, world, rank)
+            self.range = shard_angles(cfg.angles, world, rank) if world > 1 else (0, 0)
             self.prob = ncsg.ct_problem(cfg, b, mask=mask, angle_range=self.range, device=device)
         self.prob.set_state()
-        self.atu = torch.zeros(cfg.batch * cfg.n * cfg.n, dtype=torch.float32,
-                               device=f"cuda:{device}")
-        self.prob.bind_atu(self.atu)
+        self.exchange = exchange or default_exchange(cfg.n, world)
+        if world > 1:
+            self.comm = comm if comm is not None else nccl_comm(rank, world, device)
+            self.prob.set_comm(self.comm, ncsg.XCHG_SLAB if self.exchange == "slab"
+                               else ncsg.XCHG_ALLREDUCE)
         self.stream = torch.cuda.ExternalStream(self.prob.stream, device=f"cuda:{device}")
 
-    def step(self, iters: int = 1):
-        import torch
-        import torch.distributed as dist
-
-        with torch.cuda.stream(self.stream):
-            for _ in range(iters):
-                self.prob.phase_a()
-                if self.world > 1:
-                    dist.all_reduce(self.atu)
-                self.prob.phase_b()
+    def step(self, iters: int = 1, graph: bool = False):
+        self.prob.step(iters, graph=graph)
 
     def profile(self, steps: int):
         """Per-phase CUDA-event times (ms) of this rank over `steps` steps; the
-        all-reduce falls between the adjoint and FFT phases."""
+        collectives fall inside the FFT phases (slab) or between the adjoint
+        and the FFT rows (all-reduce)."""
         self.prob.profile_begin()
         self.step(steps)
         return self.prob.profile_end()
 
     def objective(self):
-        import torch
-        import torch.distributed as dist
+        """The whole problem's objective (cross-rank sums inside the library)."""
+        return self.prob.objective()
 
-        f = torch.tensor(self.prob.objective(), dtype=torch.float64)
-        if self.world > 1:
-            f = f.cuda()
-            dist.all_reduce(f)
-            f = f.cpu()
-        return f.numpy()
+    def solve(self, max_iters: int, record_every: int | None = None):
+        return self.prob.solve(max_iters, record_every=record_every)

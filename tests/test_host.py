@@ -234,3 +234,93 @@ def test_write_record_csv_format(tmp_path):
     assert lines[0] == "iter,objective,rel_subopt,seminorm_step,wall_ms"
     assert lines[1] == "0,1,0.5,0,0.10000000000000001"
     assert lines[2] == "10,0.30000000000000004,9.9999999999999995e-21,3,12.25"
+
+
+def _slab_worker(rank, world, port, out_q):
+    """CPU model of the slab-sharded circulant solve (capi.cu sharded_step,
+    fft_kernels.cu RowSlab / ColSlab addressing) with gloo collectives: the
+    same reduce-scatter / all-to-all chunking and block layouts as the device
+    path, numpy FFTs in place of the Stockham kernels."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1810_13100_b200 import multigpu, ncsg
+
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank,
+                            world_size=world)
+    n = 16
+    P, R = world, 16 // world
+    nk = n // 2 + 1
+    wc = (nk + P - 1) // P
+    rng = np.random.default_rng(7)
+    parts = rng.standard_normal((P, n, n))       # every rank's partial A^T u
+    h = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    full = parts.sum(0)
+    want = np.real(np.fft.ifft2(h * np.fft.fft2(full)))  # MaskApplier::apply
+    # reduce-scatter: rows [rank R, rank R + R)
+    t = torch.from_numpy(parts[rank].ravel().copy())
+    dist.all_reduce(t)
+    slab = t.numpy().reshape(n, n)[rank * R:(rank + 1) * R]
+    # row FFT of the own rows -> spec_slab[k][r] (k < P wc, ld R)
+    rows = np.fft.fft(slab, axis=1)[:, :nk]          # half spectrum of each row
+    spec = np.zeros((P * wc, R), np.complex128)
+    spec[:nk] = rows.T
+    # all-to-all: chunk j = columns [j wc, (j+1) wc) of my rows
+    send = torch.from_numpy(spec.reshape(P, wc * R).view(np.float64).copy())
+    gathered = [torch.empty_like(send) for _ in range(P)]
+    dist.all_gather(gathered, send)
+    recv = np.stack([g.numpy().view(np.complex128)[rank] for g in gathered])  # [i][wc*R]
+    # column pass on the ColSlab layout: bin (c, j) at ((j >> logR) wc + c) R + (j & (R-1))
+    flat = recv.ravel()
+    hs = (h + np.conj(np.roll(np.flip(h, (0, 1)), 1, (0, 1)))) / 2  # Hermitian part
+    for c in range(max(0, min(wc, nk - rank * wc))):
+        idx = [((j // R) * wc + c) * R + (j % R) for j in range(n)]
+        col = flat[idx]
+        k = rank * wc + c
+        flat[idx] = np.fft.ifft(hs[:, k] * np.fft.fft(col)) * n  # 1/N^2 later
+    recv = flat.reshape(P, wc * R)
+    send = torch.from_numpy(recv.view(np.float64).copy())
+    gathered = [torch.empty_like(send) for _ in range(P)]
+    dist.all_gather(gathered, send)
+    back = np.stack([g.numpy().view(np.complex128).reshape(P, wc * R)[rank] for g in gathered])
+    spec = back.reshape(P * wc, R)                   # [global column][my rows]
+    half = spec[:nk].T                               # my rows' half spectra
+    w_rows = np.fft.irfft(half, n=n, axis=1) / n     # C2R (hermitian) + 1/N^2 total
+    t = torch.from_numpy(w_rows.ravel().copy())
+    out = [torch.empty_like(t) for _ in range(P)]
+    dist.all_gather(out, t)                          # all-gather of the x slabs
+    got = np.concatenate([o.numpy().reshape(R, n) for o in out])
+    err = float(np.abs(got - want).max() / np.abs(want).max())
+    # the NCCL unique id crosses the process group intact (multigpu.nccl_comm)
+    obj = [ncsg.Comm.nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    out_q.put((rank, err, len(obj[0]), multigpu.default_exchange(2048, world),
+               multigpu.default_exchange(512, world)))
+    dist.destroy_process_group()
+
+
+def test_slab_exchange_layout_gloo():
+    """world_size 2 gloo: the slab decomposition of the circulant solve with
+    the library's exact chunk layouts reproduces the unsharded solve."""
+    import multiprocessing as mp
+
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_slab_worker, args=(r, 2, 29541, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=180) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, err, idlen, big, small in res:
+        assert err < 1e-12, res
+        assert idlen == 128 and big == "slab" and small == "allreduce"
+
+
+def test_replica_shares_cover_batch():
+    from paper_1810_13100_b200.multigpu import replica_share
+
+    for world in (1, 2, 4, 8):
+        sh = [replica_share(64, world, r) for r in range(world)]
+        assert sh[0][0] == 0 and sh[-1][1] == 64
+        assert all(b - a == 64 // world for a, b in sh)
