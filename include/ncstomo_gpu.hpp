@@ -24,6 +24,7 @@
 #pragma once
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -771,6 +772,45 @@ inline SplitProblem denoise_problem(std::span<const double> noisy, int n, const 
   return SplitProblem(n, std::move(blocks));
 }
 
+/// A rank's communicator for multi-GPU solves (ncsg_comm): one
+/// process per GPU; the NCCL unique id is created on rank 0
+/// (Communicator::unique_id) and shared by the caller (MPI, a file, ...).
+class Communicator {
+ public:
+  static std::array<unsigned char, 128> unique_id() {
+    std::array<unsigned char, 128> id{};
+    detail::check(ncsg_nccl_unique_id(id.data()));
+    return id;
+  }
+  /// NCCL communicator of rank `rank` of `nranks` on `device`.
+  static std::shared_ptr<Communicator> nccl(const std::array<unsigned char, 128>& id, int rank,
+                                            int nranks, int device) {
+    ncsg_comm* c = nullptr;
+    detail::check(ncsg_comm_create_nccl(id.data(), rank, nranks, device, &c));
+    return std::shared_ptr<Communicator>(new Communicator(c, rank, nranks));
+  }
+  /// nranks communicators of one in-process group (one host thread per rank).
+  static std::vector<std::shared_ptr<Communicator>> local_group(int nranks) {
+    std::vector<ncsg_comm*> cs(nranks);
+    detail::check(ncsg_comm_create_local(nranks, cs.data()));
+    std::vector<std::shared_ptr<Communicator>> out;
+    for (int r = 0; r < nranks; ++r)
+      out.emplace_back(new Communicator(cs[r], r, nranks));
+    return out;
+  }
+  ~Communicator() { ncsg_comm_destroy(c_); }
+  Communicator(const Communicator&) = delete;
+  Communicator& operator=(const Communicator&) = delete;
+  int rank() const { return rank_; }
+  int nranks() const { return nranks_; }
+  ncsg_comm* get() const { return c_; }
+
+ private:
+  Communicator(ncsg_comm* c, int rank, int nranks) : c_(c), rank_(rank), nranks_(nranks) {}
+  ncsg_comm* c_;
+  int rank_, nranks_;
+};
+
 /// SolverConfig (solvers.hpp:54-72).  m_pinv_override / m_override are the
 /// reference's explicit metric hooks; the device engine takes them as
 /// CirculantMap (anything else: std::invalid_argument).
@@ -788,6 +828,13 @@ struct SolverConfig {
   std::shared_ptr<const LinearMap> m_pinv_override;
   std::shared_ptr<const LinearMap> m_override;
   int device = 0;
+  /// Multi-GPU (no reference counterpart: the reference is serial): with a
+  /// communicator of P > 1 ranks this rank solves its angle shard -- whole
+  /// dihedral orbits when n_angles % 4 == 0, else a contiguous block -- and
+  /// the exchange (slab FFT or all-reduce, ncsg.h) runs inside the library;
+  /// the state's u then holds this rank's rays (x is replicated).
+  std::shared_ptr<Communicator> comm;
+  bool slab_exchange = true;
 };
 
 /// SolverState (solvers.hpp:74-78).
@@ -877,14 +924,33 @@ class Engine {
     d.b = prob.offset.data();
     d.device = cfg.device;
     d.sparse = prob.sparse.get();
+    const int P = cfg.comm ? cfg.comm->nranks() : 1;
+    if (P > 1) {
+      if (prob.sparse) throw std::invalid_argument("sparse projectors are not angle-sharded");
+      const int r = cfg.comm->rank();
+      if (prob.n_angles % 4 == 0) {
+        d.shard_rank = r;
+        d.shard_count = P;
+      } else {
+        const int base = prob.n_angles / P, rem = prob.n_angles % P;
+        d.angle_begin = r * base + std::min(r, rem);
+        d.angle_end = d.angle_begin + base + (r < rem ? 1 : 0);
+      }
+    }
     ncsg_problem* h = nullptr;
     check(ncsg_problem_create(&d, &h));
     h_.reset(h, [](ncsg_problem* p) { ncsg_problem_destroy(p); });
     if (n_cg > 0) check(ncsg_set_cg(h, n_cg));
+    if (P > 1) {
+      comm_ = cfg.comm;
+      check(ncsg_problem_set_comm(h, comm_->get(),
+                                  cfg.slab_exchange ? NCSG_XCHG_SLAB : NCSG_XCHG_ALLREDUCE));
+    }
   }
   ncsg_problem* get() const { return h_.get(); }
 
  private:
+  std::shared_ptr<Communicator> comm_;  // outlives the problem's use of it
   std::shared_ptr<ncsg_problem> h_;
 };
 

@@ -16,7 +16,7 @@ def _build(tmp_path):
     b.build()
     exe = os.path.join(str(tmp_path), "test_gpu_api")
     subprocess.run(["g++", "-std=c++20", "-O2", f"-I{ROOT}/include", SRC, f"-L{LIBDIR}",
-                    "-lncsg", f"-Wl,-rpath,{LIBDIR}", "-o", exe], check=True)
+                    "-lncsg", f"-Wl,-rpath,{LIBDIR}", "-pthread", "-o", exe], check=True)
     return exe
 
 
