@@ -427,6 +427,17 @@ __device__ __forceinline__ void member_range(RayRange rr, int t, bool neg, int d
   if (jhi <= jlo) jlo = jhi = 0;
 }
 
+// Predicated 128-bit shared load: zeros where p is false (no request issued).
+__device__ __forceinline__ float4 lds4p(unsigned a, bool p) {
+  float4 v;
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+      " mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n mov.b32 %3, 0;\n"
+      " @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
+      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+      : "r"(a), "r"(static_cast<int>(p)));
+  return v;
+}
 __device__ __forceinline__ float4 lds4(unsigned a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -463,6 +474,13 @@ size_t orbit_smem(int rmax) {
   return sizeof(float) * (4 * kOrbTile + kOrbWarps * 5 * rmax) + 128;
 }
 
+#ifndef NCSG_ORB_PRED
+#define NCSG_ORB_PRED 0
+#endif
+#ifndef NCSG_ORB_UNROLL
+#define NCSG_ORB_UNROLL 2
+#endif
+constexpr int kOrbUnroll = NCSG_ORB_UNROLL;  // steps per iteration of the uniform-range loop
 #ifndef NCSG_ORB_MINB
 #define NCSG_ORB_MINB 2  // two CTAs per SM: caps ptxas at 128 registers (146 without)
 #endif
@@ -619,35 +637,83 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
         unsigned sp[4];
 #pragma unroll
         for (int k = 0; k < 4; ++k) sp[k] = static_cast<unsigned>(jh[k] - jl[k]);
-        float acc[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll 2
-        for (int j = J0; j < J1; ++j) {
-          const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
-          // lanes outside their run read a cell of the slack with the same
-          // bank group as their lattice point (P % 8 == 0), so they add no
-          // conflict the lane map has not already priced in
-          const int idx_l = base + (Y >> 23) * P + (X >> 23);
-          const int idx = on ? idx_l : (idx_l & 7);
-          const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
-          const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
-          const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
-          const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
-          // bilinear weights once, then members (0, 1) and (2, 3) as f32x2
-          const float w11 = fx * fy, w01 = fx - w11, w10 = fy - w11, w00 = 1.0f - fx - w10;
-          f32x2 v01 = fmul2(pk(w00, w00), pk(q00.x, q00.y));
-          f32x2 v23 = fmul2(pk(w00, w00), pk(q00.z, q00.w));
-          v01 = ffma2(pk(w01, w01), pk(q01.x, q01.y), v01);
-          v23 = ffma2(pk(w01, w01), pk(q01.z, q01.w), v23);
-          v01 = ffma2(pk(w10, w10), pk(q10.x, q10.y), v01);
-          v23 = ffma2(pk(w10, w10), pk(q10.z, q10.w), v23);
-          v01 = ffma2(pk(w11, w11), pk(q11.x, q11.y), v01);
-          v23 = ffma2(pk(w11, w11), pk(q11.z, q11.w), v23);
-          const float2 a01 = upk(v01), a23 = upk(v23);
-          const float v[4] = {a01.x, a01.y, a23.x, a23.y};
+        // The members sample images of the same lattice points under the
+        // square's symmetries, so their valid ranges agree except for samples
+        // on the image edge up to rounding.  When every present member of
+        // every lane has the lane's union range, the accumulation needs no
+        // per-member test: lanes outside their run read zero slack cells.
+        bool uni = true;
 #pragma unroll
-          for (int k = 0; k < 4; ++k) acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v[k] : 0.f;
-          X += g.dXq;
-          Y += g.dYq;
+        for (int k = 0; k < 4; ++k)
+          if (o.t[k] >= 0 && jh[k] > jl[k] && (jl[k] != lo_all || jh[k] != hi_all)) uni = false;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)  // a present member without samples
+          if (o.t[k] >= 0 && jh[k] <= jl[k] && hi_all > 0) uni = false;
+        float acc[4] = {0.f, 0.f, 0.f, 0.f};
+        if (__all_sync(0xffffffffu, uni)) {
+          f32x2 a01 = pk(0.f, 0.f), a23 = pk(0.f, 0.f);
+#pragma unroll kOrbUnroll
+          for (int j = J0; j < J1; ++j) {
+            const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
+            // lanes outside their run read a zero cell of the slack with the
+            // same bank group as their lattice point (P % 8 == 0): no
+            // conflict the lane map has not priced in, and no contribution
+            const int idx_l = base + (Y >> 23) * P + (X >> 23);
+            const int idx = on ? idx_l : (idx_l & 7);
+            const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
+            const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+#if NCSG_ORB_PRED
+            // duplicate / finished lanes issue no load: a quarter-warp with no
+            // live lane costs no shared-memory wavefront
+            const bool ld = on && act;
+            const float4 q00 = lds4p(ad, ld), q01 = lds4p(ad + 16, ld);
+            const float4 q10 = lds4p(ad + 16 * P, ld), q11 = lds4p(ad + 16 * P + 16, ld);
+#else
+            const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
+            const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
+#endif
+            const float w11 = fx * fy, w01 = fx - w11, w10 = fy - w11, w00 = 1.0f - fx - w10;
+            a01 = ffma2(pk(w00, w00), pk(q00.x, q00.y), a01);
+            a23 = ffma2(pk(w00, w00), pk(q00.z, q00.w), a23);
+            a01 = ffma2(pk(w01, w01), pk(q01.x, q01.y), a01);
+            a23 = ffma2(pk(w01, w01), pk(q01.z, q01.w), a23);
+            a01 = ffma2(pk(w10, w10), pk(q10.x, q10.y), a01);
+            a23 = ffma2(pk(w10, w10), pk(q10.z, q10.w), a23);
+            a01 = ffma2(pk(w11, w11), pk(q11.x, q11.y), a01);
+            a23 = ffma2(pk(w11, w11), pk(q11.z, q11.w), a23);
+            X += g.dXq;
+            Y += g.dYq;
+          }
+          const float2 v01 = upk(a01), v23 = upk(a23);
+          acc[0] = v01.x, acc[1] = v01.y, acc[2] = v23.x, acc[3] = v23.y;
+        } else {
+#pragma unroll 2
+          for (int j = J0; j < J1; ++j) {
+            const bool on = static_cast<unsigned>(j - lo_xy) < span_xy;
+            const int idx_l = base + (Y >> 23) * P + (X >> 23);
+            const int idx = on ? idx_l : (idx_l & 7);
+            const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
+            const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
+            const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
+            const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
+            // bilinear weights once, then members (0, 1) and (2, 3) as f32x2
+            const float w11 = fx * fy, w01 = fx - w11, w10 = fy - w11, w00 = 1.0f - fx - w10;
+            f32x2 v01 = fmul2(pk(w00, w00), pk(q00.x, q00.y));
+            f32x2 v23 = fmul2(pk(w00, w00), pk(q00.z, q00.w));
+            v01 = ffma2(pk(w01, w01), pk(q01.x, q01.y), v01);
+            v23 = ffma2(pk(w01, w01), pk(q01.z, q01.w), v23);
+            v01 = ffma2(pk(w10, w10), pk(q10.x, q10.y), v01);
+            v23 = ffma2(pk(w10, w10), pk(q10.z, q10.w), v23);
+            v01 = ffma2(pk(w11, w11), pk(q11.x, q11.y), v01);
+            v23 = ffma2(pk(w11, w11), pk(q11.z, q11.w), v23);
+            const float2 a01 = upk(v01), a23 = upk(v23);
+            const float v[4] = {a01.x, a01.y, a23.x, a23.y};
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              acc[k] += (static_cast<unsigned>(j - jl[k]) < sp[k]) ? v[k] : 0.f;
+            X += g.dXq;
+            Y += g.dYq;
+          }
         }
         if (act) {
           unsigned fl = 0;
