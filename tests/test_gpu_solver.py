@@ -127,7 +127,8 @@ def test_small_ct_parity_with_records(ncsg, port):
     check_run(g, o)
     # seminorm rows (solvers.cpp:166-177) -- differences of iterates, fp32
     sem_g, sem_o = g.rows[0][1:, 3], o.rows[1:, 3]
-    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= 1e-3
+    print(f"seminorm rows vs oracle: {np.max(np.abs(sem_g - sem_o) / sem_o):.2e}")
+    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= TOL
 
 
 def test_pdhg_parity(ncsg, port):
@@ -395,7 +396,8 @@ def test_record_every_one_parity(ncsg, port):
     check_run(g, o)
     sem_g, sem_o = g.rows[0][1:, 3], o.rows[1:, 3]
     assert len(sem_g) == 20
-    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= 1e-3
+    print(f"record_every=1 seminorm rows vs oracle: {np.max(np.abs(sem_g - sem_o) / sem_o):.2e}")
+    assert np.max(np.abs(sem_g - sem_o) / sem_o) <= TOL
 
 
 @pytest.mark.parametrize("kind,positivity,n_cg,tol", [(0, False, 2, TOL), (0, False, 6, 5e-4),
