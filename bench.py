@@ -99,6 +99,17 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(sm)}
 
 
+def kernels_per_step(prob):
+    """Kernels of one eager step (counted by the library), the same set a
+    graph replay of one step launches."""
+    from paper_1810_13100_b200 import ncsg
+
+    n0 = ncsg.launch_count()
+    prob.step(1, graph=False)
+    prob.sync()
+    return ncsg.launch_count() - n0
+
+
 def kernel_bytes(cfg, plan):
     """Per-launch algorithmic bytes of every phase of the step AS PLANNED
     (partial-slot and partial-image counts from the live plan,
@@ -252,6 +263,7 @@ def workload(cfg):
             "detectors": cfg.det, "lambda": cfg.lam, "alpha": cfg.alpha, "beta": cfg.beta,
             "gamma": cfg.gamma, "dc": cfg.dc, "mask_scale": cfg.mask_scale, "batch": cfg.batch,
             "l2": "flushed (256 MiB write) between timed steps, outside the events",
+            "launch": "eager" if os.environ.get("NCSG_EAGER") == "1" else "CUDA graph per step",
             "parallelism": "angle-sharded" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "1 GPU"}
 
 
@@ -449,7 +461,12 @@ def bench_single(args, cfg):
     prob = ncsg.ct_problem(cfg, b, mask=mask) if cfg.kind == "ct" else ncsg.denoise_problem(
         cfg, b, mask=mask)
     prob.set_state()
-    prob.step(args.warmup)
+    # the step as a captured CUDA graph (ncsg_step_graph: one graph launch per
+    # step, its kernels chained by programmatic dependent launch); NCSG_EAGER=1
+    # times the eager per-kernel launches instead
+    graph = os.environ.get("NCSG_EAGER") != "1"
+    prob.step(args.warmup, graph=False)
+    prob.step(1, graph=graph)  # capture outside the timed region
     prob.sync()
     stream = torch.cuda.ExternalStream(prob.stream)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -463,10 +480,12 @@ def bench_single(args, cfg):
             for k in range(args.steps):
                 flush.fill_(float(k))
                 starts[k].record(stream)
-                prob.step(1)
+                prob.step(1, graph=graph)
                 ends[k].record(stream)
         torch.cuda.synchronize()
     launches = ncsg.launch_count() - launches0
+    if graph:  # graph replays do not pass through the counted launch calls
+        launches = args.steps * kernels_per_step(prob)
     prob.sync()
     # per-phase CUDA events in a separate pass, so they do not perturb `value`
     prob.profile_begin()

@@ -261,6 +261,7 @@ struct RadonDev {
   // (bp_chunks[0] = 4 * chunks, bp_chunks[1] = 0).
   bool bp_orbit = false;
   int bp_orbit_chunks = 0, bp_orbit_len = 0;
+  int bp_cluster = 1;  // chunk CTAs folded per thread-block cluster (1, 2 or 4)
   DevBuf<GatherGeom> gather;
   // Orbit-interleaved dual (optional gather input): angle t's member slot
   // 4 * orbit + member (-1: none) and the padded row of rays per orbit.

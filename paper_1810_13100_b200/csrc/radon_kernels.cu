@@ -29,6 +29,7 @@
 //     (chosen per angle by a host bank-conflict model), so two lanes of one
 //     instruction never touch the same pixel (race-free without atomics).
 //     Warps are reduced once per CTA into a partial image per angle chunk.
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -944,7 +945,11 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
 }
 
-template <int TW, int TH, int NB>
+// CL > 1: the CL chunk CTAs of a (tile, chunk group) form a thread-block
+// cluster along grid.z and fold their member tiles through distributed
+// shared memory (fixed rank order: deterministic) before the stores, so the
+// FFT row pass reads 4 partial images per chunk group instead of per chunk.
+template <int TW, int TH, int NB, int CL>
 #ifndef NCSG_GA_MINB
 #define NCSG_GA_MINB 4  // 64 registers, 4 CTAs per SM (without a minimum ptxas takes 70 -> 3 CTAs; with 1, 134)
 #endif
@@ -1177,6 +1182,39 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
   }
   __syncthreads();
   const size_t nn = a.nn;
+  if constexpr (CL > 1) {
+    // fold the cluster's member tiles: rank c stores the members m with
+    // m % CL == c, summing rank 0..CL-1's tiles in order
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();  // every CTA's tile is complete
+    const int rank = static_cast<int>(cl.block_rank());
+    const int group = chunk / CL;
+    const int n_groups = a.n_chunks / CL;
+    float* base = a.out + (static_cast<size_t>(b) * 4 * n_groups + 4 * group) * nn;
+    float* ot0 = &ot[0][0][0];
+    for (int m = rank; m < 4; m += CL) {
+      float* om = base + m * nn;
+      const bool rows = (m == 0 || m == 2);  // members 0, 2 along rows, 1, 3 along columns
+      for (int i = threadIdx.x; i < TW * TH; i += kGaThreads) {
+        const int x = rows ? i % TW : i / TH, y = rows ? i / TW : i % TH;
+        const int X = X0 + x, Y = Y0 + y;
+        if (X >= n || Y >= n) continue;
+        const int off = (m * TH + y) * (TW + 1) + x;
+        float v = 0.f;
+#pragma unroll
+        for (int r = 0; r < CL; ++r) v += cl.map_shared_rank(ot0, r)[off];
+        size_t dst;
+        if (m == 0) dst = static_cast<size_t>(Y) * n + X;
+        else if (m == 2) dst = static_cast<size_t>(Y) * n + (n - 1 - X);
+        else if (m == 1) dst = static_cast<size_t>(n - 1 - X) * n + Y;
+        else dst = static_cast<size_t>(n - 1 - X) * n + (n - 1 - Y);
+        om[dst] = v;
+      }
+    }
+    cl.sync();  // no CTA leaves while its tiles are being read
+    return;
+  }
   float* o0 = a.out + (static_cast<size_t>(b) * 4 * a.n_chunks + 4 * chunk) * nn;
   float* o1 = o0 + nn;
   float* o2 = o1 + nn;
@@ -1436,7 +1474,17 @@ void RadonDev::plan_adjoint(int batch) {
         bp_orbit_len % kGaBatch < kGaBatch / 2 && !getenv("NCSG_GA_CHUNKS"))
       bp_orbit_len = bp_orbit_len / kGaBatch * kGaBatch;
     bp_orbit_chunks = (no + bp_orbit_len - 1) / bp_orbit_len;
-    bp_chunks[0] = 4 * bp_orbit_chunks;
+    // Optional (NCSG_GA_CLUSTER=2|4): fold chunks in thread-block clusters
+    // through DSMEM, 4 partial images per cluster instead of per chunk.
+    // Measured at C3: r2c 14.7 -> 11.9 us but the adjoint 181.5 -> 224.8 us
+    // (cluster 4; 201.6 with 2) -- co-scheduling the cluster's CTAs and the
+    // fold's two cluster barriers cost more than the partial reads save.
+    bp_cluster = 1;
+    if (const char* e = getenv("NCSG_GA_CLUSTER")) {
+      const int c = atoi(e);
+      bp_cluster = (c == 2 || c == 4) && bp_orbit_chunks % c == 0 ? c : 1;
+    }
+    bp_chunks[0] = 4 * (bp_orbit_chunks / bp_cluster);
     bp_chunks[1] = 0;
     bp_chunk_len[0] = bp_chunk_len[1] = 1;
     bp_batch_planned = batch;
@@ -1674,7 +1722,25 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     a.u4_row = r.u4_row();
     a.u4_pad = kGaSW;
     dim3 grid((n + kGaTW - 1) / kGaTW, (n + kGaTH - 1) / kGaTH, a.n_chunks * batch);
-    launch_pdl(bp_gather_kernel<kGaTW, kGaTH, kGaBatch>, grid, dim3(kGaThreads), 0, s, a);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kGaThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = 1;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = r.bp_cluster;
+    cfg.attrs = at;
+    cfg.numAttrs = r.bp_cluster > 1 ? 2 : 1;
+    if (r.bp_cluster == 4)
+      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 4>, a));
+    else if (r.bp_cluster == 2)
+      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 2>, a));
+    else
+      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 1>, a));
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
     return;
