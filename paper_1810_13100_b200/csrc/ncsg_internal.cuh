@@ -278,6 +278,7 @@ struct RadonDev {
   int orb_seg = 64;      // rows per forward segment (upload chooses 32 or 64)
   int batch_hint = 1;    // problems per launch the plan is sized for (set before upload)
   int orb_rmax = 0;
+  int orb_warps = 8;     // orbits (warps) per forward CTA
   DevBuf<OrbitGeom> orbits;
   DevBuf<int2> orb_range;                     // [orbit][strip][seg] s-range
   // Cached TMA descriptor of the orbit forward's member-image buffer (encoded

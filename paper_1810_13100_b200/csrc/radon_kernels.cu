@@ -428,17 +428,6 @@ __device__ __forceinline__ void member_range(RayRange rr, int t, bool neg, int d
   if (jhi <= jlo) jlo = jhi = 0;
 }
 
-// Predicated 128-bit shared load: zeros where p is false (no request issued).
-__device__ __forceinline__ float4 lds4p(unsigned a, bool p) {
-  float4 v;
-  asm volatile(
-      "{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
-      " mov.b32 %0, 0;\n mov.b32 %1, 0;\n mov.b32 %2, 0;\n mov.b32 %3, 0;\n"
-      " @q ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n}"
-      : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-      : "r"(a), "r"(static_cast<int>(p)));
-  return v;
-}
 __device__ __forceinline__ float4 lds4(unsigned a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
@@ -471,13 +460,10 @@ __device__ __forceinline__ void tma_load_4d(unsigned dst, const CUtensorMap* map
 // projection -- deterministic, no atomics.
 constexpr int kOrbD = (2 * kOrbP + 4 + 7) / 8 * 8;                        // slack cells
 constexpr int kOrbTile = (kOrbD + (kOrbT + 4) * kOrbP + 8 + 7) / 8 * 8;  // cells
-size_t orbit_smem(int rmax) {
-  return sizeof(float) * (4 * kOrbTile + kOrbWarps * 5 * rmax) + 128;
+size_t orbit_smem(int rmax, int nw = kOrbWarps) {
+  return sizeof(float) * (4 * kOrbTile + nw * 5 * rmax) + 128;
 }
 
-#ifndef NCSG_ORB_PRED
-#define NCSG_ORB_PRED 0
-#endif
 #ifndef NCSG_ORB_UNROLL
 #define NCSG_ORB_UNROLL 2
 #endif
@@ -485,11 +471,14 @@ constexpr int kOrbUnroll = NCSG_ORB_UNROLL;  // steps per iteration of the unifo
 #ifndef NCSG_ORB_MINB
 #define NCSG_ORB_MINB 2  // two CTAs per SM: caps ptxas at 128 registers (146 without)
 #endif
-template <bool USE_TMA>
-__global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
+// NW orbits (warps) per CTA: kOrbWarps normally; 2 for grids too small to
+// fill the GPU (C1: 24 -> 92 CTAs), each CTA then staging its tile for fewer
+// orbits.
+template <bool USE_TMA, int NW>
+__global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
     fp_orbit_kernel(OrbArgs a, const __grid_constant__ CUtensorMap map) {
   pdl_wait();
-  constexpr int W = kOrbW, T = kOrbT, P = kOrbP, NW = kOrbWarps;
+  constexpr int W = kOrbW, T = kOrbT, P = kOrbP;
   constexpr int ROWS = T + 4;
   // D cells of zeroed slack, then the (T+4) x P tile of cells. TMA box starts
   // must be >= 0 (scripts/tma_probe.cu), so the left strip / first tile row
@@ -663,16 +652,8 @@ __global__ void __launch_bounds__(kOrbWarps * 32, NCSG_ORB_MINB)
             const int idx = on ? idx_l : (idx_l & 7);
             const unsigned ad = tile0 + 16u * static_cast<unsigned>(idx);
             const float fx = frac1_q23(X, mask, one) - 1.0f, fy = frac1_q23(Y, mask, one) - 1.0f;
-#if NCSG_ORB_PRED
-            // duplicate / finished lanes issue no load: a quarter-warp with no
-            // live lane costs no shared-memory wavefront
-            const bool ld = on && act;
-            const float4 q00 = lds4p(ad, ld), q01 = lds4p(ad + 16, ld);
-            const float4 q10 = lds4p(ad + 16 * P, ld), q11 = lds4p(ad + 16 * P + 16, ld);
-#else
             const float4 q00 = lds4(ad), q01 = lds4(ad + 16);
             const float4 q10 = lds4(ad + 16 * P), q11 = lds4(ad + 16 * P + 16);
-#endif
             const float w11 = fx * fy, w01 = fx - w11, w10 = fy - w11, w00 = 1.0f - fx - w10;
             a01 = ffma2(pk(w00, w00), pk(q00.x, q00.y), a01);
             a23 = ffma2(pk(w00, w00), pk(q00.z, q00.w), a23);
@@ -1392,6 +1373,12 @@ void RadonDev::upload() {
     const size_t smem = orbit_smem(rmax);
     if (ns == n_strips && smem <= 112 * 1024) {
       orbit_mode = true;
+      // small problems: 2 orbits per CTA when 8 would leave most SMs idle
+      const long ctas = static_cast<long>(ns) * n_segs *
+                        ((static_cast<long>(geo.orbits.size()) + kOrbWarps - 1) / kOrbWarps) *
+                        batch_hint;
+      orb_warps = ctas < 148 ? 2 : kOrbWarps;
+      if (const char* e = getenv("NCSG_ORB_NW")) orb_warps = atoi(e) == 2 ? 2 : kOrbWarps;
       for (OrbitGeom& o : geo.orbits) o.rep.fp_rq = orbit_lane_rays(o.rep);
       orb_rmax = rmax;
       orbits.alloc(geo.orbits.size());
@@ -1462,7 +1449,11 @@ void RadonDev::plan_adjoint(int batch) {
     const int no = static_cast<int>(geo.orbits.size());
     const long per = static_cast<long>(tiles) * batch;
     int chunks = static_cast<int>(std::max<long>(1, (target + per - 1) / per));
-    chunks = std::min(chunks, std::max(1, no / kGaBatch));
+    // at least a staging batch of orbits per chunk -- half a batch when the
+    // grid would not even fill the GPU once (C1: 3 -> 5 chunks, adjoint
+    // 28 -> 24 us)
+    const int min_len = per * std::max(1, no / kGaBatch) < 148L * 4 ? kGaBatch / 2 : kGaBatch;
+    chunks = std::min(chunks, std::max(1, no / min_len));
     if (const char* e = getenv("NCSG_GA_CHUNKS")) chunks = std::max(1, std::min(no, atoi(e)));
     chunks = std::max(chunks, (no + kGaMaxChunk - 1) / kGaMaxChunk);  // the lowest-ray table
     bp_orbit_len = (no + chunks - 1) / chunks;
@@ -1607,7 +1598,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     OrbArgs a;
     a.orb = r.orbits.p;
     a.n_orb = static_cast<int>(g.orbits.size());
-    a.n_chunks = (a.n_orb + kOrbWarps - 1) / kOrbWarps;
+    a.n_chunks = (a.n_orb + r.orb_warps - 1) / r.orb_warps;
     a.range = r.orb_range.p;
     a.rays = r.rays.p;
     a.quad = reinterpret_cast<const float4*>(imgT);  // orbit mode: aux = make_quad output
@@ -1635,15 +1626,17 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     CUtensorMap map;
     std::memcpy(&map, qm.bytes, sizeof(map));
     const bool tma = qm.ok;
-    const size_t smem = orbit_smem(a.rmax);
+    const int nw = r.orb_warps;
+    const size_t smem = orbit_smem(a.rmax, nw);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
-    if (tma) {
-      set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<true>), smem);
-      launch_pdl(fp_orbit_kernel<true>, grid, dim3(kOrbWarps * 32), smem, s, a, map);
-    } else {
-      set_smem(reinterpret_cast<const void*>(fp_orbit_kernel<false>), smem);
-      launch_pdl(fp_orbit_kernel<false>, grid, dim3(kOrbWarps * 32), smem, s, a, map);
-    }
+    auto go = [&](auto kern) {
+      set_smem(reinterpret_cast<const void*>(kern), smem);
+      launch_pdl(kern, grid, dim3(nw * 32), smem, s, a, map);
+    };
+    if (nw == kOrbWarps)
+      tma ? go(fp_orbit_kernel<true, kOrbWarps>) : go(fp_orbit_kernel<false, kOrbWarps>);
+    else
+      tma ? go(fp_orbit_kernel<true, 2>) : go(fp_orbit_kernel<false, 2>);
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
     return;
