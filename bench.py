@@ -348,8 +348,17 @@ def bench_multi(args, cfg):
     rank = int(os.environ["RANK"])
     world = int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
+    # NCSG_BENCH_GLOO=1: gloo process group and host-staged callback
+    # collectives, all ranks on cuda:0 -- a functional run of this path on a
+    # one-GPU box (the timing is then meaningless); default NCCL, one GPU per rank
+    gloo = os.environ.get("NCSG_BENCH_GLOO") == "1"
+    if gloo:
+        local = 0
     torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if gloo:
+        dist.init_process_group("gloo")
+    else:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     R = ncsg.RadonMap(cfg.n, cfg.angles, cfg.det, device=local)
     mask = instances.metric_mask(cfg)
     if cfg.batch > 1:  # replicas: this rank's problems of the batch
@@ -367,10 +376,12 @@ def bench_multi(args, cfg):
         mode = f"replicas: problems {lo}..{hi - 1} of {cfg.batch} on this rank, no collective"
     else:
         x_true, b = instances.make_instance(cfg, R.forward)
-        s = multigpu.ShardedSolver(cfg, b, mask, rank, world, local)
+        comm0 = multigpu.gloo_comm(rank, world) if gloo else None
+        s = multigpu.ShardedSolver(cfg, b, mask, rank, world, local, comm=comm0)
         prob = s.prob
         units = 1
-        mode = (f"{'orbit' if s.range == (0, 0) else 'angle'}-sharded, NCCL "
+        mode = (f"{'orbit' if s.range == (0, 0) else 'angle'}-sharded, "
+                + ("gloo host-staged callbacks (functional run, one GPU) " if gloo else "NCCL ")
                 + ("reduce-scatter + slab FFT (2 all-to-all) + all-gather of x"
                    if s.exchange == "slab" else "all-reduce of A^T u + replicated FFT solve"))
 
@@ -401,7 +412,8 @@ def bench_multi(args, cfg):
     dist.barrier()
     launches = ncsg.launch_count() - launches0
     ms_local = sum(a.elapsed_time(e) for a, e in zip(starts, ends)) / args.steps
-    t = torch.tensor([ms_local, float(units)], device="cuda")
+    dev = "cpu" if gloo else "cuda"
+    t = torch.tensor([ms_local, float(units)], device=dev)
     tm = t.clone()
     dist.all_reduce(tm, op=dist.ReduceOp.MAX)
     ms = float(tm[0].item())
@@ -423,7 +435,7 @@ def bench_multi(args, cfg):
     t0 = time.perf_counter()
     p2 = make()
     res = p2.solve(cfg.iters, record_every=cfg.iters)
-    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device="cuda")
+    dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
     dist.all_reduce(dt, op=dist.ReduceOp.MAX)
     e2e_s = float(dt.item())
     plan = prob.plan()

@@ -118,3 +118,60 @@ class ShardedSolver:
 
     def solve(self, max_iters: int, record_every: int | None = None):
         return self.prob.solve(max_iters, record_every=record_every)
+
+
+def gloo_comm(rank: int, world: int):
+    """An ncsg communicator whose collectives are host-staged torch.distributed
+    (gloo) calls: functional multi-process runs with several ranks on one GPU
+    (tests, the bench's NCSG_BENCH_GLOO mode)."""
+    import ctypes as C
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from . import ncsg
+
+    import nvidia.cuda_runtime
+
+    lib = os.path.join(os.path.dirname(nvidia.cuda_runtime.__file__), "lib", "libcudart.so.12")
+    rt = C.CDLL(lib)
+    rt.cudaMemcpy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]
+    types = {ncsg.F32: (np.float32, 4), ncsg.F64: (np.float64, 8), ncsg.I32: (np.int32, 4)}
+
+    def down(ptr, count, dt=np.float32, es=4):
+        h = np.empty(count, dt)
+        assert rt.cudaMemcpy(h.ctypes.data, ptr, count * es, 2) == 0
+        return h
+
+    def up(ptr, h):
+        h = np.ascontiguousarray(h)
+        assert rt.cudaMemcpy(ptr, h.ctypes.data, h.nbytes, 1) == 0
+        assert rt.cudaDeviceSynchronize() == 0
+
+    def all_reduce(buf, count, dt, op):
+        npt, es = types[dt]
+        t = torch.from_numpy(down(buf, count, npt, es))
+        dist.all_reduce(t, op={ncsg.SUM: dist.ReduceOp.SUM, ncsg.MIN: dist.ReduceOp.MIN,
+                               ncsg.MAX: dist.ReduceOp.MAX}[op])
+        up(buf, t.numpy())
+
+    def gather_all(snd, count):
+        t = torch.from_numpy(down(snd, count))
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [q.numpy() for q in parts]
+
+    def reduce_scatter(snd, rcv, count):
+        t = torch.from_numpy(down(snd, count * world))
+        dist.all_reduce(t)
+        up(rcv, t.numpy()[rank * count:(rank + 1) * count])
+
+    def all_gather(snd, rcv, count):
+        up(rcv, np.concatenate(gather_all(snd, count)))
+
+    def all_to_all(snd, rcv, count):
+        parts = gather_all(snd, count * world)
+        up(rcv, np.concatenate([parts[r][rank * count:(rank + 1) * count] for r in range(world)]))
+
+    return ncsg.Comm.callbacks(rank, world, all_reduce, reduce_scatter, all_gather, all_to_all)

@@ -166,3 +166,27 @@ def test_two_process_gloo_callbacks(ncsg, port, tmp_path):
         assert rel(d["x"][0], ref.x[0]) <= 1e-5
         f, fr = d["rows"][0][:, 1], ref.rows[0][:, 1]
         assert np.max(np.abs(f - fr) / np.abs(fr)) <= 1e-5
+
+
+@pytest.mark.parametrize("mode", ["slab", "allreduce"])
+def test_nccl_transport_single_rank(ncsg, port, mode):
+    # the NCCL transport itself (dlopen'd libnccl, ncclCommInitRank, reduce-
+    # scatter, grouped send/recv all-to-all, in-place all-gather, all-reduce)
+    # on a one-rank communicator: the sharded step with P = 1 must equal the
+    # plain engine, and it is graph-capturable
+    import torch  # noqa: F401  (loads the process's NCCL first)
+
+    prob, mask, gamma = small_ct(port, n=64, A=48)
+    ref = gpu_problem(ncsg, prob, gamma, mask).solve(20, record_every=10)
+    comm = ncsg.Comm.nccl(ncsg.Comm.nccl_unique_id(), 0, 1, 0)
+    p = gpu_problem(ncsg, prob, gamma, mask)
+    p.set_comm(comm, ncsg.XCHG_SLAB if mode == "slab" else ncsg.XCHG_ALLREDUCE)
+    g = p.solve(20, record_every=10)
+    assert rel(g.x[0], ref.x[0]) <= 1e-6
+    q = gpu_problem(ncsg, prob, gamma, mask)
+    q.set_comm(comm, ncsg.XCHG_SLAB if mode == "slab" else ncsg.XCHG_ALLREDUCE)
+    q.step(5, graph=True)
+    q.step(5, graph=True)
+    r = gpu_problem(ncsg, prob, gamma, mask)
+    r.step(10)
+    assert rel(q.get_state()[0], r.get_state()[0]) <= 1e-6
