@@ -228,18 +228,18 @@ __device__ __forceinline__ float2* fft_run(float2* a, float2* b, int nfft, const
                       : fft_mixed<SIGN>(a, b, nfft, sh, tw);
 }
 
-__global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
-                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
-  pdl_wait();
+// Row block bx of problem b (the kernel's blockIdx.x / .y; the fused solve
+// calls it per work item).
+__device__ __forceinline__ void rows_r2c_body(const AtuTerms& T, float2* __restrict__ specT,
+                                              const float2* __restrict__ tw, const FftShape& sh,
+                                              const RowSlab& rs, int bx, int b) {
   extern __shared__ float2 zs[];
   const int n = T.n;
-  const int y0 = rs.r0 + blockIdx.x * kRowsPerBlock;
+  const int y0 = rs.r0 + bx * kRowsPerBlock;
   const int yend = rs.r0 + rs.rows;  // rows [r0, r0 + rows) of the image
-  const int b = blockIdx.y;
   const int npair = kRowsPerBlock / 2;
   float2* zb = zs + npair * n;  // Stockham scratch
-  if (T.counter && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0)
-    atomicAdd(T.counter + 1, 1);
+  if (T.counter && bx == 0 && b == 0 && threadIdx.x == 0) atomicAdd(T.counter + 1, 1);
   // Phase 1: row-major terms, coalesced along x (4 pixels per thread when
   // the rows are float4-aligned).
   if ((n & 3) == 0) {
@@ -310,18 +310,24 @@ __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
   }
 }
 
+__global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
+                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
+  pdl_wait();
+  rows_r2c_body(T, specT, tw, sh, rs, blockIdx.x, blockIdx.y);
+}
+
 #ifndef NCSG_FFT_COLS
 #define NCSG_FFT_COLS 2
 #endif
 constexpr int kColsPerBlock = NCSG_FFT_COLS;  // columns per column-pass CTA
 
-__global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2* __restrict__ maskT,
-                                       const float2* __restrict__ tw, FftShape sh) {
-  pdl_wait();
+__device__ __forceinline__ void cols_filter_body(float2* __restrict__ specT,
+                                                 const float2* __restrict__ maskT,
+                                                 const float2* __restrict__ tw, const FftShape& sh,
+                                                 int bx, int b) {
   const int n = sh.n;
   extern __shared__ float2 zs[];
-  const int k0 = blockIdx.x * kColsPerBlock;
-  const int b = blockIdx.y;
+  const int k0 = bx * kColsPerBlock;
   const int nk = n / 2 + 1;
   const int nc = min(kColsPerBlock, nk - k0);
   float2* col = specT + (static_cast<size_t>(b) * nk + k0) * n;  // nc contiguous columns
@@ -371,6 +377,12 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
   } else {
     for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
   }
+}
+
+__global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2* __restrict__ maskT,
+                                       const float2* __restrict__ tw, FftShape sh) {
+  pdl_wait();
+  cols_filter_body(specT, maskT, tw, sh, blockIdx.x, blockIdx.y);
 }
 
 // Sharded column pass: the same transform on a rank's column slab after the
@@ -423,14 +435,13 @@ __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
-__global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
-                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
-  pdl_wait();
+__device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, const XUpdate& xu,
+                                              const float2* __restrict__ tw, const FftShape& sh,
+                                              const RowSlab& rs, int bx, int b) {
   const int n = sh.n;
   extern __shared__ float2 zs[];
-  const int y0 = rs.r0 + blockIdx.x * kRowsPerBlock;
+  const int y0 = rs.r0 + bx * kRowsPerBlock;
   const int yend = rs.r0 + rs.rows;
-  const int b = blockIdx.y;
   const int nk = n / 2 + 1;
   const size_t nn = static_cast<size_t>(n) * n;
   const float2* in = specT + static_cast<size_t>(b) * rs.bstride;
@@ -539,6 +550,12 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
       xu.xT[b * nn + static_cast<size_t>(x) * n + y] = (r & 1) ? zz.y : zz.x;
     }
   }
+}
+
+__global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
+                                    const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
+  pdl_wait();
+  rows_c2r_body(specT, xu, tw, sh, rs, blockIdx.x, blockIdx.y);
 }
 
 int log2i(int n) {
