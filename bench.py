@@ -382,8 +382,11 @@ def bench_multi(args, cfg):
         units = 1
         mode = (f"{'orbit' if s.range == (0, 0) else 'angle'}-sharded, "
                 + ("gloo host-staged callbacks (functional run, one GPU) " if gloo else "NCCL ")
-                + ("reduce-scatter + slab FFT (2 all-to-all) + all-gather of x"
-                   if s.exchange == "slab" else "all-reduce of A^T u + replicated FFT solve"))
+                + {"slab": "reduce-scatter + slab FFT (2 all-to-all) + all-gather of x",
+                   "p2p": "slab FFT with the reduce-scatter, both all-to-alls and the "
+                          "all-gather fused into the producing kernels over NVLink peer "
+                          "memory (CUDA IPC), stream-ordered barriers",
+                   "allreduce": "all-reduce of A^T u + replicated FFT solve"}[s.exchange])
 
         def make():
             q = multigpu.ShardedSolver(cfg, b, mask, rank, world, local, comm=s.comm,

@@ -316,7 +316,16 @@ ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int
  *                        inverse -> all-to-all -> slab inverse rows + x update
  *                        -> all-gather of x (N % P == 0);
  *   NCSG_XCHG_ALLREDUCE  one all-reduce of the partial A^T u, replicated
- *                        circulant solve on every rank (latency-bound sizes).
+ *                        circulant solve on every rank (latency-bound sizes);
+ *   NCSG_XCHG_P2P        the slab step with every exchange fused into the
+ *                        producing kernel over peer memory (NVLink: CUDA IPC
+ *                        mappings of the peers' buffers): the A^T u assembly
+ *                        stores each row into its owner's slot (reduce-
+ *                        scatter), the row FFT stores each bin block into its
+ *                        column owner (all-to-all), the column pass stores
+ *                        back, the x update stores its rows into every rank's
+ *                        image (all-gather); a stream-ordered barrier between
+ *                        the kernels (NCCL or local transport, <= 8 ranks).
  * Objective / seminorm records and the divergence flags are reduced across
  * ranks.  (* graph capture only with the NCCL transport.)
  * Transports: NCCL (one communicator per rank, from a unique id shared by
@@ -325,7 +334,7 @@ ncsg_status ncsg_profile_end(ncsg_problem* p, double* phase_ms, int n_phase, int
 typedef struct ncsg_comm ncsg_comm;
 typedef enum { NCSG_F32 = 0, NCSG_F64 = 1, NCSG_I32 = 2 } ncsg_dtype;
 typedef enum { NCSG_SUM = 0, NCSG_MIN = 1, NCSG_MAX = 2 } ncsg_redop;
-typedef enum { NCSG_XCHG_ALLREDUCE = 0, NCSG_XCHG_SLAB = 1 } ncsg_exchange;
+typedef enum { NCSG_XCHG_ALLREDUCE = 0, NCSG_XCHG_SLAB = 1, NCSG_XCHG_P2P = 2 } ncsg_exchange;
 /* Callback transport: device pointers; the library synchronises `stream`
  * before each call and expects the result complete in device memory on
  * return (a pageable H2D cudaMemcpy alone is not: synchronise after it, or

@@ -184,6 +184,10 @@ struct ncsg_problem {
   int slab_R = 0, slab_logR = 0, slab_wc = 0;
   DevBuf<float> atu_full, atu_slab;
   DevBuf<float2> spec_slab, spec_recv, maskT_pad;
+  // P2P mode: the receive slots [src rank][R][n] and the peers' views of
+  // recv_slots / spec_recv / spec_slab / x
+  DevBuf<float> recv_slots;
+  PeerPtrs peer_slots, peer_recv, peer_slab, peer_x;
   // phase profiling (bench.py): events recorded between the phases of do_step
   bool profiling = false;
   std::vector<cudaEvent_t> events;  // kPhases + 1 per profiled step
@@ -412,7 +416,7 @@ void sharded_step(ncsg_problem* p) {
   phase_a(p);
   float* atu = p->atu_full.p;
   AtuTerms T = atu_terms(p);
-  launch_atu_assemble(T, atu, p->batch, s);
+  if (p->xchg != NCSG_XCHG_P2P) launch_atu_assemble(T, atu, p->batch, s);
   if (p->xchg == NCSG_XCHG_ALLREDUCE) {
     C.all_reduce(atu, p->nn * p->batch, NCSG_F32, NCSG_SUM, s);
     phase_b(p, atu);
@@ -420,6 +424,47 @@ void sharded_step(ncsg_problem* p) {
   }
   const int n = p->d.n, P = C.nranks(), R = p->slab_R, wc = p->slab_wc;
   const int r0 = C.rank() * R;
+  if (p->xchg == NCSG_XCHG_P2P) {
+    // every exchange fused into its producing kernel over peer memory, a
+    // stream-ordered barrier between the kernels
+    const int nk = n / 2 + 1, rk = C.rank();
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(p->x_old.p, p->x.p, p->nn * 4, cudaMemcpyDeviceToDevice, s));
+    mark(p);
+    launch_atu_assemble_scatter(T, p->peer_slots, R, rk, s);  // reduce-scatter
+    C.barrier(s);
+    AtuTerms S;
+    S.n = n;
+    S.bp_part = p->recv_slots.p - static_cast<size_t>(r0) * n;  // rows addressed globally
+    S.nV = P;
+    S.img_stride = static_cast<size_t>(R) * n;
+    S.counter = step_counter(p);
+    RowSlab rs{r0, R, R, static_cast<size_t>(P) * wc * R};
+    rs.wc = wc;
+    rs.rank = rk;
+    rs.peers = p->peer_recv;
+    launch_fft_rows_r2c(p->fft, S, p->spec_slab.p, 1, s, rs);  // + all-to-all
+    C.barrier(s);
+    mark(p);
+    ColSlab cs{p->slab_logR, wc, rk * wc, std::max(0, std::min(wc, nk - rk * wc))};
+    cs.rank = rk;
+    cs.peers = p->peer_slab;
+    launch_fft_cols_filter_slab(p->fft, p->spec_recv.p, p->maskT_pad.p, cs, s);  // + back
+    C.barrier(s);
+    mark(p);
+    XUpdate xu;
+    xu.x = p->x.p;
+    xu.subtract = 1;
+    xu.flag = p->flag.p;
+    for (int q = 0; q < P; ++q)
+      if (q != rk) xu.x_peers.p[xu.n_peers++] = p->peer_x.p[q];
+    const RowSlab own{r0, R, R, static_cast<size_t>(P) * wc * R};
+    launch_fft_rows_c2r(p->fft, p->spec_slab.p, xu, 1, s, own);  // + all-gather
+    C.barrier(s);
+    if (p->radon && !p->radon->orbit_mode && !p->radon->geo.cls[1].empty())
+      launch_transpose(p->x.p, p->xT.p, n, 1, s);
+    forward_and_dual(p);
+    return;
+  }
   mark(p);
   C.reduce_scatter(atu, p->atu_slab.p, static_cast<size_t>(R) * n, s);
   AtuTerms S;
@@ -1550,14 +1595,15 @@ ncsg_status ncsg_problem_set_comm(ncsg_problem* p, ncsg_comm* c, int exchange) {
       return;
     }
     ncsg::Comm& C = *c->c;
-    if (exchange != NCSG_XCHG_ALLREDUCE && exchange != NCSG_XCHG_SLAB)
+    if (exchange != NCSG_XCHG_ALLREDUCE && exchange != NCSG_XCHG_SLAB &&
+        exchange != NCSG_XCHG_P2P)
       throw Error{NCSG_INVALID, "unknown exchange mode"};
     if (p->n_cg > 0) throw Error{NCSG_INVALID, "the CG x-update needs the unsharded problem"};
     if (p->d.shard_count > 1 && (p->d.shard_count != C.nranks() || p->d.shard_rank != C.rank()))
       throw Error{NCSG_INVALID, "orbit shard does not match the communicator's rank / size"};
     const int n = p->d.n, P = C.nranks();
     p->atu_full.alloc(p->nn * p->batch);
-    if (exchange == NCSG_XCHG_SLAB) {
+    if (exchange != NCSG_XCHG_ALLREDUCE) {
       const int R = n / P;
       if (p->batch != 1) throw Error{NCSG_INVALID, "the slab FFT runs one problem (batch 1)"};
       if (n % P != 0 || R % 2 != 0 || (R & (R - 1)) != 0)
@@ -1578,6 +1624,22 @@ ncsg_status ncsg_problem_set_comm(ncsg_problem* p, ncsg_comm* c, int exchange) {
                                       static_cast<size_t>(nk) * n * sizeof(float2),
                                       cudaMemcpyDeviceToDevice, p->stream.s));
       ensure_scratch(p);
+      if (exchange == NCSG_XCHG_P2P) {
+        if (P > kMaxPeers) throw Error{NCSG_INVALID, "the P2P exchange spans at most 8 ranks"};
+        p->recv_slots.alloc(static_cast<size_t>(P) * R * n);
+        NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
+        auto share = [&](void* mine, PeerPtrs& out) {
+          std::vector<void*> v = C.share_pointers(mine);
+          if (static_cast<int>(v.size()) != P)
+            throw Error{NCSG_INVALID, std::string("the ") + C.name() +
+                                          " transport has no peer memory for the P2P exchange"};
+          for (int q = 0; q < P; ++q) out.p[q] = v[q];
+        };
+        share(p->recv_slots.p, p->peer_slots);
+        share(p->spec_recv.p, p->peer_recv);
+        share(p->spec_slab.p, p->peer_slab);
+        share(p->x.p, p->peer_x);
+      }
     }
     NCSG_CUDA_CHECK(cudaStreamSynchronize(p->stream.s));
     p->comm = &C;

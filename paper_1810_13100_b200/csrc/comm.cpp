@@ -89,6 +89,38 @@ int nccl_type(ncsg_dtype t) {
 }
 int nccl_op(ncsg_redop o) { return o == NCSG_MIN ? kNcclMin : (o == NCSG_MAX ? kNcclMax : kNcclSum); }
 
+// Peer views of every rank's allocation for multi-process transports: the
+// CUDA IPC handles (64 bytes = 16 floats) all-gathered through the
+// transport itself, the peers' handles opened in this process (NVLink /
+// NVSwitch peer mappings across GPUs; plain mappings between processes that
+// share a GPU).  Opened mappings are appended to `opened` for closing.
+std::vector<void*> ipc_share(Comm& c, void* mine, std::vector<void*>& opened) {
+  cudaIpcMemHandle_t h;
+  NCSG_CUDA_CHECK(cudaIpcGetMemHandle(&h, mine));
+  static_assert(sizeof(h) % 4 == 0, "handle size");
+  const size_t nf = sizeof(h) / 4;
+  const int P = c.nranks();
+  float* d = nullptr;
+  NCSG_CUDA_CHECK(cudaMalloc(&d, nf * 4 * (P + 1)));
+  cudaStream_t s = nullptr;
+  NCSG_CUDA_CHECK(cudaMemcpy(d, &h, sizeof(h), cudaMemcpyHostToDevice));
+  c.all_gather(d, d + nf, nf, s);
+  NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+  std::vector<cudaIpcMemHandle_t> all(P);
+  NCSG_CUDA_CHECK(cudaMemcpy(all.data(), d + nf, sizeof(h) * P, cudaMemcpyDeviceToHost));
+  cudaFree(d);
+  std::vector<void*> out(P);
+  for (int r = 0; r < P; ++r) {
+    if (r == c.rank()) {
+      out[r] = mine;
+      continue;
+    }
+    NCSG_CUDA_CHECK(cudaIpcOpenMemHandle(&out[r], all[r], cudaIpcMemLazyEnablePeerAccess));
+    opened.push_back(out[r]);
+  }
+  return out;
+}
+
 class NcclComm final : public Comm {
  public:
   NcclComm(const unsigned char* id, int rank, int nranks, int device) {
@@ -100,7 +132,15 @@ class NcclComm final : public Comm {
     nccl_check(nccl().CommInitRank(&c_, nranks, uid, rank), "ncclCommInitRank");
   }
   ~NcclComm() override {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    if (scratch_) cudaFree(scratch_);
     if (c_) nccl().CommDestroy(c_);
+  }
+  std::vector<void*> share_pointers(void* mine) override { return ipc_share(*this, mine, opened_); }
+  void barrier(cudaStream_t s) override {
+    if (!scratch_) NCSG_CUDA_CHECK(cudaMalloc(&scratch_, 4));
+    nccl_check(nccl().AllReduce(scratch_, scratch_, 1, kNcclInt32, kNcclSum, c_, s),
+               "ncclAllReduce (barrier)");
   }
   void all_reduce(void* buf, size_t count, ncsg_dtype t, ncsg_redop op, cudaStream_t s) override {
     nccl_check(nccl().AllReduce(buf, buf, count, nccl_type(t), nccl_op(op), c_, s), "ncclAllReduce");
@@ -127,6 +167,8 @@ class NcclComm final : public Comm {
 
  private:
   nccl_comm_t c_ = nullptr;
+  void* scratch_ = nullptr;
+  std::vector<void*> opened_;
 };
 
 // ----------------------------------------------------------- callbacks
@@ -154,8 +196,19 @@ class CallbackComm final : public Comm {
     call(ops_.all_to_all ? ops_.all_to_all(ops_.ctx, send, recv, count, s) : -1, "all_to_all");
   }
   const char* name() const override { return "callbacks"; }
+  void barrier(cudaStream_t s) override {
+    if (!scratch_) NCSG_CUDA_CHECK(cudaMalloc(&scratch_, 4));
+    all_reduce(scratch_, 1, NCSG_I32, NCSG_SUM, s);
+  }
+  std::vector<void*> share_pointers(void* mine) override { return ipc_share(*this, mine, opened_); }
+  ~CallbackComm() override {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
+    if (scratch_) cudaFree(scratch_);
+  }
 
  private:
+  void* scratch_ = nullptr;
+  std::vector<void*> opened_;
   static void call(int rc, const char* what) {
     if (rc != 0)
       throw Error{NCSG_CUDA, std::string("communicator callback ") + what + " failed (" +
@@ -175,6 +228,7 @@ struct LocalGroup {
   int arrived = 0;
   long gen = 0;
   std::vector<std::vector<char>> host;  // per-rank staged send data
+  std::vector<void*> ptrs;              // share_pointers exchange
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
     const long g = gen;
@@ -233,6 +287,21 @@ class LocalComm final : public Comm {
     finish(recv, out.data(), out.size() * 4, s);
   }
   const char* name() const override { return "local"; }
+  std::vector<void*> share_pointers(void* mine) override {
+    {
+      std::lock_guard<std::mutex> lk(g_->mu);
+      g_->ptrs.resize(nranks_);
+      g_->ptrs[rank_] = mine;
+    }
+    g_->barrier();
+    std::vector<void*> out = g_->ptrs;
+    g_->barrier();
+    return out;
+  }
+  void barrier(cudaStream_t s) override {
+    NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
+    g_->barrier();
+  }
 
  private:
   template <class T>

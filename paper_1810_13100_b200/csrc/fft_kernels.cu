@@ -300,7 +300,14 @@ __device__ __forceinline__ void rows_r2c_body(const AtuTerms& T, float2* __restr
     const float2 zm = zq[(n - k) % n];
     const float2 va = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
     const float2 vb = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
-    float2* dst = out + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    float2* dst;
+    if (rs.peers.p[0]) {  // fused all-to-all: straight into rank k / wc's blocks
+      const int q = k / rs.wc;
+      dst = static_cast<float2*>(rs.peers.p[q]) +
+            static_cast<size_t>(rs.rank * rs.wc + (k - q * rs.wc)) * rs.ld + (y - rs.r0);
+    } else {
+      dst = out + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    }
     if (y + 1 < yend && ((n | rs.ld | rs.r0) & 1) == 0) {
       *reinterpret_cast<float4*>(dst) = make_float4(va.x, va.y, vb.x, vb.y);
     } else {
@@ -413,7 +420,11 @@ __global__ void fft_cols_filter_slab_kernel(float2* __restrict__ slab,
   z = fft_run<+1>(z, z == zs ? zb : zs, nc, sh, tw);
   for (int i = threadIdx.x; i < nc * n; i += blockDim.x) {
     const int c = i / n, j = i - c * n;
-    slab[at(c, j)] = z[i];
+    if (cs.peers.p[0])  // fused all-to-all back: block j >> logR to its rank
+      static_cast<float2*>(cs.peers.p[j >> cs.logR])
+          [(static_cast<size_t>(cs.rank * cs.wc + c0 + c) << cs.logR) + (j & (R - 1))] = z[i];
+    else
+      slab[at(c, j)] = z[i];
   }
 }
 
@@ -505,6 +516,8 @@ __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, 
       xn = make_float4(xo.x - zr[0].x, xo.y - zr[1].x, xo.z - zr[2].x, xo.w - zr[3].x);
     if (xu.x_old) *reinterpret_cast<float4*>(xu.x_old + gi) = xo;
     *reinterpret_cast<float4*>(xu.x + gi) = xn;
+    for (int q = 0; q < xu.n_peers; ++q)  // fused all-gather of the own rows
+      *reinterpret_cast<float4*>(static_cast<float*>(xu.x_peers.p[q]) + gi) = xn;
     bad |= !isfinite(xn.x) || !isfinite(xn.y) || !isfinite(xn.z) || !isfinite(xn.w);
     if (xu.xT) {
       if (r & 1) {
@@ -530,6 +543,7 @@ __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, 
       xn = w;
     }
     xu.x[gi] = xn;
+    for (int q = 0; q < xu.n_peers; ++q) static_cast<float*>(xu.x_peers.p[q])[gi] = xn;
     bad |= !isfinite(xn);
     if (xu.xT) {
       if (r & 1)

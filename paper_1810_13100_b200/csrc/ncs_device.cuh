@@ -16,7 +16,8 @@ __device__ __forceinline__ float atu_rowmajor(const AtuTerms& T, int b, int y, i
   float v = 0.f;
   if (T.bp_part) {
     const float* p = T.bp_part + b * T.part_stride + i;
-    for (int c = 0; c < T.nV; ++c) v += p[c * nn];
+    const size_t ps = T.img_stride ? T.img_stride : nn;
+    for (int c = 0; c < T.nV; ++c) v += p[c * ps];
   }
   if (T.ident) v += T.ident[b * T.ident_stride + i];
   if (T.ident2) v += T.ident2[b * T.ident_stride + i];
@@ -46,8 +47,9 @@ __device__ __forceinline__ float4 atu_rowmajor4(const AtuTerms& T, int b, int y,
   float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
   if (T.bp_part) {
     const float* p = T.bp_part + b * T.part_stride + i;
+    const size_t ps = T.img_stride ? T.img_stride : nn;
     for (int c = 0; c < T.nV; ++c) {
-      const float4 q = *reinterpret_cast<const float4*>(p + c * nn);
+      const float4 q = *reinterpret_cast<const float4*>(p + c * ps);
       v.x += q.x, v.y += q.y, v.z += q.z, v.w += q.w;
     }
   }

@@ -727,7 +727,42 @@ __global__ void atu_assemble_kernel(AtuTerms T, float* out) {
     out[b * nn + static_cast<size_t>(y) * n + x] = atu_rowmajor(T, b, y, x) + t[threadIdx.x][k];
   }
 }
+// The fused P2P reduce-scatter: this rank's A^T u (partials summed as in
+// atu_assemble_kernel), row y stored straight into its owner rank q = y / R's
+// receive slots at [src rank][y - q R][x] over peer memory (NVLink).  The
+// owner sums its P slots in rank order (deterministic).
+__global__ void atu_assemble_scatter_kernel(AtuTerms T, PeerPtrs slots, int R, int rank) {
+  __shared__ float t[32][33];
+  const int n = T.n;
+  const size_t nn = static_cast<size_t>(n) * n;
+  const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
+  const float* ph = T.bp_part ? T.bp_part + T.nV * nn : nullptr;
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = bx + k, x = by + threadIdx.x;  // transposed coordinates
+    float v = 0.f;
+    if (ph && y < n && x < n)
+      for (int c = 0; c < T.nH; ++c) v += ph[c * nn + static_cast<size_t>(y) * n + x];
+    t[k][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int k = threadIdx.y; k < 32; k += blockDim.y) {
+    const int y = by + k, x = bx + threadIdx.x;
+    if (y >= n || x >= n) continue;
+    const int q = y / R;
+    float* dst = static_cast<float*>(slots.p[q]) +
+                 (static_cast<size_t>(rank) * R + (y - q * R)) * n + x;
+    *dst = atu_rowmajor(T, 0, y, x) + t[threadIdx.x][k];
+  }
+}
 }  // namespace
+
+void launch_atu_assemble_scatter(const AtuTerms& T, const PeerPtrs& slots, int R, int rank,
+                                 cudaStream_t s) {
+  dim3 grid((T.n + 31) / 32, (T.n + 31) / 32, 1);
+  atu_assemble_scatter_kernel<<<grid, dim3(32, 8), 0, s>>>(T, slots, R, rank);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  count_launch();
+}
 
 void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t s) {
   dim3 grid((T.n + 31) / 32, (T.n + 31) / 32, batch);

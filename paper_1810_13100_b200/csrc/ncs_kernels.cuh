@@ -95,6 +95,10 @@ void launch_sub(const float* a, const float* b, float* out, size_t count, cudaSt
 namespace ncsg {
 // out[batch][n*n] = A^T u assembled from `T` (sharded multi-GPU path).
 void launch_atu_assemble(const AtuTerms& T, float* out, int batch, cudaStream_t s);
+// The same sum, batch 1, row y stored into rank y / R's slot `rank` over peer
+// memory (the fused P2P reduce-scatter of the sharded slab step).
+void launch_atu_assemble_scatter(const AtuTerms& T, const PeerPtrs& slots, int R, int rank,
+                                 cudaStream_t s);
 
 // Setup path (calibrate_scale, power-method screen): out[batch][blocks][2] =
 // per-block [sum a*b, sum c*d] over `count` elements of each batch entry.

@@ -26,6 +26,15 @@ class Comm {
   virtual const char* name() const = 0;
   // stream-ordered collectives that a CUDA graph can capture (NCCL)
   virtual bool capturable() const { return false; }
+  // Peer memory (the fused P2P exchange): every rank's `mine` (the base of a
+  // cudaMalloc allocation of the same size on every rank) as pointers this
+  // rank's kernels can store to -- NVLink peers through CUDA IPC (NCCL
+  // transport), plain pointers within one process (local group).  Empty when
+  // the transport has no peer memory.
+  virtual std::vector<void*> share_pointers(void* mine) { (void)mine; return {}; }
+  // All ranks' work on their streams so far is complete and visible to the
+  // peers' later work (stream-ordered for NCCL).
+  virtual void barrier(cudaStream_t s) = 0;
 
  protected:
   int rank_ = 0, nranks_ = 1;

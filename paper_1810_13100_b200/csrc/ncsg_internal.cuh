@@ -335,20 +335,41 @@ struct FftPlan {
   void init(int n_, cudaStream_t s);
 };
 // Spectrum layout: specT[batch][n/2+1][n] complex (column-major half spectrum).
+// Peer memory of the fused P2P exchange (<= kMaxPeers ranks of one node):
+// rank q's buffer as this rank's kernels store to it.
+constexpr int kMaxPeers = 8;
+struct PeerPtrs {
+  void* p[kMaxPeers] = {};
+};
 // Row slabs (sharded slab FFT): the row passes cover image rows [r0, r0 +
 // rows) and address bin (k, y) at k * ld + (y - r0), batch stride bstride;
-// the unsharded layout is {0, n, n, (n/2+1) n}.
+// the unsharded layout is {0, n, n, (n/2+1) n}.  With peers set (fused P2P
+// all-to-all), the R2C pass stores bin (k, y) straight into rank q = k / wc's
+// receive blocks at ((rank * wc + k % wc) * ld + (y - r0)).
 struct RowSlab {
   int r0 = 0, rows = 0, ld = 0;
   size_t bstride = 0;
-  static RowSlab full(int n) { return RowSlab{0, n, n, static_cast<size_t>(n / 2 + 1) * n}; }
+  int wc = 0, rank = 0;
+  PeerPtrs peers;
+  static RowSlab full(int n) {
+    RowSlab r;
+    r.rows = n;
+    r.ld = n;
+    r.bstride = static_cast<size_t>(n / 2 + 1) * n;
+    return r;
+  }
 };
 // Column slab of the sharded column pass: after the all-to-all a rank holds
 // P blocks [source rank i][wc columns][R rows]; bin (local column c, row j)
 // sits at ((j >> logR) * wc + c) * R + (j & (R-1)); its global column is
 // k0 + c (filter column).  ncols local columns are transformed.
+// With peers set (fused P2P all-to-all back), block i of the result is
+// stored straight into rank i's row-slab spectrum at ((rank * wc + c) << logR)
+// + (j & (R-1)).
 struct ColSlab {
   int logR = 0, wc = 0, k0 = 0, ncols = 0;
+  int rank = 0;
+  PeerPtrs peers;
 };
 // Real-to-half-spectrum row pass; `terms` (combine) describes how the real
 // input image is assembled (see ncs_kernels.cu).
@@ -371,6 +392,10 @@ struct XUpdate {
   float* xT = nullptr;      // receives the transposed result (nullable)
   int subtract = 1;
   int* flag = nullptr;      // [0] = min(step counter [1]) over non-finite results (nullable)
+  // fused P2P all-gather: the updated rows also go to these ranks' images
+  // (the own x among them counts once: x itself)
+  PeerPtrs x_peers;
+  int n_peers = 0;
 };
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s, RowSlab rs = RowSlab{});
@@ -387,6 +412,7 @@ struct AtuTerms {
   float wd = 0.f;                  // D-block weight beta/alpha
   const float* plain = nullptr;    // plain image input (mask apply), overrides the rest
   size_t part_stride = 0;          // per-batch stride of bp_part
+  size_t img_stride = 0;           // stride between partial images (0: n*n)
   size_t ident_stride = 0, ug_stride = 0;
   int* counter = nullptr;          // flag buffer: counter[1] += 1 once per step (nullable)
 };

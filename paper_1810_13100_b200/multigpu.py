@@ -7,10 +7,17 @@ rank owns its rows of R, of the sinogram dual u_s, of b and of the cached
 R x.  The step runs inside libncsg with an NCCL communicator
 (ncsg_problem_set_comm), in one of two exchange modes:
 
+  p2p        the slab decomposition below with every exchange fused into its
+             producing kernel over NVLink peer memory (CUDA IPC mappings):
+             the A^T u assembly stores rows into their owners' slots, the row
+             FFT stores bin blocks into their column owners, the column pass
+             stores back, the x update stores its rows into every rank's
+             image; a stream-ordered NCCL barrier between the kernels
+             (default for large N; falls back to slab if peer mappings fail);
   slab       partial A^T u -> NCCL reduce-scatter into N/P-row slabs -> row
              FFT of the own slab -> all-to-all -> column FFT . filter .
              inverse -> all-to-all -> inverse rows + x update of the own rows
-             -> all-gather of x (north_star's design; large N);
+             -> all-gather of x (north_star's design with NCCL collectives);
   allreduce  one all-reduce of the N^2 partial, replicated circulant solve
              (latency-bound sizes such as 512^2).
 
@@ -53,14 +60,15 @@ def replica_share(batch: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def default_exchange(n: int, world: int) -> str:
-    """slab where the image splits into power-of-two slabs and is large
-    enough for the slab FFT to pay (N >= 1024), else the all-reduce."""
+    """p2p (the fused slab exchange) where the image splits into power-of-two
+    slabs, at most 8 ranks and large enough for the slab FFT to pay
+    (N >= 1024), else the all-reduce; NCSG_XCHG=slab|p2p|allreduce overrides."""
     env = os.environ.get("NCSG_XCHG")
-    if env in ("slab", "allreduce"):
+    if env in ("slab", "allreduce", "p2p"):
         return env
     r = n // world
     ok = n % world == 0 and r % 2 == 0 and (r & (r - 1)) == 0
-    return "slab" if ok and n >= 1024 else "allreduce"
+    return "p2p" if ok and n >= 1024 and world <= 8 else "allreduce"
 
 
 def nccl_comm(rank: int, world: int, device: int):
@@ -97,8 +105,15 @@ class ShardedSolver:
         self.exchange = exchange or default_exchange(cfg.n, world)
         if world > 1:
             self.comm = comm if comm is not None else nccl_comm(rank, world, device)
-            self.prob.set_comm(self.comm, ncsg.XCHG_SLAB if self.exchange == "slab"
-                               else ncsg.XCHG_ALLREDUCE)
+            modes = {"slab": ncsg.XCHG_SLAB, "p2p": ncsg.XCHG_P2P,
+                     "allreduce": ncsg.XCHG_ALLREDUCE}
+            try:
+                self.prob.set_comm(self.comm, modes[self.exchange])
+            except (ncsg.NcsgError, ValueError):
+                if self.exchange != "p2p":
+                    raise
+                self.exchange = "slab"  # no peer mappings on this node: NCCL collectives
+                self.prob.set_comm(self.comm, ncsg.XCHG_SLAB)
         self.stream = torch.cuda.ExternalStream(self.prob.stream, device=f"cuda:{device}")
 
     def step(self, iters: int = 1, graph: bool = False):

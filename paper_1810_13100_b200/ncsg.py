@@ -46,7 +46,7 @@ class PlanInfo(C.Structure):
                 ("range", C.c_int64), ("batch", C.c_int64)]
 
 
-XCHG_ALLREDUCE, XCHG_SLAB = 0, 1
+XCHG_ALLREDUCE, XCHG_SLAB, XCHG_P2P = 0, 1, 2
 F32, F64, I32 = 0, 1, 2
 SUM, MIN, MAX = 0, 1, 2
 _AllReduceFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int, C.c_int,

@@ -2,8 +2,9 @@
 test_two_process_gloo_callbacks): both processes share cuda:0, each owns an
 orbit shard, and the library's collectives go through Python callbacks that
 stage the device buffers on the host and exchange them with torch.distributed
-(gloo over 127.0.0.1).  Writes rank r's final x and record rows to
-<out>/rank<r>.npz."""
+(gloo over 127.0.0.1); in the "p2p" mode the fused exchange stores straight
+into the other process's buffers through CUDA IPC mappings.  Writes rank r's
+final x and record rows to <out>/rank<r>.npz."""
 import os
 import sys
 
@@ -14,7 +15,7 @@ sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
 
-def main(rank, world, port, out):
+def main(rank, world, port, out, mode="slab"):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
@@ -33,7 +34,7 @@ def main(rank, world, port, out):
                      n_angles=prob.angles, n_det=prob.det, orbit_shard=(rank, world))
     comm = multigpu.gloo_comm(rank, world)  # host-staged gloo collectives
     p.set_state()
-    p.set_comm(comm, ncsg.XCHG_SLAB)
+    p.set_comm(comm, ncsg.XCHG_P2P if mode == "p2p" else ncsg.XCHG_SLAB)
     res = p.solve(30, record_every=10)
     np.savez(os.path.join(out, f"rank{rank}.npz"), x=res.x, rows=res.rows)
     dist.barrier()
@@ -41,4 +42,5 @@ def main(rank, world, port, out):
 
 
 if __name__ == "__main__":
-    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4])
+    main(int(sys.argv[1]), int(sys.argv[2]), int(sys.argv[3]), sys.argv[4],
+         sys.argv[5] if len(sys.argv) > 5 else "slab")

@@ -54,14 +54,19 @@ def sharded_problems(ncsg, prob, gamma, mask, P, shard, mode):
         p = ncsg.Problem(ncsg.CT, prob.n, prob.alpha, prob.beta, prob.lam, gamma, prob.b,
                          mask=mask, n_angles=prob.angles, n_det=prob.det, **kw)
         p.set_state()
-        p.set_comm(comms[r], ncsg.XCHG_SLAB if mode == "slab" else ncsg.XCHG_ALLREDUCE)
         probs.append(p)
+    # attaching is collective for the P2P mode (the ranks exchange their
+    # buffers' peer views): every rank on its own thread
+    x = {"slab": ncsg.XCHG_SLAB, "p2p": ncsg.XCHG_P2P, "allreduce": ncsg.XCHG_ALLREDUCE}[mode]
+    run_ranks([lambda p=p, c=c: p.set_comm(c, x) for p, c in zip(probs, comms)])
     return probs, comms
 
 
 @pytest.mark.parametrize("P,shard,mode", [(2, "orbit", "slab"), (4, "orbit", "slab"),
                                           (2, "orbit", "allreduce"), (2, "contig", "slab"),
-                                          (4, "contig", "allreduce"), (8, "orbit", "slab")])
+                                          (4, "contig", "allreduce"), (8, "orbit", "slab"),
+                                          (2, "orbit", "p2p"), (4, "orbit", "p2p"),
+                                          (8, "orbit", "p2p"), (4, "contig", "p2p")])
 def test_sharded_solve_matches_unsharded(ncsg, port, P, shard, mode):
     prob, mask, gamma = small_ct(port, n=64, A=48)
     ref = gpu_problem(ncsg, prob, gamma, mask).solve(40, record_every=10)
@@ -83,7 +88,7 @@ def test_sharded_solve_against_oracle(ncsg, port):
     # the slab-sharded engine against the fp64 oracle at the configured bar
     prob, mask, gamma = small_ct(port, n=64, A=48)
     o = port.solve(prob, gamma, mask, 60, record_every=20)
-    probs, comms = sharded_problems(ncsg, prob, gamma, mask, 4, "orbit", "slab")
+    probs, comms = sharded_problems(ncsg, prob, gamma, mask, 4, "orbit", "p2p")
     res = run_ranks([lambda p=p: p.solve(60, record_every=20) for p in probs])
     assert rel(res[0].x[0], o.x) <= 1e-4
     oo = o.rows[:, 1]
@@ -142,7 +147,8 @@ def test_slab_mode_validation(ncsg, port):
         q.set_comm(comms[0], ncsg.XCHG_ALLREDUCE)
 
 
-def test_two_process_gloo_callbacks(ncsg, port, tmp_path):
+@pytest.mark.parametrize("mode", ["slab", "p2p"])
+def test_two_process_gloo_callbacks(ncsg, port, tmp_path, mode):
     # two processes (one CUDA context each on cuda:0), the library's
     # collectives through Python callbacks over torch.distributed gloo on
     # host-staged buffers: the real CUDA phases of the slab-sharded step
@@ -156,7 +162,7 @@ def test_two_process_gloo_callbacks(ncsg, port, tmp_path):
     s.close()
     here = os.path.dirname(os.path.abspath(__file__))
     procs = [subprocess.Popen([sys.executable, os.path.join(here, "gloo_rank_worker.py"), str(r),
-                               "2", str(free), str(tmp_path)]) for r in range(2)]
+                               "2", str(free), str(tmp_path), mode]) for r in range(2)]
     for q in procs:
         assert q.wait(timeout=600) == 0
     prob, mask, gamma = small_ct(port, n=64, A=48)

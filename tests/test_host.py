@@ -314,7 +314,7 @@ def test_slab_exchange_layout_gloo():
         p.join(timeout=60)
     for rank, err, idlen, big, small in res:
         assert err < 1e-12, res
-        assert idlen == 128 and big == "slab" and small == "allreduce"
+        assert idlen == 128 and big == "p2p" and small == "allreduce"
 
 
 def test_replica_shares_cover_batch():
