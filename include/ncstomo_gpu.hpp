@@ -834,7 +834,9 @@ struct SolverConfig {
   /// the exchange (slab FFT or all-reduce, ncsg.h) runs inside the library;
   /// the state's u then holds this rank's rays (x is replicated).
   std::shared_ptr<Communicator> comm;
-  bool slab_exchange = true;
+  /// NCSG_XCHG_P2P (slab step, exchanges fused into the kernels over peer
+  /// memory), NCSG_XCHG_SLAB (NCCL collectives) or NCSG_XCHG_ALLREDUCE.
+  ncsg_exchange exchange = NCSG_XCHG_SLAB;
 };
 
 /// SolverState (solvers.hpp:74-78).
@@ -943,8 +945,7 @@ class Engine {
     if (n_cg > 0) check(ncsg_set_cg(h, n_cg));
     if (P > 1) {
       comm_ = cfg.comm;
-      check(ncsg_problem_set_comm(h, comm_->get(),
-                                  cfg.slab_exchange ? NCSG_XCHG_SLAB : NCSG_XCHG_ALLREDUCE));
+      check(ncsg_problem_set_comm(h, comm_->get(), cfg.exchange));
     }
   }
   ncsg_problem* get() const { return h_.get(); }

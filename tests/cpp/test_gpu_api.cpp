@@ -411,6 +411,7 @@ int main() {
       th.emplace_back([&, r] {
         SolverConfig c = cfg;
         c.comm = comms[r];
+        c.exchange = NCSG_XCHG_P2P;
         res[r] = ncs_solve(prob, c);
       });
     for (auto& t : th) t.join();
@@ -424,7 +425,7 @@ int main() {
       ok = ok && std::sqrt(num / den) <= 1e-5 &&
            std::abs(res[r].objective - ref.objective) <= 1e-5 * std::abs(ref.objective);
     }
-    CHECK(ok, "4-rank slab-sharded ncs_solve (cfg.comm) == unsharded");
+    CHECK(ok, "4-rank P2P slab-sharded ncs_solve (cfg.comm) == unsharded");
   }
   std::printf("%d failure(s)\n", failures);
   return failures;
