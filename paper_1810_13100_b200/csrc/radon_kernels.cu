@@ -537,8 +537,15 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
   const AngleGeom& g = o.rep;
   float* myacc = racc + warp * 4 * a.rmax;
   unsigned* myflag = rflag + warp * a.rmax;
-  for (int i = lane; i < 4 * a.rmax; i += 32) myacc[i] = 0.f;
-  for (int i = lane; i < a.rmax; i += 32) myflag[i] = 0u;
+  // one tile row per CTA (seg_tiles == 1): each lane stores its ray sums
+  // straight to the partial slot, no shared-memory ray accumulators
+  const bool direct = a.seg_tiles == 1;
+  if (!direct) {
+    for (int i = lane; i < 4 * a.rmax; i += 32) myacc[i] = 0.f;
+    for (int i = lane; i < a.rmax; i += 32) myflag[i] = 0u;
+  }
+  const int slot0 = has ? (g.dX >= 0 ? strip : a.n_strips - 1 - strip) + seg : 0;
+  float* out0 = a.part + (static_cast<size_t>(b) * a.slots + slot0) * a.m + a.s_mid;
   const unsigned mask = 0x7fffffu, one = 0x3f800000u;
   unsigned phase = 0;
 
@@ -697,7 +704,11 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
             Y += g.dYq;
           }
         }
-        if (act) {
+        if (act && direct) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (jh[k] > jl[k]) out0[static_cast<size_t>(o.t[k]) * a.det + s] = acc[k];
+        } else if (act) {
           unsigned fl = 0;
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -710,9 +721,8 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
     }
   }
   __syncwarp();
-  if (has) {
-    const int slot = (g.dX >= 0 ? strip : a.n_strips - 1 - strip) + seg;
-    float* out = a.part + (static_cast<size_t>(b) * a.slots + slot) * a.m + a.s_mid;
+  if (has && !direct) {
+    float* out = out0;
     for (int s = slo + lane; s <= shi; s += 32) {
       const unsigned fl = myflag[s - slo];
 #pragma unroll
@@ -1627,7 +1637,7 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     std::memcpy(&map, qm.bytes, sizeof(map));
     const bool tma = qm.ok;
     const int nw = r.orb_warps;
-    const size_t smem = orbit_smem(a.rmax, nw);
+    const size_t smem = orbit_smem(a.seg_tiles == 1 ? 0 : a.rmax, nw);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     auto go = [&](auto kern) {
       set_smem(reinterpret_cast<const void*>(kern), smem);
