@@ -230,6 +230,10 @@ __device__ __forceinline__ float2* fft_run(float2* a, float2* b, int nfft, const
 
 // Row block bx of problem b (the kernel's blockIdx.x / .y; the fused solve
 // calls it per work item).
+// PEERS: the fused P2P all-to-all store (a separate instance, so the plain
+// passes keep their register budget: the peer table indexed at run time
+// lives in local memory).
+template <bool PEERS>
 __device__ __forceinline__ void rows_r2c_body(const AtuTerms& T, float2* __restrict__ specT,
                                               const float2* __restrict__ tw, const FftShape& sh,
                                               const RowSlab& rs, int bx, int b) {
@@ -301,7 +305,7 @@ __device__ __forceinline__ void rows_r2c_body(const AtuTerms& T, float2* __restr
     const float2 va = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
     const float2 vb = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
     float2* dst;
-    if (rs.peers.p[0]) {  // fused all-to-all: straight into rank k / wc's blocks
+    if (PEERS) {  // fused all-to-all: straight into rank k / wc's blocks
       const int q = k / rs.wc;
       dst = static_cast<float2*>(rs.peers.p[q]) +
             static_cast<size_t>(rs.rank * rs.wc + (k - q * rs.wc)) * rs.ld + (y - rs.r0);
@@ -317,10 +321,11 @@ __device__ __forceinline__ void rows_r2c_body(const AtuTerms& T, float2* __restr
   }
 }
 
+template <bool PEERS>
 __global__ void fft_rows_r2c_kernel(AtuTerms T, float2* __restrict__ specT,
                                     const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
   pdl_wait();
-  rows_r2c_body(T, specT, tw, sh, rs, blockIdx.x, blockIdx.y);
+  rows_r2c_body<PEERS>(T, specT, tw, sh, rs, blockIdx.x, blockIdx.y);
 }
 
 #ifndef NCSG_FFT_COLS
@@ -394,6 +399,7 @@ __global__ void fft_cols_filter_kernel(float2* __restrict__ specT, const float2*
 
 // Sharded column pass: the same transform on a rank's column slab after the
 // all-to-all (ColSlab addressing: P row blocks of R bins per column).
+template <bool PEERS>
 __global__ void fft_cols_filter_slab_kernel(float2* __restrict__ slab,
                                             const float2* __restrict__ maskT,
                                             const float2* __restrict__ tw, FftShape sh,
@@ -420,7 +426,7 @@ __global__ void fft_cols_filter_slab_kernel(float2* __restrict__ slab,
   z = fft_run<+1>(z, z == zs ? zb : zs, nc, sh, tw);
   for (int i = threadIdx.x; i < nc * n; i += blockDim.x) {
     const int c = i / n, j = i - c * n;
-    if (cs.peers.p[0])  // fused all-to-all back: block j >> logR to its rank
+    if (PEERS)  // fused all-to-all back: block j >> logR to its rank
       static_cast<float2*>(cs.peers.p[j >> cs.logR])
           [(static_cast<size_t>(cs.rank * cs.wc + c0 + c) << cs.logR) + (j & (R - 1))] = z[i];
     else
@@ -446,6 +452,7 @@ __global__ void fft_cols_forward_kernel(float2* __restrict__ specT,
   for (int j = threadIdx.x; j < nc * n; j += blockDim.x) col[j] = z[j];
 }
 
+template <bool PEERS>
 __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, const XUpdate& xu,
                                               const float2* __restrict__ tw, const FftShape& sh,
                                               const RowSlab& rs, int bx, int b) {
@@ -516,7 +523,7 @@ __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, 
       xn = make_float4(xo.x - zr[0].x, xo.y - zr[1].x, xo.z - zr[2].x, xo.w - zr[3].x);
     if (xu.x_old) *reinterpret_cast<float4*>(xu.x_old + gi) = xo;
     *reinterpret_cast<float4*>(xu.x + gi) = xn;
-    for (int q = 0; q < xu.n_peers; ++q)  // fused all-gather of the own rows
+    for (int q = 0; PEERS && q < xu.n_peers; ++q)  // fused all-gather of the own rows
       *reinterpret_cast<float4*>(static_cast<float*>(xu.x_peers.p[q]) + gi) = xn;
     bad |= !isfinite(xn.x) || !isfinite(xn.y) || !isfinite(xn.z) || !isfinite(xn.w);
     if (xu.xT) {
@@ -543,7 +550,7 @@ __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, 
       xn = w;
     }
     xu.x[gi] = xn;
-    for (int q = 0; q < xu.n_peers; ++q) static_cast<float*>(xu.x_peers.p[q])[gi] = xn;
+    for (int q = 0; PEERS && q < xu.n_peers; ++q) static_cast<float*>(xu.x_peers.p[q])[gi] = xn;
     bad |= !isfinite(xn);
     if (xu.xT) {
       if (r & 1)
@@ -566,10 +573,11 @@ __device__ __forceinline__ void rows_c2r_body(const float2* __restrict__ specT, 
   }
 }
 
+template <bool PEERS>
 __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu,
                                     const float2* __restrict__ tw, FftShape sh, RowSlab rs) {
   pdl_wait();
-  rows_c2r_body(specT, xu, tw, sh, rs, blockIdx.x, blockIdx.y);
+  rows_c2r_body<PEERS>(specT, xu, tw, sh, rs, blockIdx.x, blockIdx.y);
 }
 
 int log2i(int n) {
@@ -622,10 +630,12 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
-  ensure_smem(reinterpret_cast<const void*>(fft_rows_r2c_kernel), smem);
+  const bool peers = rs.peers.p[0] != nullptr;
+  auto kern = peers ? fft_rows_r2c_kernel<true> : fft_rows_r2c_kernel<false>;
+  ensure_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((rs.rows + kRowsPerBlock - 1) / kRowsPerBlock, batch);
   // the loader (sums of adjoint partial images) wants more threads than the FFT
-  launch_pdl(fft_rows_r2c_kernel, grid, dim3(fft_threads(kRowsPerBlock * n / 4)), smem, s, terms,
+  launch_pdl(kern, grid, dim3(fft_threads(kRowsPerBlock * n / 4)), smem, s, terms,
              specT, f.tw.p, f.shape, rs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -659,9 +669,10 @@ void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* m
   const int n = f.n;
   if (cs.ncols <= 0) return;
   size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
-  ensure_smem(reinterpret_cast<const void*>(fft_cols_filter_slab_kernel), smem);
+  auto kern = cs.peers.p[0] ? fft_cols_filter_slab_kernel<true> : fft_cols_filter_slab_kernel<false>;
+  ensure_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((cs.ncols + kColsPerBlock - 1) / kColsPerBlock, 1);
-  launch_pdl(fft_cols_filter_slab_kernel, grid, dim3(fft_threads(kColsPerBlock * n / 8)), smem, s,
+  launch_pdl(kern, grid, dim3(fft_threads(kColsPerBlock * n / 8)), smem, s,
              slab, maskT, f.tw.p, f.shape, cs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
@@ -672,9 +683,10 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n + sizeof(float) * kRowsPerBlock * n;
-  ensure_smem(reinterpret_cast<const void*>(fft_rows_c2r_kernel), smem);
+  auto kern = xu.n_peers > 0 ? fft_rows_c2r_kernel<true> : fft_rows_c2r_kernel<false>;
+  ensure_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((rs.rows + kRowsPerBlock - 1) / kRowsPerBlock, batch);
-  launch_pdl(fft_rows_c2r_kernel, grid, dim3(fft_threads((kRowsPerBlock / 2) * n / 4)), smem, s,
+  launch_pdl(kern, grid, dim3(fft_threads((kRowsPerBlock / 2) * n / 4)), smem, s,
              specT, xu, f.tw.p, f.shape, rs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
