@@ -1,0 +1,13 @@
+# Round-end measurement set: tests, bench lines per config, reference arm,
+# ncu launch list and per-config ncu --set full captures (into gpurun_out/).
+set -x
+timeout 2400 python -m pytest tests -m gpu -q 2>&1 | tail -15 > gpurun_out/final_pytest.log
+python bench.py --steps 20 --warmup 5 > gpurun_out/final_bench_c3.json 2> gpurun_out/final_bench_c3.err
+for c in c1 c2 c4 c5; do
+  python bench.py --steps 20 --warmup 5 --config $c --no-cpu-baseline > gpurun_out/final_bench_$c.json 2> gpurun_out/final_bench_$c.err
+done
+python bench.py --impl reference --steps 3 --warmup 0 > gpurun_out/final_bench_reference.json 2> gpurun_out/final_bench_reference.err
+python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/final_plain.log 2>&1 &&
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/final_ncu_launches.log 2>&1
+timeout 1500 bash scripts/gpu/ncu_cfg.sh c3 c1 c2 c5 c4
