@@ -353,6 +353,10 @@ ncsg_status ncsg_comm_create_nccl(const unsigned char id[128], int rank, int nra
 ncsg_status ncsg_comm_create_callbacks(const ncsg_comm_ops* ops, ncsg_comm** out);
 /* nranks communicators of one in-process group (out[r] = rank r). */
 ncsg_status ncsg_comm_create_local(int nranks, ncsg_comm** out);
+/* A rank of a communicator whose collectives do nothing: times one rank's
+ * kernels of the sharded step on one GPU (scaling projections; results are
+ * meaningless). */
+ncsg_status ncsg_comm_create_null(int rank, int nranks, ncsg_comm** out);
 ncsg_status ncsg_comm_destroy(ncsg_comm* c);
 /* Attach (or with NULL detach) the communicator; `exchange` = ncsg_exchange.
  * The communicator must outlive the problem's use of it. */

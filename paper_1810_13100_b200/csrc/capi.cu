@@ -1581,6 +1581,16 @@ ncsg_status ncsg_comm_create_local(int nranks, ncsg_comm** out) {
   });
 }
 
+ncsg_status ncsg_comm_create_null(int rank, int nranks, ncsg_comm** out) {
+  return guard([&] {
+    if (!out || nranks < 1 || rank < 0 || rank >= nranks)
+      throw Error{NCSG_INVALID, "invalid null communicator arguments"};
+    auto c = std::make_unique<ncsg_comm>();
+    c->c.reset(ncsg::make_null_comm(rank, nranks));
+    *out = c.release();
+  });
+}
+
 ncsg_status ncsg_comm_destroy(ncsg_comm* c) {
   return guard([&] { delete c; });
 }

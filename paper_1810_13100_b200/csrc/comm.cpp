@@ -327,7 +327,27 @@ class LocalComm final : public Comm {
   std::shared_ptr<LocalGroup> g_;
 };
 
+// No exchange at all: every collective returns at once.  A timing tool --
+// one rank's kernels of the sharded step, stream-ordered and uninterrupted,
+// for projecting multi-GPU step times on one GPU (scripts/shard_step_time.py).
+class NullComm final : public Comm {
+ public:
+  NullComm(int rank, int nranks) {
+    rank_ = rank;
+    nranks_ = nranks;
+  }
+  void all_reduce(void*, size_t, ncsg_dtype, ncsg_redop, cudaStream_t) override {}
+  void reduce_scatter(const float*, float*, size_t, cudaStream_t) override {}
+  void all_gather(const float*, float*, size_t, cudaStream_t) override {}
+  void all_to_all(const float*, float*, size_t, cudaStream_t) override {}
+  void barrier(cudaStream_t) override {}
+  const char* name() const override { return "null"; }
+  bool capturable() const override { return true; }
+};
+
 }  // namespace
+
+Comm* make_null_comm(int rank, int nranks) { return new NullComm(rank, nranks); }
 
 Comm* make_nccl_comm(const unsigned char* id, int rank, int nranks, int device) {
   return new NcclComm(id, rank, nranks, device);

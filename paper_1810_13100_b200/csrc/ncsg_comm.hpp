@@ -43,6 +43,7 @@ class Comm {
 Comm* make_nccl_comm(const unsigned char* id, int rank, int nranks, int device);
 void nccl_unique_id(unsigned char* out);
 Comm* make_callback_comm(const ncsg_comm_ops& ops);
+Comm* make_null_comm(int rank, int nranks);
 std::vector<Comm*> make_local_group(int nranks);
 
 }  // namespace ncsg

@@ -177,6 +177,7 @@ def lib():
     L.ncsg_comm_create_callbacks.argtypes = [C.POINTER(CommOps), C.POINTER(C.c_void_p)]
     L.ncsg_comm_create_local.argtypes = [C.c_int, C.POINTER(C.c_void_p)]
     L.ncsg_comm_destroy.argtypes = [C.c_void_p]
+    L.ncsg_comm_create_null.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_void_p)]
     L.ncsg_problem_set_comm.argtypes = [C.c_void_p, C.c_void_p, C.c_int]
     _lib = L
     return L
@@ -585,6 +586,13 @@ class Comm:
         h = C.c_void_p()
         _check(lib().ncsg_comm_create_nccl(unique_id, rank, nranks, device, C.byref(h)),
                "comm_create_nccl")
+        return cls(h)
+
+    @classmethod
+    def null(cls, rank: int, nranks: int) -> "Comm":
+        """A rank whose collectives do nothing (timing one rank's kernels)."""
+        h = C.c_void_p()
+        _check(lib().ncsg_comm_create_null(rank, nranks, C.byref(h)), "comm_create_null")
         return cls(h)
 
     @classmethod

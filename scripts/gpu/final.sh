@@ -11,3 +11,4 @@ python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/fin
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches.csv \
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/final_ncu_launches.log 2>&1
 timeout 1500 bash scripts/gpu/ncu_cfg.sh c3 c1 c2 c5 c4
+NCSG_OUT=gpurun_out/r2_shard_projection.json python scripts/shard_step_time.py c3 c4 c5 2>&1 | tail -3
