@@ -36,7 +36,11 @@ def main(names):
         rows = {}
         for world in (1, 2, 4, 8):
             xchg = multigpu.default_exchange(cfg.n, world) if world > 1 else "none"
-            if world == 1:
+            if cfg.batch > 1:  # replicas: batch / P independent problems per rank
+                xchg = "replicas" if world > 1 else "none"
+                share = cfg.batch // world
+                p = ncsg.ct_problem(cfg, b[:share], mask=mask, batch=share)
+            elif world == 1:
                 p = ncsg.ct_problem(cfg, b, mask=mask)
             else:
                 p = ncsg.ct_problem(cfg, b, mask=mask, orbit_shard=(0, world))
@@ -55,7 +59,8 @@ def main(names):
             torch.cuda.synchronize()
             ms = ev[0].elapsed_time(ev[1]) / k
             n2 = cfg.n * cfg.n
-            if world == 1:
+            units = cfg.batch // world if cfg.batch > 1 else 1  # problems per rank-step
+            if world == 1 or cfg.batch > 1:
                 comm_us = 0.0
             elif xchg == "allreduce":  # ring all-reduce: 2 (P-1)/P of 4 n^2 bytes
                 comm_us = COLL_LAT_US + 2 * (world - 1) / world * 4 * n2 / (NVLINK_GBS * 1e3)
@@ -65,10 +70,11 @@ def main(names):
                 ag = (world - 1) / world * 4 * n2
                 comm_us = 4 * COLL_LAT_US + (rs + a2a + ag) / (NVLINK_GBS * 1e3)
             step_ms = ms + comm_us * 1e-3
+            rate = 1000.0 / step_ms * (units * world if cfg.batch > 1 else 1)
             rows[world] = {"exchange": xchg, "rank_compute_ms": ms, "exchange_us_model": comm_us,
-                           "projected_ms_per_step": step_ms, "projected_it_s": 1000.0 / step_ms}
+                           "projected_ms_per_step": step_ms, "projected_it_s": rate}
             print(name, world, xchg, f"compute {ms:.4f} ms + exchange {comm_us:.1f} us "
-                  f"-> {1000.0 / step_ms:.0f} it/s (projected)", flush=True)
+                  f"-> {rate:.0f} it/s (projected)", flush=True)
             del p
         out["configs"][name] = rows
     dst = os.environ.get("NCSG_OUT", "profiles/r2_shard_projection.json")
