@@ -20,9 +20,11 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
+#include "fft_pow2.cuh"
 #include "ncs_device.cuh"
 #include "ncsg_internal.cuh"
 
@@ -580,11 +582,294 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
   rows_c2r_body<PEERS>(specT, xu, tw, sh, rs, blockIdx.x, blockIdx.y);
 }
 
+// ---- power-of-two fast path: the register-resident engine (fft_pow2.cuh) --
+// Same passes and fusions as above; each row pass CTA holds G row pairs (one
+// transform group of N/16 threads each, extra threads only load), the column
+// pass G columns.
+
+__device__ __forceinline__ void cp_async8(float2* dst, const float2* src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
+}
+
+template <int LOGN, bool PEERS>
+__global__ void __launch_bounds__(512) fft_rows_r2c_p2(AtuTerms T, float2* __restrict__ specT,
+                                                       const float2* __restrict__ twt, RowSlab rs,
+                                                       int G) {
+  pdl_wait();
+  using Ge = p2::Geo<LOGN>;
+  constexpr int N = Ge::N, NP = Ge::NP, TT = Ge::T;
+  extern __shared__ float2 zs[];
+  const int b = blockIdx.y;
+  const int rows = 2 * G;
+  const int y0 = rs.r0 + blockIdx.x * rows;
+  const int yend = rs.r0 + rs.rows;
+  if (T.counter && blockIdx.x == 0 && b == 0 && threadIdx.x == 0) atomicAdd(T.counter + 1, 1);
+  // row-major terms, four pixels per thread (N % 4 == 0), into pair r/2's
+  // buffer (real part: even row, imaginary part: odd row)
+  for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x) {
+    const int r = (4 * i) >> LOGN, x = 4 * i - (r << LOGN);
+    const int y = y0 + r;
+    const float4 v = y < yend ? atu_rowmajor4(T, b, y, x) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float2* slot = zs + (r >> 1) * NP + p2::pad(x);
+    if (r & 1) {
+      slot[0].y = v.x, slot[1].y = v.y, slot[2].y = v.z, slot[3].y = v.w;
+    } else {
+      slot[0].x = v.x, slot[1].x = v.y, slot[2].x = v.z, slot[3].x = v.w;
+    }
+  }
+  // transposed (class-H) partials, coalesced along y
+  if (!T.plain && T.bp_part && T.nH > 0) {
+    __syncthreads();
+    const size_t nn = static_cast<size_t>(N) * N;
+    const float* base = T.bp_part + b * T.part_stride + T.nV * nn;
+    for (int i = threadIdx.x; i < rows * N; i += blockDim.x) {
+      const int x = i / rows, r = i - x * rows;
+      const int y = y0 + r;
+      if (y >= yend) continue;
+      float v = 0.f;
+      const float* p = base + static_cast<size_t>(x) * N + y;
+      for (int c = 0; c < T.nH; ++c) v += p[c * nn];
+      float2* slot = zs + (r >> 1) * NP + p2::pad(x);
+      if (r & 1)
+        slot->y += v;
+      else
+        slot->x += v;
+    }
+  }
+  __syncthreads();
+  const int g = threadIdx.x / TT, t = threadIdx.x % TT;
+  const bool active = g < G;
+  float2* buf = zs + (active ? g : 0) * NP;
+  float2 v[16];
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = buf[p2::pad(t + TT * e)];
+  }
+  p2::fft<LOGN, -1>(v, buf, t, twt, active);
+  __syncthreads();
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) buf[p2::pad(t + TT * e)] = v[e];
+  }
+  __syncthreads();
+  // unpack the two real rows of each pair: A = (Z_k + conj Z_-k)/2,
+  // B = (Z_k - conj Z_-k)/(2i); both rows' bin k leave as one float4
+  const int nk = N / 2 + 1;
+  float2* out = specT + static_cast<size_t>(b) * rs.bstride;
+  for (int i = threadIdx.x; i < nk * G; i += blockDim.x) {
+    const int k = i / G, q = i - k * G;
+    const int y = y0 + 2 * q;
+    if (y >= yend) continue;
+    const float2* zq = zs + q * NP;
+    const float2 zk = zq[p2::pad(k)];
+    const float2 zm = zq[p2::pad((N - k) & (N - 1))];
+    const float2 va = make_float2(0.5f * (zk.x + zm.x), 0.5f * (zk.y - zm.y));
+    const float2 vb = make_float2(0.5f * (zk.y + zm.y), -0.5f * (zk.x - zm.x));
+    float2* dst;
+    if (PEERS) {  // fused all-to-all: straight into rank k / wc's blocks
+      const int qq = k / rs.wc;
+      dst = static_cast<float2*>(rs.peers.p[qq]) +
+            static_cast<size_t>(rs.rank * rs.wc + (k - qq * rs.wc)) * rs.ld + (y - rs.r0);
+    } else {
+      dst = out + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    }
+    if (y + 1 < yend && ((rs.ld | rs.r0) & 1) == 0) {
+      *reinterpret_cast<float4*>(dst) = make_float4(va.x, va.y, vb.x, vb.y);
+    } else {
+      dst[0] = va;
+      if (y + 1 < yend) dst[1] = vb;
+    }
+  }
+}
+
+template <int LOGN>
+__global__ void __launch_bounds__(512) fft_cols_filter_p2(float2* __restrict__ specT,
+                                                          const float2* __restrict__ maskT,
+                                                          const float2* __restrict__ twt, int G) {
+  pdl_wait();
+  using Ge = p2::Geo<LOGN>;
+  constexpr int N = Ge::N, NP = Ge::NP, TT = Ge::T;
+  extern __shared__ float2 zs[];
+  const int b = blockIdx.y;
+  const int nk = N / 2 + 1;
+  const int g = threadIdx.x / TT, t = threadIdx.x % TT;
+  const int k = blockIdx.x * G + g;
+  const bool active = g < G && k < nk;
+  float2* buf = zs + (g < G ? g : 0) * NP;
+  float2* fm = zs + G * NP + (g < G ? g : 0) * N;  // this group's filter column
+  float2* col = specT + (static_cast<size_t>(b) * nk + (active ? k : 0)) * N;
+  float2 v[16];
+  if (active) {
+    // the filter streams into shared memory while the column transforms;
+    // each thread later reads only the entries it copied (no barrier)
+    const float2* mk = maskT + static_cast<size_t>(k) * N;
+#pragma unroll
+    for (int e = 0; e < 16; ++e) cp_async8(fm + t + TT * e, mk + t + TT * e);
+    asm volatile("cp.async.commit_group;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = col[t + TT * e];
+  }
+  p2::fft<LOGN, -1>(v, buf, t, twt, active);
+  if (active) {
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = p2::cmul(v[e], fm[t + TT * e]);
+  }
+  p2::fft<LOGN, +1>(v, buf, t, twt, active);
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) col[t + TT * e] = v[e];
+  }
+}
+
+template <int LOGN, bool PEERS>
+__global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict__ specT, XUpdate xu,
+                                                       const float2* __restrict__ twt, RowSlab rs,
+                                                       int G) {
+  pdl_wait();
+  using Ge = p2::Geo<LOGN>;
+  constexpr int N = Ge::N, NP = Ge::NP, TT = Ge::T;
+  extern __shared__ float2 zs[];
+  const int b = blockIdx.y;
+  const int rows = 2 * G;
+  const int y0 = rs.r0 + blockIdx.x * rows;
+  const int yend = rs.r0 + rs.rows;
+  const int nk = N / 2 + 1;
+  const size_t nn = static_cast<size_t>(N) * N;
+  const float2* in = specT + static_cast<size_t>(b) * rs.bstride;
+  float* xs = reinterpret_cast<float*>(zs + G * NP);  // rows x N: x before the update
+  const bool pre = xu.subtract != 0;
+  if (pre) {  // x streams in while the spectrum loads and transforms
+    for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x) {
+      const int r = (4 * i) >> LOGN, x = 4 * i - (r << LOGN);
+      if (y0 + r >= yend) continue;
+      const float* src = xu.x + b * nn + static_cast<size_t>(y0 + r) * N + x;
+      const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(xs + 4 * i));
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // Z = G_a + i G_b with the Hermitian extension (G_r[N-k] = conj G_r[k]):
+  // one thread per (row pair, k) reads both rows' bins as one float4
+  for (int i = threadIdx.x; i < nk * G; i += blockDim.x) {
+    const int k = i / G, q = i - k * G;
+    const int y = y0 + 2 * q;
+    float4 gg = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float2* src = in + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
+    if (y + 1 < yend && ((rs.ld | rs.r0) & 1) == 0) {
+      gg = *reinterpret_cast<const float4*>(src);
+    } else if (y < yend) {
+      const float2 ga = src[0];
+      gg.x = ga.x, gg.y = ga.y;
+      if (y + 1 < yend) {
+        const float2 gb = src[1];
+        gg.z = gb.x, gg.w = gb.y;
+      }
+    }
+    float2* zq = zs + q * NP;
+    zq[p2::pad(k)] = make_float2(gg.x - gg.w, gg.y + gg.z);
+    if (k > 0 && 2 * k != N) zq[p2::pad(N - k)] = make_float2(gg.x + gg.w, gg.z - gg.y);
+  }
+  __syncthreads();
+  const int g = threadIdx.x / TT, t = threadIdx.x % TT;
+  const bool active = g < G;
+  float2* buf = zs + (active ? g : 0) * NP;
+  float2 v[16];
+  if (active) {
+#pragma unroll
+    for (int e = 0; e < 16; ++e) v[e] = buf[p2::pad(t + TT * e)];
+  }
+  p2::fft<LOGN, +1>(v, buf, t, twt, active);
+  if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  int bad = 0;
+  if (active) {
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int r = 2 * g + rr;
+      const int y = y0 + r;
+      if (y >= yend) continue;
+      float* xrow = xu.x + b * nn + static_cast<size_t>(y) * N;
+      float* orow = xu.x_old ? xu.x_old + b * nn + static_cast<size_t>(y) * N : nullptr;
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int x = t + TT * e;
+        const float w = rr ? v[e].y : v[e].x;
+        float xn;
+        if (pre) {
+          const float xo = xs[r * N + x];
+          if (orow) orow[x] = xo;
+          xn = xo - w;
+        } else {
+          xn = w;
+        }
+        xrow[x] = xn;
+        for (int qq = 0; PEERS && qq < xu.n_peers; ++qq)
+          static_cast<float*>(xu.x_peers.p[qq])[b * nn + static_cast<size_t>(y) * N + x] = xn;
+        bad |= !isfinite(xn);
+        if (rr)
+          v[e].y = xn;
+        else
+          v[e].x = xn;
+      }
+    }
+  }
+  if (xu.flag && __syncthreads_or(bad) && threadIdx.x == 0)
+    atomicMin(xu.flag, *(volatile int*)(xu.flag + 1));
+  if (xu.xT) {
+    __syncthreads();
+    if (active) {
+#pragma unroll
+      for (int e = 0; e < 16; ++e) buf[p2::pad(t + TT * e)] = v[e];
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < rows * N; i += blockDim.x) {
+      const int x = i / rows, r = i - x * rows;
+      const int y = y0 + r;
+      if (y >= yend) continue;
+      const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
+      xu.xT[b * nn + static_cast<size_t>(x) * N + y] = (r & 1) ? zz.y : zz.x;
+    }
+  }
+}
+
 int log2i(int n) {
   int l = 0;
   while ((1 << l) < n) ++l;
   return l;
 }
+
+bool p2_enabled(int logn) {
+  static const bool off = std::getenv("NCSG_FFT_P2") && std::atoi(std::getenv("NCSG_FFT_P2")) == 0;
+  return !off && logn >= p2::kMinLog && logn <= p2::kMaxLog;
+}
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+// Row pairs per row-pass CTA / columns per column-pass CTA.
+int p2_row_groups() {
+  static const int g = std::max(1, std::min(8, env_int("NCSG_FFT_RG", 2)));
+  return g;
+}
+int p2_col_groups(int T) {
+  static const int cg = env_int("NCSG_FFT_CG", 0);
+  if (cg > 0) return std::max(1, std::min(16, cg));
+  return std::max(1, 128 / T);
+}
+
+#define NCSG_P2_SWITCH(LOGN_EXPR, MACRO) \
+  switch (LOGN_EXPR) {                   \
+    case 6: MACRO(6); break;             \
+    case 7: MACRO(7); break;             \
+    case 8: MACRO(8); break;             \
+    case 9: MACRO(9); break;             \
+    case 10: MACRO(10); break;           \
+    case 11: MACRO(11); break;           \
+    case 12: MACRO(12); break;           \
+    default: break;                      \
+  }
 
 int fft_threads(int work) { return std::max(64, std::min(512, work)); }
 
@@ -622,6 +907,30 @@ void FftPlan::init(int n_, cudaStream_t s) {
   tw.alloc(h.size());
   NCSG_CUDA_CHECK(cudaMemcpyAsync(tw.p, h.data(), h.size() * sizeof(float2),
                                   cudaMemcpyHostToDevice, s));
+  // stage twiddles of the register-resident engine: stage s (span Ns = 16^s,
+  // radix R) at tw_off(s) + (r - 1) Ns + k = exp(-2 pi i r k / (Ns R))
+  std::vector<float2> h2;
+  if (shape.logn >= 0 && p2_enabled(shape.logn)) {
+    const int logn = shape.logn;
+    const int nst = (logn + 3) / 4, llr = logn - 4 * (nst - 1);
+    h2.assign(p2::tw_len(logn), make_float2(0.f, 0.f));
+    long long ns = 16;
+    for (int st = 1; st < nst; ++st, ns *= 16) {
+      const int R = st == nst - 1 ? (1 << llr) : 16;
+      for (int r = 1; r < R; ++r)
+        for (long long k = 0; k < ns; ++k) {
+          const double ang = -2.0 * 3.14159265358979323846 * static_cast<double>(r * k) /
+                             static_cast<double>(ns * R);
+          h2[p2::tw_off(st) + (r - 1) * ns + k] =
+              make_float2(static_cast<float>(std::cos(ang)), static_cast<float>(std::sin(ang)));
+        }
+    }
+    tw2.alloc(h2.size());
+    NCSG_CUDA_CHECK(cudaMemcpyAsync(tw2.p, h2.data(), h2.size() * sizeof(float2),
+                                    cudaMemcpyHostToDevice, s));
+  } else {
+    tw2.release();
+  }
   NCSG_CUDA_CHECK(cudaStreamSynchronize(s));
 }
 
@@ -629,8 +938,25 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
                          cudaStream_t s, RowSlab rs) {
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
-  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
   const bool peers = rs.peers.p[0] != nullptr;
+  if (f.tw2.p) {
+    const int G = p2_row_groups(), T = n / 16;
+    const size_t sm = sizeof(float2) * G * p2::pad(n);
+    const int threads = std::max(G * T, std::min(512, G * n / 2));
+    dim3 grid((rs.rows + 2 * G - 1) / (2 * G), batch);
+#define NCSG_R2C(L)                                                                        \
+  {                                                                                        \
+    auto kern = peers ? fft_rows_r2c_p2<L, true> : fft_rows_r2c_p2<L, false>;              \
+    ensure_smem(reinterpret_cast<const void*>(kern), sm);                                  \
+    launch_pdl(kern, grid, dim3(threads), sm, s, terms, specT, f.tw2.p, rs, G);            \
+  }
+    NCSG_P2_SWITCH(f.shape.logn, NCSG_R2C)
+#undef NCSG_R2C
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
+  size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n;
   auto kern = peers ? fft_rows_r2c_kernel<true> : fft_rows_r2c_kernel<false>;
   ensure_smem(reinterpret_cast<const void*>(kern), smem);
   dim3 grid((rs.rows + kRowsPerBlock - 1) / kRowsPerBlock, batch);
@@ -644,6 +970,21 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
 void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT, int batch,
                             cudaStream_t s) {
   const int n = f.n;
+  if (f.tw2.p) {
+    const int T = n / 16, G = p2_col_groups(T);
+    const size_t sm = sizeof(float2) * G * (p2::pad(n) + n);
+    dim3 grid((n / 2 + 1 + G - 1) / G, batch);
+#define NCSG_COLS(L)                                                                   \
+  {                                                                                    \
+    ensure_smem(reinterpret_cast<const void*>(fft_cols_filter_p2<L>), sm);             \
+    launch_pdl(fft_cols_filter_p2<L>, grid, dim3(G * T), sm, s, specT, maskT, f.tw2.p, G); \
+  }
+    NCSG_P2_SWITCH(f.shape.logn, NCSG_COLS)
+#undef NCSG_COLS
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   size_t smem = 2 * sizeof(float2) * kColsPerBlock * n;
   ensure_smem(reinterpret_cast<const void*>(fft_cols_filter_kernel), smem);
   dim3 grid((n / 2 + 1 + kColsPerBlock - 1) / kColsPerBlock, batch);
@@ -682,6 +1023,24 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
                          cudaStream_t s, RowSlab rs) {
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
+  if (f.tw2.p) {
+    const int G = p2_row_groups(), T = n / 16;
+    const size_t sm = sizeof(float2) * G * p2::pad(n) + sizeof(float) * 2 * G * n;
+    const int threads = std::max(G * T, 128);
+    dim3 grid((rs.rows + 2 * G - 1) / (2 * G), batch);
+    const bool peers = xu.n_peers > 0;
+#define NCSG_C2R(L)                                                                 \
+  {                                                                                 \
+    auto kern = peers ? fft_rows_c2r_p2<L, true> : fft_rows_c2r_p2<L, false>;       \
+    ensure_smem(reinterpret_cast<const void*>(kern), sm);                           \
+    launch_pdl(kern, grid, dim3(threads), sm, s, specT, xu, f.tw2.p, rs, G);        \
+  }
+    NCSG_P2_SWITCH(f.shape.logn, NCSG_C2R)
+#undef NCSG_C2R
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    count_launch();
+    return;
+  }
   size_t smem = 2 * sizeof(float2) * (kRowsPerBlock / 2) * n + sizeof(float) * kRowsPerBlock * n;
   auto kern = xu.n_peers > 0 ? fft_rows_c2r_kernel<true> : fft_rows_c2r_kernel<false>;
   ensure_smem(reinterpret_cast<const void*>(kern), smem);

@@ -331,7 +331,8 @@ struct FftShape {
 struct FftPlan {
   int n = 0;
   FftShape shape;
-  DevBuf<float2> tw;  // exp(-2 pi i k / n), k < n
+  DevBuf<float2> tw;   // exp(-2 pi i k / n), k < n
+  DevBuf<float2> tw2;  // stage twiddles of the power-of-two engine (fft_pow2.cuh), or empty
   void init(int n_, cudaStream_t s);
 };
 // Spectrum layout: specT[batch][n/2+1][n] complex (column-major half spectrum).
