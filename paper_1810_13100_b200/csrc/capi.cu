@@ -162,6 +162,7 @@ struct ncsg_problem {
   int64_t flag_base = 0;          // iteration at the last reset_flag
   size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
   bool sharded = false;            // angle- or orbit-sharded (multi-GPU phases)
+  bool dual_fused = false;         // this step's inverse row pass did the x-only dual blocks
   // Orbit-interleaved copy of the sinogram dual (gather-mode adjoint input),
   // written by the dual update; fresh while u has not been written otherwise.
   DevBuf<float> u4;
@@ -324,6 +325,29 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
               : nullptr;
   xu.subtract = 1;
   xu.flag = p->flag.p;
+  // DENOISE: every dual block needs only x, so the whole dual update runs in
+  // the inverse row pass that produces x (unsharded power-of-two problems)
+  // and the step is three kernels.  (CT keeps the stand-alone dual kernel:
+  // fusing only its D block measured no gain at C1/C3/C5.)
+  p->dual_fused = false;
+  if (p->d.kind == NCSG_DENOISE && !p->sharded && !p->comm && !plain) {
+    DualFuse& df = xu.df;
+    df.alpha = static_cast<float>(p->d.alpha);
+    df.s_quad = static_cast<float>(1.0 / (1.0 + p->d.alpha));
+    df.wd = p->wd;
+    df.bound = p->bound;
+    df.u_stride = p->range;
+    df.flag = p->flag.p;
+    float* u = p->u.p;
+    if (p->d.kind == NCSG_DENOISE) {
+      df.ud = u;
+      df.bd = p->b.p;
+    }
+    df.ug = u + p->m0;
+    if (p->d.positivity) df.up = u + p->m0 + p->g;
+    df.on = fft_fuses_dual(p->fft, df) ? 1 : 0;
+    p->dual_fused = df.on != 0;
+  }
   mark(p);
   launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
 }
@@ -377,7 +401,11 @@ void forward_and_dual(ncsg_problem* p) {
       a.n_orb = static_cast<int>(p->radon->geo.orbits.size());
     }
   }
-  launch_dual_update(a, p->batch, s);
+  // x-only blocks already updated by the inverse row pass: the data block
+  // alone (CT / PET), nothing for DENOISE
+  a.data_only = p->dual_fused ? 1 : 0;
+  if (!(p->dual_fused && p->d.kind == NCSG_DENOISE)) launch_dual_update(a, p->batch, s);
+  p->dual_fused = false;
   p->u4_fresh = p->u4.n > 0;
   mark(p);
 }

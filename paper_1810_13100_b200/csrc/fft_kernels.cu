@@ -587,6 +587,30 @@ __global__ void fft_rows_c2r_kernel(const float2* __restrict__ specT, XUpdate xu
 // transform group of N/16 threads each, extra threads only load), the column
 // pass G columns.
 
+__device__ __forceinline__ void mbar_init1(unsigned bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait0(unsigned bar) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(bar)
+      : "memory");
+}
+// 1-D bulk copy global -> shared (16-byte aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, unsigned bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+      "l"(src), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
 __device__ __forceinline__ void cp_async8(float2* dst, const float2* src) {
   const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(d), "l"(src) : "memory");
@@ -731,10 +755,14 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
   using Ge = p2::Geo<LOGN>;
   constexpr int N = Ge::N, NP = Ge::NP, TT = Ge::T;
   extern __shared__ float2 zs[];
+  const DualFuse& df = xu.df;
   const int b = blockIdx.y;
-  const int rows = 2 * G;
-  const int y0 = rs.r0 + blockIdx.x * rows;
+  const int rows = 2 * G;                      // rows transformed
+  const int keep = df.on ? rows - 1 : rows;    // rows owned (x written)
+  const int y0 = rs.r0 + blockIdx.x * keep;
   const int yend = rs.r0 + rs.rows;
+  const int yown = min(yend, y0 + keep);       // owned rows [y0, yown)
+  const int ylim = df.on ? min(N, y0 + rows) : yend;  // transformed rows [y0, ylim)
   const int nk = N / 2 + 1;
   const size_t nn = static_cast<size_t>(N) * N;
   const float2* in = specT + static_cast<size_t>(b) * rs.bstride;
@@ -743,12 +771,51 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
   if (pre) {  // x streams in while the spectrum loads and transforms
     for (int i = threadIdx.x; i < rows * N / 4; i += blockDim.x) {
       const int r = (4 * i) >> LOGN, x = 4 * i - (r << LOGN);
-      if (y0 + r >= yend) continue;
+      if (y0 + r >= ylim) continue;
       const float* src = xu.x + b * nn + static_cast<size_t>(y0 + r) * N + x;
       const unsigned dst = static_cast<unsigned>(__cvta_generic_to_shared(xs + 4 * i));
       asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  // fused dual: the owned rows of every x-only dual block (and the data
+  // term) stream into shared memory by bulk copies while the row transforms
+  // run -- each block's owned rows are one contiguous range, 16-byte aligned
+  // (N % 4 == 0) except the h block's, whose range is widened to alignment
+  __shared__ __align__(8) unsigned long long dbar;
+  const unsigned dbar_a = static_cast<unsigned>(__cvta_generic_to_shared(&dbar));
+  float* dsm = xs + rows * N;  // [ud | bd | up] keep x N each, then h, then v
+  const int nown = max(0, yown - y0);
+  const int nv = max(0, min(nown, N - 1 - y0));
+  const size_t h0 = static_cast<size_t>(y0) * (N - 1), h0a = h0 & ~static_cast<size_t>(3);
+  float* s_ud = dsm;
+  float* s_bd = s_ud + (df.ud ? keep * N : 0);
+  float* s_up = s_bd + (df.ud ? keep * N : 0);
+  float* s_h = s_up + (df.up ? keep * N : 0);
+  float* s_v = s_h + (df.ug ? keep * N + 4 : 0);
+  if (df.on && threadIdx.x == 0) {
+    mbar_init1(dbar_a);
+    unsigned bytes = 0;
+    const size_t rowoff = static_cast<size_t>(y0) * N;
+    if (df.ud && nown) bytes += 2u * nown * N * 4;
+    if (df.up && nown) bytes += nown * N * 4;
+    size_t hb = 0;
+    if (df.ug && nown) {
+      const size_t h1 = static_cast<size_t>(y0 + nown) * (N - 1);
+      hb = ((h1 + 3) & ~static_cast<size_t>(3)) - h0a;
+      bytes += static_cast<unsigned>(hb * 4) + nv * N * 4;
+    }
+    mbar_arrive_tx(dbar_a, bytes);
+    if (df.ud && nown) {
+      bulk_g2s(s_ud, df.ud + b * df.u_stride + rowoff, nown * N * 4, dbar_a);
+      bulk_g2s(s_bd, df.bd + b * nn + rowoff, nown * N * 4, dbar_a);
+    }
+    if (df.up && nown) bulk_g2s(s_up, df.up + b * df.u_stride + rowoff, nown * N * 4, dbar_a);
+    if (df.ug && nown) {
+      const float* ug = df.ug + b * df.u_stride;
+      bulk_g2s(s_h, ug + h0a, static_cast<unsigned>(hb * 4), dbar_a);
+      if (nv) bulk_g2s(s_v, ug + static_cast<size_t>(N) * (N - 1) + rowoff, nv * N * 4, dbar_a);
+    }
   }
   // Z = G_a + i G_b with the Hermitian extension (G_r[N-k] = conj G_r[k]):
   // one thread per (row pair, k) reads both rows' bins as one float4
@@ -757,12 +824,12 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
     const int y = y0 + 2 * q;
     float4 gg = make_float4(0.f, 0.f, 0.f, 0.f);
     const float2* src = in + static_cast<size_t>(k) * rs.ld + (y - rs.r0);
-    if (y + 1 < yend && ((rs.ld | rs.r0) & 1) == 0) {
+    if (y + 1 < ylim && (((y - rs.r0) | rs.ld) & 1) == 0) {  // 16-byte aligned pair
       gg = *reinterpret_cast<const float4*>(src);
-    } else if (y < yend) {
+    } else if (y < ylim) {
       const float2 ga = src[0];
       gg.x = ga.x, gg.y = ga.y;
-      if (y + 1 < yend) {
+      if (y + 1 < ylim) {
         const float2 gb = src[1];
         gg.z = gb.x, gg.w = gb.y;
       }
@@ -789,7 +856,8 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
     for (int rr = 0; rr < 2; ++rr) {
       const int r = 2 * g + rr;
       const int y = y0 + r;
-      if (y >= yend) continue;
+      if (y >= ylim) continue;
+      const bool own = y < yown;
       float* xrow = xu.x + b * nn + static_cast<size_t>(y) * N;
       float* orow = xu.x_old ? xu.x_old + b * nn + static_cast<size_t>(y) * N : nullptr;
 #pragma unroll
@@ -799,15 +867,17 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
         float xn;
         if (pre) {
           const float xo = xs[r * N + x];
-          if (orow) orow[x] = xo;
+          if (orow && own) orow[x] = xo;
           xn = xo - w;
         } else {
           xn = w;
         }
-        xrow[x] = xn;
-        for (int qq = 0; PEERS && qq < xu.n_peers; ++qq)
-          static_cast<float*>(xu.x_peers.p[qq])[b * nn + static_cast<size_t>(y) * N + x] = xn;
-        bad |= !isfinite(xn);
+        if (own) {
+          xrow[x] = xn;
+          for (int qq = 0; PEERS && qq < xu.n_peers; ++qq)
+            static_cast<float*>(xu.x_peers.p[qq])[b * nn + static_cast<size_t>(y) * N + x] = xn;
+          bad |= !isfinite(xn);
+        }
         if (rr)
           v[e].y = xn;
         else
@@ -817,20 +887,79 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
   }
   if (xu.flag && __syncthreads_or(bad) && threadIdx.x == 0)
     atomicMin(xu.flag, *(volatile int*)(xu.flag + 1));
-  if (xu.xT) {
+  if (xu.xT || df.on) {  // the new rows in natural order: zs[pair][pad(x)]
     __syncthreads();
     if (active) {
 #pragma unroll
       for (int e = 0; e < 16; ++e) buf[p2::pad(t + TT * e)] = v[e];
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < rows * N; i += blockDim.x) {
-      const int x = i / rows, r = i - x * rows;
+  }
+  if (xu.xT) {
+    for (int i = threadIdx.x; i < keep * N; i += blockDim.x) {
+      const int x = i / keep, r = i - x * keep;
       const int y = y0 + r;
-      if (y >= yend) continue;
+      if (y >= yown) continue;
       const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
       xu.xT[b * nn + static_cast<size_t>(x) * N + y] = (r & 1) ? zz.y : zz.x;
     }
+  }
+  if (df.on) {
+    // dual update of the owned rows (dual_update_kernel's identity, D and
+    // positivity sections, same arithmetic): x_new from zs, x_old from xs,
+    // the duals and data from the bulk-copied rows
+    mbar_wait0(dbar_a);
+    auto xn_at = [&](int r, int x) -> float {
+      const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
+      return (r & 1) ? zz.y : zz.x;
+    };
+    const float alpha = df.alpha;
+    int badu = 0;
+    if (df.ud) {
+      float* ud = df.ud + b * df.u_stride + static_cast<size_t>(y0) * N;
+      for (int i = threadIdx.x; i < nown * N; i += blockDim.x) {
+        const int r = i >> LOGN, x = i & (N - 1);
+        const float un = (s_ud[i] + alpha * (2.f * xn_at(r, x) - xs[i] - s_bd[i])) * df.s_quad;
+        ud[i] = un;
+        badu |= isnan(un);
+      }
+    }
+    if (df.ug) {
+      float* ug = df.ug + b * df.u_stride;
+      const float wd = df.wd, bd = df.bound;
+      const int hoff = static_cast<int>(h0 - h0a);
+      // h block: rows of N - 1 edges
+      for (int i = threadIdx.x; i < nown * (N - 1); i += blockDim.x) {
+        const int r = i / (N - 1), x = i - r * (N - 1);
+        const float an = wd * (xn_at(r, x) - xn_at(r, x + 1));
+        const float ao = wd * (xs[r * N + x] - xs[r * N + x + 1]);
+        const float z = s_h[hoff + i] + alpha * (2.f * an - ao - 0.f);
+        ug[h0 + i] = z < -bd ? -bd : (z > bd ? bd : z);
+        badu |= isnan(z);
+      }
+      // v block: rows y < N - 1 (row y + 1 is transformed here too)
+      float* vb = ug + static_cast<size_t>(N) * (N - 1) + static_cast<size_t>(y0) * N;
+      for (int i = threadIdx.x; i < nv * N; i += blockDim.x) {
+        const int r = i >> LOGN, x = i & (N - 1);
+        const float an = wd * (xn_at(r, x) - xn_at(r + 1, x));
+        const float ao = wd * (xs[i] - xs[i + N]);
+        const float z = s_v[i] + alpha * (2.f * an - ao - 0.f);
+        vb[i] = z < -bd ? -bd : (z > bd ? bd : z);
+        badu |= isnan(z);
+      }
+    }
+    if (df.up) {
+      float* up = df.up + b * df.u_stride + static_cast<size_t>(y0) * N;
+      for (int i = threadIdx.x; i < nown * N; i += blockDim.x) {
+        const int r = i >> LOGN, x = i & (N - 1);
+        const float z = s_up[i] + alpha * (2.f * xn_at(r, x) - xs[i]);
+        up[i] = z < 0.f ? z : 0.f;
+        badu |= isnan(z);
+      }
+    }
+    // dual NaN (check_finite's second test, solvers.cpp:252-254): flag word 2
+    if (df.flag && __syncthreads_or(badu) && threadIdx.x == 0)
+      atomicMin(df.flag + 2, *(volatile int*)(df.flag + 1));
   }
 }
 
@@ -852,6 +981,24 @@ int env_int(const char* name, int dflt) {
 int p2_row_groups() {
   static const int g = std::max(1, std::min(8, env_int("NCSG_FFT_RG", 2)));
   return g;
+}
+// Shared memory of the dual-fused inverse row pass with G row pairs and
+// `arrays` bulk-copied dual / data rows.
+size_t p2_fuse_smem(int n, int G, int arrays) {
+  return sizeof(float2) * G * p2::pad(n) + sizeof(float) * 2 * G * n +
+         sizeof(float) * arrays * (2 * G - 1) * n + 16;
+}
+constexpr size_t kFuseSmemCap = 200 * 1024;
+// Row pairs per CTA of the dual-fused inverse row pass (2G - 1 rows kept):
+// the largest of 4, 3, 2 whose staging fits (0: none does).
+int p2_fuse_groups(int n, int arrays) {
+  static const int g = env_int("NCSG_FFT_FG", 0);
+  int G = g > 0 ? std::max(2, std::min(8, g)) : (n >= 512 ? 4 : 2);
+  while (G >= 2 && p2_fuse_smem(n, G, arrays) > kFuseSmemCap) --G;
+  return G >= 2 ? G : 0;
+}
+int fuse_arrays(const DualFuse& df) {
+  return (df.ud ? 2 : 0) + (df.up ? 1 : 0) + (df.ug ? 2 : 0);
 }
 int p2_col_groups(int T) {
   static const int cg = env_int("NCSG_FFT_CG", 0);
@@ -1019,15 +1166,23 @@ void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* m
   count_launch();
 }
 
+bool fft_fuses_dual(const FftPlan& f, const DualFuse& df) {
+  static const bool off = std::getenv("NCSG_FUSE_DUAL") && std::atoi(std::getenv("NCSG_FUSE_DUAL")) == 0;
+  return !off && f.tw2.p != nullptr && p2_fuse_groups(f.n, fuse_arrays(df)) > 0;
+}
+
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s, RowSlab rs) {
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
   if (f.tw2.p) {
-    const int G = p2_row_groups(), T = n / 16;
-    const size_t sm = sizeof(float2) * G * p2::pad(n) + sizeof(float) * 2 * G * n;
+    const int G = xu.df.on ? p2_fuse_groups(n, fuse_arrays(xu.df)) : p2_row_groups(), T = n / 16;
+    if (G == 0) throw Error{NCSG_INVALID, "fused dual update does not fit in shared memory"};
+    const size_t sm = xu.df.on ? p2_fuse_smem(n, G, fuse_arrays(xu.df))
+                               : sizeof(float2) * G * p2::pad(n) + sizeof(float) * 2 * G * n;
     const int threads = std::max(G * T, 128);
-    dim3 grid((rs.rows + 2 * G - 1) / (2 * G), batch);
+    const int keep = xu.df.on ? 2 * G - 1 : 2 * G;
+    dim3 grid((rs.rows + keep - 1) / keep, batch);
     const bool peers = xu.n_peers > 0;
 #define NCSG_C2R(L)                                                                 \
   {                                                                                 \

@@ -6,6 +6,13 @@
 
 namespace ncsg {
 
+// Loads of the partial-image sums kept in flight per thread (the row pass
+// loader sums up to 48 adjoint partials per pixel at C3).
+#ifndef NCSG_PART_UNROLL
+#define NCSG_PART_UNROLL 4
+#endif
+constexpr int kPartUnroll = NCSG_PART_UNROLL;
+
 // A^T u (or a plain image) at (y, x) from the row-major terms.  The
 // transposed class-H partials are added separately (coalesced by columns).
 __device__ __forceinline__ float atu_rowmajor(const AtuTerms& T, int b, int y, int x) {
@@ -17,6 +24,7 @@ __device__ __forceinline__ float atu_rowmajor(const AtuTerms& T, int b, int y, i
   if (T.bp_part) {
     const float* p = T.bp_part + b * T.part_stride + i;
     const size_t ps = T.img_stride ? T.img_stride : nn;
+#pragma unroll kPartUnroll
     for (int c = 0; c < T.nV; ++c) v += p[c * ps];
   }
   if (T.ident) v += T.ident[b * T.ident_stride + i];
@@ -48,6 +56,7 @@ __device__ __forceinline__ float4 atu_rowmajor4(const AtuTerms& T, int b, int y,
   if (T.bp_part) {
     const float* p = T.bp_part + b * T.part_stride + i;
     const size_t ps = T.img_stride ? T.img_stride : nn;
+#pragma unroll kPartUnroll
     for (int c = 0; c < T.nV; ++c) {
       const float4 q = *reinterpret_cast<const float4*>(p + c * ps);
       v.x += q.x, v.y += q.y, v.z += q.z, v.w += q.w;

@@ -443,7 +443,9 @@ __global__ void stacked_rest_kernel(StackArgs a) {
 #endif
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s) {
   size_t big = std::max<size_t>(a.m_end - a.m_begin, 2 * static_cast<size_t>(a.n) * a.n);
-  dim3 grid(grid_for(big, 256, 148 * NCSG_DUAL_WAVES), a.positivity ? 3 : 2, batch);
+  if (a.data_only) big = a.m_end - a.m_begin;
+  dim3 grid(grid_for(big, 256, 148 * NCSG_DUAL_WAVES), a.data_only ? 1 : (a.positivity ? 3 : 2),
+            batch);
   launch_pdl(dual_update_kernel, grid, dim3(256), 0, s, a);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();

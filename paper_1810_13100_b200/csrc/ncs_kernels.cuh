@@ -35,6 +35,7 @@ struct DualArgs {
   // rays of the listed (own) orbits.
   const int4* orb_t = nullptr;
   int n_orb = 0;
+  int data_only = 0;  // section 0 only (the x-only blocks were fused into the row pass)
 };
 void launch_dual_update(const DualArgs& a, int batch, cudaStream_t s);
 // Rebuilds u4 from u0 (fields u0, u_stride, m, det, u4, slot, u4_row, u4_pad, u4_stride).

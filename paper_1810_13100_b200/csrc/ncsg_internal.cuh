@@ -387,6 +387,21 @@ void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* m
 void launch_fft_cols_forward(const FftPlan& f, float2* specT, int batch, cudaStream_t s);
 // Inverse rows (C2R) fused with the x update: out = x_in - w (or w when
 // x_in == nullptr); optional x_old copy, transposed copy, finiteness flag.
+// The dual update of the blocks whose forward map needs only x -- identity
+// (DENOISE data, QuadraticConj), D (ScaledL1Conj) and positivity (NonnegConj)
+// -- fused into the inverse row pass that produces x (Engine::step's dual
+// half, solvers.cpp:146-156, for those blocks).  Each CTA then keeps 2G - 1
+// rows and also transforms the next row, which the v-block of D needs.
+struct DualFuse {
+  int on = 0;
+  float alpha = 0.f, s_quad = 0.f, wd = 0.f, bound = 0.f;
+  float* ud = nullptr;       // identity-block dual (DENOISE data), nullable
+  const float* bd = nullptr; // its data term b
+  float* ug = nullptr;       // gradient dual (h block then v block), nullable
+  float* up = nullptr;       // positivity dual, nullable
+  size_t u_stride = 0;       // per-problem stride of the duals
+  int* flag = nullptr;       // [2] = min(step counter [1]) over NaN duals
+};
 struct XUpdate {
   float* x = nullptr;       // updated in place (x -= w) ; if subtract == 0: x = w
   float* x_old = nullptr;   // receives the pre-update x (nullable)
@@ -397,7 +412,11 @@ struct XUpdate {
   // (the own x among them counts once: x itself)
   PeerPtrs x_peers;
   int n_peers = 0;
+  DualFuse df;              // power-of-two path, unsharded rows only
 };
+// Whether launch_fft_rows_c2r can take XUpdate::df = df (the power-of-two
+// path, staging within shared memory; NCSG_FUSE_DUAL=0 turns the fusion off).
+bool fft_fuses_dual(const FftPlan& f, const DualFuse& df);
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s, RowSlab rs = RowSlab{});
 
