@@ -665,16 +665,16 @@ __global__ void __launch_bounds__(512) fft_rows_r2c_p2(AtuTerms T, float2* __res
   const int g = threadIdx.x / TT, t = threadIdx.x % TT;
   const bool active = g < G;
   float2* buf = zs + (active ? g : 0) * NP;
-  float2 v[16];
+  float2 v[Ge::E];
   if (active) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[p2::pad(t + TT * e)];
+    for (int e = 0; e < Ge::E; ++e) v[e] = buf[p2::pad(t + TT * e)];
   }
   p2::fft<LOGN, -1>(v, buf, t, twt, active);
   __syncthreads();
   if (active) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) buf[p2::pad(t + TT * e)] = v[e];
+    for (int e = 0; e < Ge::E; ++e) buf[p2::pad(t + TT * e)] = v[e];
   }
   __syncthreads();
   // unpack the two real rows of each pair: A = (Z_k + conj Z_-k)/2,
@@ -723,27 +723,27 @@ __global__ void __launch_bounds__(512) fft_cols_filter_p2(float2* __restrict__ s
   float2* buf = zs + (g < G ? g : 0) * NP;
   float2* fm = zs + G * NP + (g < G ? g : 0) * N;  // this group's filter column
   float2* col = specT + (static_cast<size_t>(b) * nk + (active ? k : 0)) * N;
-  float2 v[16];
+  float2 v[Ge::E];
   if (active) {
     // the filter streams into shared memory while the column transforms;
     // each thread later reads only the entries it copied (no barrier)
     const float2* mk = maskT + static_cast<size_t>(k) * N;
 #pragma unroll
-    for (int e = 0; e < 16; ++e) cp_async8(fm + t + TT * e, mk + t + TT * e);
+    for (int e = 0; e < Ge::E; ++e) cp_async8(fm + t + TT * e, mk + t + TT * e);
     asm volatile("cp.async.commit_group;" ::: "memory");
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = col[t + TT * e];
+    for (int e = 0; e < Ge::E; ++e) v[e] = col[t + TT * e];
   }
   p2::fft<LOGN, -1>(v, buf, t, twt, active);
   if (active) {
     asm volatile("cp.async.wait_group 0;" ::: "memory");
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = p2::cmul(v[e], fm[t + TT * e]);
+    for (int e = 0; e < Ge::E; ++e) v[e] = p2::cmul(v[e], fm[t + TT * e]);
   }
   p2::fft<LOGN, +1>(v, buf, t, twt, active);
   if (active) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) col[t + TT * e] = v[e];
+    for (int e = 0; e < Ge::E; ++e) col[t + TT * e] = v[e];
   }
 }
 
@@ -842,10 +842,10 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
   const int g = threadIdx.x / TT, t = threadIdx.x % TT;
   const bool active = g < G;
   float2* buf = zs + (active ? g : 0) * NP;
-  float2 v[16];
+  float2 v[Ge::E];
   if (active) {
 #pragma unroll
-    for (int e = 0; e < 16; ++e) v[e] = buf[p2::pad(t + TT * e)];
+    for (int e = 0; e < Ge::E; ++e) v[e] = buf[p2::pad(t + TT * e)];
   }
   p2::fft<LOGN, +1>(v, buf, t, twt, active);
   if (pre) asm volatile("cp.async.wait_group 0;" ::: "memory");
@@ -861,7 +861,7 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
       float* xrow = xu.x + b * nn + static_cast<size_t>(y) * N;
       float* orow = xu.x_old ? xu.x_old + b * nn + static_cast<size_t>(y) * N : nullptr;
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
+      for (int e = 0; e < Ge::E; ++e) {
         const int x = t + TT * e;
         const float w = rr ? v[e].y : v[e].x;
         float xn;
@@ -891,7 +891,7 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
     __syncthreads();
     if (active) {
 #pragma unroll
-      for (int e = 0; e < 16; ++e) buf[p2::pad(t + TT * e)] = v[e];
+      for (int e = 0; e < Ge::E; ++e) buf[p2::pad(t + TT * e)] = v[e];
     }
     __syncthreads();
   }
@@ -1059,11 +1059,12 @@ void FftPlan::init(int n_, cudaStream_t s) {
   std::vector<float2> h2;
   if (shape.logn >= 0 && p2_enabled(shape.logn)) {
     const int logn = shape.logn;
-    const int nst = (logn + 3) / 4, llr = logn - 4 * (nst - 1);
+    const int le = p2::kLE, E = 1 << le;
+    const int nst = (logn + le - 1) / le, llr = logn - le * (nst - 1);
     h2.assign(p2::tw_len(logn), make_float2(0.f, 0.f));
-    long long ns = 16;
-    for (int st = 1; st < nst; ++st, ns *= 16) {
-      const int R = st == nst - 1 ? (1 << llr) : 16;
+    long long ns = E;
+    for (int st = 1; st < nst; ++st, ns *= E) {
+      const int R = st == nst - 1 ? (1 << llr) : E;
       for (int r = 1; r < R; ++r)
         for (long long k = 0; k < ns; ++k) {
           const double ang = -2.0 * 3.14159265358979323846 * static_cast<double>(r * k) /
@@ -1087,7 +1088,7 @@ void launch_fft_rows_r2c(const FftPlan& f, const AtuTerms& terms, float2* specT,
   if (rs.rows == 0) rs = RowSlab::full(n);
   const bool peers = rs.peers.p[0] != nullptr;
   if (f.tw2.p) {
-    const int G = p2_row_groups(), T = n / 16;
+    const int G = p2_row_groups(), T = n >> p2::kLE;
     const size_t sm = sizeof(float2) * G * p2::pad(n);
     const int threads = std::max(G * T, std::min(512, G * n / 2));
     dim3 grid((rs.rows + 2 * G - 1) / (2 * G), batch);
@@ -1118,7 +1119,7 @@ void launch_fft_cols_filter(const FftPlan& f, float2* specT, const float2* maskT
                             cudaStream_t s) {
   const int n = f.n;
   if (f.tw2.p) {
-    const int T = n / 16, G = p2_col_groups(T);
+    const int T = n >> p2::kLE, G = p2_col_groups(T);
     const size_t sm = sizeof(float2) * G * (p2::pad(n) + n);
     dim3 grid((n / 2 + 1 + G - 1) / G, batch);
 #define NCSG_COLS(L)                                                                   \
@@ -1176,7 +1177,7 @@ void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& x
   const int n = f.n;
   if (rs.rows == 0) rs = RowSlab::full(n);
   if (f.tw2.p) {
-    const int G = xu.df.on ? p2_fuse_groups(n, fuse_arrays(xu.df)) : p2_row_groups(), T = n / 16;
+    const int G = xu.df.on ? p2_fuse_groups(n, fuse_arrays(xu.df)) : p2_row_groups(), T = n >> p2::kLE;
     if (G == 0) throw Error{NCSG_INVALID, "fused dual update does not fit in shared memory"};
     const size_t sm = xu.df.on ? p2_fuse_smem(n, G, fuse_arrays(xu.df))
                                : sizeof(float2) * G * p2::pad(n) + sizeof(float) * 2 * G * n;

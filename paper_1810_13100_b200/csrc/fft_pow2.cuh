@@ -1,12 +1,13 @@
 // Register-resident Stockham FFT for power-of-two lengths 64 <= N <= 4096
 // (the circulant solve's fast path, circulant.cpp:27-37 / fft.cpp:37-48).
 //
-// A group of T = N/16 threads transforms one length-N sequence.  Thread t of
-// the group holds the 16 values of indices t + T*e (e = 0..15, the cyclic
-// distribution) in registers, both on entry and on exit, so global loads and
-// stores of a row or column are coalesced across the group.  The transform is
-// NST = ceil(log2 N / 4) Stockham stages: radix 16 (a 4 x 4 split in
-// registers) except a radix 2/4/8 last stage when log2 N % 4 != 0.  Stage 0
+// A group of T = N/E threads (E = 16, or 8 with NCSG_FFT_LE=3) transforms one
+// length-N sequence.  Thread t of the group holds the E values of indices
+// t + T*e (the cyclic distribution) in registers, both on entry and on exit,
+// so global loads and stores of a row or column are coalesced across the
+// group.  The transform is NST = ceil(log2 N / log2 E) Stockham stages: radix
+// E (16 as a 4 x 4 split in registers) except a smaller last stage when
+// log2 N is not a multiple of log2 E.  Stage 0
 // runs on the registers as loaded; between stages the group exchanges through
 // a shared-memory buffer padded by one slot per 16 (pad(p) = p + p/16), which
 // makes the stride-16 writes of the early stages conflict-free per half-warp.
@@ -25,29 +26,37 @@ constexpr int kMinLog = 6, kMaxLog = 12;
 
 __host__ __device__ constexpr int pad(int p) { return p + (p >> 4); }
 
+// Values per thread E = 2^LE (16 by default; 8 doubles the threads per
+// transform for more latency hiding at the price of one more stage).
+#ifndef NCSG_FFT_LE
+#define NCSG_FFT_LE 4
+#endif
+constexpr int kLE = NCSG_FFT_LE;
+
 template <int LOGN>
 struct Geo {
   static constexpr int N = 1 << LOGN;
-  static constexpr int E = 16;                      // values per thread
-  static constexpr int T = N / E;                   // threads per transform
-  static constexpr int NST = (LOGN + 3) / 4;        // stages
-  static constexpr int LLR = LOGN - 4 * (NST - 1);  // log2 of the last stage's radix (1..4)
-  static constexpr int NP = pad(N);                 // padded buffer length (float2)
+  static constexpr int LE = kLE;
+  static constexpr int E = 1 << LE;                      // values per thread
+  static constexpr int T = N / E;                        // threads per transform
+  static constexpr int NST = (LOGN + LE - 1) / LE;       // stages
+  static constexpr int LLR = LOGN - LE * (NST - 1);      // log2 of the last stage's radix
+  static constexpr int NP = pad(N);                      // padded buffer length (float2)
 };
 
 // Offset of stage s's twiddles (s >= 1) in the table: every stage before the
-// last is radix 16 with (16 - 1) * Ns entries.
+// last is radix E with (E - 1) * Ns entries.
 __host__ __device__ constexpr int tw_off(int s) {
-  int off = 0, ns = 16;
-  for (int i = 1; i < s; ++i) off += 15 * ns, ns *= 16;
+  int off = 0, ns = 1 << kLE;
+  for (int i = 1; i < s; ++i) off += ((1 << kLE) - 1) * ns, ns <<= kLE;
   return off;
 }
 // Table length for log2 N = logn.
 __host__ __device__ constexpr int tw_len(int logn) {
-  const int nst = (logn + 3) / 4;
-  const int llr = logn - 4 * (nst - 1);
+  const int nst = (logn + kLE - 1) / kLE;
+  const int llr = logn - kLE * (nst - 1);
   int ns = 1;
-  for (int i = 1; i < nst; ++i) ns *= 16;
+  for (int i = 1; i < nst; ++i) ns <<= kLE;
   return tw_off(nst - 1) + ((1 << llr) - 1) * ns;
 }
 
@@ -154,12 +163,12 @@ __device__ __forceinline__ void dft(float2* v) {
 // Stage S >= 1: read the group's buffer (cyclic), twiddle, DFT; the outputs
 // of item q at r land in v[q + Q r] (Q = 16 / R items per thread).
 template <int LOGN, int S, int SIGN>
-__device__ __forceinline__ void stage_in(float2 (&v)[16], const float2* buf, int t,
+__device__ __forceinline__ void stage_in(float2 (&v)[1 << kLE], const float2* buf, int t,
                                          const float2* __restrict__ twt) {
   using G = Geo<LOGN>;
-  constexpr int R = (S == G::NST - 1) ? (1 << G::LLR) : 16;
-  constexpr int Q = 16 / R;
-  constexpr int Ns = 1 << (4 * S);
+  constexpr int R = (S == G::NST - 1) ? (1 << G::LLR) : G::E;
+  constexpr int Q = G::E / R;
+  constexpr int Ns = 1 << (kLE * S);
   constexpr int NR = G::N / R;
   const float2* tw = twt + tw_off(S);
 #pragma unroll
@@ -181,19 +190,20 @@ __device__ __forceinline__ void stage_in(float2 (&v)[16], const float2* buf, int
   }
 }
 
-// Write a radix-16 stage's outputs (item j = t, span Ns) to Stockham positions.
+// Write a radix-E stage's outputs (item j = t, span Ns) to Stockham positions.
 template <int S>
-__device__ __forceinline__ void stage_out(const float2 (&v)[16], float2* buf, int t) {
-  constexpr int Ns = 1 << (4 * S);
+__device__ __forceinline__ void stage_out(const float2 (&v)[1 << kLE], float2* buf, int t) {
+  constexpr int E = 1 << kLE;
+  constexpr int Ns = 1 << (kLE * S);
   const int k = t & (Ns - 1);
-  const int o = (t - k) * 16 + k;
+  const int o = (t - k) * E + k;
 #pragma unroll
-  for (int r = 0; r < 16; ++r) buf[pad(o + r * Ns)] = v[r];
+  for (int r = 0; r < E; ++r) buf[pad(o + r * Ns)] = v[r];
 }
 
 template <int LOGN, int S, int SIGN>
 struct Stages {
-  __device__ __forceinline__ static void run(float2 (&v)[16], float2* buf, int t,
+  __device__ __forceinline__ static void run(float2 (&v)[1 << kLE], float2* buf, int t,
                                              const float2* __restrict__ twt, bool active) {
     using G = Geo<LOGN>;
     if (active) stage_in<LOGN, S, SIGN>(v, buf, t, twt);
@@ -210,9 +220,9 @@ struct Stages {
 // forward / +1 inverse).  buf: the group's NP-entry buffer, clobbered; the
 // engine's first barrier orders its writes after any earlier reads of buf.
 template <int LOGN, int SIGN>
-__device__ __forceinline__ void fft(float2 (&v)[16], float2* buf, int t,
+__device__ __forceinline__ void fft(float2 (&v)[1 << kLE], float2* buf, int t,
                                     const float2* __restrict__ twt, bool active) {
-  if (active) dft16<SIGN>(v);
+  if (active) dft<(1 << kLE), SIGN>(v);
   __syncthreads();
   if (active) stage_out<0>(v, buf, t);
   __syncthreads();
