@@ -143,7 +143,13 @@ def kernel_bytes(cfg, plan):
     # dual: data block (CT: F partial slots + u r/w + ax r/w + b; denoise:
     # u r/w + b), gradient block u_g r/w, x and x_old
     data = 4 * (F * m + 5 * m) if ct else 4 * 3 * n
-    out["dual_update"] = ("hbm", data + 4 * 2 * g + 4 * 2 * n)
+    dual = data + 4 * 2 * g + 4 * 2 * n
+    if plan.get("dual_fused"):
+        # DENOISE: the whole dual update runs inside the inverse row pass
+        # (x and x_old are already on chip there)
+        out["fft_rows_c2r"] = ("hbm", out["fft_rows_c2r"][1] + dual - 4 * 2 * n)
+    else:
+        out["dual_update"] = ("hbm", dual)
     return {k: (bound, B * v) for k, (bound, v) in out.items()}
 
 

@@ -373,6 +373,7 @@ typedef struct ncsg_plan_info {
   int transposed_copy;/* 1: the x update also writes x^T (per-angle class-H forward) */
   int64_t samples;    /* bilinear samples per R application (own angles) */
   int64_t m0, g, range, batch;
+  int dual_fused;     /* 1: the whole dual update runs in the inverse row pass (DENOISE) */
 } ncsg_plan_info;
 ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out);
 /* Kernel launches issued by this library since load. */

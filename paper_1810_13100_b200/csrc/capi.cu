@@ -304,6 +304,7 @@ void phase_b(ncsg_problem* p, const float* plain = nullptr) {
   forward_and_dual(p);
 }
 
+bool fuse_dual_terms(const ncsg_problem* p, DualFuse& df);
 void phase_b_circulant(ncsg_problem* p, const float* plain) {
   cudaStream_t s = p->stream.s;
   AtuTerms T = atu_terms(p);
@@ -325,31 +326,35 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
               : nullptr;
   xu.subtract = 1;
   xu.flag = p->flag.p;
-  // DENOISE: every dual block needs only x, so the whole dual update runs in
-  // the inverse row pass that produces x (unsharded power-of-two problems)
-  // and the step is three kernels.  (CT keeps the stand-alone dual kernel:
-  // fusing only its D block measured no gain at C1/C3/C5.)
   p->dual_fused = false;
-  if (p->d.kind == NCSG_DENOISE && !p->sharded && !p->comm && !plain) {
-    DualFuse& df = xu.df;
-    df.alpha = static_cast<float>(p->d.alpha);
-    df.s_quad = static_cast<float>(1.0 / (1.0 + p->d.alpha));
-    df.wd = p->wd;
-    df.bound = p->bound;
-    df.u_stride = p->range;
-    df.flag = p->flag.p;
-    float* u = p->u.p;
-    if (p->d.kind == NCSG_DENOISE) {
-      df.ud = u;
-      df.bd = p->b.p;
-    }
-    df.ug = u + p->m0;
-    if (p->d.positivity) df.up = u + p->m0 + p->g;
-    df.on = fft_fuses_dual(p->fft, df) ? 1 : 0;
-    p->dual_fused = df.on != 0;
+  if (!plain && fuse_dual_terms(p, xu.df)) {
+    xu.df.on = 1;
+    p->dual_fused = true;
   }
   mark(p);
   launch_fft_rows_c2r(p->fft, p->spec.p, xu, p->batch, s);
+}
+
+// DENOISE: every dual block needs only x, so the whole dual update runs in
+// the inverse row pass that produces x (unsharded power-of-two problems) and
+// the step is three kernels.  (CT keeps the stand-alone dual kernel: fusing
+// only its D block measured no gain at C1/C3/C5.)  Fills df (on = 0) and
+// returns whether the fusion applies.
+bool fuse_dual_terms(const ncsg_problem* p, DualFuse& df) {
+  df = DualFuse{};
+  if (p->d.kind != NCSG_DENOISE || p->sharded || p->comm) return false;
+  df.alpha = static_cast<float>(p->d.alpha);
+  df.s_quad = static_cast<float>(1.0 / (1.0 + p->d.alpha));
+  df.wd = p->wd;
+  df.bound = p->bound;
+  df.u_stride = p->range;
+  df.flag = p->flag.p;
+  float* u = p->u.p;
+  df.ud = u;  // identity (data) block, then D, then positivity
+  df.bd = p->b.p;
+  df.ug = u + p->m0;
+  if (p->d.positivity) df.up = u + p->m0 + p->g;
+  return fft_fuses_dual(p->fft, df);
 }
 
 // Engine::step after the x update (solvers.cpp:146-158): R x+ for the own
@@ -1704,6 +1709,8 @@ ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out) {
     r.g = static_cast<int64_t>(p->g);
     r.range = static_cast<int64_t>(p->range);
     r.batch = p->batch;
+    DualFuse df;
+    r.dual_fused = fuse_dual_terms(p, df) ? 1 : 0;
     *out = r;
   });
 }

@@ -31,7 +31,9 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 ALIAS = {"bp_gather_kernel": "adjoint", "bp_tile_kernel": "adjoint", "fp_orbit_kernel": "forward",
          "fp_strip_kernel": "forward", "fft_rows_r2c_kernel": "fft_rows_r2c",
          "fft_cols_filter_kernel": "fft_cols", "fft_rows_c2r_kernel": "fft_rows_c2r",
-         "make_quad_kernel": "make_quad", "dual_update_kernel": "dual_update"}
+         "make_quad_kernel": "make_quad", "dual_update_kernel": "dual_update",
+         "fft_rows_r2c_p2": "fft_rows_r2c", "fft_cols_filter_p2": "fft_cols",
+         "fft_rows_c2r_p2": "fft_rows_c2r"}
 
 
 def short(name: str) -> str:
