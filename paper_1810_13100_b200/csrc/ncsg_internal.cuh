@@ -278,7 +278,8 @@ struct RadonDev {
   int orb_seg = 64;      // rows per forward segment (upload chooses 32 or 64)
   int batch_hint = 1;    // problems per launch the plan is sized for (set before upload)
   int orb_rmax = 0;
-  int orb_warps = 8;     // orbits (warps) per forward CTA
+  int orb_warps = 8;     // warps per forward CTA
+  int orb_split = 1;     // warps per orbit (small grids: 4, each every 4th ray group)
   DevBuf<OrbitGeom> orbits;
   DevBuf<int2> orb_range;                     // [orbit][strip][seg] s-range
   // Cached TMA descriptor of the orbit forward's member-image buffer (encoded

@@ -388,6 +388,7 @@ struct OrbArgs {
   const OrbitGeom* orb;
   int n_orb;
   int n_chunks;               // orbit chunks per batch problem
+  int split;                  // warps per orbit (each sweeps every split-th ray group)
   const int2* range;          // [orbit][strip][seg]
   const RayRange* rays;
   const float4* quad;         // [batch][n][n] (x, x1, x2, x3) per pixel (make_quad_kernel)
@@ -503,7 +504,8 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
   const int chunk = blockIdx.z - b * a.n_chunks;
   const int X0 = strip * W;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int oi = chunk * NW + warp;
+  const int oi = chunk * (NW / a.split) + warp / a.split;
+  const int sub = warp % a.split;  // this warp's share of the orbit's ray groups
   const bool has = oi < a.n_orb;
   const int n = a.n;
   const float c = 0.5f * (n - 1);
@@ -596,11 +598,14 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
       const int R = g.fp_rq, G = 4 * R;
       const int loff = (lane >> 3) * R + min(lane & 7, R - 1);
       const bool dup = (lane & 7) >= R;
+      const int GS = G * a.split;  // ray groups of this warp: sub, sub + split, ...
+      const int tfirst = tlo + sub * G;
       RayRange nxt[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(tlo + loff, thi), true);
-      for (int sb = tlo; sb <= thi; sb += G) {
+        nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(tfirst + loff, thi),
+                             tfirst <= thi);
+      for (int sb = tfirst; sb <= thi; sb += GS) {
         const int s_raw = sb + loff;
         const int s = min(s_raw, thi);
         const bool act = !dup && s_raw <= thi;
@@ -608,8 +613,8 @@ __global__ void __launch_bounds__(NW * 32, NCSG_ORB_MINB * kOrbWarps / NW)
 #pragma unroll
         for (int k = 0; k < 4; ++k) {  // prefetch the next group's ray ranges
           cur[k] = nxt[k];
-          nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(s_raw + G, thi),
-                               sb + G <= thi);
+          nxt[k] = member_rays(a.rays, a.det, a.s_mid, o.t[k], min(s_raw + GS, thi),
+                               sb + GS <= thi);
         }
         // shared run: ownership of the rep's lattice (x strip, y tile row)
         const RayRange all{-0x3fffffff, 0x3fffffff};
@@ -1427,6 +1432,17 @@ void RadonDev::upload() {
                         batch_hint;
       orb_warps = ctas < 148 ? 2 : kOrbWarps;
       if (const char* e = getenv("NCSG_ORB_NW")) orb_warps = atoi(e) == 2 ? 2 : kOrbWarps;
+      // and those CTAs run kOrbWarps warps, kOrbWarps / 2 per orbit, each
+      // sweeping every (kOrbWarps / 2)-th ray group: 4x the warps in flight
+      orb_split = 1;
+      if (orb_warps == 2) {
+        orb_warps = kOrbWarps;
+        orb_split = kOrbWarps / 2;
+      }
+      if (const char* e = getenv("NCSG_ORB_SPLIT")) {
+        const int sp = atoi(e);
+        if (sp >= 1 && kOrbWarps % sp == 0) orb_split = sp;
+      }
       choose_lane_rays(geo.orbits);
       orb_rmax = rmax;
       orbits.alloc(geo.orbits.size());
@@ -1646,7 +1662,13 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     OrbArgs a;
     a.orb = r.orbits.p;
     a.n_orb = static_cast<int>(g.orbits.size());
-    a.n_chunks = (a.n_orb + r.orb_warps - 1) / r.orb_warps;
+    // the split needs direct stores (one tile row per CTA): with per-warp
+    // ray accumulators across tile rows a ray's groups must stay in one warp
+    int nw = r.orb_warps;
+    a.split = r.orb_split;
+    if (r.orb_seg / kOrbT != 1 && a.split > 1) nw /= a.split, a.split = 1;
+    const int per_cta = nw / a.split;  // orbits per CTA
+    a.n_chunks = (a.n_orb + per_cta - 1) / per_cta;
     a.range = r.orb_range.p;
     a.rays = r.rays.p;
     a.quad = reinterpret_cast<const float4*>(imgT);  // orbit mode: aux = make_quad output
@@ -1674,7 +1696,6 @@ void launch_radon_forward_partial(const RadonDev& r, const float* img, const flo
     CUtensorMap map;
     std::memcpy(&map, qm.bytes, sizeof(map));
     const bool tma = qm.ok;
-    const int nw = r.orb_warps;
     const size_t smem = orbit_smem(a.seg_tiles == 1 ? 0 : a.rmax, nw);
     dim3 grid(r.n_strips, r.n_segs, a.n_chunks * batch);
     auto go = [&](auto kern) {
