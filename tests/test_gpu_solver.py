@@ -273,6 +273,42 @@ def test_c5_batched_parity(ncsg, port):
 
 
 @pytest.mark.slow
+def test_c5_all_problems_against_golden(ncsg, port):
+    # all 64 problems of C5 at the configured 500 iterations against the
+    # oracle's solve_template runs (solvers.cpp:267-337), committed as
+    # tests/golden/c5_full.npz by make_c5_golden.py: record rows of every
+    # problem, x and u at a seeded sample of entries
+    path = os.path.join(GOLDEN, "c5_full.npz")
+    if not os.path.exists(path):
+        pytest.skip("c5 golden not generated")
+    from paper_1810_13100_b200 import configs, instances
+
+    gd = np.load(path)
+    cfg = configs.get("c5")
+    mask = instances.metric_mask(cfg)
+    bs = []
+    for q in range(cfg.batch):
+        _, b = instances.make_instance(cfg, lambda im: port.radon_forward(im, cfg.angles, cfg.det),
+                                       problem=q)
+        np.testing.assert_allclose(np.ravel(b)[:256], gd["b_head"][q], rtol=1e-12)
+        bs.append(b)
+    proto = Prob(0, cfg.n, cfg.angles, cfg.det, cfg.alpha, cfg.beta, cfg.lam, bs[0])
+    g = gpu_problem(ncsg, proto, cfg.gamma, mask, batch_b=np.stack(bs)).solve(
+        cfg.iters, record_every=cfg.iters // 2)
+    worst = [0.0, 0.0, 0.0]
+    for q in range(cfg.batch):
+        ex = rel(np.ravel(g.x[q])[gd["x_idx"]], gd["x_sample"][q])
+        eu = rel(np.ravel(g.u[q])[gd["u_idx"]], gd["u_sample"][q])
+        oo = gd["rows"][q][:, 1]
+        np.testing.assert_array_equal(g.rows[q][:, 0], gd["rows"][q][:, 0])
+        ef = float(np.max(np.abs(g.rows[q][:, 1] - oo) / np.abs(oo)))
+        worst = [max(worst[0], ex), max(worst[1], eu), max(worst[2], ef)]
+        assert ex <= TOL and eu <= TOL and ef <= TOL, (q, ex, eu, ef)
+    print(f"c5 64 problems x 500 iterations: worst x {worst[0]:.2e}, u {worst[1]:.2e}, "
+          f"objective {worst[2]:.2e}")
+
+
+@pytest.mark.slow
 def test_c4_few_iterations(ncsg, port):
     cfg, prob, mask = config_case("c4", port)
     if not cfg.pinned:
