@@ -1057,6 +1057,9 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
       // z_u - 1/2 = (du0 + u) * cu + fk + K is affine in u (cu, K per orbit)
       const float cu = -g.ay * g.inv_dy, K1 = -g.inv_dy - 1.5f;
       const f32x2 negD = pk(-g.dx, -g.dy), D2 = pk(2.0f * g.dx, 2.0f * g.dy);
+      // rays 1 and 2: z_u = z0 + u cu and their floors as one f32x2 pair
+      const f32x2 CU12 = pk(cu, 2.0f * cu);
+      const f32x2 MAG = pk(12582912.0f, 12582912.0f), NMAG = pk(-12582912.0f, -12582912.0f);
       const float4* Uo = U4[buf][o];
       const int sl = slo[ob - o_begin + o];
       long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
@@ -1073,11 +1076,13 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
         // B0 = du0 A - (fk - 1) D = du0 A - fk1p D + 2 D, B_{u+1} = B_u + A
         const float z0 = fmaf(du0, cu, fk1p + K1);
         f32x2 Bu = ffma2(pk(du0, du0), A, ffma2(pk(fk1p, fk1p), negD, D2));
+        // floor (round-to-nearest of z - 1/2): ray 0 scalar, rays 1, 2 paired
+        const float zl0 = __fsub_rn(__fadd_rn(z0, 12582912.0f), 12582912.0f);
+        const float2 zl12 = upk(fadd2(fadd2(fadd2(pk(z0, z0), CU12), MAG), NMAG));
 #pragma unroll
         for (int u = 0; u < 3; ++u) {
           if (u > 0) Bu = fadd2(Bu, A);
-          const float zl = __fsub_rn(__fadd_rn(u == 0 ? z0 : __fadd_rn(z0, u * cu), 12582912.0f),
-                                     12582912.0f);  // floor (round-to-nearest of z - 1/2)
+          const float zl = u == 0 ? zl0 : (u == 1 ? zl12.x : zl12.y);
           f32x2 e = ffma2(pk(zl, zl), D, Bu);  // (ex, ey)
           float2 v = upk(e);
           float w = tent(v.x) * tent(v.y);
