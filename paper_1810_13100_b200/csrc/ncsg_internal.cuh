@@ -221,6 +221,14 @@ constexpr int kGaMaxChunk = 1024;                   // orbits per chunk (lowest-
 // lattice is p(s, k) = c + s a + k d, and pixel (X, Y) has the continuous
 // lattice coordinates (sigma, kappa) = M^-1 (q - c), M = [a d], kept in Q32
 // fixed point as affine functions of (X, Y).
+// One skipped window sample of a border pixel (bp_gather_kernel): ray s of
+// the orbit, the members it is invalid for (bit m), its bilinear weight.
+struct GaBorderEntry {
+  float w;
+  short s;
+  unsigned char mask;
+  unsigned char pad;
+};
 struct GatherGeom {
   long long s0, sx, sy;  // sigma(X, Y) = s0 + X sx + Y sy   (Q32)
   long long k0, kx, ky;  // kappa(X, Y) = k0 + X kx + Y ky   (Q32)
@@ -263,6 +271,14 @@ struct RadonDev {
   int bp_orbit_chunks = 0, bp_orbit_len = 0;
   int bp_cluster = 1;  // chunk CTAs folded per thread-block cluster (1, 2 or 4)
   DevBuf<GatherGeom> gather;
+  // Border-pixel corrections of the gather adjoint (plan_adjoint): for each
+  // edge tile e (ga_tile_edge[tile] = e, -1 inside), item (orbit o, border
+  // pixel k in row-major order) at ga_bt_base[e] + o * nbp_e + k owns the
+  // entries [ga_bt_off[item], ga_bt_off[item + 1]) -- the window samples of
+  // that pixel the reference skips (outside the image square or the member
+  // rays' replayed ranges), in candidate order
+  DevBuf<int> ga_tile_edge, ga_bt_base, ga_bt_off;
+  DevBuf<GaBorderEntry> ga_bt_ent;
   // Orbit-interleaved dual (optional gather input): angle t's member slot
   // 4 * orbit + member (-1: none) and the padded row of rays per orbit.
   DevBuf<int> angle_slot;
@@ -293,6 +309,7 @@ struct RadonDev {
   mutable QuadMap quad_map;
   void upload();
   void plan_adjoint(int batch);
+  void build_gather_border_table();
   int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }
   // Forward partial slots per ray (fp_partial[batch][slots][m]).
   int fp_slots() const { return orbit_mode ? n_strips + n_segs - 1 : n_strips; }

@@ -915,7 +915,102 @@ struct GaArgs {
   size_t nn, u_stride;
   const float4* u4;  // orbit-interleaved u ([batch][orbit][u4_row], nullable)
   int u4_row, u4_pad;
+  // border-pixel correction table (RadonDev::ga_* ; see ncsg_internal.cuh)
+  const int* tile_edge;
+  const int* bt_base;
+  const int* bt_off;
+  const GaBorderEntry* bt_ent;
 };
+
+// Border pixels (image row / column 0 or n-1) of the TW x TH tile at (X0, Y0)
+// in row-major order -- deterministic, so the correction table's item index
+// of a pixel is the same in every launch.  A warp scans one 32-pixel row.
+template <int TW, int TH, int NT>
+__device__ __forceinline__ void tile_border_list(int X0, int Y0, int n, int2* bpix, int* rowcnt,
+                                                 int* nbp) {
+  static_assert(TW == 32 && NT % 32 == 0 && TH % (NT / 32) == 0, "a warp per tile row");
+  constexpr int NW = NT / 32, RP = TH / NW;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned bal[RP];
+#pragma unroll
+  for (int p = 0; p < RP; ++p) {
+    const int row = w + p * NW, X = X0 + lane, Y = Y0 + row;
+    const bool f = X < n && Y < n && (X == 0 || Y == 0 || X == n - 1 || Y == n - 1);
+    bal[p] = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) rowcnt[row] = __popc(bal[p]);
+  }
+  __syncthreads();
+#pragma unroll
+  for (int p = 0; p < RP; ++p) {
+    const int row = w + p * NW;
+    if ((bal[p] >> lane) & 1u) {
+      int k = __popc(bal[p] & ((1u << lane) - 1u));
+      for (int r = 0; r < row; ++r) k += rowcnt[r];
+      bpix[k] = make_int2(lane, row);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int r = 0; r < TH; ++r) t += rowcnt[r];
+    *nbp = t;
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ float tent(float e);
+__device__ __forceinline__ int q32_floor(long long v);
+__device__ __forceinline__ float q32_frac(long long v);
+__device__ __forceinline__ float floor_rn(float z);
+
+// The window samples of border pixel (X, Y) and orbit g that the gather's
+// main loop counts but the reference skips (radon.cpp:87-97: outside the
+// image square, or outside a member ray's replayed valid range): f(s, mask,
+// w) per sample, in candidate order, mask = the members it is invalid for
+// (present members on detector rays only -- the others stage zeros).  A
+// sample farther than kEps inside the image square is valid for every member.
+template <class F>
+__device__ __forceinline__ void border_skipped(const GatherGeom& g, int X, int Y, int n,
+                                               const RayRange* rays, int det, int s_mid, F&& f) {
+  const float lim = static_cast<float>(n - 1);
+  constexpr float kEps = 4e-3f;  // > fp32 rounding of X + e for X < 4096
+  const float ax = g.ax, ay = g.ay, dx = g.dx, dy = g.dy;
+  const float Xf = static_cast<float>(X), Yf = static_cast<float>(Y);
+  const long long sq = g.s0 + X * g.sx + Y * g.sy;
+  const long long kq = g.k0 + X * g.kx + Y * g.ky;
+  const int sf = q32_floor(sq), kf = q32_floor(kq);
+  const float fs = q32_frac(sq), fk = q32_frac(kq);
+  const int u0 = fs - g.rho > -1.0f ? 0 : -1;
+  for (int u = 0; u < 3; ++u) {
+    const float du = static_cast<float>(u0 + u) - fs;
+    const float vf = floor_rn(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
+    const int sr = sf + u0 + u;
+    if (sr < -s_mid || sr > s_mid) continue;  // off the detector: staged zeros
+    for (int j = 0; j < 3; ++j) {
+      const float dv = vf + j - fk;
+      const float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
+      const float w = tent(ex) * tent(ey);
+      const float px = Xf + ex, py = Yf + ey;
+      const float lo = fminf(px, py), hi = fmaxf(px, py);
+      if (w == 0.f || (lo > kEps && hi < lim - kEps)) continue;
+      const bool out = lo < -kEps || hi > lim + kEps;
+      const int tau = g.dir * (kf + static_cast<int>(vf) + j);
+      unsigned mask = 0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        const int t = g.t[m];
+        if (t < 0) continue;
+        bool valid = false;
+        if (!out) {
+          const RayRange rr = rays[static_cast<size_t>(t) * det + s_mid + sr];
+          const int tm = m >= 2 ? -tau : tau;
+          valid = tm >= rr.first && tm <= rr.last;
+        }
+        if (!valid) mask |= 1u << m;
+      }
+      if (mask) f(sr, mask, w);
+    }
+  }
+}
 
 __device__ __forceinline__ float tent(float e) { return __saturatef(1.0f - fabsf(e)); }
 
@@ -965,6 +1060,7 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
   __shared__ int2 bpix[MAXB];         // border pixels of this tile (tile-local)
   __shared__ float4 bacc[MAXB];       // their corrections
   __shared__ int nbp;
+  __shared__ int rowcnt[TH];
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   const int b = blockIdx.z / a.n_chunks;
   const int chunk = blockIdx.z - b * a.n_chunks;
@@ -981,20 +1077,16 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
 #pragma unroll
   for (int p = 0; p < PX; ++p) acc_xy[p] = acc_zw[p] = pk(0.f, 0.f);
   const long long Xt = X0 + tx, Yt = Y0 + ty;
-  // Border pixels (image row / column 0 or n-1) of this tile.
-  if (threadIdx.x == 0) nbp = 0;
-  __syncthreads();
-#pragma unroll
-  for (int p = 0; p < PX; ++p) {
-    const int X = X0 + tx, Y = Y0 + ty + p * RS;
-    if (X < n && Y < n && (X == 0 || Y == 0 || X == n - 1 || Y == n - 1)) {
-      const int k = atomicAdd(&nbp, 1);
-      bpix[k] = make_int2(tx, ty + p * RS);
-      bacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
+  // Border pixels (image row / column 0 or n-1) of this tile, row-major, and
+  // the tile's slice of the correction table.
+  const int edge = a.tile_edge[blockIdx.y * gridDim.x + blockIdx.x];
+  if (edge >= 0) {
+    tile_border_list<TW, TH, kGaThreads>(X0, Y0, n, bpix, rowcnt, &nbp);
+    for (int k = threadIdx.x; k < nbp; k += kGaThreads) bacc[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+  } else if (threadIdx.x == 0) {
+    nbp = 0;
   }
-  const float lim = static_cast<float>(n - 1);
-  constexpr float kEps = 4e-3f;  // > fp32 rounding of X + e for X < 4096
+  const int bt_base = edge >= 0 ? a.bt_base[edge] : 0;
 
   // Lowest staged ray of every orbit of the chunk for this tile: sigma over
   // the tile corners minus the window half-extent.
@@ -1098,55 +1190,27 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
         }
       }
     }
-    // Border pixels: the loop above took every window sample as valid. A
-    // sample farther than kEps inside the image square is (for every
-    // member); the others -- outside, or on the edge up to rounding -- are
-    // checked against each member's replayed ray range and the invalid ones
-    // taken back out. Items (border pixel, orbit): NB lanes per pixel,
-    // reduced in a fixed order.
+    // Border pixels: the loop above took every window sample as valid; the
+    // samples the reference skips (border_skipped, precomputed per (border
+    // pixel, orbit) by ga_border_table_kernel) are taken back out.  Items
+    // (border pixel, orbit): NB lanes per pixel, reduced in a fixed order.
     const int nbt = (nbp * NB + 31) / 32 * 32;
+#pragma unroll 4
     for (int it = threadIdx.x; it < nbt; it += kGaThreads) {
       const int bq = it / NB, o = it % NB;
       float cr[4] = {0.f, 0.f, 0.f, 0.f};
       if (bq < nbp && o < nb) {
-        const GatherGeom& g = G[buf][o];
-        const float ax = g.ax, ay = g.ay, dx = g.dx, dy = g.dy;
-        const int2 bl = bpix[bq];
-        const int X = X0 + bl.x, Y = Y0 + bl.y;
-        const float Xf = static_cast<float>(X), Yf = static_cast<float>(Y);
-        const long long sq = g.s0 + X * g.sx + Y * g.sy;
-        const long long kq = g.k0 + X * g.kx + Y * g.ky;
-        const int sf = q32_floor(sq), kf = q32_floor(kq);
-        const float fs = q32_frac(sq), fk = q32_frac(kq);
-        const int u0 = fs - g.rho > -1.0f ? 0 : -1;
-        const int r0 = sf + u0 - slo[ob - o_begin + o];
-        for (int u = 0; u < 3; ++u) {
-          const float du = static_cast<float>(u0 + u) - fs;
-          const float vf = floor_rn(fmaf(-du, ay, -1.0f) * g.inv_dy + fk) + 1.0f;
-          const float4 uv = U4[buf][o][r0 + u];
+        const int item = bt_base + (ob + o) * nbp + bq;
+        const int q1 = __ldg(a.bt_off + item + 1);
+        const float4* Uo = U4[buf][o];
+        const int sl = slo[ob - o_begin + o];
+        for (int q = __ldg(a.bt_off + item); q < q1; ++q) {
+          const GaBorderEntry en = a.bt_ent[q];
+          const float4 uv = Uo[en.s - sl];
           const float um[4] = {uv.x, uv.y, uv.z, uv.w};
-          for (int j = 0; j < 3; ++j) {
-            const float dv = vf + j - fk;
-            const float ex = fmaf(du, ax, dv * dx), ey = fmaf(du, ay, dv * dy);
-            const float w = tent(ex) * tent(ey);
-            const float px = Xf + ex, py = Yf + ey;
-            const float lo = fminf(px, py), hi = fmaxf(px, py);
-            if (w == 0.f || (lo > kEps && hi < lim - kEps)) continue;
-            const bool out = lo < -kEps || hi > lim + kEps;
-            const int sr = sf + u0 + u;
-            const int tau = g.dir * (kf + static_cast<int>(vf) + j);
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              bool valid = false;
-              const int t = g.t[m];
-              if (!out && t >= 0 && sr >= -a.s_mid && sr <= a.s_mid) {
-                const RayRange rr = a.rays[static_cast<size_t>(t) * a.det + a.s_mid + sr];
-                const int tm = m >= 2 ? -tau : tau;
-                valid = tm >= rr.first && tm <= rr.last;
-              }
-              if (!valid) cr[m] -= w * um[m];
-            }
-          }
+          for (int m = 0; m < 4; ++m)
+            if ((en.mask >> m) & 1u) cr[m] -= en.w * um[m];
         }
       }
 #pragma unroll
@@ -1235,6 +1299,49 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
     if (X < n && Y < n) {
       o1[static_cast<size_t>(n - 1 - X) * n + Y] = ot[1][y][x];
       o3[static_cast<size_t>(n - 1 - X) * n + (n - 1 - Y)] = ot[3][y][x];
+    }
+  }
+}
+
+// The gather adjoint's border-pixel correction table (GaArgs::bt_*), built
+// once per plan: pass 0 counts each (edge tile, orbit, border pixel) item's
+// skipped samples, pass 1 writes them at the host's exclusive prefix sums.
+struct GaTableArgs {
+  const GatherGeom* geo;
+  int n_orb;
+  const int2* edge_tiles;  // tile coordinates of edge tile e
+  const int* base;         // first item of edge tile e
+  const RayRange* rays;
+  int n, det, s_mid;
+  int* cnt;
+  const int* off;
+  GaBorderEntry* ent;
+  int pass;
+};
+constexpr int kGaTableOrbits = 16;  // orbits per table-build CTA
+__global__ void __launch_bounds__(kGaThreads) ga_border_table_kernel(GaTableArgs a) {
+  __shared__ int2 bpix[2 * (kGaTW + kGaTH)];
+  __shared__ int rowcnt[kGaTH];
+  __shared__ int nbp;
+  const int e = blockIdx.x;
+  const int2 tl = a.edge_tiles[e];
+  const int X0 = tl.x * kGaTW, Y0 = tl.y * kGaTH;
+  tile_border_list<kGaTW, kGaTH, kGaThreads>(X0, Y0, a.n, bpix, rowcnt, &nbp);
+  const int o0 = blockIdx.y * kGaTableOrbits, o1 = min(a.n_orb, o0 + kGaTableOrbits);
+  for (int it = threadIdx.x; it < (o1 - o0) * nbp; it += blockDim.x) {
+    const int o = o0 + it / nbp, k = it - (it / nbp) * nbp;
+    const int item = a.base[e] + o * nbp + k;
+    const GatherGeom g = a.geo[o];
+    const int X = X0 + bpix[k].x, Y = Y0 + bpix[k].y;
+    if (a.pass == 0) {
+      int c = 0;
+      border_skipped(g, X, Y, a.n, a.rays, a.det, a.s_mid, [&](int, unsigned, float) { ++c; });
+      a.cnt[item] = c;
+    } else {
+      int q = a.off[item];
+      border_skipped(g, X, Y, a.n, a.rays, a.det, a.s_mid, [&](int sr, unsigned mask, float w) {
+        a.ent[q++] = GaBorderEntry{w, static_cast<short>(sr), static_cast<unsigned char>(mask), 0};
+      });
     }
   }
 }
@@ -1507,6 +1614,73 @@ void RadonDev::upload() {
   }
 }
 
+// The border-pixel correction table of the gather adjoint (see
+// RadonDev::ga_*): edge tiles and their items on the host, the skipped
+// samples by ga_border_table_kernel (count, host prefix sum, fill).
+void RadonDev::build_gather_border_table() {
+  const int n = geo.n;
+  const int tx = (n + kGaTW - 1) / kGaTW, ty = (n + kGaTH - 1) / kGaTH;
+  const int n_orb = static_cast<int>(geo.orbits.size());
+  std::vector<int> tile_edge(static_cast<size_t>(tx) * ty, -1), base;
+  std::vector<int2> edges;
+  long long items = 0;
+  for (int j = 0; j < ty; ++j)
+    for (int i = 0; i < tx; ++i) {
+      int nb = 0;  // border pixels of the tile (the count tile_border_list finds)
+      for (int y = j * kGaTH; y < std::min(n, (j + 1) * kGaTH); ++y)
+        for (int x = i * kGaTW; x < std::min(n, (i + 1) * kGaTW); ++x)
+          nb += (x == 0 || y == 0 || x == n - 1 || y == n - 1) ? 1 : 0;
+      if (nb == 0) continue;
+      tile_edge[static_cast<size_t>(j) * tx + i] = static_cast<int>(edges.size());
+      edges.push_back(make_int2(i, j));
+      base.push_back(static_cast<int>(items));
+      items += static_cast<long long>(nb) * n_orb;
+    }
+  if (items >= (1LL << 31)) throw Error{NCSG_INVALID, "gather border table too large"};
+  auto up = [](auto& buf, const auto& v) {
+    buf.alloc(v.size());
+    if (!v.empty())
+      NCSG_CUDA_CHECK(cudaMemcpy(buf.p, v.data(), v.size() * sizeof(v[0]), cudaMemcpyHostToDevice));
+  };
+  up(ga_tile_edge, tile_edge);
+  up(ga_bt_base, base);
+  DevBuf<int2> edge_dev;
+  up(edge_dev, edges);
+  DevBuf<int> cnt;
+  cnt.alloc(static_cast<size_t>(items) + 1);
+  GaTableArgs a{};
+  a.geo = gather.p;
+  a.n_orb = n_orb;
+  a.edge_tiles = edge_dev.p;
+  a.base = ga_bt_base.p;
+  a.rays = rays.p;
+  a.n = n;
+  a.det = geo.n_det;
+  a.s_mid = geo.s_mid;
+  a.cnt = cnt.p;
+  std::vector<int> off(static_cast<size_t>(items) + 1, 0);
+  if (!edges.empty() && n_orb > 0) {
+    dim3 grid(static_cast<unsigned>(edges.size()), (n_orb + kGaTableOrbits - 1) / kGaTableOrbits);
+    a.pass = 0;
+    ga_border_table_kernel<<<grid, kGaThreads>>>(a);
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    NCSG_CUDA_CHECK(cudaMemcpy(off.data() + 1, cnt.p, static_cast<size_t>(items) * sizeof(int),
+                               cudaMemcpyDeviceToHost));
+    for (size_t i = 1; i < off.size(); ++i) off[i] += off[i - 1];
+  }
+  up(ga_bt_off, off);
+  ga_bt_ent.alloc(std::max<size_t>(1, static_cast<size_t>(off.back())));
+  if (!edges.empty() && n_orb > 0 && off.back() > 0) {
+    a.off = ga_bt_off.p;
+    a.ent = ga_bt_ent.p;
+    a.pass = 1;
+    dim3 grid(static_cast<unsigned>(edges.size()), (n_orb + kGaTableOrbits - 1) / kGaTableOrbits);
+    ga_border_table_kernel<<<grid, kGaThreads>>>(a);
+    NCSG_CUDA_CHECK(cudaGetLastError());
+    NCSG_CUDA_CHECK(cudaDeviceSynchronize());
+  }
+}
+
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
   bp_orbit = orbit_mode && !getenv("NCSG_NO_GATHER");
@@ -1548,6 +1722,7 @@ void RadonDev::plan_adjoint(int batch) {
     bp_chunks[1] = 0;
     bp_chunk_len[0] = bp_chunk_len[1] = 1;
     bp_batch_planned = batch;
+    build_gather_border_table();
     return;
   }
   int bw, bt, bpitch;
@@ -1788,6 +1963,10 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     a.u4 = reinterpret_cast<const float4*>(u4);
     a.u4_row = r.u4_row();
     a.u4_pad = kGaSW;
+    a.tile_edge = r.ga_tile_edge.p;
+    a.bt_base = r.ga_bt_base.p;
+    a.bt_off = r.ga_bt_off.p;
+    a.bt_ent = r.ga_bt_ent.p;
     dim3 grid((n + kGaTW - 1) / kGaTW, (n + kGaTH - 1) / kGaTH, a.n_chunks * batch);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
