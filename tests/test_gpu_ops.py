@@ -184,7 +184,10 @@ def test_grad_parity(ncsg, port):
     assert g[0] == -1 and g[2] == -8 and g[6] == 1 - 8 and g[11] == 32 - 256
 
 
-@pytest.mark.parametrize("n", [8, 16, 128, 512, 1024, 2048])
+# 8-32: shared-memory Stockham passes; 64-4096: the register-resident
+# power-of-two engine (fft_pow2.cuh), every last-stage radix (64: 16x4,
+# 128: 16x8, 256: 16x16, 512: 16x16x2, 2048: 16x16x8, 4096: 16x16x16)
+@pytest.mark.parametrize("n", [8, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
 def test_mask_apply_parity(ncsg, port, n):
     rng = np.random.default_rng(n)
     x = rng.standard_normal((n, n))
