@@ -162,6 +162,7 @@ struct ncsg_problem {
   int64_t flag_base = 0;          // iteration at the last reset_flag
   size_t m_begin = 0, m_end = 0;  // own rays of the data block (CT)
   bool sharded = false;            // angle- or orbit-sharded (multi-GPU phases)
+  bool quad_fused = false;         // this step's inverse row pass wrote the orbit member planes
   bool dual_fused = false;         // this step's inverse row pass did the x-only dual blocks
   // Orbit-interleaved copy of the sinogram dual (gather-mode adjoint input),
   // written by the dual update; fresh while u has not been written otherwise.
@@ -296,6 +297,7 @@ void forward_and_dual(ncsg_problem* p);
 
 // plain != nullptr: A^T u was assembled (and all-reduced) into `plain`.
 void phase_b(ncsg_problem* p, const float* plain = nullptr) {
+  p->quad_fused = false;
   if (p->n_cg > 0 && !plain) {
     x_update_cg(p);
   } else {
@@ -326,6 +328,16 @@ void phase_b_circulant(ncsg_problem* p, const float* plain) {
               : nullptr;
   xu.subtract = 1;
   xu.flag = p->flag.p;
+  // Orbit mode: the inverse row pass writes the member planes itself while
+  // they stay in L2 until the forward reads them (C1 18.5k -> 19.3k it/s, C3
+  // +0.3%); its column-direction 4-byte stores cost more than make_quad once
+  // the planes are large (C5's 67 MB: +36 us in the row pass for -21 us).
+  constexpr size_t kQuadFuseBytes = 24u << 20;
+  if (p->d.kind != NCSG_DENOISE && p->radon && p->radon->orbit_mode && fft_writes_quad(p->fft) &&
+      p->batch * p->nn * sizeof(float4) <= kQuadFuseBytes) {
+    xu.quad = reinterpret_cast<float4*>(p->xT.p);  // orbit mode: xT holds the member planes
+    p->quad_fused = true;
+  }
   p->dual_fused = false;
   if (!plain && fuse_dual_terms(p, xu.df)) {
     xu.df.on = 1;
@@ -362,8 +374,9 @@ bool fuse_dual_terms(const ncsg_problem* p, DualFuse& df) {
 void forward_and_dual(ncsg_problem* p) {
   cudaStream_t s = p->stream.s;
   mark(p);
-  if (p->d.kind != NCSG_DENOISE && p->radon && p->radon->orbit_mode)
+  if (p->d.kind != NCSG_DENOISE && p->radon && p->radon->orbit_mode && !p->quad_fused)
     launch_make_planes(p->x.p, p->xT.p, p->d.n, p->batch, s);
+  p->quad_fused = false;
   mark(p);
   if (p->d.kind != NCSG_DENOISE) proj_forward(p, p->x.p, p->xT.p, p->fp_part.p, p->batch);
   mark(p);

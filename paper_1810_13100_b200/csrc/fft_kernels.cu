@@ -887,7 +887,7 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
   }
   if (xu.flag && __syncthreads_or(bad) && threadIdx.x == 0)
     atomicMin(xu.flag, *(volatile int*)(xu.flag + 1));
-  if (xu.xT || df.on) {  // the new rows in natural order: zs[pair][pad(x)]
+  if (xu.xT || xu.quad || df.on) {  // the new rows in natural order: zs[pair][pad(x)]
     __syncthreads();
     if (active) {
 #pragma unroll
@@ -902,6 +902,33 @@ __global__ void __launch_bounds__(512) fft_rows_c2r_p2(const float2* __restrict_
       if (y >= yown) continue;
       const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
       xu.xT[b * nn + static_cast<size_t>(x) * N + y] = (r & 1) ? zz.y : zz.x;
+    }
+  }
+  if (xu.quad) {
+    // orbit mode: the new rows go straight into the member planes the
+    // forward reads (make_quad_kernel's layout, no separate pass):
+    //   quad[r][c] = (x[r][c], x[N-1-c][r], x[r][N-1-c], x[N-1-c][N-1-r]),
+    // so x[y][x] is member 0 of quad[y][x], 2 of quad[y][N-1-x] (along quad
+    // rows), 1 of quad[x][N-1-y] and 3 of quad[N-1-x][N-1-y] (along quad
+    // columns: the CTA's rows are consecutive cells there)
+    float* qf = reinterpret_cast<float*>(xu.quad + b * nn);
+    for (int i = threadIdx.x; i < keep * N; i += blockDim.x) {
+      const int r = i >> LOGN, x = i & (N - 1);
+      const int y = y0 + r;
+      if (y >= yown) continue;
+      const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
+      const float v = (r & 1) ? zz.y : zz.x;
+      qf[4 * (static_cast<size_t>(y) * N + x)] = v;
+      qf[4 * (static_cast<size_t>(y) * N + (N - 1 - x)) + 2] = v;
+    }
+    for (int i = threadIdx.x; i < keep * N; i += blockDim.x) {
+      const int x = i / keep, r = i - x * keep;
+      const int y = y0 + r;
+      if (y >= yown) continue;
+      const float2 zz = zs[(r >> 1) * NP + p2::pad(x)];
+      const float v = (r & 1) ? zz.y : zz.x;
+      qf[4 * (static_cast<size_t>(x) * N + (N - 1 - y)) + 1] = v;
+      qf[4 * (static_cast<size_t>(N - 1 - x) * N + (N - 1 - y)) + 3] = v;
     }
   }
   if (df.on) {
@@ -1165,6 +1192,11 @@ void launch_fft_cols_filter_slab(const FftPlan& f, float2* slab, const float2* m
              slab, maskT, f.tw.p, f.shape, cs);
   NCSG_CUDA_CHECK(cudaGetLastError());
   count_launch();
+}
+
+bool fft_writes_quad(const FftPlan& f) {
+  static const bool off = std::getenv("NCSG_FUSE_QUAD") && std::atoi(std::getenv("NCSG_FUSE_QUAD")) == 0;
+  return !off && f.tw2.p != nullptr;
 }
 
 bool fft_fuses_dual(const FftPlan& f, const DualFuse& df) {

@@ -424,6 +424,9 @@ struct XUpdate {
   float* x = nullptr;       // updated in place (x -= w) ; if subtract == 0: x = w
   float* x_old = nullptr;   // receives the pre-update x (nullable)
   float* xT = nullptr;      // receives the transposed result (nullable)
+  // orbit mode: receives the new x as the four dihedral member planes
+  // (make_quad_kernel's layout), power-of-two full-row path only (nullable)
+  float4* quad = nullptr;
   int subtract = 1;
   int* flag = nullptr;      // [0] = min(step counter [1]) over non-finite results (nullable)
   // fused P2P all-gather: the updated rows also go to these ranks' images
@@ -435,6 +438,9 @@ struct XUpdate {
 // Whether launch_fft_rows_c2r can take XUpdate::df = df (the power-of-two
 // path, staging within shared memory; NCSG_FUSE_DUAL=0 turns the fusion off).
 bool fft_fuses_dual(const FftPlan& f, const DualFuse& df);
+// Whether launch_fft_rows_c2r can take XUpdate::quad (the power-of-two path;
+// NCSG_FUSE_QUAD=0 keeps the stand-alone make_quad_kernel).
+bool fft_writes_quad(const FftPlan& f);
 void launch_fft_rows_c2r(const FftPlan& f, const float2* specT, const XUpdate& xu, int batch,
                          cudaStream_t s, RowSlab rs = RowSlab{});
 
