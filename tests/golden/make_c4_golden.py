@@ -34,7 +34,8 @@ def main():
     dt = time.time() - t0
     rng = np.random.default_rng(0)
     idx = np.sort(rng.choice(o.u.size, 100000, replace=False))
-    out = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c4_full.npz")
+    out = os.environ.get("NCS_GOLDEN_OUT") or os.path.join(
+        os.path.dirname(os.path.abspath(__file__)), "c4_full.npz")
     np.savez_compressed(out, x=o.x.astype(np.float32), u_idx=idx, u_sample=o.u.ravel()[idx],
                         rows=o.rows, b_head=np.ravel(b)[:4096], seconds=dt)
     print(f"wrote {out} ({os.path.getsize(out) / 1e6:.2f} MB) after {dt:.0f} s")
