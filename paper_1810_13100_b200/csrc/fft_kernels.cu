@@ -148,7 +148,8 @@ __device__ float2* fft_stockham(float2* a, float2* b, int nfft, int n, int logn,
   return a;
 }
 
-// ---- mixed-radix Stockham (sizes 2^a 3^b 5^c 7^d that are not powers of 2)
+// ---- mixed-radix Stockham (sizes that are not powers of 2: radix 2/3/4/5/7/8
+// butterflies in registers, any other prime factor by stockham_stage_prime)
 template <int R, int SIGN>
 __device__ __forceinline__ void dft_small(float2* v) {
   if constexpr (R == 2 || R == 4 || R == 8) {
@@ -199,6 +200,40 @@ __device__ void stockham_stage_mixed(const float2* in, float2* out, int nfft, in
   }
 }
 
+// Any other prime radix R (11, 13, ... up to n itself): one OUTPUT element per
+// thread, out[(j - k) R + k + ro Ns] = sum_r in[j + r n/R] w_n^{r e}, with
+// e = k n/(Ns R) + ro n/R (the stage twiddle w_{Ns R}^{r k} and the R-point
+// DFT factor w_R^{r ro} are both powers of w_n, so one table entry per term).
+// O(n R) per sequence: the reference's FFTW takes any N (fft.cpp:18-29), so
+// does this path; sizes with large prime factors are slow, not rejected.
+template <int SIGN>
+__device__ void stockham_stage_prime(const float2* in, float2* out, int nfft, int n, int Ns, int R,
+                                     const float2* __restrict__ tw) {
+  const int m = n / R;
+  const int step = n / (Ns * R);
+  for (int oi = threadIdx.x; oi < nfft * n; oi += blockDim.x) {
+    const int q = oi / n, o = oi - q * n;
+    // o = (j - k) R + k + ro Ns with k < Ns, ro < R
+    const int blk = o / (Ns * R), rem = o - blk * (Ns * R);
+    const int ro = rem / Ns, k = rem - ro * Ns;
+    const int j = blk * Ns + k;
+    const float2* src = in + q * n + j;
+    const int e = k * step + ro * m;  // < n
+    float re = 0.f, im = 0.f;
+    int idx = 0;
+    for (int r = 0; r < R; ++r) {
+      float2 w = __ldg(tw + idx);
+      if (SIGN > 0) w.y = -w.y;
+      const float2 v = src[r * m];
+      re += v.x * w.x - v.y * w.y;
+      im += v.x * w.y + v.y * w.x;
+      idx += e;
+      if (idx >= n) idx -= n;
+    }
+    out[oi] = make_float2(re, im);
+  }
+}
+
 template <int SIGN>
 __device__ float2* fft_mixed(float2* a, float2* b, int nfft, const FftShape& sh,
                              const float2* __restrict__ tw) {
@@ -212,7 +247,8 @@ __device__ float2* fft_mixed(float2* a, float2* b, int nfft, const FftShape& sh,
       case 4: stockham_stage_mixed<4, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
       case 5: stockham_stage_mixed<5, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
       case 7: stockham_stage_mixed<7, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
-      default: stockham_stage_mixed<8, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      case 8: stockham_stage_mixed<8, SIGN>(a, b, nfft, sh.n, Ns, tw); break;
+      default: stockham_stage_prime<SIGN>(a, b, nfft, sh.n, Ns, R, tw); break;
     }
     Ns *= R;
     float2* t = a;
@@ -1057,7 +1093,7 @@ void FftPlan::init(int n_, cudaStream_t s) {
   if (n >= 8 && (n & (n - 1)) == 0) {
     shape.logn = log2i(n);  // radix-8 fast path
   } else {
-    // 2^a 3^b 5^c 7^d: radix 8 / 4 / 2 for the power of two, then 3, 5, 7
+    // radix 8 / 4 / 2 for the power of two, then 3, 5, 7, then any other prime
     int r = n;
     auto push = [&](int f) {
       if (shape.nst >= 24) throw Error{NCSG_INVALID, "FFT size has too many factors"};
@@ -1068,10 +1104,11 @@ void FftPlan::init(int n_, cudaStream_t s) {
     while (r % 2 == 0) push(2), r /= 2;
     for (int f : {3, 5, 7})
       while (r % f == 0) push(f), r /= f;
-    if (r != 1)
-      throw Error{NCSG_INVALID,
-                  "GPU FFT sizes need prime factors 2, 3, 5 and 7 (got a factor " +
-                      std::to_string(r) + ")"};
+    // remaining prime factors (11, 13, ...): the generic one-output-per-thread stage
+    for (int f = 11; r > 1; f += 2) {
+      if (static_cast<long long>(f) * f > r) f = r;
+      while (r % f == 0) push(f), r /= f;
+    }
   }
   std::vector<float2> h(n);
   for (int k = 0; k < n; ++k) {

@@ -221,9 +221,15 @@ def test_mask_apply_mixed_radix_sizes(ncsg, port, n):
     assert rel(ncsg.mask_apply(h, x), want) <= 1e-5
 
 
-def test_fft_rejects_other_primes(ncsg):
-    with pytest.raises(ValueError, match="prime factors"):
-        ncsg.mask_apply(np.ones((22, 22)), np.ones((22, 22)))
+@pytest.mark.parametrize("n", [11, 22, 26, 33, 97, 121, 143, 187, 251, 442, 509])
+def test_mask_apply_other_prime_factors(ncsg, port, n):
+    # FFTW takes any N (fft.cpp:18-29): prime factors above 7 (11, 13, 17, ...,
+    # prime N itself) run the one-output-per-thread generic Stockham stage
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((n, n))
+    h = (port.laplacian_mask(n) + port.radon_mask(n, 3.0, 5.0)
+         + 0.3j * rng.standard_normal((n, n)))
+    assert rel(ncsg.mask_apply(h, x), port.mask_apply(h, x)) <= 1e-5
 
 
 @pytest.mark.parametrize("n,views,rays", [(16, 12, 21), (32, 24, 45), (64, 40, 91)])

@@ -162,6 +162,21 @@ def test_denoise_small_parity(ncsg, port):
     check_run(g, o)
 
 
+@pytest.mark.parametrize("n", [61, 66])
+def test_denoise_other_prime_sizes(ncsg, port, n):
+    # image sizes with a prime factor above 7 (61 prime, 66 = 2 x 3 x 11): the
+    # reference's FFTW takes any N (fft.cpp:18-29)
+    from paper_1810_13100_b200 import datagen
+
+    x = datagen.phantom(n, 5, 3)
+    b = x + 0.1 * datagen.stream_noise(x.shape, 4)
+    prob = Prob(1, n, 0, 0, 1.0, 1.0, 0.05, b)
+    mask = np.ones((n, n)) + port.laplacian_mask(n)
+    o = port.solve(prob, 1e-3, mask, 100, record_every=50)
+    g = gpu_problem(ncsg, prob, 1e-3, mask).solve(100, record_every=50)
+    check_run(g, o)
+
+
 def test_divergence_raises(ncsg, port):
     # test_solvers.cpp:627-644: far too small gamma diverges -> DivergenceError
     prob, mask, gamma = small_ct(port, n=16, A=16)
