@@ -24,17 +24,24 @@ def main(rank, world, port, out, mode="slab"):
     from paper_1810_13100_b200 import ncsg
     from test_gpu_solver import small_ct
 
+    # "nccl-<exchange>": one GPU per rank and the library's NCCL transport
+    # (test_two_gpu_nccl_matches_unsharded; needs >= `world` GPUs)
+    nccl = mode.startswith("nccl-")
+    mode = mode[5:] if nccl else mode
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_1810_13100_b200 import multigpu
 
     port_ = Port()
     prob, mask, gamma = small_ct(port_, n=64, A=48)
-    torch.cuda.set_device(0)
+    dev = rank if nccl else 0
+    torch.cuda.set_device(dev)
     p = ncsg.Problem(ncsg.CT, prob.n, prob.alpha, prob.beta, prob.lam, gamma, prob.b, mask=mask,
-                     n_angles=prob.angles, n_det=prob.det, orbit_shard=(rank, world))
-    comm = multigpu.gloo_comm(rank, world)  # host-staged gloo collectives
+                     n_angles=prob.angles, n_det=prob.det, orbit_shard=(rank, world), device=dev)
+    # NCCL over NVLink, or host-staged gloo collectives on a shared GPU
+    comm = multigpu.nccl_comm(rank, world, dev) if nccl else multigpu.gloo_comm(rank, world)
     p.set_state()
-    p.set_comm(comm, ncsg.XCHG_P2P if mode == "p2p" else ncsg.XCHG_SLAB)
+    p.set_comm(comm, {"p2p": ncsg.XCHG_P2P, "slab": ncsg.XCHG_SLAB,
+                      "allreduce": ncsg.XCHG_ALLREDUCE}[mode])
     res = p.solve(30, record_every=10)
     np.savez(os.path.join(out, f"rank{rank}.npz"), x=res.x, rows=res.rows)
     dist.barrier()
