@@ -238,9 +238,24 @@ def cpu_reference_rate(cfg, b, mask, iters_hi=3, iters_lo=1):
     run(iters_hi)
     t_hi = time.perf_counter() - t
     per = max(1e-9, (t_hi - t_lo) / (iters_hi - iters_lo))
-    return {"value": 1.0 / per, "unit": "it/s", "cores": cores, "kind": kind,
-            "sample": f"{cfg.name} ncs_solve {iters_hi} vs {iters_lo} iterations, "
-                      f"difference of wall times ({t_hi:.1f}s, {t_lo:.1f}s), same b and mask"}
+    out = {"value": 1.0 / per, "unit": "it/s", "cores": cores, "kind": kind,
+           "sample": f"{cfg.name} ncs_solve {iters_hi} vs {iters_lo} iterations, "
+                     f"difference of wall times ({t_hi:.1f}s, {t_lo:.1f}s), same b and mask"}
+    if kind == "reference":
+        # beside the serial reference: the OpenMP restatement (oracle/ncs_oracle.c,
+        # ray- and angle-parallel projectors) on every host core, same sample
+        try:
+            port, nt = Port(), max(1, len(os.sched_getaffinity(0)))
+            tp = []
+            for k in (iters_lo, iters_hi):
+                t = time.perf_counter()
+                port.solve(prob, cfg.gamma, mask, k, threads=nt)
+                tp.append(time.perf_counter() - t)
+            out["openmp_port"] = {"value": 1.0 / max(1e-9, (tp[1] - tp[0]) / (iters_hi - iters_lo)),
+                                  "unit": "it/s", "cores": nt, "kind": "port"}
+        except Exception as e:  # noqa: BLE001 - extra information only
+            out["openmp_port"] = {"value": None, "error": str(e)}
+    return out
 
 
 def run_reference(args, cfg):
