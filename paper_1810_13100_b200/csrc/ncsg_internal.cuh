@@ -216,6 +216,10 @@ constexpr int kGaTW = 32, kGaTH = NCSG_GA_TH, kGaThreads = 256;
 constexpr int kGaPx = kGaTW * kGaTH / kGaThreads;  // pixels per thread
 constexpr int kGaBatch = NCSG_GA_BATCH, kGaWaves = NCSG_GA_WAVES;
 constexpr int kGaSW = kGaTW + kGaTH + 8;            // staged rays per orbit and tile
+#ifndef NCSG_GA_WT_PF
+#define NCSG_GA_WT_PF 4
+#endif
+constexpr int kGaWtPf = NCSG_GA_WT_PF;  // table mode: orbits prefetched ahead into L2
 constexpr int kGaMaxChunk = 1024;                   // orbits per chunk (lowest-ray table)
 // Per-orbit constants of the gather (host fp64 from the Q32 lattice): the
 // lattice is p(s, k) = c + s a + k d, and pixel (X, Y) has the continuous
@@ -279,6 +283,12 @@ struct RadonDev {
   // rays' replayed ranges), in candidate order
   DevBuf<int> ga_tile_edge, ga_bt_base, ga_bt_off;
   DevBuf<GaBorderEntry> ga_bt_ent;
+  // Window-weight table of the gather adjoint: W[orbit][tile][plane][thread]
+  // float4 (12 bytes per (pixel, orbit)); state 0 = not built yet, 1 = in use,
+  // -1 = unavailable (disabled, over the size cap or out of memory)
+  DevBuf<float> ga_wtab;
+  int ga_wtab_state = 0;
+  bool ga_wtab_stream = false;
   // Orbit-interleaved dual (optional gather input): angle t's member slot
   // 4 * orbit + member (-1: none) and the padded row of rays per orbit.
   DevBuf<int> angle_slot;
@@ -310,6 +320,7 @@ struct RadonDev {
   void upload();
   void plan_adjoint(int batch);
   void build_gather_border_table();
+  void build_gather_weight_table();
   int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }
   // Forward partial slots per ray (fp_partial[batch][slots][m]).
   int fp_slots() const { return orbit_mode ? n_strips + n_segs - 1 : n_strips; }

@@ -920,6 +920,12 @@ struct GaArgs {
   const int* bt_base;
   const int* bt_off;
   const GaBorderEntry* bt_ent;
+  // window-weight table (RadonDev::ga_wtab): W[orbit][tile][float4 plane][thread],
+  // the geometry-only factor sum_k tent(ex) tent(ey) of every (pixel, orbit,
+  // candidate ray), built once per plan; wt_stream: larger than L2, read with
+  // evict-first loads
+  const float* wtab;
+  int wt_stream, wt_pf;  // wt_pf: orbits prefetched ahead into L2
 };
 
 // Border pixels (image row / column 0 or n-1) of the TW x TH tile at (X0, Y0)
@@ -1043,11 +1049,15 @@ __device__ __forceinline__ void cp_async16(unsigned dst, const void* src) {
 // cluster along grid.z and fold their member tiles through distributed
 // shared memory (fixed rank order: deterministic) before the stores, so the
 // FFT row pass reads 4 partial images per chunk group instead of per chunk.
-template <int TW, int TH, int NB, int CL>
+template <int TW, int TH, int NB, int CL, bool WT>
 #ifndef NCSG_GA_MINB
 #define NCSG_GA_MINB 4  // 64 registers, 4 CTAs per SM (without a minimum ptxas takes 70 -> 3 CTAs; with 1, 134)
 #endif
-__global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaArgs a) {
+#ifndef NCSG_GA_WT_MINB
+#define NCSG_GA_WT_MINB 3  // table mode: 80 registers (two weight sets + accumulators spill at 64)
+#endif
+__global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MINB)
+    bp_gather_kernel(GaArgs a) {
   pdl_wait();
   constexpr int PX = TW * TH / kGaThreads;
   constexpr int SW = TW + TH + 8;
@@ -1131,6 +1141,37 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
+  // table mode: the thread's 3 * PX weights of one orbit are 3 * PX / 4
+  // consecutive float4 planes of the (orbit, tile) block, [plane][thread] --
+  // a CTA reads 12 KB contiguous per orbit; the block of orbit o + kGaWtPf
+  // is prefetched into L2 a line per thread
+  static_assert(!WT || (NB % 2 == 0 && (3 * PX) % 4 == 0), "table mode register sets");
+  constexpr int WQ = 3 * PX / 4;
+  [[maybe_unused]] float4 wA[WQ], wB[WQ];
+  [[maybe_unused]] const size_t wtile =
+      (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * WQ * kGaThreads;
+  [[maybe_unused]] const size_t worb = static_cast<size_t>(gridDim.x) * gridDim.y * WQ * kGaThreads;
+  [[maybe_unused]] auto wload = [&](int og, float4 (&w)[WQ]) {
+    const float4* Wn = reinterpret_cast<const float4*>(a.wtab) + og * worb + wtile + threadIdx.x;
+#pragma unroll
+    for (int j = 0; j < WQ; ++j)
+      w[j] = a.wt_stream ? __ldcs(Wn + j * kGaThreads) : __ldg(Wn + j * kGaThreads);
+    if (a.wt_stream && og + a.wt_pf < o_end && threadIdx.x < WQ * kGaThreads / 8)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(
+          reinterpret_cast<const float4*>(a.wtab) + (og + a.wt_pf) * worb + wtile +
+          8 * threadIdx.x));
+  };
+  if constexpr (WT) {
+    if (o_begin < o_end) {
+      if (a.wt_stream)
+        for (int f = 1; f < a.wt_pf && o_begin + f < o_end; ++f)
+          if (threadIdx.x < WQ * kGaThreads / 8)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(
+                reinterpret_cast<const float4*>(a.wtab) + (o_begin + f) * worb + wtile +
+                8 * threadIdx.x));
+      wload(o_begin, wA);
+    }
+  }
   int buf = 0;
   if (o_begin < o_end) stage(o_begin, 0);
   for (int ob = o_begin; ob < o_end; ob += NB, buf ^= 1) {
@@ -1142,6 +1183,46 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
       asm volatile("cp.async.wait_group 0;" ::: "memory");
     }
     __syncthreads();
+    if constexpr (WT) {
+      // Table mode: the three window weights of every (pixel, orbit) stream
+      // from HBM (coalesced 128-byte rows; two register sets, the next
+      // orbit's loads in flight while this one accumulates -- staging batches
+      // are even except a chunk's last, so every batch starts on set A); only
+      // the first candidate ray's index is recomputed (integer).
+      auto accumulate = [&](int o, const float4 (&wq)[WQ]) {
+        float w[PX][3];
+#pragma unroll
+        for (int j = 0; j < WQ; ++j) {
+          const float t[4] = {wq[j].x, wq[j].y, wq[j].z, wq[j].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c) w[(4 * j + c) / 3][(4 * j + c) % 3] = t[c];
+        }
+        const GatherGeom& g = G[buf][o];
+        const float4* Uo = U4[buf][o];
+        const int sl = slo[ob - o_begin + o];
+        long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
+#pragma unroll
+        for (int p = 0; p < PX; ++p) {
+          if (p > 0) sq += RS * g.sy;
+          const bool first = q32_frac1(sq) > g.rho;
+          const int r0 = q32_floor(sq) - (first ? 0 : 1) - sl;
+#pragma unroll
+          for (int u = 0; u < 3; ++u) {
+            const float4 uv = Uo[r0 + u];
+            acc_xy[p] = ffma2(pk(w[p][u], w[p][u]), pk(uv.x, uv.y), acc_xy[p]);
+            acc_zw[p] = ffma2(pk(w[p][u], w[p][u]), pk(uv.z, uv.w), acc_zw[p]);
+          }
+        }
+      };
+      for (int o = 0; o < nb; o += 2) {
+        if (ob + o + 1 < o_end) wload(ob + o + 1, wB);
+        accumulate(o, wA);
+        if (o + 1 < nb) {
+          if (ob + o + 2 < o_end) wload(ob + o + 2, wA);
+          accumulate(o + 1, wB);
+        }
+      }
+    } else
     for (int o = 0; o < nb; ++o) {
       const GatherGeom& g = G[buf][o];
       const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
@@ -1301,6 +1382,70 @@ __global__ void __launch_bounds__(kGaThreads, NCSG_GA_MINB) bp_gather_kernel(GaA
       o3[static_cast<size_t>(n - 1 - X) * n + (n - 1 - Y)] = ot[3][y][x];
     }
   }
+}
+
+// The gather adjoint's window-weight table (GaArgs::wtab): for every (orbit,
+// pixel) the three candidate rays' weights w_u = sum of the three candidate
+// tent products -- bp_gather_kernel's direct-mode arithmetic, instruction for
+// instruction, evaluated once per plan instead of once per step.  The weights
+// depend on the geometry only (like the reference's ray table, radon.cpp:43-71,
+// or a stored system matrix): the adjoint of a step is then w . u over three
+// staged ray cells per (pixel, orbit), bound by streaming 12 bytes per (pixel,
+// orbit) from HBM instead of by the FMA pipe.
+struct GaWtabArgs {
+  const GatherGeom* geo;
+  int n_orb, n;
+  size_t nn;
+  float* wtab;
+};
+__global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs a) {
+  constexpr int TW = kGaTW, TH = kGaTH, PX = kGaPx, RS = kGaThreads / TW;
+  const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
+  const int tx = threadIdx.x % TW, ty = threadIdx.x / TW;
+  const long long Xt = X0 + tx, Yt = Y0 + ty;
+  static_assert((3 * PX) % 4 == 0, "whole float4 planes per thread");
+  const GatherGeom g = a.geo[blockIdx.z];
+  float wv[3 * PX];
+  const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
+  const float cu = -g.ay * g.inv_dy, K1 = -g.inv_dy - 1.5f;
+  const f32x2 negD = pk(-g.dx, -g.dy), D2 = pk(2.0f * g.dx, 2.0f * g.dy);
+  const f32x2 CU12 = pk(cu, 2.0f * cu);
+  const f32x2 MAG = pk(12582912.0f, 12582912.0f), NMAG = pk(-12582912.0f, -12582912.0f);
+  long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
+  long long kq = g.k0 + Xt * g.kx + Yt * g.ky;
+#pragma unroll
+  for (int p = 0; p < PX; ++p) {
+    if (p > 0) sq += RS * g.sy, kq += RS * g.ky;
+    const float fs1 = q32_frac1(sq), fk1p = q32_frac1(kq);
+    const bool first = fs1 > g.rho;
+    const float du0 = (first ? 1.0f : 0.0f) - fs1;
+    const float z0 = fmaf(du0, cu, fk1p + K1);
+    f32x2 Bu = ffma2(pk(du0, du0), A, ffma2(pk(fk1p, fk1p), negD, D2));
+    const float zl0 = __fsub_rn(__fadd_rn(z0, 12582912.0f), 12582912.0f);
+    const float2 zl12 = upk(fadd2(fadd2(fadd2(pk(z0, z0), CU12), MAG), NMAG));
+#pragma unroll
+    for (int u = 0; u < 3; ++u) {
+      if (u > 0) Bu = fadd2(Bu, A);
+      const float zl = u == 0 ? zl0 : (u == 1 ? zl12.x : zl12.y);
+      f32x2 e = ffma2(pk(zl, zl), D, Bu);
+      float2 v = upk(e);
+      float w = tent(v.x) * tent(v.y);
+      e = fadd2(e, D);
+      v = upk(e);
+      w = fmaf(tent(v.x), tent(v.y), w);
+      e = fadd2(e, D);
+      v = upk(e);
+      w = fmaf(tent(v.x), tent(v.y), w);
+      wv[p * 3 + u] = w;
+    }
+  }
+  // [orbit][tile][plane j][thread]: float4 j holds weights 4j .. 4j+3 of (p, u) order
+  float4* Wo = reinterpret_cast<float4*>(a.wtab) +
+               ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
+                blockIdx.x) * (3 * PX / 4) * kGaThreads + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < 3 * PX / 4; ++j)
+    Wo[j * kGaThreads] = make_float4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]);
 }
 
 // The gather adjoint's border-pixel correction table (GaArgs::bt_*), built
@@ -1681,6 +1826,42 @@ void RadonDev::build_gather_border_table() {
   }
 }
 
+// The window-weight table of the gather adjoint (ga_weight_table_kernel):
+// 12 bytes per (pixel, orbit).  Skipped (the adjoint then evaluates the
+// windows every step) with NCSG_GA_WTAB=0, above NCSG_GA_WTAB_MAX_GB (default
+// 64) or when the allocation fails.
+void RadonDev::build_gather_weight_table() {
+  if (ga_wtab_state != 0) return;
+  ga_wtab_state = -1;
+  if (const char* e = getenv("NCSG_GA_WTAB"))
+    if (atoi(e) == 0) return;
+  const size_t nn = static_cast<size_t>(geo.n) * geo.n, n_orb = geo.orbits.size();
+  const size_t tiles = static_cast<size_t>((geo.n + kGaTW - 1) / kGaTW) *
+                       ((geo.n + kGaTH - 1) / kGaTH);
+  const size_t count = 3 * tiles * kGaTW * kGaTH * n_orb;  // whole tiles (edge tiles padded)
+  double cap_gb = 64.0;
+  if (const char* e = getenv("NCSG_GA_WTAB_MAX_GB")) cap_gb = atof(e);
+  if (n_orb == 0 || count * sizeof(float) > cap_gb * 1e9) return;
+  float* w = nullptr;
+  if (cudaMalloc(&w, count * sizeof(float)) != cudaSuccess) {
+    cudaGetLastError();  // out of memory: direct mode
+    return;
+  }
+  ga_wtab.p = w;
+  ga_wtab.n = count;
+  GaWtabArgs a{gather.p, static_cast<int>(n_orb), geo.n, nn, w};
+  dim3 grid((geo.n + kGaTW - 1) / kGaTW, (geo.n + kGaTH - 1) / kGaTH,
+            static_cast<unsigned>(n_orb));
+  ga_weight_table_kernel<<<grid, kGaThreads>>>(a);
+  NCSG_CUDA_CHECK(cudaGetLastError());
+  NCSG_CUDA_CHECK(cudaDeviceSynchronize());
+  // tables that cannot stay in L2 next to the step's working set are read
+  // with evict-first loads
+  ga_wtab_stream = count * sizeof(float) > (48u << 20);
+  if (const char* e = getenv("NCSG_GA_WTAB_STREAM")) ga_wtab_stream = atoi(e) != 0;
+  ga_wtab_state = 1;
+}
+
 void RadonDev::plan_adjoint(int batch) {
   const int n = geo.n;
   bp_orbit = orbit_mode && !getenv("NCSG_NO_GATHER");
@@ -1723,6 +1904,7 @@ void RadonDev::plan_adjoint(int batch) {
     bp_chunk_len[0] = bp_chunk_len[1] = 1;
     bp_batch_planned = batch;
     build_gather_border_table();
+    build_gather_weight_table();
     return;
   }
   int bw, bt, bpitch;
@@ -1981,12 +2163,25 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     at[1].val.clusterDim.z = r.bp_cluster;
     cfg.attrs = at;
     cfg.numAttrs = r.bp_cluster > 1 ? 2 : 1;
+    a.wtab = r.ga_wtab_state == 1 ? r.ga_wtab.p : nullptr;
+    a.wt_stream = r.ga_wtab_stream ? 1 : 0;
+    static const int wt_pf = [] {
+      const char* e = getenv("NCSG_GA_WT_PF");
+      return e ? std::max(1, atoi(e)) : kGaWtPf;
+    }();
+    a.wt_pf = wt_pf;
     if (r.bp_cluster == 4)
-      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 4>, a));
+      NCSG_CUDA_CHECK(
+          cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 4, false>, a));
     else if (r.bp_cluster == 2)
-      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 2>, a));
+      NCSG_CUDA_CHECK(
+          cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 2, false>, a));
+    else if (a.wtab)
+      NCSG_CUDA_CHECK(
+          cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 1, true>, a));
     else
-      NCSG_CUDA_CHECK(cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 1>, a));
+      NCSG_CUDA_CHECK(
+          cudaLaunchKernelEx(&cfg, bp_gather_kernel<kGaTW, kGaTH, kGaBatch, 1, false>, a));
     NCSG_CUDA_CHECK(cudaGetLastError());
     count_launch();
     return;
