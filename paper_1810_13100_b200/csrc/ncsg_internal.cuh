@@ -284,9 +284,9 @@ struct RadonDev {
   DevBuf<int> ga_tile_edge, ga_bt_base, ga_bt_off;
   DevBuf<GaBorderEntry> ga_bt_ent;
   // Window-weight table of the gather adjoint: W[orbit][tile][plane][thread]
-  // float4 (12 bytes per (pixel, orbit)); state 0 = not built yet, 1 = in use,
+  // uint4 (three 21-bit fixed-point weights = 8 bytes per (pixel, orbit)); state 0 = not built yet, 1 = in use,
   // -1 = unavailable (disabled, over the size cap or out of memory)
-  DevBuf<float> ga_wtab;
+  DevBuf<uint4> ga_wtab;
   int ga_wtab_state = 0;
   bool ga_wtab_stream = false;
   // Orbit-interleaved dual (optional gather input): angle t's member slot

@@ -920,11 +920,11 @@ struct GaArgs {
   const int* bt_base;
   const int* bt_off;
   const GaBorderEntry* bt_ent;
-  // window-weight table (RadonDev::ga_wtab): W[orbit][tile][float4 plane][thread],
+  // window-weight table (RadonDev::ga_wtab): W[orbit][tile][uint4 plane][thread],
   // the geometry-only factor sum_k tent(ex) tent(ey) of every (pixel, orbit,
-  // candidate ray), built once per plan; wt_stream: larger than L2, read with
+  // candidate ray) as 21-bit fixed point, built once per plan; wt_stream: larger than L2, read with
   // evict-first loads
-  const float* wtab;
+  const uint4* wtab;
   int wt_stream, wt_pf;  // wt_pf: orbits prefetched ahead into L2
 };
 
@@ -1141,34 +1141,33 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  // table mode: the thread's 3 * PX weights of one orbit are 3 * PX / 4
-  // consecutive float4 planes of the (orbit, tile) block, [plane][thread] --
-  // a CTA reads 12 KB contiguous per orbit; the block of orbit o + kGaWtPf
-  // is prefetched into L2 a line per thread
-  static_assert(!WT || (NB % 2 == 0 && (3 * PX) % 4 == 0), "table mode register sets");
-  constexpr int WQ = 3 * PX / 4;
-  [[maybe_unused]] float4 wA[WQ], wB[WQ];
+  // table mode: a pixel's three weights are 21-bit fixed point (step 2^-20)
+  // in two words; the thread's PX pixels of one orbit are PX / 2 consecutive
+  // uint4 planes of the (orbit, tile) block, [plane][thread] -- a CTA reads
+  // 8 KB contiguous per orbit; the block of orbit o + wt_pf is prefetched
+  // into L2 a line per thread
+  static_assert(!WT || (NB % 2 == 0 && PX % 2 == 0), "table mode register sets");
+  constexpr int WQ = PX / 2;
+  [[maybe_unused]] uint4 wA[WQ], wB[WQ];
   [[maybe_unused]] const size_t wtile =
       (static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * WQ * kGaThreads;
   [[maybe_unused]] const size_t worb = static_cast<size_t>(gridDim.x) * gridDim.y * WQ * kGaThreads;
-  [[maybe_unused]] auto wload = [&](int og, float4 (&w)[WQ]) {
-    const float4* Wn = reinterpret_cast<const float4*>(a.wtab) + og * worb + wtile + threadIdx.x;
+  [[maybe_unused]] auto wload = [&](int og, uint4 (&w)[WQ]) {
+    const uint4* Wn = a.wtab + og * worb + wtile + threadIdx.x;
 #pragma unroll
     for (int j = 0; j < WQ; ++j)
       w[j] = a.wt_stream ? __ldcs(Wn + j * kGaThreads) : __ldg(Wn + j * kGaThreads);
     if (a.wt_stream && og + a.wt_pf < o_end && threadIdx.x < WQ * kGaThreads / 8)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(
-          reinterpret_cast<const float4*>(a.wtab) + (og + a.wt_pf) * worb + wtile +
-          8 * threadIdx.x));
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.wtab + (og + a.wt_pf) * worb + wtile +
+                                                    8 * threadIdx.x));
   };
   if constexpr (WT) {
     if (o_begin < o_end) {
       if (a.wt_stream)
         for (int f = 1; f < a.wt_pf && o_begin + f < o_end; ++f)
           if (threadIdx.x < WQ * kGaThreads / 8)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(
-                reinterpret_cast<const float4*>(a.wtab) + (o_begin + f) * worb + wtile +
-                8 * threadIdx.x));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.wtab + (o_begin + f) * worb + wtile +
+                                                          8 * threadIdx.x));
       wload(o_begin, wA);
     }
   }
@@ -1189,13 +1188,22 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
       // orbit's loads in flight while this one accumulates -- staging batches
       // are even except a chunk's last, so every batch starts on set A); only
       // the first candidate ray's index is recomputed (integer).
-      auto accumulate = [&](int o, const float4 (&wq)[WQ]) {
+      auto accumulate = [&](int o, const uint4 (&wq)[WQ]) {
+        // unpack: q | 0x4B000000 is the float 2^23 + q, and (2^23 + q) 2^-20 - 8
+        // = q 2^-20 exactly
         float w[PX][3];
 #pragma unroll
         for (int j = 0; j < WQ; ++j) {
-          const float t[4] = {wq[j].x, wq[j].y, wq[j].z, wq[j].w};
+          const unsigned lo[2] = {wq[j].x, wq[j].z}, hi[2] = {wq[j].y, wq[j].w};
 #pragma unroll
-          for (int c = 0; c < 4; ++c) w[(4 * j + c) / 3][(4 * j + c) % 3] = t[c];
+          for (int c = 0; c < 2; ++c) {
+            const unsigned q0 = lo[c] & 0x1fffffu;
+            const unsigned q1 = __funnelshift_r(lo[c], hi[c], 21) & 0x1fffffu;
+            const unsigned q2 = hi[c] >> 10;
+            w[2 * j + c][0] = fmaf(__uint_as_float(q0 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
+            w[2 * j + c][1] = fmaf(__uint_as_float(q1 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
+            w[2 * j + c][2] = fmaf(__uint_as_float(q2 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
+          }
         }
         const GatherGeom& g = G[buf][o];
         const float4* Uo = U4[buf][o];
@@ -1390,20 +1398,20 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
 // instruction, evaluated once per plan instead of once per step.  The weights
 // depend on the geometry only (like the reference's ray table, radon.cpp:43-71,
 // or a stored system matrix): the adjoint of a step is then w . u over three
-// staged ray cells per (pixel, orbit), bound by streaming 12 bytes per (pixel,
+// staged ray cells per (pixel, orbit), bound by streaming 8 bytes per (pixel,
 // orbit) from HBM instead of by the FMA pipe.
 struct GaWtabArgs {
   const GatherGeom* geo;
   int n_orb, n;
   size_t nn;
-  float* wtab;
+  uint4* wtab;
 };
 __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs a) {
   constexpr int TW = kGaTW, TH = kGaTH, PX = kGaPx, RS = kGaThreads / TW;
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   const int tx = threadIdx.x % TW, ty = threadIdx.x / TW;
   const long long Xt = X0 + tx, Yt = Y0 + ty;
-  static_assert((3 * PX) % 4 == 0, "whole float4 planes per thread");
+  static_assert(PX % 2 == 0, "whole uint4 planes per thread");
   const GatherGeom g = a.geo[blockIdx.z];
   float wv[3 * PX];
   const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
@@ -1439,13 +1447,24 @@ __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs 
       wv[p * 3 + u] = w;
     }
   }
-  // [orbit][tile][plane j][thread]: float4 j holds weights 4j .. 4j+3 of (p, u) order
-  float4* Wo = reinterpret_cast<float4*>(a.wtab) +
-               ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
-                blockIdx.x) * (3 * PX / 4) * kGaThreads + threadIdx.x;
+  // 21-bit fixed point, step 2^-20 (w < 1.6: at most 1 + 2 (1 - 1/sqrt 2) of y
+  // tents, x tents <= 1), three per pixel in two words; [orbit][tile][plane j]
+  // [thread]: uint4 j holds pixels 2j, 2j + 1
+  unsigned lo[PX], hi[PX];
 #pragma unroll
-  for (int j = 0; j < 3 * PX / 4; ++j)
-    Wo[j * kGaThreads] = make_float4(wv[4 * j], wv[4 * j + 1], wv[4 * j + 2], wv[4 * j + 3]);
+  for (int p = 0; p < PX; ++p) {
+    unsigned q[3];
+#pragma unroll
+    for (int u = 0; u < 3; ++u)
+      q[u] = min(__float2uint_rn(wv[p * 3 + u] * 1048576.0f), 0x1fffffu);
+    lo[p] = q[0] | (q[1] << 21);
+    hi[p] = (q[1] >> 11) | (q[2] << 10);
+  }
+  uint4* Wo = a.wtab + ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
+                        blockIdx.x) * (PX / 2) * kGaThreads + threadIdx.x;
+#pragma unroll
+  for (int j = 0; j < PX / 2; ++j)
+    Wo[j * kGaThreads] = make_uint4(lo[2 * j], hi[2 * j], lo[2 * j + 1], hi[2 * j + 1]);
 }
 
 // The gather adjoint's border-pixel correction table (GaArgs::bt_*), built
@@ -1827,7 +1846,7 @@ void RadonDev::build_gather_border_table() {
 }
 
 // The window-weight table of the gather adjoint (ga_weight_table_kernel):
-// 12 bytes per (pixel, orbit).  Skipped (the adjoint then evaluates the
+// 8 bytes per (pixel, orbit).  Skipped (the adjoint then evaluates the
 // windows every step) with NCSG_GA_WTAB=0, above NCSG_GA_WTAB_MAX_GB (default
 // 64) or when the allocation fails.
 void RadonDev::build_gather_weight_table() {
@@ -1838,12 +1857,13 @@ void RadonDev::build_gather_weight_table() {
   const size_t nn = static_cast<size_t>(geo.n) * geo.n, n_orb = geo.orbits.size();
   const size_t tiles = static_cast<size_t>((geo.n + kGaTW - 1) / kGaTW) *
                        ((geo.n + kGaTH - 1) / kGaTH);
-  const size_t count = 3 * tiles * kGaTW * kGaTH * n_orb;  // whole tiles (edge tiles padded)
+  // uint4 = two pixels; whole tiles (edge tiles padded)
+  const size_t count = tiles * kGaTW * kGaTH / 2 * n_orb;
   double cap_gb = 64.0;
   if (const char* e = getenv("NCSG_GA_WTAB_MAX_GB")) cap_gb = atof(e);
-  if (n_orb == 0 || count * sizeof(float) > cap_gb * 1e9) return;
-  float* w = nullptr;
-  if (cudaMalloc(&w, count * sizeof(float)) != cudaSuccess) {
+  if (n_orb == 0 || count * sizeof(uint4) > cap_gb * 1e9) return;
+  uint4* w = nullptr;
+  if (cudaMalloc(&w, count * sizeof(uint4)) != cudaSuccess) {
     cudaGetLastError();  // out of memory: direct mode
     return;
   }
@@ -1857,7 +1877,7 @@ void RadonDev::build_gather_weight_table() {
   NCSG_CUDA_CHECK(cudaDeviceSynchronize());
   // tables that cannot stay in L2 next to the step's working set are read
   // with evict-first loads
-  ga_wtab_stream = count * sizeof(float) > (48u << 20);
+  ga_wtab_stream = count * sizeof(uint4) > (48u << 20);
   if (const char* e = getenv("NCSG_GA_WTAB_STREAM")) ga_wtab_stream = atoi(e) != 0;
   ga_wtab_state = 1;
 }
