@@ -336,6 +336,13 @@ def roofline_of(cfg, plan, phase_avg, clocks):
         ach = nbytes / (ms * 1e-3) / 1e9
         row = {"bound": bound, "launch_ms": ms, "bytes_per_launch": nbytes, "achieved": ach,
                "peak": peaks_gbs[bound], "unit": "GB/s", "frac": ach / peaks_gbs[bound]}
+        if k == "adjoint" and plan.get("adjoint_table_bytes"):
+            # table mode: the window weights (geometry only, built per plan)
+            # stream from HBM once per launch (from L2 when the table fits, C1/C5)
+            tb = int(plan["adjoint_table_bytes"])
+            row["table_bytes_per_launch"] = tb
+            row["table_hbm_gbs"] = tb / (ms * 1e-3) / 1e9
+            row["table_hbm_frac"] = row["table_hbm_gbs"] / peaks_gbs["hbm"]
         kp = prof.get("kernels", {}).get(k)
         if kp:
             row["traffic"] = kp.get("dram_bytes")

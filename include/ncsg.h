@@ -374,6 +374,10 @@ typedef struct ncsg_plan_info {
   int64_t samples;    /* bilinear samples per R application (own angles) */
   int64_t m0, g, range, batch;
   int dual_fused;     /* 1: the whole dual update runs in the inverse row pass (DENOISE) */
+  int64_t adjoint_table_bytes; /* gather adjoint's window-weight table streamed per R^T
+                                  application (8 B per (pixel, orbit)); 0: windows evaluated
+                                  every step (NCSG_GA_WTAB=0, over NCSG_GA_WTAB_MAX_GB, or no
+                                  memory) */
 } ncsg_plan_info;
 ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out);
 /* Kernel launches issued by this library since load. */

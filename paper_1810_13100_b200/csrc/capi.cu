@@ -1315,6 +1315,7 @@ ncsg_status ncsg_problem_create(const ncsg_problem_desc* desc, ncsg_problem** ou
       p->radon->upload();
       clk.mark("upload");
       p->radon->plan_adjoint(d.batch);
+      clk.mark("plan_adjoint");
     } else {
       p->m0 = p->nn;
       p->m_begin = 0;
@@ -1713,6 +1714,10 @@ ncsg_status ncsg_problem_plan(const ncsg_problem* p, ncsg_plan_info* out) {
       r.n_orbits = static_cast<int>(p->radon->geo.orbits.size());
       r.samples = p->radon->geo.samples;
       r.transposed_copy = (!p->radon->orbit_mode && !p->radon->geo.cls[1].empty()) ? 1 : 0;
+      r.adjoint_table_bytes =
+          p->radon->bp_orbit && p->radon->ga_wtab_state == 1
+              ? static_cast<int64_t>(p->radon->ga_wtab.n * sizeof(uint4))
+              : 0;
     }
     if (p->d.kind != NCSG_DENOISE) {
       r.fp_slots = proj_slots(p);

@@ -43,7 +43,8 @@ class PlanInfo(C.Structure):
     _fields_ = [("orbit_forward", C.c_int), ("gather_adjoint", C.c_int), ("fp_slots", C.c_int),
                 ("bp_partials", C.c_int), ("n_orbits", C.c_int), ("transposed_copy", C.c_int),
                 ("samples", C.c_int64), ("m0", C.c_int64), ("g", C.c_int64),
-                ("range", C.c_int64), ("batch", C.c_int64), ("dual_fused", C.c_int)]
+                ("range", C.c_int64), ("batch", C.c_int64), ("dual_fused", C.c_int),
+                ("adjoint_table_bytes", C.c_int64)]
 
 
 XCHG_ALLREDUCE, XCHG_SLAB, XCHG_P2P = 0, 1, 2

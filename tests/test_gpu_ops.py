@@ -130,6 +130,37 @@ def test_radon_c4_size(ncsg, port):
     assert R.sample_count() == 8581547248  # SURVEY.md §8 sizes table
 
 
+def test_gather_adjoint_table_and_direct_modes(ncsg, port, monkeypatch):
+    # the gather adjoint with its window-weight table (built per plan, 21-bit
+    # fixed-point weights) and with the windows evaluated every step
+    # (NCSG_GA_WTAB=0; also the fallback above NCSG_GA_WTAB_MAX_GB) agree with
+    # each other and with radon.cpp:104-127
+    n, A = 96, 64  # not a multiple of the 32 x 32 tile: padded edge tiles
+    D = ncsg.default_detector_count(n)
+    u = np.random.default_rng(3).standard_normal((A, D))
+    want = port.radon_adjoint(u, n)
+    got = {}
+    for mode, env in (("table", {}), ("direct", {"NCSG_GA_WTAB": "0"}),
+                      ("capped", {"NCSG_GA_WTAB_MAX_GB": "0.000001"})):
+        for k in ("NCSG_GA_WTAB", "NCSG_GA_WTAB_MAX_GB"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        got[mode] = ncsg.RadonMap(n, A, D).adjoint(u)
+        assert rel(got[mode], want) <= TOL
+    assert np.array_equal(got["direct"], got["capped"])
+    assert rel(got["table"], got["direct"]) <= 2e-6
+    for k in ("NCSG_GA_WTAB", "NCSG_GA_WTAB_MAX_GB"):
+        monkeypatch.delenv(k, raising=False)
+    b = np.zeros((A, D))
+    p = ncsg.Problem(ncsg.CT, n, 0.1, 0.1, 0.01, 1.0, b, n_angles=A, n_det=D)
+    plan = p.plan()  # 8 bytes per (pixel of the 3 x 3 whole tiles, orbit)
+    assert plan["adjoint_table_bytes"] == 8 * plan["n_orbits"] * 9 * 1024
+    monkeypatch.setenv("NCSG_GA_WTAB", "0")
+    q = ncsg.Problem(ncsg.CT, n, 0.1, 0.1, 0.01, 1.0, b, n_angles=A, n_det=D)
+    assert q.plan()["adjoint_table_bytes"] == 0
+
+
 def test_adjoint_identity_and_determinism(ncsg):
     n, A, D = 128, 180, 185
     rng = np.random.default_rng(3)
