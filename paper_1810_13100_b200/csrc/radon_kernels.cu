@@ -1157,7 +1157,7 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
 #pragma unroll
     for (int j = 0; j < WQ; ++j)
       w[j] = a.wt_stream ? __ldcs(Wn + j * kGaThreads) : __ldg(Wn + j * kGaThreads);
-    if (a.wt_stream && og + a.wt_pf < o_end && threadIdx.x < WQ * kGaThreads / 8)
+    if (a.wt_stream && a.wt_pf > 0 && og + a.wt_pf < o_end && threadIdx.x < WQ * kGaThreads / 8)
       asm volatile("prefetch.global.L2 [%0];" ::"l"(a.wtab + (og + a.wt_pf) * worb + wtile +
                                                     8 * threadIdx.x));
   };
@@ -2187,7 +2187,7 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     a.wt_stream = r.ga_wtab_stream ? 1 : 0;
     static const int wt_pf = [] {
       const char* e = getenv("NCSG_GA_WT_PF");
-      return e ? std::max(1, atoi(e)) : kGaWtPf;
+      return e ? std::max(0, atoi(e)) : kGaWtPf;  // 0: no L2 prefetch
     }();
     a.wt_pf = wt_pf;
     if (r.bp_cluster == 4)
