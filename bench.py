@@ -554,6 +554,11 @@ def bench_single(args, cfg):
             "data": "synthetic", "config": workload(cfg), "roofline": roofline,
             "phases_ms": phase_avg, "gpu_launches": launches, "clocks": clocks,
             "samples_per_projection": S}
+    # the timed problem, its events and the flush buffer are released before the
+    # end-to-end calls (each creates its own problem, as a user's call would)
+    del prob, stream, starts, ends, flush, R
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
     if not args.no_e2e:
         line["e2e"] = e2e_rate(cfg, b, mask, args.steps)
     if not args.no_cpu_baseline:
