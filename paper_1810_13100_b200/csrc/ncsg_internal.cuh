@@ -217,7 +217,7 @@ constexpr int kGaPx = kGaTW * kGaTH / kGaThreads;  // pixels per thread
 constexpr int kGaBatch = NCSG_GA_BATCH, kGaWaves = NCSG_GA_WAVES;
 constexpr int kGaSW = kGaTW + kGaTH + 8;            // staged rays per orbit and tile
 #ifndef NCSG_GA_WT_PF
-#define NCSG_GA_WT_PF 4
+#define NCSG_GA_WT_PF 2
 #endif
 constexpr int kGaWtPf = NCSG_GA_WT_PF;  // table mode: orbits prefetched ahead into L2
 constexpr int kGaMaxChunk = 1024;                   // orbits per chunk (lowest-ray table)

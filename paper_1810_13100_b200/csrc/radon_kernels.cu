@@ -1087,6 +1087,7 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
 #pragma unroll
   for (int p = 0; p < PX; ++p) acc_xy[p] = acc_zw[p] = pk(0.f, 0.f);
   const long long Xt = X0 + tx, Yt = Y0 + ty;
+  [[maybe_unused]] const long long Yw = Y0 + PX * ty;  // table mode: rows PX * ty + p
   // Border pixels (image row / column 0 or n-1) of this tile, row-major, and
   // the tile's slice of the correction table.
   const int edge = a.tile_edge[blockIdx.y * gridDim.x + blockIdx.x];
@@ -1141,11 +1142,11 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
 
-  // table mode: a pixel's three weights are 21-bit fixed point (step 2^-20)
-  // in two words; the thread's PX pixels of one orbit are PX / 2 consecutive
+  // table mode: a pixel's three weights are 20-bit fixed point (step 2^-19)
+  // plus a 3-bit first-ray index difference in two words; the thread's PX pixels of one orbit are PX / 2 consecutive
   // uint4 planes of the (orbit, tile) block, [plane][thread] -- a CTA reads
   // 8 KB contiguous per orbit; the block of orbit o + wt_pf is prefetched
-  // into L2 a line per thread
+  // into L2 by one bulk prefetch
   static_assert(!WT || (NB % 2 == 0 && PX % 2 == 0), "table mode register sets");
   constexpr int WQ = PX / 2;
   [[maybe_unused]] uint4 wA[WQ], wB[WQ];
@@ -1157,17 +1158,19 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
 #pragma unroll
     for (int j = 0; j < WQ; ++j)
       w[j] = a.wt_stream ? __ldcs(Wn + j * kGaThreads) : __ldg(Wn + j * kGaThreads);
-    if (a.wt_stream && a.wt_pf > 0 && og + a.wt_pf < o_end && threadIdx.x < WQ * kGaThreads / 8)
-      asm volatile("prefetch.global.L2 [%0];" ::"l"(a.wtab + (og + a.wt_pf) * worb + wtile +
-                                                    8 * threadIdx.x));
+    if (a.wt_stream && a.wt_pf > 0 && og + a.wt_pf < o_end && threadIdx.x == 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                       a.wtab + (og + a.wt_pf) * worb + wtile),
+                   "r"(static_cast<unsigned>(WQ * kGaThreads * sizeof(uint4))));
   };
   if constexpr (WT) {
     if (o_begin < o_end) {
       if (a.wt_stream)
         for (int f = 1; f < a.wt_pf && o_begin + f < o_end; ++f)
-          if (threadIdx.x < WQ * kGaThreads / 8)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(a.wtab + (o_begin + f) * worb + wtile +
-                                                          8 * threadIdx.x));
+          if (threadIdx.x == 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             a.wtab + (o_begin + f) * worb + wtile),
+                         "r"(static_cast<unsigned>(WQ * kGaThreads * sizeof(uint4))));
       wload(o_begin, wA);
     }
   }
@@ -1189,36 +1192,49 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
       // are even except a chunk's last, so every batch starts on set A); only
       // the first candidate ray's index is recomputed (integer).
       auto accumulate = [&](int o, const uint4 (&wq)[WQ]) {
-        // unpack: q | 0x4B000000 is the float 2^23 + q, and (2^23 + q) 2^-20 - 8
-        // = q 2^-20 exactly
-        float w[PX][3];
+        // A thread's pixels are PX consecutive rows of one column, taken in
+        // pairs: |d sigma / dy| <= 1/sqrt 2 < 1, so the first candidate rays of
+        // the two pixels of a pair differ by at most one and their windows
+        // share four consecutive ray cells (4 LDS.128 per pair instead of 6);
+        // a pixel whose window starts one cell later has its weights shifted
+        // by selects.  The table carries the index differences (3 bits per
+        // pixel), so only pixel 0's first ray is recomputed.
+        const GatherGeom& g = G[buf][o];
+        const float4* Uo = U4[buf][o];
+        const long long sq = g.s0 + Xt * g.sx + Yw * g.sy;
+        const bool first = q32_frac1(sq) > g.rho;
+        const int R0 = q32_floor(sq) - (first ? 0 : 1) - slo[ob - o_begin + o];
 #pragma unroll
         for (int j = 0; j < WQ; ++j) {
           const unsigned lo[2] = {wq[j].x, wq[j].z}, hi[2] = {wq[j].y, wq[j].w};
+          float w[2][3];
 #pragma unroll
           for (int c = 0; c < 2; ++c) {
-            const unsigned q0 = lo[c] & 0x1fffffu;
-            const unsigned q1 = __funnelshift_r(lo[c], hi[c], 21) & 0x1fffffu;
-            const unsigned q2 = hi[c] >> 10;
-            w[2 * j + c][0] = fmaf(__uint_as_float(q0 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
-            w[2 * j + c][1] = fmaf(__uint_as_float(q1 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
-            w[2 * j + c][2] = fmaf(__uint_as_float(q2 | 0x4b000000u), 9.5367431640625e-7f, -8.0f);
+            // q | 0x4B000000 is the float 2^23 + q; (2^23 + q) 2^-19 - 16 = q 2^-19 exactly
+            const unsigned q0 = lo[c] & 0xfffffu;
+            const unsigned q1 = __funnelshift_r(lo[c], hi[c], 20) & 0xfffffu;
+            const unsigned q2 = (hi[c] >> 8) & 0xfffffu;
+            w[c][0] = fmaf(__uint_as_float(q0 | 0x4b000000u), 1.9073486328125e-6f, -16.0f);
+            w[c][1] = fmaf(__uint_as_float(q1 | 0x4b000000u), 1.9073486328125e-6f, -16.0f);
+            w[c][2] = fmaf(__uint_as_float(q2 | 0x4b000000u), 1.9073486328125e-6f, -16.0f);
           }
-        }
-        const GatherGeom& g = G[buf][o];
-        const float4* Uo = U4[buf][o];
-        const int sl = slo[ob - o_begin + o];
-        long long sq = g.s0 + Xt * g.sx + Yt * g.sy;
+          const int ea = static_cast<int>(hi[0] >> 28) - 2;     // first ray of pixel a - R0
+          const int delta = static_cast<int>(hi[1] >> 28) - 1;  // pixel b's - pixel a's
+          const bool sa = delta < 0, sb = delta > 0;            // which window starts a cell later
+          const int lo_i = R0 + ea - (sa ? 1 : 0);
+          const float4 c0 = Uo[lo_i], c1 = Uo[lo_i + 1], c2 = Uo[lo_i + 2];
+          const float4 c3 = Uo[min(lo_i + 3, SW - 1)];  // weight 0 unless a window is shifted
+          const float xa[4] = {sa ? 0.f : w[0][0], sa ? w[0][0] : w[0][1], sa ? w[0][1] : w[0][2],
+                               sa ? w[0][2] : 0.f};
+          const float xb[4] = {sb ? 0.f : w[1][0], sb ? w[1][0] : w[1][1], sb ? w[1][1] : w[1][2],
+                               sb ? w[1][2] : 0.f};
+          const float4 cc[4] = {c0, c1, c2, c3};
 #pragma unroll
-        for (int p = 0; p < PX; ++p) {
-          if (p > 0) sq += RS * g.sy;
-          const bool first = q32_frac1(sq) > g.rho;
-          const int r0 = q32_floor(sq) - (first ? 0 : 1) - sl;
-#pragma unroll
-          for (int u = 0; u < 3; ++u) {
-            const float4 uv = Uo[r0 + u];
-            acc_xy[p] = ffma2(pk(w[p][u], w[p][u]), pk(uv.x, uv.y), acc_xy[p]);
-            acc_zw[p] = ffma2(pk(w[p][u], w[p][u]), pk(uv.z, uv.w), acc_zw[p]);
+          for (int k = 0; k < 4; ++k) {
+            acc_xy[2 * j] = ffma2(pk(xa[k], xa[k]), pk(cc[k].x, cc[k].y), acc_xy[2 * j]);
+            acc_zw[2 * j] = ffma2(pk(xa[k], xa[k]), pk(cc[k].z, cc[k].w), acc_zw[2 * j]);
+            acc_xy[2 * j + 1] = ffma2(pk(xb[k], xb[k]), pk(cc[k].x, cc[k].y), acc_xy[2 * j + 1]);
+            acc_zw[2 * j + 1] = ffma2(pk(xb[k], xb[k]), pk(cc[k].z, cc[k].w), acc_zw[2 * j + 1]);
           }
         }
       };
@@ -1321,7 +1337,7 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
   float(*ot)[TH][TW + 1] = reinterpret_cast<float(*)[TH][TW + 1]>(&U4[0][0][0]);
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
-    const int y = ty + p * RS;
+    const int y = WT ? PX * ty + p : ty + p * RS;
     const float2 v01 = upk(acc_xy[p]), v23 = upk(acc_zw[p]);
     ot[0][y][tx] = v01.x;
     ot[1][y][tx] = v01.y;
@@ -1405,15 +1421,17 @@ struct GaWtabArgs {
   int n_orb, n;
   size_t nn;
   uint4* wtab;
+  int* bad;  // set when a first-ray difference does not fit its code
 };
 __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs a) {
-  constexpr int TW = kGaTW, TH = kGaTH, PX = kGaPx, RS = kGaThreads / TW;
+  constexpr int TW = kGaTW, TH = kGaTH, PX = kGaPx;
+  static_assert(PX % 2 == 0, "pixel pairs, whole uint4 planes per thread");
   const int X0 = blockIdx.x * TW, Y0 = blockIdx.y * TH;
   const int tx = threadIdx.x % TW, ty = threadIdx.x / TW;
-  const long long Xt = X0 + tx, Yt = Y0 + ty;
-  static_assert(PX % 2 == 0, "whole uint4 planes per thread");
+  const long long Xt = X0 + tx, Yt = Y0 + PX * ty;  // the table-mode pixel map: rows PX ty + p
   const GatherGeom g = a.geo[blockIdx.z];
   float wv[3 * PX];
+  int R[PX];  // first candidate ray of pixel p
   const f32x2 A = pk(g.ax, g.ay), D = pk(g.dx, g.dy);
   const float cu = -g.ay * g.inv_dy, K1 = -g.inv_dy - 1.5f;
   const f32x2 negD = pk(-g.dx, -g.dy), D2 = pk(2.0f * g.dx, 2.0f * g.dy);
@@ -1423,9 +1441,10 @@ __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs 
   long long kq = g.k0 + Xt * g.kx + Yt * g.ky;
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
-    if (p > 0) sq += RS * g.sy, kq += RS * g.ky;
+    if (p > 0) sq += g.sy, kq += g.ky;
     const float fs1 = q32_frac1(sq), fk1p = q32_frac1(kq);
     const bool first = fs1 > g.rho;
+    R[p] = q32_floor(sq) - (first ? 0 : 1);
     const float du0 = (first ? 1.0f : 0.0f) - fs1;
     const float z0 = fmaf(du0, cu, fk1p + K1);
     f32x2 Bu = ffma2(pk(du0, du0), A, ffma2(pk(fk1p, fk1p), negD, D2));
@@ -1447,18 +1466,22 @@ __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs 
       wv[p * 3 + u] = w;
     }
   }
-  // 21-bit fixed point, step 2^-20 (w < 1.6: at most 1 + 2 (1 - 1/sqrt 2) of y
-  // tents, x tents <= 1), three per pixel in two words; [orbit][tile][plane j]
-  // [thread]: uint4 j holds pixels 2j, 2j + 1
+  // 20-bit fixed point, step 2^-19 (w < 1.6: at most 1 + 2 (1 - 1/sqrt 2) of y
+  // tents, x tents <= 1), three per pixel in two words, plus a 3-bit code: an
+  // even pixel's first ray minus pixel 0's (+2; |.| <= 2 over two rows), an
+  // odd pixel's minus its pair partner's (+1; |.| <= 1 over one row, because
+  // |d sigma / dy| <= 1/sqrt 2).  [orbit][tile][plane j][thread]: uint4 j
+  // holds pixels 2j, 2j + 1.  A difference out of range flags the table bad.
   unsigned lo[PX], hi[PX];
 #pragma unroll
   for (int p = 0; p < PX; ++p) {
     unsigned q[3];
 #pragma unroll
-    for (int u = 0; u < 3; ++u)
-      q[u] = min(__float2uint_rn(wv[p * 3 + u] * 1048576.0f), 0x1fffffu);
-    lo[p] = q[0] | (q[1] << 21);
-    hi[p] = (q[1] >> 11) | (q[2] << 10);
+    for (int u = 0; u < 3; ++u) q[u] = min(__float2uint_rn(wv[p * 3 + u] * 524288.0f), 0xfffffu);
+    const int code = (p & 1) ? R[p] - R[p - 1] + 1 : R[p] - R[0] + 2;
+    if (code < 0 || code > ((p & 1) ? 2 : 4)) atomicExch(a.bad, 1);
+    lo[p] = q[0] | (q[1] << 20);
+    hi[p] = (q[1] >> 12) | (q[2] << 8) | (static_cast<unsigned>(code & 7) << 28);
   }
   uint4* Wo = a.wtab + ((static_cast<size_t>(blockIdx.z) * gridDim.y + blockIdx.y) * gridDim.x +
                         blockIdx.x) * (PX / 2) * kGaThreads + threadIdx.x;
@@ -1869,12 +1892,20 @@ void RadonDev::build_gather_weight_table() {
   }
   ga_wtab.p = w;
   ga_wtab.n = count;
-  GaWtabArgs a{gather.p, static_cast<int>(n_orb), geo.n, nn, w};
+  DevBuf<int> bad;
+  bad.alloc(1);
+  NCSG_CUDA_CHECK(cudaMemset(bad.p, 0, sizeof(int)));
+  GaWtabArgs a{gather.p, static_cast<int>(n_orb), geo.n, nn, w, bad.p};
   dim3 grid((geo.n + kGaTW - 1) / kGaTW, (geo.n + kGaTH - 1) / kGaTH,
             static_cast<unsigned>(n_orb));
   ga_weight_table_kernel<<<grid, kGaThreads>>>(a);
   NCSG_CUDA_CHECK(cudaGetLastError());
-  NCSG_CUDA_CHECK(cudaDeviceSynchronize());
+  int h_bad = 0;
+  NCSG_CUDA_CHECK(cudaMemcpy(&h_bad, bad.p, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h_bad) {  // a geometry outside the pair model: direct mode
+    ga_wtab.release();
+    return;
+  }
   // tables that cannot stay in L2 next to the step's working set are read
   // with evict-first loads
   ga_wtab_stream = count * sizeof(uint4) > (48u << 20);

@@ -149,7 +149,7 @@ def test_gather_adjoint_table_and_direct_modes(ncsg, port, monkeypatch):
         got[mode] = ncsg.RadonMap(n, A, D).adjoint(u)
         assert rel(got[mode], want) <= TOL
     assert np.array_equal(got["direct"], got["capped"])
-    assert rel(got["table"], got["direct"]) <= 2e-6
+    assert rel(got["table"], got["direct"]) <= 4e-6
     for k in ("NCSG_GA_WTAB", "NCSG_GA_WTAB_MAX_GB"):
         monkeypatch.delenv(k, raising=False)
     b = np.zeros((A, D))
