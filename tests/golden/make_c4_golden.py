@@ -1,8 +1,9 @@
 """Generates tests/golden/c4_full.npz: the oracle's C4 NCS solve (2048^2,
 2048 x 2897, the BASELINE 300 iterations) from the pinned parameters, for
 test_gpu_solver.test_c4_full_against_golden.  Run once on a CPU host
-(`python tests/golden/make_c4_golden.py [threads]`, ~3 h with 7 OpenMP
-threads: ~30 s per iteration); the GPU box never runs the oracle solve at this
+(`python tests/golden/make_c4_golden.py [threads]`: 11 287 s with 7 OpenMP
+threads, ~10 s per iteration with the 16 host threads of a GPU box --
+scripts/gpu/c4_golden.sh); the GPU box never runs the oracle solve at this
 size, only the one oracle forward that rebuilds b.  Stores x (fp32), a seeded
 sample of u, the record rows (record_every = 75, solve_template's rows) and the
 head of b (to check the instance is the same).  Follows solve_template
