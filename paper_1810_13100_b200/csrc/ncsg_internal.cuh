@@ -288,7 +288,6 @@ struct RadonDev {
   // -1 = unavailable (disabled, over the size cap or out of memory)
   DevBuf<uint4> ga_wtab;
   int ga_wtab_state = 0;
-  bool ga_wtab_stream = false;
   // Orbit-interleaved dual (optional gather input): angle t's member slot
   // 4 * orbit + member (-1: none) and the padded row of rays per orbit.
   DevBuf<int> angle_slot;
@@ -321,6 +320,7 @@ struct RadonDev {
   void plan_adjoint(int batch);
   void build_gather_border_table();
   void build_gather_weight_table();
+  bool gather_table_streams(int batch) const;
   int n_partials() const { return bp_chunks[0] + bp_chunks[1]; }
   // Forward partial slots per ray (fp_partial[batch][slots][m]).
   int fp_slots() const { return orbit_mode ? n_strips + n_segs - 1 : n_strips; }

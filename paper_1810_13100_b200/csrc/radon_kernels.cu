@@ -1906,11 +1906,15 @@ void RadonDev::build_gather_weight_table() {
     ga_wtab.release();
     return;
   }
-  // tables that cannot stay in L2 next to the step's working set are read
-  // with evict-first loads
-  ga_wtab_stream = count * sizeof(uint4) > (48u << 20);
-  if (const char* e = getenv("NCSG_GA_WTAB_STREAM")) ga_wtab_stream = atoi(e) != 0;
   ga_wtab_state = 1;
+}
+
+// Tables that cannot stay in L2 next to the step's working set are read with
+// evict-first loads; a batch re-reads its table once per problem, so it keeps
+// plain loads up to most of the 126 MB L2.
+bool RadonDev::gather_table_streams(int batch) const {
+  if (const char* e = getenv("NCSG_GA_WTAB_STREAM")) return atoi(e) != 0;
+  return ga_wtab.n * sizeof(uint4) > (batch > 1 ? (96u << 20) : (48u << 20));
 }
 
 void RadonDev::plan_adjoint(int batch) {
@@ -2215,7 +2219,7 @@ void launch_radon_adjoint_partial(const RadonDev& r, const float* u, size_t u_st
     cfg.attrs = at;
     cfg.numAttrs = r.bp_cluster > 1 ? 2 : 1;
     a.wtab = r.ga_wtab_state == 1 ? r.ga_wtab.p : nullptr;
-    a.wt_stream = r.ga_wtab_stream ? 1 : 0;
+    a.wt_stream = r.gather_table_streams(batch) ? 1 : 0;
     static const int wt_pf = [] {
       const char* e = getenv("NCSG_GA_WT_PF");
       return e ? std::max(0, atoi(e)) : kGaWtPf;  // 0: no L2 prefetch
