@@ -215,7 +215,10 @@ constexpr int kBpWaves = NCSG_BP_WAVES;  // adjoint: target CTAs = 148 * 3 * wav
 constexpr int kGaTW = 32, kGaTH = NCSG_GA_TH, kGaThreads = 256;
 constexpr int kGaPx = kGaTW * kGaTH / kGaThreads;  // pixels per thread
 constexpr int kGaBatch = NCSG_GA_BATCH, kGaWaves = NCSG_GA_WAVES;
-constexpr int kGaSW = kGaTW + kGaTH + 8;            // staged rays per orbit and tile
+#ifndef NCSG_GA_SW_EXTRA
+#define NCSG_GA_SW_EXTRA 0  // extra staged cells (experiments with taller tiles: epilogue space)
+#endif
+constexpr int kGaSW = kGaTW + kGaTH + 8 + NCSG_GA_SW_EXTRA;  // staged rays per orbit and tile
 #ifndef NCSG_GA_WT_PF
 #define NCSG_GA_WT_PF 2
 #endif

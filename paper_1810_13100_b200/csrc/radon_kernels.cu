@@ -1060,7 +1060,7 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
     bp_gather_kernel(GaArgs a) {
   pdl_wait();
   constexpr int PX = TW * TH / kGaThreads;
-  constexpr int SW = TW + TH + 8;
+  constexpr int SW = TW + TH + 8 + NCSG_GA_SW_EXTRA;
   static_assert(kGaThreads % TW == 0 && kGaThreads % TH == 0, "tile rows / columns per pass");
   static_assert(NB <= 32 && (NB & (NB - 1)) == 0, "border items reduce within a warp");
   __shared__ __align__(16) float4 U4[2][NB][SW];
@@ -1198,12 +1198,13 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
         // share four consecutive ray cells (4 LDS.128 per pair instead of 6);
         // a pixel whose window starts one cell later has its weights shifted
         // by selects.  The table carries the index differences (3 bits per
-        // pixel), so only pixel 0's first ray is recomputed.
+        // pixel: pair to pair, and within a pair), so only pixel 0's first ray
+        // is recomputed.
         const GatherGeom& g = G[buf][o];
         const float4* Uo = U4[buf][o];
         const long long sq = g.s0 + Xt * g.sx + Yw * g.sy;
         const bool first = q32_frac1(sq) > g.rho;
-        const int R0 = q32_floor(sq) - (first ? 0 : 1) - slo[ob - o_begin + o];
+        int Ra = q32_floor(sq) - (first ? 0 : 1) - slo[ob - o_begin + o];
 #pragma unroll
         for (int j = 0; j < WQ; ++j) {
           const unsigned lo[2] = {wq[j].x, wq[j].z}, hi[2] = {wq[j].y, wq[j].w};
@@ -1218,10 +1219,10 @@ __global__ void __launch_bounds__(kGaThreads, WT ? NCSG_GA_WT_MINB : NCSG_GA_MIN
             w[c][1] = fmaf(__uint_as_float(q1 | 0x4b000000u), 1.9073486328125e-6f, -16.0f);
             w[c][2] = fmaf(__uint_as_float(q2 | 0x4b000000u), 1.9073486328125e-6f, -16.0f);
           }
-          const int ea = static_cast<int>(hi[0] >> 28) - 2;     // first ray of pixel a - R0
+          Ra += static_cast<int>(hi[0] >> 28) - 2;  // pixel a's first ray - the previous pair's
           const int delta = static_cast<int>(hi[1] >> 28) - 1;  // pixel b's - pixel a's
           const bool sa = delta < 0, sb = delta > 0;            // which window starts a cell later
-          const int lo_i = R0 + ea - (sa ? 1 : 0);
+          const int lo_i = Ra - (sa ? 1 : 0);
           const float4 c0 = Uo[lo_i], c1 = Uo[lo_i + 1], c2 = Uo[lo_i + 2];
           const float4 c3 = Uo[min(lo_i + 3, SW - 1)];  // weight 0 unless a window is shifted
           const float xa[4] = {sa ? 0.f : w[0][0], sa ? w[0][0] : w[0][1], sa ? w[0][1] : w[0][2],
@@ -1468,7 +1469,8 @@ __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs 
   }
   // 20-bit fixed point, step 2^-19 (w < 1.6: at most 1 + 2 (1 - 1/sqrt 2) of y
   // tents, x tents <= 1), three per pixel in two words, plus a 3-bit code: an
-  // even pixel's first ray minus pixel 0's (+2; |.| <= 2 over two rows), an
+  // even pixel's first ray minus the previous even pixel's (+2; |.| <= 2 over
+  // two rows), an
   // odd pixel's minus its pair partner's (+1; |.| <= 1 over one row, because
   // |d sigma / dy| <= 1/sqrt 2).  [orbit][tile][plane j][thread]: uint4 j
   // holds pixels 2j, 2j + 1.  A difference out of range flags the table bad.
@@ -1478,7 +1480,7 @@ __global__ void __launch_bounds__(kGaThreads) ga_weight_table_kernel(GaWtabArgs 
     unsigned q[3];
 #pragma unroll
     for (int u = 0; u < 3; ++u) q[u] = min(__float2uint_rn(wv[p * 3 + u] * 524288.0f), 0xfffffu);
-    const int code = (p & 1) ? R[p] - R[p - 1] + 1 : R[p] - R[0] + 2;
+    const int code = (p & 1) ? R[p] - R[p - 1] + 1 : (p ? R[p] - R[p - 2] + 2 : 2);
     if (code < 0 || code > ((p & 1) ? 2 : 4)) atomicExch(a.bad, 1);
     lo[p] = q[0] | (q[1] << 20);
     hi[p] = (q[1] >> 12) | (q[2] << 8) | (static_cast<unsigned>(code & 7) << 28);
